@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 fusion + property-query path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+
+A step = one full pass of the hot path over one object: voxel-domain bbox, the per-object
+G = fmap @ text^T table, the fused project / depth-test / gather / normalise / similarity /
+softmax / regression / voxel + integrate partials kernel, (N>1: partial all-reduce), voxel-mass
+finalisation. Default workload: BASELINE config 5 (16M points, 64 views, 37x37x1024 bf16 maps,
+K=128, 512^3 grid) — the config BASELINE quotes at 1/2/4/8 GPUs; it fits one B200. Points are
+range-sharded across ranks (strong scaling); views are replicated.
+
+`value` = point-view samples/s over the whole job with inputs resident in HBM; `e2e` = the same
+through the public API with inputs uploaded from pinned host memory and per-point properties +
+mass read back inside the timed region. `--impl reference` times the CPU oracle port of the
+reference (rank 0 only) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 1024 * 1024
+SIMT_FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # nominal at max clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=None, help="points in the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-simt", action="store_true")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------------------------
+def algorithmic_bytes(cfg, n, nv, k, p, d, fmap_bytes, cells, kpad):
+    """Compulsory HBM bytes of one fused-kernel launch (SURVEY §8d formula + the bitset/counts the
+    kernel writes + the G table it reads): points 12N; depth V*H*W*4; maps V*Hf*Wf*D*b; text K*D*4
+    and table K*P*4 (read by prepare / the kernel); G cells*Kpad*4; outputs N*(4P + 4 code +
+    4 count + 4*ceil(V/32) mask)."""
+    h = w = cfg.image
+    hf, wf, _ = cfg.fmap
+    nwords = (nv + 31) // 32
+    return (12 * n + nv * h * w * 4 + nv * hf * wf * d * fmap_bytes + k * d * 4 + k * p * 4
+            + cells * kpad * 4 + n * (4 * p + 4 + 4 + 4 * nwords))
+
+
+def cpu_oracle_run(wl, sample: int):
+    """Time the oracle port of the reference on the first `sample` points (all views)."""
+    from oracle import propfield_oracle as O
+
+    views = wl.views(f32_maps=True)
+    pts = wl.points[:sample]
+    # JIT warm-up of the numba kernels on a tiny slice (excluded, like kernels.warmup())
+    O.fuse_and_query(pts[:64], views, wl.text, wl.values, wl.cfg.temperature, wl.cfg.eps, 8)
+    t0 = time.perf_counter()
+    out = O.fuse_and_query(pts, views, wl.text, wl.values, wl.cfg.temperature, wl.cfg.eps, wl.cfg.grid)
+    dt = time.perf_counter() - t0
+    return dt, out
+
+
+def default_cpu_sample(cfg) -> int:
+    # ~10-20 s of CPU work at the reference's ~1 M samples/s
+    return int(min(cfg.n, max(2000, 12_000_000 // max(1, cfg.nviews) // max(1, cfg.d // 512))))
+
+
+def cores_used() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------------------------
+def run_reference(args, cfg):
+    """`--impl reference`: the reference algorithm (CPU oracle port) on the host cores, rank 0."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from paper_2511_03126_b200 import workloads
+
+    sample = args.cpu_sample or max(2000, default_cpu_sample(cfg) // 4)
+    wl = workloads.generate(cfg, device_splat=cfg.n > 500_000)
+    wl.points = wl.points[:sample] if wl.points.shape[0] > sample else wl.points
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, _ = cpu_oracle_run(wl, sample)
+        if i >= args.warmup:
+            times.append(dt)
+    t = statistics.mean(times)
+    value = sample * cfg.nviews / t
+    line = {
+        "impl": "reference", "metric": "point-view samples/sec", "value": value, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_desc(cfg),
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores_used(), "kind": "port",
+                         "sample": f"first {sample} of {cfg.n} points x {cfg.nviews} views per step"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_desc(cfg):
+    hf, wf, d = cfg.fmap
+    return {"workload": f"{cfg.name}: N={cfg.n} points, V={cfg.nviews} views, {cfg.image}^2 depth, "
+                        f"{hf}x{wf}x{d} {'bf16' if cfg.bf16 else 'f32'} maps, K={cfg.k}, {cfg.grid}^3 grid",
+            "points": cfg.n, "views": cfg.nviews, "image": cfg.image, "fmap": list(cfg.fmap),
+            "feature_storage": "bf16" if cfg.bf16 else "f32", "materials": cfg.k, "grid": cfg.grid,
+            "temperature": cfg.temperature, "eps": cfg.eps}
+
+
+# ---------------------------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2511_03126_b200 as pf
+    from paper_2511_03126_b200 import _lib, workloads
+    from paper_2511_03126_b200.dist import global_bbox, shard_range
+
+    wl = workloads.generate(cfg, device_splat=True)
+    n_total = cfg.n
+    lo, hi = shard_range(n_total, rank, world)
+    nv = cfg.nviews
+    R = np.stack([p.rotation for p in wl.poses])
+    tv = np.stack([p.translation for p in wl.poses])
+    intr = np.tile([wl.intrinsics.fx, wl.intrinsics.fy, wl.intrinsics.cx, wl.intrinsics.cy], (nv, 1))
+    if cfg.bf16:
+        fmap_dev = torch.from_numpy(wl.fmaps.view(np.int16)).to(dev).view(torch.bfloat16)
+    else:
+        fmap_dev = torch.from_numpy(wl.fmaps).to(dev)
+    depth_dev = wl.depth.to(dev)
+    views = pf.ViewSet.from_tensors(R, tv, intr, depth_dev, fmap_dev, device=dev)
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta, density_col=0, device=dev)
+    pts_host = np.ascontiguousarray(wl.points[lo:hi])
+    pts = torch.from_numpy(pts_host).to(dev)
+    n = pts.shape[0]
+    bufs = pf.FuseBuffers(n, views, tables, cfg.grid, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        bufs.reset()
+        if world > 1:
+            _lib.call("pf_bbox", pts.data_ptr(), n, bufs.lo_hi.data_ptr(), stream.cuda_stream)
+            global_bbox(bufs.lo_hi)
+            lohi = bufs.lo_hi
+        else:
+            lohi = None
+        if ev:
+            ev[0].record(stream)
+        pf.fuse_prepare(views, tables, bufs)
+        if ev:
+            ev[1].record(stream)
+        res = pf.fuse_and_query(pts, views, tables, temperature=cfg.temperature, epsilon=cfg.eps,
+                                grid=cfg.grid, lo_hi=lohi, buffers=bufs, reduce=False,
+                                prepared=True, force_simt=args.force_simt, reset=False)
+        if ev:
+            ev[2].record(stream)
+        if world > 1:
+            res.allreduce()
+        res.finalize()
+        return res
+
+    inputs_bytes = (pts.numel() * 4 + depth_dev.numel() * 4 + fmap_dev.numel() * fmap_dev.element_size())
+    flush = inputs_bytes < 2 * L2_BYTES
+    scratch = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if flush else None
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    evs = [[mk() for _ in range(4)] for _ in range(args.steps)]
+    starts = [mk() for _ in range(args.steps)]
+    clk = ClockSampler(local)
+    launches0 = _lib.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    for i in range(args.steps):
+        if flush:
+            scratch.fill_(float(i))  # L2 flush between steps (outside the step's events)
+        starts[i].record(stream)
+        res = step(evs[i])
+        evs[i][3].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    launches = _lib.launch_count() - launches0
+    step_ms = [starts[i].elapsed_time(evs[i][3]) for i in range(args.steps)]
+    kern_ms = [evs[i][1].elapsed_time(evs[i][2]) for i in range(args.steps)]
+    prep_ms = [evs[i][0].elapsed_time(evs[i][1]) for i in range(args.steps)]
+    t_step = sum(step_ms) / args.steps
+    t_kern = sum(kern_ms) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([t_step, t_kern], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_kern = (float(x) for x in tt.cpu())
+    mass = res.mass_kg()
+    part = res.host_partials()
+
+    # ---- end to end through the public API, host buffers ---------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        h_pts = pin(pts_host)
+        h_depth = wl.depth.cpu().pin_memory()
+        h_fmap = (torch.from_numpy(wl.fmaps.view(np.int16)).pin_memory() if cfg.bf16
+                  else pin(wl.fmaps))
+        h_text, h_vals, h_mt = pin(wl.text), pin(wl.values.astype(np.float32)), pin(wl.mid_theta.astype(np.float32))
+        h_props = torch.empty((n, tables.p), dtype=torch.float32).pin_memory()
+        h_mass = torch.empty(2, dtype=torch.float64).pin_memory()
+        d_fmap_raw = views.fmap.view(torch.int16) if cfg.bf16 else views.fmap
+
+        def e2e_step():
+            pts.copy_(h_pts, non_blocking=True)
+            views.depth.copy_(h_depth.reshape(-1), non_blocking=True)
+            d_fmap_raw.copy_(h_fmap.reshape(-1), non_blocking=True)
+            tables.text.copy_(h_text, non_blocking=True)
+            tables.values.copy_(h_vals, non_blocking=True)
+            tables.mid_theta.copy_(h_mt, non_blocking=True)
+            r = step()
+            h_props.copy_(r.props, non_blocking=True)
+            h_mass.copy_(bufs.mass, non_blocking=True)
+
+        bi = (h_pts.numel() * 4 + h_depth.numel() * 4 + h_fmap.numel() * 2 * (1 if cfg.bf16 else 2)
+              + (h_text.numel() + h_vals.numel() + h_mt.numel()) * 4)
+        bo = h_props.numel() * 4 + 16
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        a, b = mk(), mk()
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        t_e2e = a.elapsed_time(b) / args.steps
+        if world > 1:
+            import torch.distributed as dist
+
+            tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        e2e = {"value": n_total * nv / (t_e2e * 1e-3), "unit": "samples/s", "ms_per_step": t_e2e,
+               "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo)}
+
+    if rank != 0:
+        return
+    # ---- roofline of the dominant kernel --------------------------------------------------------
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak_src = "measured"
+    except Exception:
+        peak_src = "fallback"
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    cells = nv * cfg.fmap[0] * cfg.fmap[1]
+    kpad = 32 * ((cfg.k + 31) // 32)
+    algo = algorithmic_bytes(cfg, n, nv, cfg.k, tables.p, cfg.d, 2 if cfg.bf16 else 4, cells, kpad)
+    achieved = algo / (t_kern * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get(cfg.name, {}).get("fuse_bytes_per_launch")
+    vis_pairs = part["visible_pairs"]
+    fma_flop = 2.0 * vis_pairs / max(1, world) * 4 * (cfg.d + kpad)  # gather + G-table taps
+    line = {
+        "metric": "point-view samples/sec",
+        "value": n_total * nv / (t_step * 1e-3),
+        "unit": "samples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_step,
+        "latency_ms_per_object": t_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {**config_desc(cfg), "parallelism": f"point-range x{world}",
+                   "l2": ("inputs larger than L2" if not flush else "L2 flushed between steps")},
+        "stages_ms": {"fuse_kernel": t_kern, "prepare_G": sum(prep_ms) / args.steps,
+                      "rest(bbox,zero,voxel-mass,allreduce)": t_step - t_kern - sum(prep_ms) / args.steps},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "k_fuse_simt", "algorithmic_bytes_per_launch": algo,
+                     "compute": {"simt_fma_tflops": fma_flop / (t_kern * 1e-3) / 1e12,
+                                 "simt_peak_tflops_nominal": SIMT_FP32_PEAK_TFLOPS}},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "result": {"mass_kg": mass, "featured": part["featured"], "visible_pairs": vis_pairs,
+                   "visible_fraction": vis_pairs / (n * nv)},
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        sample = args.cpu_sample or default_cpu_sample(cfg)
+        dt, ref = cpu_oracle_run(wl, sample)
+        cpu_val = sample * nv / dt
+        line["cpu_baseline"] = {"value": cpu_val, "unit": "samples/s", "cores": cores_used(),
+                                "kind": "port",
+                                "sample": f"first {sample} of {cfg.n} points x {nv} views, full path "
+                                          "(numba kernels single-threaded as in the reference; BLAS threaded)"}
+        # parity spot-check of the same sample on the GPU (bench is allowed to run the oracle)
+        sub = torch.from_numpy(np.ascontiguousarray(wl.points[:sample])).to(dev)
+        r2 = pf.fuse_and_query(sub, views, tables, temperature=cfg.temperature, epsilon=cfg.eps,
+                               grid=cfg.grid)
+        cnt = r2.counts.cpu().numpy()
+        props = r2.props.cpu().numpy().astype(np.float64)
+        featured = ref["counts"] > 0
+        rel = np.abs(props[featured, 0] - ref["props"][featured, 0]) / np.abs(ref["props"][featured, 0])
+        line["parity_sample"] = {"points": sample, "counts_equal": bool(np.array_equal(cnt, ref["counts"])),
+                                 "density_max_rel_err": float(rel.max()) if rel.size else 0.0,
+                                 "voxel_mass_rel_err": abs(r2.mass_kg() - ref["mass"]) / max(1e-30, ref["mass"])}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    from paper_2511_03126_b200 import workloads
+
+    cfg = workloads.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

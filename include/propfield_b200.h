@@ -1,0 +1,209 @@
+/*
+ * propfield_b200.h — C ABI of the B200-native fusion + property-query path.
+ *
+ * Drop-in boundary for the reference's hot path. Each entry point below names the
+ * reference interface it replaces (file:line under /root/reference/pkg/src/propfield/). The Python
+ * package paper_2511_03126_b200 binds these symbols with ctypes (INTEGRATION.md shows the binding);
+ * any other FFI (cffi, a C++ caller, cgo) can bind them the same way.
+ *
+ * Conventions (all entry points):
+ *   - Every pointer argument is a DEVICE pointer unless its name ends in `_host`.
+ *   - The caller allocates every buffer (outputs and workspace). The library never allocates or
+ *     frees caller memory and keeps no global device state; `pf_*_workspace_bytes` size workspaces.
+ *   - Calls are stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream) and are
+ *     re-entrant for distinct output buffers. Nothing synchronises unless documented.
+ *   - Return value: PF_OK (0) or a PF_ERR_* status. `pf_last_error()` returns a thread-local
+ *     message for the last failing call on this thread. The Python binding maps statuses to the
+ *     reference's exception classes (errors.py:4-37): VALUE -> ValueError, STRUCTURE ->
+ *     BundleStructureError, MATERIAL -> MaterialError, CUDA -> CudaError.
+ *   - There is no CPU fallback and no backend switch: without a CUDA device every call fails
+ *     with PF_ERR_CUDA.
+ */
+#ifndef PROPFIELD_B200_H
+#define PROPFIELD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_ABI_VERSION 1
+
+enum pf_status {
+  PF_OK = 0,
+  PF_ERR_VALUE = 1,     /* bad scalar argument, e.g. temperature <= 0 (grounding.py:170-171) */
+  PF_ERR_STRUCTURE = 2, /* inconsistent shapes / unsupported layout (bundle.py:45-55,105-116)   */
+  PF_ERR_MATERIAL = 3,  /* NaN similarity / missing property (grounding.py:69-72,173-174)       */
+  PF_ERR_CUDA = 4       /* CUDA runtime failure (no reference twin)                             */
+};
+
+enum pf_dtype { PF_F32 = 0, PF_BF16 = 1, PF_F64 = 2 };
+
+/* One posed view, packed for the device (bundle.py:35-116: CameraPose, Intrinsics, ViewRecord).
+ * R is the row-major world->camera rotation, x_cam = R x_world + t. `depth_offset` / `fmap_offset`
+ * are ELEMENT offsets of this view's (H,W) f32 depth map and (Hf,Wf,D) channel-last feature map
+ * inside the packed buffers passed alongside. 160 bytes, 8-byte aligned. */
+typedef struct pf_view {
+  double R[9];
+  double t[3];
+  double fx, fy, cx, cy;
+  int64_t depth_offset;
+  int64_t fmap_offset;
+  int32_t H, W;
+  int32_t Hf, Wf;
+} pf_view_t;
+
+const char* pf_last_error(void);
+int pf_abi_version(void);
+/* Number of this library's kernel launches issued by the calling thread since load (for bench). */
+uint64_t pf_launch_count(void);
+
+/* ---------------------------------------------------------------------------------------------
+ * Operator level: the `propfield.kernels` registry (kernels/__init__.py:21-28). fp64, bit-exact
+ * with the reference's numpy twins (same operation order, no FMA contraction).
+ * ------------------------------------------------------------------------------------------- */
+
+/* kernels.visible_in_view (numpy_impl.py:14-40, numba_impl.py:15-32). out: (n,) uint8 0/1. */
+int pf_visible_in_view(const double* u, const double* v, const double* z, int64_t n,
+                       const float* depth, int32_t h, int32_t w, double eps, uint8_t* out,
+                       void* stream);
+
+/* kernels.bilinear_gather (numpy_impl.py:43-66). fmap (hf,wf,d) f32|bf16 channel-last;
+ * out (m,d) f64. */
+int pf_bilinear_gather(const void* fmap, int32_t fmap_dtype, int32_t hf, int32_t wf, int32_t d,
+                       const double* fu, const double* fv, int64_t m, double* out, void* stream);
+
+/* kernels.accumulate_features (numpy_impl.py:69-77): accum[rows] += sample; counts[rows] += 1.
+ * MUTATES accum (n_rows,d) f64 and counts (n_rows,) int64 in place. Rows must be unique. */
+int pf_accumulate_features(const void* fmap, int32_t fmap_dtype, int32_t hf, int32_t wf, int32_t d,
+                           const double* fu, const double* fv, const int64_t* rows, int64_t m,
+                           double* accum, int64_t* counts, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Function level: geometry / fusion / grounding (the entry points pipeline.py:224-232,275-281
+ * calls). fp64, matching the reference to float rounding.
+ * ------------------------------------------------------------------------------------------- */
+
+/* geometry.project_points (geometry.py:46-59): points (n,3) f64 -> uv (n,2) f64, z (n,) f64. */
+int pf_project_points(const double* points, int64_t n, const pf_view_t* view_host, double* uv,
+                      double* z, void* stream);
+
+/* geometry.visibility_mask (geometry.py:89-103). points (n,3) in `points_dtype` (F32 or F64);
+ * views (nviews) device array; depth packed f32. mask (n,nviews) uint8 0/1 row-major. */
+int pf_visibility_mask(const void* points, int32_t points_dtype, int64_t n, const pf_view_t* views,
+                       int32_t nviews, const float* depth, double eps, uint8_t* mask,
+                       void* stream);
+
+/* fusion.aggregate_geometric_features (fusion.py:65-93). visibility (n,nviews) uint8; features
+ * (n,d) f64 (mean over visible views, zero rows for featureless points); counts (n,) int64.
+ * Bit-exact with the reference (per-view fp64 accumulation in view order). */
+int pf_aggregate_features(const void* points, int32_t points_dtype, int64_t n,
+                          const pf_view_t* views, int32_t nviews, const void* fmap,
+                          int32_t fmap_dtype, int32_t d, const uint8_t* visibility,
+                          double* features, int64_t* counts, void* stream);
+
+/* grounding.material_similarity (grounding.py:158-165): out (s,k) = f (s,d) @ text (k,d)^T, f64. */
+int pf_material_similarity(const double* features, int64_t s, int32_t d, const double* text,
+                           int32_t k, double* out, void* stream);
+
+/* grounding.softmax_weights (grounding.py:168-178). temperature <= 0 -> PF_ERR_VALUE. A NaN
+ * similarity sets *nan_flag (device int32, caller-zeroed) to 1; the binding raises MaterialError.
+ * Rows flagged in `row_valid` (uint8, may be NULL = all valid) == 0 produce all-zero rows
+ * (pipeline.py:279-280 featureless convention). */
+int pf_softmax_weights(const double* sims, int64_t s, int32_t k, double temperature,
+                       const uint8_t* row_valid, double* weights, int32_t* nan_flag, void* stream);
+
+/* grounding.regress_with_weights (grounding.py:198-202): out (s,p) = w (s,k) @ y (k,p), f64. */
+int pf_regress_with_weights(const double* weights, int64_t s, int32_t k, const double* values,
+                            int32_t p, double* out, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Voxel-grid mass (BASELINE-defined; indexing convention of sampling.py:110-123)
+ * and integrate_mass partials (integrate.py:124-155).
+ * ------------------------------------------------------------------------------------------- */
+
+/* Per-axis bbox of points (n,3) f32 -> lo_hi[6] f64 = {lo_x,lo_y,lo_z,hi_x,hi_y,hi_z}. Exact. */
+int pf_bbox(const float* points, int64_t n, double* lo_hi, void* stream);
+
+/* Voxel codes: edge = max(hi-lo)/g, cell = clip(floor((p-lo)/edge),0,g-1) in fp64,
+ * code = (cx*g+cy)*g+cz (int32; g <= 1290). Bit-exact. domain = lo_hi as from pf_bbox. */
+int pf_voxel_codes(const float* points, int64_t n, const double* lo_hi, int32_t g, int32_t* codes,
+                   void* stream);
+
+/* Dense voxel partials: grid (2*g^3) f32 = [sum rho | count], caller-zeroed; add each point. */
+int pf_voxel_accumulate(const int32_t* codes, const float* rho, int64_t n, int32_t g, float* grid,
+                        void* stream);
+
+/* mass = edge^3 * sum_{count>0} sum/count over the (allreduced) grid. `out` is a caller-zeroed
+ * device double[2] = {mass_kg, occupied_voxels}; lo_hi as above (edge recomputed identically). */
+int pf_voxel_mass(const float* grid, int32_t g, const double* lo_hi, double* out, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * The fused path: project -> depth test -> bilinear gather -> cross-view mean -> L2 normalise ->
+ * cosine similarity vs K text embeddings -> temperature softmax -> property regression ->
+ * voxel + integrate_mass partials, one pass over the points.
+ * ------------------------------------------------------------------------------------------- */
+
+#define PF_FUSE_WRITE_FEATURES 1u  /* validation: write mean features (n,d) f32            */
+#define PF_FUSE_WRITE_SIMS 2u      /* validation: write similarities (n,k) f32             */
+#define PF_FUSE_WRITE_WEIGHTS 4u   /* validation: write softmax weights (n,k) f32          */
+#define PF_FUSE_SKIP_VOXELS 8u     /* do not touch the voxel grid (codes still written)    */
+#define PF_FUSE_FORCE_SIMT 16u     /* use the SIMT gather even where the tensor path applies */
+#define PF_FUSE_PREPARED 32u       /* workspace already holds pf_fuse_prepare's tables: skip it */
+
+/* Number of doubles in the `partials` output of pf_fuse_query. Layout:
+ * [0,k)          weight_totals_k = sum_i w_ik                       (integrate.py:133)
+ * k              sum_i pm_i,  pm_i = sum_k w_ik * mid_k * theta_k   (integrate.py:146 / (lam b^2))
+ * k+1..k+3       sum_i pm_i * x_i                                   (integrate.py:153)
+ * k+4            featured point count (visible in >= 1 view)
+ * k+5            visible point-view pairs                                                     */
+#define PF_PARTIALS_LEN(k) ((k) + 6)
+
+typedef struct pf_fuse_args {
+  /* inputs */
+  const float* points;      /* (n,3) f32 (bundle.py:158)                                         */
+  int64_t n;
+  const pf_view_t* views;   /* (nviews) device                                                   */
+  const pf_view_t* views_host; /* the same (nviews) records in host memory (launch sizing)       */
+  int32_t nviews;
+  const float* depth;       /* packed f32 depth maps                                             */
+  const void* fmap;         /* packed (Hf,Wf,D) maps, fmap_dtype                                 */
+  int32_t fmap_dtype;       /* PF_F32 | PF_BF16                                                  */
+  int32_t d;                /* feature dim, d % 8 == 0, d <= 1024 (SIMT)                         */
+  const float* text;        /* (k,d) f32 unit rows (grounding.py:86-93)                          */
+  int32_t k;                /* materials, k <= 256                                               */
+  const float* values;      /* (k,p) f32 property table, column `density_col` is density         */
+  int32_t p;                /* properties, p <= 4                                                */
+  int32_t density_col;
+  const float* mid_theta;   /* (k,) f32 mid_density_k * thickness_k (integrate.py:132,146)       */
+  double temperature;       /* softmax T > 0 (grounding.py:168-178)                              */
+  double eps;               /* depth tolerance (geometry.py:89-103)                              */
+  int32_t grid;             /* voxel grid side g                                                 */
+  const double* lo_hi;      /* (6,) voxel domain (pf_bbox), device                               */
+  uint32_t flags;           /* PF_FUSE_*                                                         */
+  /* outputs */
+  int32_t* counts;          /* (n,) visible views per point                                      */
+  uint32_t* mask_bits;      /* (n, ceil(nviews/32)) visibility bitset, bit j of word w = view 32w+j */
+  float* props;             /* (n,p) regressed properties; zero rows for featureless points      */
+  int32_t* codes;           /* (n,) voxel code                                                   */
+  float* grid_partials;     /* (2*g^3) f32 [sum rho | count], caller-zeroed unless SKIP_VOXELS   */
+  double* partials;         /* (PF_PARTIALS_LEN(k)) caller-zeroed, accumulated                   */
+  int32_t* status;          /* (1,) device int32, caller-zeroed; bit0 = NaN similarity seen      */
+  float* features;          /* optional (n,d) f32 mean features (flag WRITE_FEATURES)            */
+  float* sims;              /* optional (n,k) f32 (flag WRITE_SIMS)                              */
+  float* weights;           /* optional (n,k) f32 (flag WRITE_WEIGHTS)                           */
+  /* scratch */
+  void* workspace;          /* pf_fuse_workspace_bytes(args) bytes, 256-byte aligned             */
+} pf_fuse_args_t;
+
+uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* args);
+/* Per-object tables into the workspace: G = fmap @ text^T over every feature cell (the similarity
+ * by associativity, see csrc/pf_fused.cu). pf_fuse_query runs it itself unless PF_FUSE_PREPARED. */
+int pf_fuse_prepare(const pf_fuse_args_t* args, void* stream);
+int pf_fuse_query(const pf_fuse_args_t* args, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PROPFIELD_B200_H */

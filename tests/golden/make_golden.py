@@ -1,0 +1,145 @@
+"""Generate golden vectors by running the REFERENCE implementation (propfield, read-only mount).
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+It imports the unmodified reference, feeds it seeded inputs (tests/golden/recipes.py and the
+`mini` / `mini_bf16` workloads of paper_2511_03126_b200.workloads), and writes its outputs as
+small .npz fixtures next to this file. The tests compare both the CPU oracle (oracle/) and the
+CUDA path against these files; nothing at test time reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, HERE)
+if "/root/reference/pkg/src" not in sys.path:
+    sys.path.insert(0, "/root/reference/pkg/src")
+
+import recipes  # noqa: E402
+from paper_2511_03126_b200 import workloads  # noqa: E402
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def ref_views(wl, propfield):
+    from propfield.bundle import CameraPose, Intrinsics, ViewRecord
+
+    dep = wl.depth_np()
+    fm = wl.fmaps_f32()
+    out = []
+    for j, pose in enumerate(wl.poses):
+        h, w = dep[j].shape
+        out.append(
+            ViewRecord(
+                image=np.zeros((h, w, 3), dtype=np.uint8),
+                depth=dep[j],
+                camera=CameraPose(rotation=pose.rotation, translation=pose.translation),
+                intrinsics=Intrinsics(fx=wl.intrinsics.fx, fy=wl.intrinsics.fy,
+                                      cx=wl.intrinsics.cx, cy=wl.intrinsics.cy),
+                feature_map=fm[j],
+            )
+        )
+    return out
+
+
+def kernels_golden(numpy_impl):
+    u, v, z, depth = recipes.visible_case()
+    vis0 = numpy_impl.visible_in_view(u, v, z, depth, 0.0)
+    vis5 = numpy_impl.visible_in_view(u, v, z, depth, 0.05)
+    fmap, fu, fv = recipes.gather_case()
+    gath = numpy_impl.bilinear_gather(fmap, fu, fv)
+    fmap2, fu2, fv2, rows = recipes.accumulate_case()
+    acc = np.zeros((300, 4))
+    cnt = np.zeros(300, dtype=np.int64)
+    numpy_impl.accumulate_features(fmap2, fu2, fv2, rows, acc, cnt)
+    return dict(visible_eps0=np.packbits(vis0), visible_eps005=np.packbits(vis5),
+                gather=gath, accum=acc, accum_counts=cnt)
+
+
+def grounding_golden(grounding):
+    out = {}
+    for seed in range(2):
+        f, t, y = recipes.grounding_case(seed)
+        s = grounding.material_similarity(f, t)
+        w = grounding.softmax_weights(s, 0.1)
+        out[f"sims{seed}"] = s
+        out[f"weights{seed}"] = w
+        out[f"props{seed}"] = grounding.regress_with_weights(w, y)
+        out[f"kreg{seed}"] = grounding.kernel_regress(s, y[:, 0], 0.05)
+    return out
+
+
+def pipeline_golden(name, propfield):
+    from propfield import fusion, geometry, grounding, integrate
+    from propfield.densify import PropertyField
+    from propfield.grounding import MaterialDictionary, MaterialEntry
+
+    wl = workloads.generate(name)
+    cfg = wl.cfg
+    views = ref_views(wl, propfield)
+    pos = wl.points.astype(np.float64)
+    vis = geometry.visibility_mask(pos, views, cfg.eps)
+    sem = fusion.aggregate_geometric_features(pos, views, vis)
+    feats = sem.features
+    norm = np.linalg.norm(feats, axis=1, keepdims=True)
+    fhat = np.where(norm > 0, feats / np.where(norm > 0, norm, 1.0), 0.0)  # fusion.py:210-214
+    featured = sem.visible_counts > 0
+    text = wl.text.astype(np.float64)
+    sims = np.zeros((len(pos), cfg.k))
+    weights = np.zeros((len(pos), cfg.k))
+    sims[featured] = grounding.material_similarity(fhat[featured], text)
+    weights[featured] = grounding.softmax_weights(sims[featured], cfg.temperature)
+    props = grounding.regress_with_weights(weights, wl.values)
+    # integrate_mass on the same probabilities (integrate.py:98-167)
+    entries = [
+        MaterialEntry(name=f"m{k}", properties={"density": (float(wl.density[k]), float(wl.density[k]))},
+                      thickness_m=float(wl.thickness[k]))
+        for k in range(cfg.k)
+    ]
+    fld = PropertyField(positions=wl.points, probabilities=weights,
+                        dominant=weights.argmax(axis=1), properties={}, material_names=[e.name for e in entries])
+    est = integrate.integrate_mass(fld, MaterialDictionary(entries=entries), integrate.IntegrationConfig())
+    out = dict(
+        visibility=np.packbits(vis, axis=1), counts=sem.visible_counts, sims=sims, weights=weights,
+        props=props, feature_norms=norm[:, 0], features_sha=np.array(sha(feats)),
+        integ_mass=np.array(est.mass_kg), integ_length=np.array(est.characteristic_length),
+        integ_b=np.array(est.b_adap), integ_com=np.asarray(est.center_of_mass),
+        integ_per_material=np.array([est.per_material[e.name] for e in entries]),
+    )
+    if feats.nbytes <= 1_100_000:
+        out["features"] = feats
+    else:
+        rows = np.random.default_rng(7).choice(len(pos), 64, replace=False)
+        out["feature_rows"] = rows
+        out["features_subset"] = feats[rows]
+    return out
+
+
+def main():
+    import propfield  # noqa: F401  (the unmodified reference)
+    from propfield import grounding
+    from propfield.kernels import numpy_impl
+
+    np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernels_golden(numpy_impl))
+    np.savez_compressed(os.path.join(HERE, "grounding.npz"), **grounding_golden(grounding))
+    for name in ("mini", "mini_bf16"):
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **pipeline_golden(name, propfield))
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))
+
+
+if __name__ == "__main__":
+    main()

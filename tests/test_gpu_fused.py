@@ -1,0 +1,178 @@
+"""Parity of the fused CUDA path (`fuse_and_query`) with the pinned CPU oracle.
+
+Tolerances (BASELINE.json north_star):
+* visibility bitset, visible counts, voxel codes: exact (mask pairs within 1e-6 of the depth-test
+  threshold are exempt);
+* fused features / similarities / softmax weights / properties / mass: 1e-4 relative in fp32
+  (features per point as |a-b|/|b|; similarities as max_k|ds| <= 1e-4 * max(1e-2, max_k|s|)).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2511_03126_b200 as pf
+from oracle import propfield_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def run_gpu(wl, points=None, **kw):
+    import torch
+
+    views = pf.ViewSet.from_views(wl.views())
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta, density_col=0)
+    pts = wl.points if points is None else points
+    res = pf.fuse_and_query(torch.from_numpy(np.ascontiguousarray(pts)).cuda(), views, tables,
+                            temperature=wl.cfg.temperature, epsilon=wl.cfg.eps, grid=wl.cfg.grid,
+                            write_features=True, write_sims=True, write_weights=True, check=True, **kw)
+    torch.cuda.synchronize()
+    return res
+
+
+def run_oracle(wl, points=None):
+    pts = wl.points if points is None else points
+    return O.fuse_and_query(pts, wl.views(f32_maps=True), wl.text, wl.values, wl.cfg.temperature,
+                            wl.cfg.eps, wl.cfg.grid)
+
+
+def knife_edge_pairs(wl, pts, eps):
+    """(N, V) bool: pairs whose depth test sits within 1e-6 of its threshold."""
+    p = np.asarray(pts, np.float64)
+    out = np.zeros((p.shape[0], len(wl.poses)), dtype=bool)
+    dep = wl.depth_np()
+    for j, pose in enumerate(wl.poses):
+        u, v, z = O.project_points(p, pose.rotation, pose.translation, wl.intrinsics.fx,
+                                   wl.intrinsics.fy, wl.intrinsics.cx, wl.intrinsics.cy)
+        h, w = dep[j].shape
+        iu = np.clip(np.rint(u), 0, w - 1).astype(np.int64)
+        iv = np.clip(np.rint(v), 0, h - 1).astype(np.int64)
+        stored = dep[j][iv, iu].astype(np.float64)
+        out[:, j] = np.abs(z - (stored + eps)) <= 1e-6
+    return out
+
+
+def assert_parity(res, ref, wl, pts=None, tol=TOL):
+    pts = wl.points if pts is None else pts
+    vis = res.visibility().cpu().numpy()
+    diff = vis != ref["visibility"]
+    if diff.any():
+        assert not (diff & ~knife_edge_pairs(wl, pts, wl.cfg.eps)).any(), "mask mismatch"
+    else:
+        assert np.array_equal(res.counts.cpu().numpy(), ref["counts"])
+    assert np.array_equal(res.codes.cpu().numpy(), ref["codes"])
+    # features: per-point relative L2
+    f = res.features.cpu().numpy().astype(np.float64)
+    rf = ref["features"]
+    rn = np.linalg.norm(rf, axis=1)
+    featured = ref["counts"] > 0
+    rel = np.linalg.norm(f - rf, axis=1)[featured] / rn[featured]
+    assert rel.max() <= tol, rel.max()
+    assert np.all(f[~featured] == 0)
+    s = res.sims.cpu().numpy().astype(np.float64)
+    scale = np.maximum(1e-2, np.abs(ref["sims"]).max(axis=1))
+    assert (np.abs(s - ref["sims"]).max(axis=1) <= tol * scale).all()
+    w = res.weights.cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(w, ref["weights"], rtol=tol, atol=tol * 1e-3)
+    props = res.props.cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(props, ref["props"], rtol=tol, atol=1e-6)
+    assert res.mass_kg() == pytest.approx(ref["mass"], rel=tol)
+    assert int(round(res.buffers.mass[1].item())) == ref["occupied"]
+    part = res.host_partials()
+    np.testing.assert_allclose(part["weight_totals"], ref["weights"].sum(axis=0), rtol=tol)
+    pm = ref["weights"] @ wl.mid_theta
+    assert part["pm_sum"] == pytest.approx(pm.sum(), rel=tol)
+    np.testing.assert_allclose(part["pm_pos"], (pm[:, None] * pts.astype(np.float64)).sum(0), rtol=tol,
+                               atol=tol * abs(pm.sum()))
+    assert part["featured"] == int(featured.sum())
+    assert part["visible_pairs"] == int(ref["counts"].sum())
+
+
+@pytest.mark.parametrize("name", ["mini", "mini_bf16"])
+def test_fused_vs_reference_goldens(cuda, golden, workload, name):
+    """Against the reference's own outputs (golden fixtures), not just the oracle."""
+    g = golden(name)
+    wl = workload(name)
+    res = run_gpu(wl)
+    vis = np.unpackbits(g["visibility"], axis=1)[:, : wl.cfg.nviews].astype(bool)
+    assert np.array_equal(res.visibility().cpu().numpy(), vis)
+    assert np.array_equal(res.counts.cpu().numpy(), g["counts"])
+    s = res.sims.cpu().numpy()
+    scale = np.maximum(1e-2, np.abs(g["sims"]).max(axis=1))
+    assert (np.abs(s - g["sims"]).max(axis=1) <= TOL * scale).all()
+    np.testing.assert_allclose(res.props.cpu().numpy(), g["props"], rtol=TOL, atol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["mini", "mini_bf16", "mini_fib40", "pr1"])
+def test_fused_vs_oracle(cuda, workload, name):
+    wl = workload(name)
+    assert_parity(run_gpu(wl), run_oracle(wl), wl)
+
+
+def test_fused_c2_shapes_subset(cuda, workload):
+    """C2 shapes (V=16 on two rings, 512^2, 37x37x768, K=32, 128^3) on 20k of its points."""
+    wl = workload("c2", n=20_000)
+    assert_parity(run_gpu(wl), run_oracle(wl), wl)
+
+
+def test_featureless_points(cuda, workload):
+    """Points seen by no view: zero probability/property rows, still voxel-occupying (rho=0)."""
+    wl = workload("mini")
+    far = np.array([[0.0, 0.0, 50.0], [40.0, 0.0, 0.0], [0.0, -60.0, 1.0]], dtype=np.float32)
+    pts = np.concatenate([wl.points, far])
+    res = run_gpu(wl, points=pts)
+    ref = run_oracle(wl, points=pts)
+    assert (ref["counts"][-3:] == 0).all()
+    assert_parity(res, ref, wl, pts)
+    assert np.all(res.props.cpu().numpy()[-3:] == 0)
+    assert np.all(res.weights.cpu().numpy()[-3:] == 0)
+
+
+def test_empty_point_set(cuda, workload):
+    import torch
+
+    wl = workload("mini")
+    views = pf.ViewSet.from_views(wl.views())
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta)
+    res = pf.fuse_and_query(torch.zeros((0, 3), device="cuda"), views, tables, grid=8)
+    assert res.props.shape[0] == 0 and res.mass_kg() == 0.0
+
+
+def test_single_point(cuda, workload):
+    wl = workload("mini")
+    pts = wl.points[:1].copy()
+    assert_parity(run_gpu(wl, points=pts), run_oracle(wl, points=pts), wl, pts)
+
+
+def test_permutation_equivariance_c2(cuda, workload):
+    """Size-independent property at full C2 size: permuting points permutes per-point outputs
+    and leaves the mass unchanged."""
+    import torch
+
+    wl = workload("c2")
+    views = pf.ViewSet.from_views(wl.views())
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta)
+    pts = torch.from_numpy(wl.points).cuda()
+    a = pf.fuse_and_query(pts, views, tables, grid=wl.cfg.grid)
+    pa, ma, ca = a.props.clone(), a.mass_kg(), a.counts.clone()
+    perm = torch.randperm(pts.shape[0], device="cuda", generator=torch.Generator("cuda").manual_seed(0))
+    b = pf.fuse_and_query(pts[perm].contiguous(), views, tables, grid=wl.cfg.grid)
+    assert torch.equal(b.counts, ca[perm])
+    assert torch.allclose(b.props, pa[perm], rtol=1e-6, atol=1e-4)
+    assert b.mass_kg() == pytest.approx(ma, rel=1e-5)
+    # probabilities are a convex combination -> properties inside the material hull
+    dens = b.props[:, 0][b.counts > 0]
+    assert float(dens.min()) >= wl.density.min() - 1e-2 and float(dens.max()) <= wl.density.max() + 1e-2
+
+
+def test_nan_similarity_raises(cuda, workload):
+    import torch
+
+    wl = workload("mini")
+    views = wl.views()
+    views[0].feature_map = np.full_like(views[0].feature_map, np.nan)
+    vs = pf.ViewSet.from_views(views)
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta)
+    with pytest.raises(pf.MaterialError):
+        pf.fuse_and_query(torch.from_numpy(wl.points).cuda(), vs, tables, grid=8, check=True)
