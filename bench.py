@@ -261,10 +261,15 @@ def run_ours(args, cfg):
     evs = [[mk() for _ in range(4)] for _ in range(args.steps)]
     starts = [mk() for _ in range(args.steps)]
     clk = ClockSampler(local)
+    clk.start()
+    # soak: untimed steps for >= 0.8 s so the clock samples (200 ms period) see the GPU under load
+    t_soak = time.time()
+    while time.time() - t_soak < 0.8:
+        step()
+        torch.cuda.synchronize()
     launches0 = _lib.launch_count()
     barrier()
     torch.cuda.synchronize()
-    clk.start()
     for i in range(args.steps):
         if flush:
             scratch.fill_(float(i))  # L2 flush between steps (outside the step's events)

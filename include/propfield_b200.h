@@ -203,6 +203,15 @@ uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* args);
 int pf_fuse_prepare(const pf_fuse_args_t* args, void* stream);
 int pf_fuse_query(const pf_fuse_args_t* args, void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * Diagnostics (no reference twin).
+ * ------------------------------------------------------------------------------------------- */
+
+/* C (128,n) f32 = A (128,k) bf16 row-major @ B (k,n) bf16 row-major through the tile kernel's
+ * tcgen05 operand layouts / descriptors / TMEM read-back. k % 64 == 0 (<= 256), n % 16 == 0. */
+int pf_selftest_umma(const void* a_bf16, const void* b_bf16, float* c, int32_t k, int32_t n,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

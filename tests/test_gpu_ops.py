@@ -210,3 +210,20 @@ class TestVoxelMass:
         ref_mass, ref_occ = O.voxel_mass(ref_codes, rho.astype(np.float32), edge)
         assert occ == ref_occ
         assert mass == pytest.approx(ref_mass, rel=1e-5)
+
+
+class TestTensorCorePlumbing:
+    @pytest.mark.parametrize("k,n", [(64, 128), (128, 128), (256, 64), (192, 256), (64, 16)])
+    def test_umma_selftest_matches_matmul(self, cuda, k, n):
+        import torch
+
+        from paper_2511_03126_b200 import _lib
+
+        g = torch.Generator(device="cuda").manual_seed(k * 1000 + n)
+        a = torch.randn(128, k, device="cuda", generator=g).to(torch.bfloat16)
+        b = torch.randn(k, n, device="cuda", generator=g).to(torch.bfloat16)
+        c = torch.empty(128, n, device="cuda", dtype=torch.float32)
+        _lib.call("pf_selftest_umma", a.data_ptr(), b.data_ptr(), c.data_ptr(), k, n,
+                  torch.cuda.current_stream().cuda_stream)
+        ref = a.float() @ b.float()
+        torch.testing.assert_close(c, ref, rtol=1e-5, atol=1e-4)
