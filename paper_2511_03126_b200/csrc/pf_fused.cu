@@ -18,9 +18,11 @@
 //      (grounding.py:198-202), voxel code + dense voxel partials, and the
 //      integrate_mass partial sums (integrate.py:133-155), reduced per block then atomically.
 // Featureless points (count 0) get zero probability / property rows (pipeline.py:279-280).
+#include <climits>
 #include <mutex>
 
 #include "pf_common.cuh"
+#include "pf_tile.cuh"
 
 namespace pf {
 namespace {
@@ -98,6 +100,8 @@ struct FuseParams {
   float* features;
   float* sims;
   float* weights;
+  const int32_t* list;      // optional: process only these point indices (tile-path overflow)
+  const int32_t* list_len;  // device count of `list`
 };
 
 struct __align__(16) TapEntry {
@@ -165,7 +169,9 @@ __global__ void __launch_bounds__(kFuseThreads, 2) k_fuse_simt(FuseParams P) {
 
   constexpr int CPL = VEC * NCHUNK;
   const int64_t nwarps = (int64_t)gridDim.x * kFuseWarps;
-  for (int64_t i = blockIdx.x * (int64_t)kFuseWarps + warp; i < P.n; i += nwarps) {
+  const int64_t total = P.list ? (int64_t)*P.list_len : P.n;
+  for (int64_t t = blockIdx.x * (int64_t)kFuseWarps + warp; t < total; t += nwarps) {
+    const int64_t i = P.list ? (int64_t)P.list[t] : t;
     const float px = __ldg(P.points + 3 * i), py = __ldg(P.points + 3 * i + 1),
                 pz = __ldg(P.points + 3 * i + 2);
     // ---- phase 1: lanes over views -----------------------------------------------------------
@@ -391,7 +397,7 @@ int launch_fuse(const FuseParams& prm, size_t smem, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ.blocks_per_sm, kern, kFuseThreads, smem);
     if (occ.blocks_per_sm < 1) occ.blocks_per_sm = 1;
   });
-  int64_t want = (prm.n + kFuseWarps - 1) / kFuseWarps;
+  int64_t want = prm.list ? INT64_MAX : (prm.n + kFuseWarps - 1) / kFuseWarps;
   int64_t cap = (int64_t)occ.sms * occ.blocks_per_sm;
   int blocks = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   kern<<<blocks, kFuseThreads, smem, st>>>(prm);
@@ -417,10 +423,27 @@ static int64_t total_cells(const pf_fuse_args_t* a) {
 
 static int kpl_of(int k) { return (k + 31) / 32; }
 
-uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* a) {
-  if (!a || !a->views_host || a->d <= 0 || a->k <= 0) return 0;
+// The tensor-core tile path (pf_tile.cu) applies to bf16 maps with D a multiple of 128, <= 64
+// views, feature grids <= 255 per side and <= 128 padded materials.
+static bool tile_path_ok(const pf_fuse_args_t* a) {
+  if (a->fmap_dtype != PF_BF16 || a->d % 128 != 0 || a->nviews > tile::kMaxViewsTC) return false;
+  if (32 * kpl_of(a->k) > tile::kMaxKpadTC || (a->flags & PF_FUSE_FORCE_SIMT)) return false;
+  for (int j = 0; j < a->nviews; ++j)
+    if (a->views_host[j].Hf > 255 || a->views_host[j].Wf > 255) return false;
+  return true;
+}
+
+static uint64_t g_bytes(const pf_fuse_args_t* a) {
   const uint64_t g = (uint64_t)total_cells(a) * (uint64_t)(32 * kpl_of(a->k)) * sizeof(float);
   return (g + 255) & ~uint64_t(255);
+}
+
+uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* a) {
+  if (!a || !a->views_host || a->d <= 0 || a->k <= 0) return 0;
+  uint64_t bytes = g_bytes(a);
+  if (tile_path_ok(a))
+    bytes += tile::tile_layout(a->n, a->nviews, total_cells(a), 32 * kpl_of(a->k)).bytes;
+  return bytes;
 }
 
 static int validate(const pf_fuse_args_t* a) {
@@ -492,6 +515,39 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
   const size_t smem = sizeof(pf_view_t) * a->nviews + sizeof(float) * kpad * (kMaxP + 1) +
                       sizeof(double) * (kpad + 8) + sizeof(TapEntry) * kFuseWarps * a->nviews + 16;
   const int d = a->d;
+  if (tile_path_ok(a)) {
+    const int64_t cells = total_cells(a);
+    const int kpadg = kpad;
+    unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
+    const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg);
+    tile::TileParams T{};
+    T.spts = reinterpret_cast<const float4*>(ws + L.spts);
+    T.perm = reinterpret_cast<const int32_t*>(ws + L.perm);
+    T.n = a->n; T.views = a->views; T.nv = a->nviews; T.nwords = (a->nviews + 31) / 32; T.d = d;
+    T.depth = a->depth; T.fmap = a->fmap; T.Gbf = reinterpret_cast<const uint16_t*>(ws + L.gbf);
+    T.kpadg = kpadg; T.k = a->k; T.p = a->p; T.density_col = a->density_col;
+    T.values = a->values; T.mid_theta = a->mid_theta; T.inv_temp = prm.inv_temp; T.eps = a->eps;
+    T.grid = a->grid; T.cells3 = (int64_t)a->grid * a->grid * a->grid; T.lo_hi = a->lo_hi;
+    T.mask_bits = a->mask_bits; T.counts = a->counts; T.codes = a->codes; T.props = a->props;
+    T.grid_partials = (a->flags & PF_FUSE_SKIP_VOXELS) ? nullptr : a->grid_partials;
+    T.features = (a->flags & PF_FUSE_WRITE_FEATURES) ? a->features : nullptr;
+    T.sims = (a->flags & PF_FUSE_WRITE_SIMS) ? a->sims : nullptr;
+    T.weights = (a->flags & PF_FUSE_WRITE_WEIGHTS) ? a->weights : nullptr;
+    T.status = a->status;
+    T.tile_desc = reinterpret_cast<uint2*>(ws + L.desc);
+    T.tile_kt = reinterpret_cast<int32_t*>(ws + L.kt);
+    T.tile_part = reinterpret_cast<float*>(ws + L.part);
+    T.ovf_list = reinterpret_cast<int32_t*>(ws + L.ovf) + 1;
+    T.ovf_count = reinterpret_cast<int32_t*>(ws + L.ovf);
+    T.partials = a->partials;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(128 + kpadg)) cols <<= 1;
+    T.tmem_cols = cols;
+    if (int rc = tile::run_tile_path(T, L, ws, a->points, a->n, cells, G, kpad, st)) return rc;
+    // overflow tiles (more taps than fit in shared memory) run through the SIMT kernel
+    prm.list = T.ovf_list;
+    prm.list_len = T.ovf_count;
+  }
   if (a->fmap_dtype == PF_F32) {
     if (d == 128) return launch_fuse<PF_F32, 4, 1>(prm, smem, st);
     if (d == 256) return launch_fuse<PF_F32, 4, 2>(prm, smem, st);

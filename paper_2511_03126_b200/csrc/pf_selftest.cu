@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128, 1) k_umma_selftest(const uint16_t* __rest
   for (int c0 = 0; c0 < N; c0 += 32) {
     float v[32];
     tc::tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + c0, v);
-    for (int i = 0; i < 32; ++i) C[(int64_t)tid * N + c0 + i] = v[i];
+    for (int i = 0; i < 32 && c0 + i < N; ++i) C[(int64_t)tid * N + c0 + i] = v[i];
   }
   tc::fence_before_sync();
   __syncthreads();

@@ -1,0 +1,641 @@
+// Tensor-core tile path of the fused query for bf16 feature maps (BASELINE configs 3 and 5).
+//
+// Why: the per-point gather F_i = sum_taps w * f_tap reads 4 taps x D channels per visible view; at
+// C5 (16M points x 64 views x D=1024) the SIMT kernel moves ~20 GB through L2 and sits at ~250 ms
+// (profiles/r01_ncu_c5_simt.txt). Points that are close in space share their taps, so a tile of
+// 128 spatially-sorted points needs only ~150 distinct (view, cell) taps. The tile's fused
+// features are then a dense contraction  F_tile (128 x D) = W (128 x Kt) . Fmap_taps (Kt x D)
+// — the bilinear weights of every point against every tap of its tile (zero where a point does not
+// use a tap) — which runs on the 5th-generation tensor cores (tcgen05.mma, bf16 in, fp32 in TMEM).
+// The similarity needs only <F_i, t_k> and |F_i| (fusion.py:210-214, grounding.py:158-165):
+//   S_tile (128 x K) = W . G_taps,  G = fmap @ text^T (per cell, precomputed),
+// and |F_i|^2 from the D-chunks of F_tile drained out of TMEM. Softmax / regression / voxel and
+// integrate partials run in the epilogue with one thread per point (grounding.py:168-202,
+// integrate.py:133-155).
+//
+// Kernels:
+//   k_sort_keys / k_scan_* / k_sort_scatter — counting sort of the points by a 21-bit Morton key of
+//       a 128^3 grid over the bbox (spatial coherence of tiles; no library sort);
+//   k_tile_prep  — per tile: exact visibility (fp32 projection with a rigorous error bound, exact
+//       fp64 fallback near any decision boundary -> bit-identical masks), counts, voxel codes, and
+//       the per-view tap windows of the tile;
+//   k_tile_mma   — per tile: build W in smem (K-major, 128-B swizzle), stream the taps' feature
+//       rows chunk by chunk (cp.async, N-major swizzled), tcgen05.mma into TMEM, drain |F|^2, then
+//       S = W . G and the epilogue. Tiles whose tap count exceeds KT_MAX fall back to the SIMT
+//       kernel through an overflow list.
+#include <climits>
+
+#include "pf_common.cuh"
+#include "pf_tc.cuh"
+#include "pf_tile.cuh"
+
+namespace pf {
+namespace tile {
+
+// ---- fp32 projection with a rigorous error bound ----------------------------------------------------
+__device__ __forceinline__ ViewF make_viewf(const pf_view_t& v, int d) {
+  ViewF w;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) w.R[q] = (float)v.R[q];
+  w.t[0] = (float)v.t[0];
+  w.t[1] = (float)v.t[1];
+  w.t[2] = (float)v.t[2];
+  w.fx = (float)v.fx;
+  w.fy = (float)v.fy;
+  w.cx = (float)v.cx;
+  w.cy = (float)v.cy;
+  w.ru = (float)((double)v.Wf / (double)v.W);
+  w.rv = (float)((double)v.Hf / (double)v.H);
+  w.tmax = fmaxf(fmaxf(fabsf(w.t[0]), fabsf(w.t[1])), fabsf(w.t[2]));
+  w.H = v.H;
+  w.W = v.W;
+  w.Hf = v.Hf;
+  w.Wf = v.Wf;
+  w.cell_base = (int32_t)(v.fmap_offset / d);
+  w.depth_off = v.depth_offset;
+  return w;
+}
+
+struct ProjF {
+  float u, v, z, e;  // e: bound on |cam_c - cam_c(exact)| for each camera coordinate
+  float a, b;        // X/z, Y/z
+};
+
+__device__ __forceinline__ float cam_f32(const float* R, float t, float px, float py, float pz) {
+  return __fadd_rn(__fmaf_rn(R[2], pz, __fmaf_rn(R[1], py, __fmul_rn(R[0], px))), t);
+}
+
+__device__ __forceinline__ ProjF project_f32(const ViewF& w, float px, float py, float pz) {
+  ProjF o;
+  const float X = cam_f32(w.R + 0, w.t[0], px, py, pz);
+  const float Y = cam_f32(w.R + 3, w.t[1], px, py, pz);
+  o.z = cam_f32(w.R + 6, w.t[2], px, py, pz);
+  o.a = __fdiv_rn(X, o.z);
+  o.b = __fdiv_rn(Y, o.z);
+  o.u = __fmaf_rn(w.fx, o.a, w.cx);
+  o.v = __fmaf_rn(w.fy, o.b, w.cy);
+  // |R_ij| <= 1: each camera coordinate has magnitude <= |p|_1 + |t|_inf. f32 R/t representation
+  // (2^-24 relative) plus 4 roundings of that magnitude is < 5*2^-24; take 2^-20 (>3x margin).
+  o.e = (fabsf(px) + fabsf(py) + fabsf(pz) + w.tmax) * 9.5367431640625e-07f;
+  return o;
+}
+
+// error bound of u = fx*X/z + cx given |X - X*|, |z - z*| <= e and |z| >= 2e
+__device__ __forceinline__ float pix_err(float f, float c, float num, float ratio, float z, float e) {
+  const float az = fabsf(z);
+  const float da = e / az + 2.f * e * (fabsf(num) + e) / (az * az) + 6.0e-8f * fabsf(ratio);
+  return 2.f * (fabsf(f) * da + 1.2e-7f * (fabsf(f * ratio) + fabsf(c)) + 1e-6f);
+}
+
+// Exact visibility decision (numpy_impl.py:31-40 on fp64 projections): fast fp32 path when the
+// fp32 result is provably on the same side of every decision boundary, exact fp64 otherwise.
+__device__ __forceinline__ bool visible_exact(const ViewF& w, const pf_view_t& w64, const float* depth,
+                                              float px, float py, float pz, double eps, ProjF& q) {
+  q = project_f32(w, px, py, pz);
+  const float e = q.e;
+  bool ambiguous = !(fabsf(q.z) > 2.f * e) || !isfinite(q.u) || !isfinite(q.v);
+  if (!ambiguous) {
+    if (q.z < 0.f) return false;  // |z| > 2e: the sign is certain
+    const float X = q.a * q.z, Y = q.b * q.z;
+    const float eu = pix_err(w.fx, w.cx, X, q.a, q.z, e);
+    const float ev = pix_err(w.fy, w.cy, Y, q.b, q.z, e);
+    const float du = fabsf(q.u - floorf(q.u) - 0.5f), dv = fabsf(q.v - floorf(q.v) - 0.5f);
+    if (eu >= 0.25f || ev >= 0.25f || du <= eu || dv <= ev) {
+      ambiguous = true;
+    } else {
+      const float ru = rintf(q.u), rv = rintf(q.v);
+      if (!(ru >= 0.f && ru < (float)w.W && rv >= 0.f && rv < (float)w.H)) return false;
+      const double stored = (double)__ldg(depth + w.depth_off + (int64_t)rv * w.W + (int64_t)ru);
+      if (!(stored > 0.0)) return false;
+      const double thr = stored + eps;
+      const double zd = (double)q.z;
+      if (zd + (double)e < thr) return true;
+      if (zd - (double)e > thr) return false;
+      ambiguous = true;
+    }
+  }
+  // exact fp64 decision, identical to the reference arithmetic (pf_common.cuh)
+  const Proj p64 = project(w64, (double)px, (double)py, (double)pz);
+  return depth_test(depth + w64.depth_offset, w64.H, w64.W, p64.u, p64.v, p64.z, eps);
+}
+
+// bilinear taps of a visible sample from the fp32 projection (fusion.py:83-86 +
+// numpy_impl.py:50-57); k_tile_prep and k_tile_mma call this with bit-identical inputs.
+__device__ __forceinline__ TapF taps_f32(const ViewF& w, float u, float v) {
+  TapF t;
+  const float fu = __fsub_rn(__fmul_rn(__fadd_rn(u, 0.5f), w.ru), 0.5f);
+  const float fv = __fsub_rn(__fmul_rn(__fadd_rn(v, 0.5f), w.rv), 0.5f);
+  const float x = fminf(fmaxf(fu, 0.f), (float)(w.Wf - 1));
+  const float y = fminf(fmaxf(fv, 0.f), (float)(w.Hf - 1));
+  const float x0 = floorf(x), y0 = floorf(y);
+  t.x0 = (int)x0;
+  t.y0 = (int)y0;
+  t.dx = t.x0 < w.Wf - 1 ? 1 : 0;
+  t.dy = t.y0 < w.Hf - 1 ? 1 : 0;
+  t.wx = __fsub_rn(x, x0);
+  t.wy = __fsub_rn(y, y0);
+  return t;
+}
+
+// ---- counting sort by a coarse Morton key --------------------------------------------------------------
+__device__ __forceinline__ uint32_t spread3(uint32_t x) {
+  x &= 0x3ffu;
+  x = (x | (x << 16)) & 0x030000ffu;
+  x = (x | (x << 8)) & 0x0300f00fu;
+  x = (x | (x << 4)) & 0x030c30c3u;
+  x = (x | (x << 2)) & 0x09249249u;
+  return x;
+}
+
+__global__ void k_sort_keys(const float* __restrict__ p, int64_t n, const double* __restrict__ lo_hi,
+                            uint32_t* __restrict__ keys, uint32_t* __restrict__ hist) {
+  const float lx = (float)lo_hi[0], ly = (float)lo_hi[1], lz = (float)lo_hi[2];
+  const float ext = fmaxf(fmaxf((float)(lo_hi[3] - lo_hi[0]), (float)(lo_hi[4] - lo_hi[1])),
+                          (float)(lo_hi[5] - lo_hi[2]));
+  const float inv = ext > 0.f ? (float)kSortCells / ext : 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int cx = min(max((int)((__ldg(p + 3 * i) - lx) * inv), 0), kSortCells - 1);
+    const int cy = min(max((int)((__ldg(p + 3 * i + 1) - ly) * inv), 0), kSortCells - 1);
+    const int cz = min(max((int)((__ldg(p + 3 * i + 2) - lz) * inv), 0), kSortCells - 1);
+    const uint32_t key = spread3(cx) | (spread3(cy) << 1) | (spread3(cz) << 2);
+    keys[i] = key;
+    atomicAdd(hist + key, 1u);
+  }
+}
+
+// exclusive scan of kSortBins counters: per-block scan of 4096 (1024 threads x 4), block totals,
+// then add. In place on `hist`.
+__global__ void __launch_bounds__(1024) k_scan_blocks(uint32_t* __restrict__ hist, uint32_t* __restrict__ totals) {
+  __shared__ uint32_t warp_sums[32];
+  const int64_t base = (int64_t)blockIdx.x * 4096 + threadIdx.x * 4;
+  uint4 v = *reinterpret_cast<const uint4*>(hist + base);
+  const uint32_t s0 = v.x, s1 = s0 + v.y, s2 = s1 + v.z, s3 = s2 + v.w;
+  uint32_t incl = s3;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t ws = warp_sums[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, ws, o);
+      if (lane >= o) ws += t;
+    }
+    warp_sums[lane] = ws;
+  }
+  __syncthreads();
+  const uint32_t excl = incl - s3 + (wid > 0 ? warp_sums[wid - 1] : 0u);
+  *reinterpret_cast<uint4*>(hist + base) = make_uint4(excl, excl + s0, excl + s1, excl + s2);
+  if (threadIdx.x == 1023) totals[blockIdx.x] = excl + s3;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_totals(uint32_t* __restrict__ totals, int nblocks) {
+  __shared__ uint32_t s[1024];
+  const int t = threadIdx.x;
+  s[t] = t < nblocks ? totals[t] : 0u;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const uint32_t v = t >= o ? s[t - o] : 0u;
+    __syncthreads();
+    s[t] += v;
+    __syncthreads();
+  }
+  if (t < nblocks) totals[t] = s[t] - (t < nblocks ? totals[t] : 0u);
+}
+
+__global__ void k_scan_add(uint32_t* __restrict__ hist, const uint32_t* __restrict__ totals) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  hist[i] += totals[i / 4096];
+}
+
+__global__ void k_sort_scatter(const float* __restrict__ p, int64_t n, const uint32_t* __restrict__ keys,
+                               uint32_t* __restrict__ cursor, int32_t* __restrict__ perm,
+                               float4* __restrict__ spts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t pos = atomicAdd(cursor + keys[i], 1u);
+    perm[pos] = (int32_t)i;
+    spts[pos] = make_float4(__ldg(p + 3 * i), __ldg(p + 3 * i + 1), __ldg(p + 3 * i + 2), 0.f);
+  }
+}
+
+// ---- k_tile_prep ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTile) k_tile_prep(TileParams P) {
+  __shared__ ViewF sv[kMaxViewsTC];
+  __shared__ pf_view_t sv64[kMaxViewsTC];
+  __shared__ int wx0[kMaxViewsTC], wx1[kMaxViewsTC], wy0[kMaxViewsTC], wy1[kMaxViewsTC];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int j = tid; j < P.nv; j += kTile) {
+    sv64[j] = P.views[j];
+    sv[j] = make_viewf(P.views[j], P.d);
+    wx0[j] = INT_MAX;
+    wy0[j] = INT_MAX;
+    wx1[j] = -1;
+    wy1[j] = -1;
+  }
+  __syncthreads();
+  const int64_t tile = blockIdx.x;
+  const int64_t jpt = tile * kTile + tid;
+  const bool valid = jpt < P.n;
+  float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+  int32_t i = 0;
+  if (valid) {
+    p = P.spts[jpt];
+    i = P.perm[jpt];
+  }
+  uint32_t words[kMaxViewsTC / 32] = {0u, 0u};
+  int cnt = 0;
+  for (int v = 0; v < P.nv; ++v) {
+    bool vis = false;
+    int tx0 = INT_MAX, ty0 = INT_MAX, tx1 = -1, ty1 = -1;
+    if (valid) {
+      ProjF q;
+      vis = visible_exact(sv[v], sv64[v], P.depth, p.x, p.y, p.z, P.eps, q);
+      if (vis) {
+        const TapF t = taps_f32(sv[v], q.u, q.v);
+        tx0 = t.x0;
+        ty0 = t.y0;
+        tx1 = t.x0 + t.dx;
+        ty1 = t.y0 + t.dy;
+        words[v >> 5] |= 1u << (v & 31);
+        ++cnt;
+      }
+    }
+    const int ax0 = __reduce_min_sync(0xffffffffu, tx0), ay0 = __reduce_min_sync(0xffffffffu, ty0);
+    const int ax1 = __reduce_max_sync(0xffffffffu, tx1), ay1 = __reduce_max_sync(0xffffffffu, ty1);
+    if (lane == 0 && ax1 >= 0) {
+      atomicMin(wx0 + v, ax0);
+      atomicMin(wy0 + v, ay0);
+      atomicMax(wx1 + v, ax1);
+      atomicMax(wy1 + v, ay1);
+    }
+  }
+  if (valid) {
+    for (int w = 0; w < P.nwords; ++w) P.mask_bits[(int64_t)i * P.nwords + w] = words[w];
+    P.counts[i] = cnt;
+    double lo[3];
+    const double edge = voxel_edge(P.lo_hi, P.grid, lo);
+    P.codes[i] = voxel_code(p.x, p.y, p.z, lo, edge, P.grid);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int base = 0;
+    uint2* desc = P.tile_desc + tile * P.nv;
+    for (int v = 0; v < P.nv; ++v) {
+      int w = 0, h = 0;
+      if (wx1[v] >= 0) {
+        w = wx1[v] - wx0[v] + 1;
+        h = wy1[v] - wy0[v] + 1;
+      }
+      const int x0 = w ? wx0[v] : 0, y0 = h ? wy0[v] : 0;
+      desc[v] = make_uint2((uint32_t)min(base, 65535) | ((uint32_t)x0 << 16) | ((uint32_t)y0 << 24),
+                           (uint32_t)w | ((uint32_t)h << 8));
+      base += w * h;
+    }
+    P.tile_kt[tile] = base;
+  }
+}
+
+// ---- k_tile_mma ----------------------------------------------------------------------------------------
+__device__ __forceinline__ uint16_t f2bf(float f) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+__global__ void __launch_bounds__(kTile, 2) k_tile_mma(TileParams P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = smem;                          // 128 x KT_MAX bf16, K-major SW128
+  unsigned char* sB = smem + kTile * kKtMax * 2;     // KT_MAX x 128 bf16, N-major SW128
+  float* sRed = reinterpret_cast<float*>(smem);      // epilogue: [128][kRedStride] (reuses A+B)
+  __shared__ ViewF sv[kMaxViewsTC];
+  __shared__ uint2 sdesc[kMaxViewsTC];
+  __shared__ int32_t scell[kKtMax];
+  __shared__ float svals[kMaxKpadTC * 4];
+  __shared__ float smt[kMaxKpadTC];
+  __shared__ float sred6[4][8];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_base_s;
+  __shared__ int s_kt;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tile = blockIdx.x;
+  if (tid == 0) s_kt = P.tile_kt[tile];
+  for (int j = tid; j < P.nv; j += kTile) {
+    sv[j] = make_viewf(P.views[j], P.d);
+    sdesc[j] = P.tile_desc[tile * P.nv + j];
+  }
+  for (int j = tid; j < P.kpadg * 4; j += kTile) {
+    const int kk = j >> 2, pp = j & 3;
+    svals[j] = (kk < P.k && pp < P.p) ? P.values[kk * P.p + pp] : 0.f;
+  }
+  for (int j = tid; j < P.kpadg; j += kTile) smt[j] = j < P.k ? P.mid_theta[j] : 0.f;
+  __syncthreads();
+  const int kt = s_kt;
+  const int ktp = (kt + 15) & ~15;
+  const int64_t jpt = tile * kTile + tid;
+  const bool valid = jpt < P.n;
+  const int32_t i = valid ? P.perm[jpt] : 0;
+  if (ktp > kKtMax || kt == 0) {
+    // overflow (or nothing visible anywhere in the tile): the SIMT kernel handles these points
+    if (valid) P.ovf_list[atomicAdd(P.ovf_count, 1)] = i;
+    for (int kk = tid; kk < P.k + 6; kk += kTile) P.tile_part[tile * (int64_t)(P.k + 6) + kk] = 0.f;
+    return;
+  }
+  const float4 p = valid ? P.spts[jpt] : make_float4(0.f, 0.f, 0.f, 0.f);
+
+  // row -> global cell table for the B loads (pad rows repeat a valid cell; their A columns are 0)
+  for (int v = tid; v < P.nv; v += kTile) {
+    const uint2 ds = sdesc[v];
+    const int base = ds.x & 0xffff, x0 = (ds.x >> 16) & 0xff, y0 = ds.x >> 24;
+    const int w = ds.y & 0xff, h = (ds.y >> 8) & 0xff;
+    for (int a = 0; a < w * h; ++a)
+      scell[base + a] = sv[v].cell_base + (y0 + a / w) * sv[v].Wf + x0 + a % w;
+  }
+  // zero A (ktp columns) with 16-byte stores
+  {
+    const int n16 = kTile * ktp * 2 / 16;
+    uint4* a4 = reinterpret_cast<uint4*>(sA);
+    // A atom columns are [128 rows][128 B]; columns beyond ktp within the last atom are never read
+    for (int e = tid; e < ((ktp + 63) / 64) * kTile * 8; e += kTile) a4[e] = make_uint4(0, 0, 0, 0);
+    (void)n16;
+  }
+  __syncthreads();
+  for (int r = ktp - 1 - tid; r >= kt; r -= kTile) scell[r] = scell[0];
+  // scatter this point's bilinear weights into its A row
+  int count = 0;
+  if (valid) {
+    count = P.counts[i];
+    for (int w = 0; w < P.nwords; ++w) {
+      uint32_t bits = P.mask_bits[(int64_t)i * P.nwords + w];
+      while (bits) {
+        const int v = w * 32 + __ffs(bits) - 1;
+        bits &= bits - 1;
+        const ProjF q = project_f32(sv[v], p.x, p.y, p.z);
+        const TapF t = taps_f32(sv[v], q.u, q.v);
+        float w00 = (1.f - t.wy) * (1.f - t.wx), w01 = (1.f - t.wy) * t.wx;
+        float w10 = t.wy * (1.f - t.wx), w11 = t.wy * t.wx;
+        if (!t.dx) { w00 += w01; w10 += w11; w01 = w11 = 0.f; }
+        if (!t.dy) { w00 += w10; w01 += w11; w10 = w11 = 0.f; }
+        const uint2 ds = sdesc[v];
+        const int base = ds.x & 0xffff, x0 = (ds.x >> 16) & 0xff, y0 = ds.x >> 24;
+        const int ww = ds.y & 0xff;
+        const int c00 = base + (t.y0 - y0) * ww + (t.x0 - x0);
+        *reinterpret_cast<uint16_t*>(sA + tc::a_off(tid, c00, kTile)) = f2bf(w00);
+        if (t.dx) *reinterpret_cast<uint16_t*>(sA + tc::a_off(tid, c00 + 1, kTile)) = f2bf(w01);
+        if (t.dy) *reinterpret_cast<uint16_t*>(sA + tc::a_off(tid, c00 + ww, kTile)) = f2bf(w10);
+        if (t.dx && t.dy) *reinterpret_cast<uint16_t*>(sA + tc::a_off(tid, c00 + ww + 1, kTile)) = f2bf(w11);
+      }
+    }
+  }
+  if (tid == 0) tc::mbar_init(&mbar, 1);
+  const uint32_t ncols = P.tmem_cols;
+  if (warp == 0) tc::tmem_alloc(&tmem_base_s, ncols);
+  tc::fence_async_shared();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = tmem_base_s;
+  const uint32_t t_lane = (uint32_t)(warp * 32) << 16;
+  const uint32_t tD = tbase, tS = tbase + 128;
+
+  const int nd = P.d / 128;  // feature chunks of 128 channels; chunk nd = the G table (S)
+  float ss = 0.f;
+  uint32_t phase = 0;
+  const float invc = count > 0 ? 1.f / (float)count : 0.f;
+  for (int c = 0; c <= nd; ++c) {
+    const bool is_s = c == nd;
+    const int ncol = is_s ? P.kpadg : 128;
+    const int qn = ncol / 8;
+    // stream this chunk's tap rows into B (N-major, 128-B swizzle)
+    for (int e = tid; e < ktp * qn; e += kTile) {
+      const int r = e / qn, q = e % qn;
+      const int64_t cell = scell[r];
+      const void* src = is_s ? (const void*)(P.Gbf + cell * P.kpadg + q * 8)
+                             : (const void*)(reinterpret_cast<const uint16_t*>(P.fmap) + cell * P.d + c * 128 + q * 8);
+      tc::cp_async16(tc::smem_u32(sB + tc::b_chunk_off(r, q, ktp)), src);
+    }
+    tc::cp_async_wait_all();
+    tc::fence_async_shared();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    if (tid == 0) {
+      const uint32_t idesc = tc::idesc_bf16_f32(128, ncol, false, true);
+      const uint32_t a0 = tc::smem_u32(sA), b0 = tc::smem_u32(sB);
+      for (int s = 0; s < ktp / 16; ++s) {
+        const uint64_t ad = tc::smem_desc_sw128(a0 + (s >> 2) * kTile * 128 + (s & 3) * 32, 16, 1024);
+        const uint64_t bd = tc::smem_desc_sw128(b0 + s * 2048, ktp * 128, 1024);
+        tc::mma_bf16(is_s ? tS : tD, ad, bd, idesc, s > 0 ? 1u : 0u);
+      }
+      tc::mma_commit(&mbar);
+    }
+    tc::mbar_wait(&mbar, phase);
+    phase ^= 1u;
+    tc::fence_after_sync();
+    if (!is_s) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        float v[32];
+        tc::tmem_ld32(tD + t_lane + c0, v);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) ss = fmaf(v[q], v[q], ss);
+        if (P.features && valid) {
+          float* dst = P.features + (int64_t)i * P.d + c * 128 + c0;
+#pragma unroll
+          for (int q = 0; q < 32; q += 4)
+            *reinterpret_cast<float4*>(dst + q) =
+                make_float4(v[q] * invc, v[q + 1] * invc, v[q + 2] * invc, v[q + 3] * invc);
+        }
+      }
+      tc::fence_before_sync();
+      __syncthreads();
+      tc::fence_after_sync();
+    }
+  }
+
+  // ---- epilogue: thread = point; S row in TMEM -----------------------------------------------------
+  const bool featured = valid && count > 0;
+  const float inv = ss > 0.f ? 1.f / sqrtf(ss) : 0.f;
+  const float it = P.inv_temp;
+  float m = -INFINITY;
+  bool nan = false;
+  for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
+    float v[32];
+    tc::tmem_ld32(tS + t_lane + c0, v);
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      if (c0 + q < P.k) {
+        const float s = v[q] * inv;
+        nan |= isnan(s);
+        m = fmaxf(m, s * it);
+      }
+    }
+  }
+  if (featured && nan) atomicOr(P.status, 1);
+  float se = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f, pl3 = 0.f, pml = 0.f;
+  for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
+    float v[32];
+    tc::tmem_ld32(tS + t_lane + c0, v);
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int kk = c0 + q;
+      if (kk < P.k) {
+        const float e = expf(v[q] * inv * it - m);
+        se += e;
+        pl0 = fmaf(e, svals[kk * 4 + 0], pl0);
+        pl1 = fmaf(e, svals[kk * 4 + 1], pl1);
+        pl2 = fmaf(e, svals[kk * 4 + 2], pl2);
+        pl3 = fmaf(e, svals[kk * 4 + 3], pl3);
+        pml = fmaf(e, smt[kk], pml);
+      }
+    }
+  }
+  const float rs = featured ? 1.f / se : 0.f;
+  // third pass: normalised weights -> reduction buffer (+ optional validation outputs)
+  for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
+    float v[32];
+    tc::tmem_ld32(tS + t_lane + c0, v);
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int kk = c0 + q;
+      const float s = v[q] * inv;
+      const float wgt = (kk < P.k && featured) ? expf(s * it - m) * rs : 0.f;
+      sRed[tid * kRedStride + kk] = wgt;
+      if (kk < P.k && valid) {
+        if (P.sims) P.sims[(int64_t)i * P.k + kk] = featured ? s : 0.f;
+        if (P.weights) P.weights[(int64_t)i * P.k + kk] = wgt;
+      }
+    }
+  }
+  const float prop[4] = {pl0 * rs, pl1 * rs, pl2 * rs, pl3 * rs};
+  const float pm = pml * rs;
+  if (valid) {
+    for (int pp = 0; pp < P.p; ++pp) P.props[(int64_t)i * P.p + pp] = prop[pp];
+    if (P.grid_partials) {
+      const int32_t code = P.codes[i];
+      atomicAdd(P.grid_partials + code, prop[P.density_col]);
+      atomicAdd(P.grid_partials + P.cells3 + code, 1.0f);
+    }
+  }
+  // block partials: weight totals by column sums, scalars by warp + block reduction
+  float r6[6] = {pm, pm * p.x, pm * p.y, pm * p.z, featured ? 1.f : 0.f, (float)count};
+#pragma unroll
+  for (int q = 0; q < 6; ++q) r6[q] = warp_sum(r6[q]);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 6; ++q) sred6[warp][q] = r6[q];
+  tc::fence_before_sync();
+  __syncthreads();
+  float* out = P.tile_part + tile * (int64_t)(P.k + 6);
+  for (int kk = tid; kk < P.k; kk += kTile) {
+    float acc = 0.f;
+    for (int r = 0; r < kTile; ++r) acc += sRed[r * kRedStride + kk];
+    out[kk] = acc;
+  }
+  if (tid < 6) out[P.k + tid] = sred6[0][tid] + sred6[1][tid] + sred6[2][tid] + sred6[3][tid];
+  if (warp == 0) tc::tmem_dealloc(tbase, ncols);
+}
+
+__global__ void k_tile_partials(const float* __restrict__ tile_part, int64_t ntiles, int ncol,
+                                double* __restrict__ partials) {
+  const int col = threadIdx.x;
+  if (col >= ncol) return;
+  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+  double acc = 0.0;
+  for (int64_t t = t0; t < t1; ++t) acc += (double)tile_part[t * ncol + col];
+  if (acc != 0.0) atomicAdd(partials + col, acc);
+}
+
+// G in bf16 (cells x kpadg) for the tensor path, from the fp32 table of the SIMT path
+__global__ void k_g_bf16(const float* __restrict__ G, int64_t cells, int kpad, int kpadg,
+                         uint16_t* __restrict__ Gbf) {
+  const int64_t total = cells * kpadg;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / kpadg;
+    const int k = (int)(e - c * kpadg);
+    Gbf[e] = f2bf(k < kpad ? G[c * kpad + k] : 0.f);
+  }
+}
+
+}  // namespace tile
+}  // namespace pf
+
+// ---- host orchestration -----------------------------------------------------------------------------
+namespace pf {
+namespace tile {
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg) {
+  TileLayout L{};
+  const int64_t ntiles = (n + kTile - 1) / kTile;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  L.ntiles = ntiles;
+  L.keys = take(sizeof(uint32_t) * (size_t)n);
+  L.hist = take(sizeof(uint32_t) * (size_t)kSortBins);
+  L.totals = take(sizeof(uint32_t) * 1024);
+  L.perm = take(sizeof(int32_t) * (size_t)n);
+  L.spts = take(sizeof(float4) * (size_t)n);
+  L.desc = take(sizeof(uint2) * (size_t)ntiles * nv);
+  L.kt = take(sizeof(int32_t) * (size_t)ntiles);
+  L.part = take(sizeof(float) * (size_t)ntiles * (kMaxKpadTC + 6));
+  L.ovf = take(sizeof(int32_t) * (size_t)(n + 1));
+  L.gbf = take(sizeof(uint16_t) * (size_t)cells * kpadg);
+  L.bytes = off;
+  return L;
+}
+
+size_t tile_smem_bytes() {
+  const size_t ab = (size_t)kTile * kKtMax * 2 * 2;
+  const size_t red = (size_t)kTile * kRedStride * 4;
+  return (ab > red ? ab : red) + 1024;
+}
+
+int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const float* points,
+                  int64_t n, int64_t cells, const float* G, int kpad, cudaStream_t st) {
+  uint32_t* keys = reinterpret_cast<uint32_t*>(ws + L.keys);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
+  uint32_t* totals = reinterpret_cast<uint32_t*>(ws + L.totals);
+  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kSortBins, st);
+  cudaMemsetAsync(P.ovf_count, 0, sizeof(int32_t), st);
+  k_sort_keys<<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist);
+  if (int rc = check_launch("sort_keys")) return rc;
+  k_scan_blocks<<<kSortBins / 4096, 1024, 0, st>>>(hist, totals);
+  if (int rc = check_launch("scan_blocks")) return rc;
+  k_scan_totals<<<1, 1024, 0, st>>>(totals, kSortBins / 4096);
+  if (int rc = check_launch("scan_totals")) return rc;
+  k_scan_add<<<kSortBins / 256, 256, 0, st>>>(hist, totals);
+  if (int rc = check_launch("scan_add")) return rc;
+  k_sort_scatter<<<grid_for(n, 256), 256, 0, st>>>(points, n, keys, hist, const_cast<int32_t*>(P.perm),
+                                                   const_cast<float4*>(P.spts));
+  if (int rc = check_launch("sort_scatter")) return rc;
+  k_g_bf16<<<grid_for(cells * P.kpadg, 256), 256, 0, st>>>(G, cells, kpad, P.kpadg,
+                                                          const_cast<uint16_t*>(P.Gbf));
+  if (int rc = check_launch("g_bf16")) return rc;
+  k_tile_prep<<<(unsigned)L.ntiles, kTile, 0, st>>>(P);
+  if (int rc = check_launch("tile_prep")) return rc;
+  const size_t smem = tile_smem_bytes();
+  cudaFuncSetAttribute(k_tile_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_tile_mma<<<(unsigned)L.ntiles, kTile, smem, st>>>(P);
+  if (int rc = check_launch("tile_mma")) return rc;
+  const int ncol = P.k + 6;
+  k_tile_partials<<<256, ((ncol + 31) / 32) * 32, 0, st>>>(P.tile_part, L.ntiles, ncol, P.partials);
+  return check_launch("tile_partials");
+}
+
+}  // namespace tile
+}  // namespace pf

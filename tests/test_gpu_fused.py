@@ -16,6 +16,12 @@ from oracle import propfield_oracle as O
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-4
+TOL_BF16 = 1e-2  # bf16-feature mode (tensor-core tile path: bf16 weights and G table)
+
+
+def tol_for(wl, force_simt=False):
+    """The tile path (bf16 maps, D % 128 == 0) computes in bf16 x bf16 -> fp32: 1e-2 bar."""
+    return TOL_BF16 if (wl.cfg.bf16 and wl.cfg.d % 128 == 0 and not force_simt) else TOL
 
 
 def run_gpu(wl, points=None, **kw):
@@ -94,26 +100,71 @@ def test_fused_vs_reference_goldens(cuda, golden, workload, name):
     """Against the reference's own outputs (golden fixtures), not just the oracle."""
     g = golden(name)
     wl = workload(name)
-    res = run_gpu(wl)
-    vis = np.unpackbits(g["visibility"], axis=1)[:, : wl.cfg.nviews].astype(bool)
-    assert np.array_equal(res.visibility().cpu().numpy(), vis)
-    assert np.array_equal(res.counts.cpu().numpy(), g["counts"])
-    s = res.sims.cpu().numpy()
-    scale = np.maximum(1e-2, np.abs(g["sims"]).max(axis=1))
-    assert (np.abs(s - g["sims"]).max(axis=1) <= TOL * scale).all()
-    np.testing.assert_allclose(res.props.cpu().numpy(), g["props"], rtol=TOL, atol=1e-6)
+    for force in (False, True):
+        tol = tol_for(wl, force)
+        res = run_gpu(wl, force_simt=force)
+        vis = np.unpackbits(g["visibility"], axis=1)[:, : wl.cfg.nviews].astype(bool)
+        assert np.array_equal(res.visibility().cpu().numpy(), vis)
+        assert np.array_equal(res.counts.cpu().numpy(), g["counts"])
+        s = res.sims.cpu().numpy()
+        scale = np.maximum(1e-2, np.abs(g["sims"]).max(axis=1))
+        assert (np.abs(s - g["sims"]).max(axis=1) <= tol * scale).all()
+        np.testing.assert_allclose(res.props.cpu().numpy(), g["props"], rtol=tol, atol=1e-6)
 
 
 @pytest.mark.parametrize("name", ["mini", "mini_bf16", "mini_fib40", "pr1"])
 def test_fused_vs_oracle(cuda, workload, name):
     wl = workload(name)
-    assert_parity(run_gpu(wl), run_oracle(wl), wl)
+    assert_parity(run_gpu(wl), run_oracle(wl), wl, tol=tol_for(wl))
+
+
+def test_bf16_simt_path_meets_fp32_bar(cuda, workload):
+    wl = workload("mini_bf16")
+    assert_parity(run_gpu(wl, force_simt=True), run_oracle(wl), wl, tol=TOL)
+
+
+@pytest.mark.parametrize("name", ["c5", "c3"])
+def test_tile_path_large_config_shapes(cuda, workload, name):
+    """Tensor-core tile path on the real C5 / C3 view + map + material shapes (subset of points
+    so the oracle finishes in seconds): masks / counts / codes exact, the rest at the bf16 bar."""
+    wl = workload(name, n=24_000)
+    assert_parity(run_gpu(wl), run_oracle(wl), wl, tol=TOL_BF16)
 
 
 def test_fused_c2_shapes_subset(cuda, workload):
     """C2 shapes (V=16 on two rings, 512^2, 37x37x768, K=32, 128^3) on 20k of its points."""
     wl = workload("c2", n=20_000)
     assert_parity(run_gpu(wl), run_oracle(wl), wl)
+
+
+def test_tile_vs_simt_full_c5(cuda):
+    """Full BASELINE C5 size (16M points x 64 views): the tile path's exact visibility (fp32 with
+    error bound + fp64 fallback) must reproduce the fp64 SIMT path bit for bit; per-point
+    properties and the voxel mass agree at the bf16 bar."""
+    import torch
+
+    from paper_2511_03126_b200 import workloads
+
+    wl = workloads.generate("c5", device_splat=True)
+    nv = wl.cfg.nviews
+    R = np.stack([p.rotation for p in wl.poses])
+    tv = np.stack([p.translation for p in wl.poses])
+    intr = np.tile([wl.intrinsics.fx, wl.intrinsics.fy, wl.intrinsics.cx, wl.intrinsics.cy], (nv, 1))
+    fmap = torch.from_numpy(wl.fmaps.view(np.int16)).cuda().view(torch.bfloat16)
+    views = pf.ViewSet.from_tensors(R, tv, intr, wl.depth.cuda(), fmap)
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta)
+    pts = torch.from_numpy(wl.points).cuda()
+    a = pf.fuse_and_query(pts, views, tables, grid=wl.cfg.grid, check=True)
+    ca, ma, pa, ka, mass_a = (a.counts.clone(), a.mask_bits.clone(), a.props.clone(), a.codes.clone(),
+                              a.mass_kg())
+    b = pf.fuse_and_query(pts, views, tables, grid=wl.cfg.grid, force_simt=True, check=True)
+    assert torch.equal(ca, b.counts)
+    assert torch.equal(ma, b.mask_bits)
+    assert torch.equal(ka, b.codes)
+    feat = b.counts > 0
+    rel = ((pa[:, 0] - b.props[:, 0]).abs() / b.props[:, 0].abs().clamp_min(1e-30))[feat]
+    assert float(rel.max()) <= TOL_BF16
+    assert mass_a == pytest.approx(b.mass_kg(), rel=TOL_BF16)
 
 
 def test_featureless_points(cuda, workload):
