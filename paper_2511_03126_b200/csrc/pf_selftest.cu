@@ -70,7 +70,8 @@ extern "C" int pf_selftest_umma(const void* a, const void* b, float* c, int32_t 
                                 void* stream) {
   if (k < 16 || k % 64 != 0 || k > 256 || n < 16 || n % 16 != 0 || n > 256)
     return set_error(PF_ERR_VALUE, "selftest_umma: need k in {64..256, %%64} and n in {16..256, %%16}");
-  const size_t smem = 128 * (size_t)k * 2 + (size_t)k * n * 2 + 1024;
+  // B occupies whole 128-byte swizzle rows: ceil(n/64) halves of k rows x 128 B
+  const size_t smem = 128 * (size_t)k * 2 + (size_t)((n + 63) / 64) * k * 128 + 1024;
   cudaFuncSetAttribute(k_umma_selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_umma_selftest<<<1, 128, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const uint16_t*>(a), reinterpret_cast<const uint16_t*>(b), c, k, n);
