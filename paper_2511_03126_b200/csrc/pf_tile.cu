@@ -58,66 +58,73 @@ __device__ __forceinline__ ViewF make_viewf(const pf_view_t& v, int d) {
 
 struct ProjF {
   float u, v, z, e;  // e: bound on |cam_c - cam_c(exact)| for each camera coordinate
-  float a, b;        // X/z, Y/z
+  float X, Y, rz;    // camera x, y and the rounded reciprocal of z
 };
 
 __device__ __forceinline__ float cam_f32(const float* R, float t, float px, float py, float pz) {
   return __fadd_rn(__fmaf_rn(R[2], pz, __fmaf_rn(R[1], py, __fmul_rn(R[0], px))), t);
 }
 
+// u = fx * (X * (1/z)) + cx with explicitly rounded ops (k_tile_prep and k_tile_mma must agree
+// bit for bit, so nothing is left to contraction choices)
 __device__ __forceinline__ ProjF project_f32(const ViewF& w, float px, float py, float pz) {
   ProjF o;
-  const float X = cam_f32(w.R + 0, w.t[0], px, py, pz);
-  const float Y = cam_f32(w.R + 3, w.t[1], px, py, pz);
+  o.X = cam_f32(w.R + 0, w.t[0], px, py, pz);
+  o.Y = cam_f32(w.R + 3, w.t[1], px, py, pz);
   o.z = cam_f32(w.R + 6, w.t[2], px, py, pz);
-  o.a = __fdiv_rn(X, o.z);
-  o.b = __fdiv_rn(Y, o.z);
-  o.u = __fmaf_rn(w.fx, o.a, w.cx);
-  o.v = __fmaf_rn(w.fy, o.b, w.cy);
+  o.rz = __frcp_rn(o.z);
+  o.u = __fmaf_rn(w.fx, __fmul_rn(o.X, o.rz), w.cx);
+  o.v = __fmaf_rn(w.fy, __fmul_rn(o.Y, o.rz), w.cy);
   // |R_ij| <= 1: each camera coordinate has magnitude <= |p|_1 + |t|_inf. f32 R/t representation
   // (2^-24 relative) plus 4 roundings of that magnitude is < 5*2^-24; take 2^-20 (>3x margin).
   o.e = (fabsf(px) + fabsf(py) + fabsf(pz) + w.tmax) * 9.5367431640625e-07f;
   return o;
 }
 
-// error bound of u = fx*X/z + cx given |X - X*|, |z - z*| <= e and |z| >= 2e
-__device__ __forceinline__ float pix_err(float f, float c, float num, float ratio, float z, float e) {
-  const float az = fabsf(z);
-  const float da = e / az + 2.f * e * (fabsf(num) + e) / (az * az) + 6.0e-8f * fabsf(ratio);
-  return 2.f * (fabsf(f) * da + 1.2e-7f * (fabsf(f * ratio) + fabsf(c)) + 1e-6f);
+// Bound on |u - u64| for u = f * num/z + c, given |num - num*|, |z - z*| <= e and |z| >= 2e:
+// |a - a*| <= e/|z| + 2e(|num| + e)/z^2 + 2^-23|a| (rcp + mul roundings); the fma adds
+// 2^-24 |f a + c| and f / c representation 2^-24 each. Doubled for safety. No divisions.
+__device__ __forceinline__ float pix_err(float f, float c, float num, float arz, float e) {
+  const float a = fabsf(num) * arz;
+  const float da = e * arz * (1.f + 2.f * (fabsf(num) + e) * arz) + 1.2e-7f * a;
+  return 2.f * (fabsf(f) * da + 1.2e-7f * (fabsf(f) * a + fabsf(c)) + 1e-6f);
 }
 
-// Exact visibility decision (numpy_impl.py:31-40 on fp64 projections): fast fp32 path when the
-// fp32 result is provably on the same side of every decision boundary, exact fp64 otherwise.
-__device__ __forceinline__ bool visible_exact(const ViewF& w, const pf_view_t& w64, const float* depth,
-                                              float px, float py, float pz, double eps, ProjF& q) {
-  q = project_f32(w, px, py, pz);
+// Classification of one (point, view) sample before the depth lookup.
+enum : int { kInvisible = 0, kNeedDepth = 1, kAmbiguous = 2 };
+
+__device__ __forceinline__ int classify(const ViewF& w, const ProjF& q, int64_t& didx) {
   const float e = q.e;
-  bool ambiguous = !(fabsf(q.z) > 2.f * e) || !isfinite(q.u) || !isfinite(q.v);
-  if (!ambiguous) {
-    if (q.z < 0.f) return false;  // |z| > 2e: the sign is certain
-    const float X = q.a * q.z, Y = q.b * q.z;
-    const float eu = pix_err(w.fx, w.cx, X, q.a, q.z, e);
-    const float ev = pix_err(w.fy, w.cy, Y, q.b, q.z, e);
-    const float du = fabsf(q.u - floorf(q.u) - 0.5f), dv = fabsf(q.v - floorf(q.v) - 0.5f);
-    if (eu >= 0.25f || ev >= 0.25f || du <= eu || dv <= ev) {
-      ambiguous = true;
-    } else {
-      const float ru = rintf(q.u), rv = rintf(q.v);
-      if (!(ru >= 0.f && ru < (float)w.W && rv >= 0.f && rv < (float)w.H)) return false;
-      const double stored = (double)__ldg(depth + w.depth_off + (int64_t)rv * w.W + (int64_t)ru);
-      if (!(stored > 0.0)) return false;
-      const double thr = stored + eps;
-      const double zd = (double)q.z;
-      if (zd + (double)e < thr) return true;
-      if (zd - (double)e > thr) return false;
-      ambiguous = true;
-    }
-  }
-  // exact fp64 decision, identical to the reference arithmetic (pf_common.cuh)
+  if (!(fabsf(q.z) > 2.f * e) || !isfinite(q.u) || !isfinite(q.v)) return kAmbiguous;
+  if (q.z < 0.f) return kInvisible;  // |z| > 2e: the sign is certain
+  const float arz = fabsf(q.rz) * 1.0000005f;
+  const float eu = pix_err(w.fx, w.cx, q.X, arz, e);
+  const float ev = pix_err(w.fy, w.cy, q.Y, arz, e);
+  const float du = fabsf(q.u - floorf(q.u) - 0.5f), dv = fabsf(q.v - floorf(q.v) - 0.5f);
+  if (eu >= 0.25f || ev >= 0.25f || du <= eu || dv <= ev) return kAmbiguous;
+  const float ru = rintf(q.u), rv = rintf(q.v);
+  if (!(ru >= 0.f && ru < (float)w.W && rv >= 0.f && rv < (float)w.H)) return kInvisible;
+  didx = w.depth_off + (int64_t)rv * w.W + (int64_t)ru;
+  return kNeedDepth;
+}
+
+// depth test for a decided pixel: z64 <= stored + eps (f64) decided in f32 with margin
+__device__ __forceinline__ int depth_decide(const ProjF& q, float stored, float eps_f) {
+  if (!(stored > 0.f)) return kInvisible;
+  const float thr = __fadd_rn(stored, eps_f);
+  const float m = q.e + 2.4e-7f * fabsf(thr) + 1e-9f;
+  if (q.z + m < thr) return kNeedDepth;  // visible
+  if (q.z - m > thr) return kInvisible;
+  return kAmbiguous;
+}
+
+// exact fp64 decision, identical to the reference arithmetic (pf_common.cuh)
+__device__ __forceinline__ bool visible_f64(const pf_view_t& w64, const float* depth, float px,
+                                            float py, float pz, double eps) {
   const Proj p64 = project(w64, (double)px, (double)py, (double)pz);
   return depth_test(depth + w64.depth_offset, w64.H, w64.W, p64.u, p64.v, p64.z, eps);
 }
+
 
 // bilinear taps of a visible sample from the fp32 projection (fusion.py:83-86 +
 // numpy_impl.py:50-57); k_tile_prep and k_tile_mma call this with bit-identical inputs.
@@ -249,31 +256,54 @@ __global__ void __launch_bounds__(kTile) k_tile_prep(TileParams P) {
     p = P.spts[jpt];
     i = P.perm[jpt];
   }
+  const float eps_f = (float)P.eps;
   uint32_t words[kMaxViewsTC / 32] = {0u, 0u};
   int cnt = 0;
-  for (int v = 0; v < P.nv; ++v) {
-    bool vis = false;
-    int tx0 = INT_MAX, ty0 = INT_MAX, tx1 = -1, ty1 = -1;
-    if (valid) {
-      ProjF q;
-      vis = visible_exact(sv[v], sv64[v], P.depth, p.x, p.y, p.z, P.eps, q);
-      if (vis) {
-        const TapF t = taps_f32(sv[v], q.u, q.v);
-        tx0 = t.x0;
-        ty0 = t.y0;
-        tx1 = t.x0 + t.dx;
-        ty1 = t.y0 + t.dy;
-        words[v >> 5] |= 1u << (v & 31);
-        ++cnt;
+  constexpr int U = 4;  // views in flight per thread (independent depth loads)
+  for (int v0 = 0; v0 < P.nv; v0 += U) {
+    ProjF q[U];
+    int st[U];
+    float stored[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      st[u] = kInvisible;
+      stored[u] = 0.f;
+      const int v = v0 + u;
+      if (valid && v < P.nv) {
+        q[u] = project_f32(sv[v], p.x, p.y, p.z);
+        int64_t didx = 0;
+        st[u] = classify(sv[v], q[u], didx);
+        if (st[u] == kNeedDepth) stored[u] = __ldg(P.depth + didx);
       }
     }
-    const int ax0 = __reduce_min_sync(0xffffffffu, tx0), ay0 = __reduce_min_sync(0xffffffffu, ty0);
-    const int ax1 = __reduce_max_sync(0xffffffffu, tx1), ay1 = __reduce_max_sync(0xffffffffu, ty1);
-    if (lane == 0 && ax1 >= 0) {
-      atomicMin(wx0 + v, ax0);
-      atomicMin(wy0 + v, ay0);
-      atomicMax(wx1 + v, ax1);
-      atomicMax(wy1 + v, ay1);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = v0 + u;
+      if (v >= P.nv) break;
+      int s = st[u];
+      if (s == kNeedDepth) s = depth_decide(q[u], stored[u], eps_f);
+      bool vis = s == kNeedDepth;
+      if (s == kAmbiguous) vis = visible_f64(sv64[v], P.depth, p.x, p.y, p.z, P.eps);
+      if (__any_sync(0xffffffffu, vis)) {
+        int tx0 = INT_MAX, ty0 = INT_MAX, tx1 = -1, ty1 = -1;
+        if (vis) {
+          const TapF t = taps_f32(sv[v], q[u].u, q[u].v);
+          tx0 = t.x0;
+          ty0 = t.y0;
+          tx1 = t.x0 + t.dx;
+          ty1 = t.y0 + t.dy;
+          words[v >> 5] |= 1u << (v & 31);
+          ++cnt;
+        }
+        const int ax0 = __reduce_min_sync(0xffffffffu, tx0), ay0 = __reduce_min_sync(0xffffffffu, ty0);
+        const int ax1 = __reduce_max_sync(0xffffffffu, tx1), ay1 = __reduce_max_sync(0xffffffffu, ty1);
+        if (lane == 0) {
+          atomicMin(wx0 + v, ax0);
+          atomicMin(wy0 + v, ay0);
+          atomicMax(wx1 + v, ax1);
+          atomicMax(wy1 + v, ay1);
+        }
+      }
     }
   }
   if (valid) {
@@ -302,6 +332,7 @@ __global__ void __launch_bounds__(kTile) k_tile_prep(TileParams P) {
   }
 }
 
+
 // ---- k_tile_mma ----------------------------------------------------------------------------------------
 __device__ __forceinline__ uint16_t f2bf(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));
@@ -311,16 +342,17 @@ __global__ void __launch_bounds__(kTile, 2) k_tile_mma(TileParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sA = smem;                          // 128 x KT_MAX bf16, K-major SW128
-  unsigned char* sB = smem + kTile * kKtMax * 2;     // KT_MAX x 128 bf16, N-major SW128
-  float* sRed = reinterpret_cast<float*>(smem);      // epilogue: [128][kRedStride] (reuses A+B)
+  unsigned char* sA = smem;                            // 128 x KT_MAX bf16, K-major SW128
+  unsigned char* sB = smem + kTile * kKtMax * 2;       // 2 stages x (KT_MAX x 64) bf16, N-major SW128
+  float* sRed = reinterpret_cast<float*>(smem);        // epilogue: [128][kRedStride] (reuses A+B)
   __shared__ ViewF sv[kMaxViewsTC];
   __shared__ uint2 sdesc[kMaxViewsTC];
   __shared__ int32_t scell[kKtMax];
-  __shared__ float svals[kMaxKpadTC * 4];
+  __shared__ __align__(16) float svals[kMaxKpadTC * 4];
   __shared__ float smt[kMaxKpadTC];
+  __shared__ float srs[kTile];
   __shared__ float sred6[4][8];
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t mbar[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ int s_kt;
 
@@ -358,17 +390,44 @@ __global__ void __launch_bounds__(kTile, 2) k_tile_mma(TileParams P) {
     for (int a = 0; a < w * h; ++a)
       scell[base + a] = sv[v].cell_base + (y0 + a / w) * sv[v].Wf + x0 + a % w;
   }
-  // zero A (ktp columns) with 16-byte stores
+  // zero A: ceil(ktp/64) atom columns of [128 rows][128 B]
   {
-    const int n16 = kTile * ktp * 2 / 16;
     uint4* a4 = reinterpret_cast<uint4*>(sA);
-    // A atom columns are [128 rows][128 B]; columns beyond ktp within the last atom are never read
-    for (int e = tid; e < ((ktp + 63) / 64) * kTile * 8; e += kTile) a4[e] = make_uint4(0, 0, 0, 0);
-    (void)n16;
+    for (int e = tid; e < ((ktp + 63) >> 6) * kTile * 8; e += kTile) a4[e] = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
   for (int r = ktp - 1 - tid; r >= kt; r -= kTile) scell[r] = scell[0];
-  // scatter this point's bilinear weights into its A row
+  __syncthreads();
+
+  // chunk schedule: nd feature chunks of 64 channels (TMEM D double buffer), then ns S chunks
+  const int nd = P.d >> 6;
+  const int ns = (P.kpadg + 63) >> 6;
+  const int nch = nd + ns;
+  auto chunk_cols = [&](int c) { return c < nd ? 64 : min(64, P.kpadg - 64 * (c - nd)); };
+  // B loader: thread -> fixed 16-byte column q, rows r0, r0 + rstep, ...
+  auto issue_load = [&](int c) {
+    const int ncol = chunk_cols(c);
+    const int qn = ncol >> 3;  // 8 or 4 (power of two)
+    const int q = tid & (qn - 1);
+    const int rstep = kTile / qn;
+    unsigned char* stage = sB + (c & 1) * (kKtMax * 128);
+    const uint16_t* base;
+    int64_t rowlen;
+    if (c < nd) {
+      base = reinterpret_cast<const uint16_t*>(P.fmap) + c * 64 + q * 8;
+      rowlen = P.d;
+    } else {
+      base = P.Gbf + (c - nd) * 64 + q * 8;
+      rowlen = P.kpadg;
+    }
+    const uint32_t sbase = tc::smem_u32(stage);
+    for (int r = tid / qn; r < ktp; r += rstep)
+      tc::cp_async16(sbase + tc::b_chunk_off(r, q, ktp), base + (int64_t)scell[r] * rowlen);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue_load(0);
+
+  // scatter this point's bilinear weights into its A row (overlaps the first B load)
   int count = 0;
   if (valid) {
     count = P.counts[i];
@@ -381,8 +440,8 @@ __global__ void __launch_bounds__(kTile, 2) k_tile_mma(TileParams P) {
         const TapF t = taps_f32(sv[v], q.u, q.v);
         float w00 = (1.f - t.wy) * (1.f - t.wx), w01 = (1.f - t.wy) * t.wx;
         float w10 = t.wy * (1.f - t.wx), w11 = t.wy * t.wx;
-        if (!t.dx) { w00 += w01; w10 += w11; w01 = w11 = 0.f; }
-        if (!t.dy) { w00 += w10; w01 += w11; w10 = w11 = 0.f; }
+        if (!t.dx) { w00 += w01; w10 += w11; }
+        if (!t.dy) { w00 += w10; w01 += w11; }
         const uint2 ds = sdesc[v];
         const int base = ds.x & 0xffff, x0 = (ds.x >> 16) & 0xff, y0 = ds.x >> 24;
         const int ww = ds.y & 0xff;
@@ -394,123 +453,119 @@ __global__ void __launch_bounds__(kTile, 2) k_tile_mma(TileParams P) {
       }
     }
   }
-  if (tid == 0) tc::mbar_init(&mbar, 1);
+  if (tid == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+  }
   const uint32_t ncols = P.tmem_cols;
   if (warp == 0) tc::tmem_alloc(&tmem_base_s, ncols);
-  tc::fence_async_shared();
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = tmem_base_s;
   const uint32_t t_lane = (uint32_t)(warp * 32) << 16;
-  const uint32_t tD = tbase, tS = tbase + 128;
-
-  const int nd = P.d / 128;  // feature chunks of 128 channels; chunk nd = the G table (S)
-  float ss = 0.f;
-  uint32_t phase = 0;
+  const uint32_t tS = tbase + 128;
   const float invc = count > 0 ? 1.f / (float)count : 0.f;
-  for (int c = 0; c <= nd; ++c) {
-    const bool is_s = c == nd;
-    const int ncol = is_s ? P.kpadg : 128;
-    const int qn = ncol / 8;
-    // stream this chunk's tap rows into B (N-major, 128-B swizzle)
-    for (int e = tid; e < ktp * qn; e += kTile) {
-      const int r = e / qn, q = e % qn;
-      const int64_t cell = scell[r];
-      const void* src = is_s ? (const void*)(P.Gbf + cell * P.kpadg + q * 8)
-                             : (const void*)(reinterpret_cast<const uint16_t*>(P.fmap) + cell * P.d + c * 128 + q * 8);
-      tc::cp_async16(tc::smem_u32(sB + tc::b_chunk_off(r, q, ktp)), src);
+  float ss = 0.f;
+
+  auto drain = [&](int c) {  // |F|^2 (and optional mean features) from TMEM D buffer c & 1
+    const uint32_t tD = tbase + (uint32_t)((c & 1) * 64);
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 32) {
+      float v[32];
+      tc::tmem_ld32(tD + t_lane + c0, v);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) ss = fmaf(v[q], v[q], ss);
+      if (P.features && valid) {
+        float* dst = P.features + (int64_t)i * P.d + c * 64 + c0;
+#pragma unroll
+        for (int q = 0; q < 32; q += 4)
+          *reinterpret_cast<float4*>(dst + q) =
+              make_float4(v[q] * invc, v[q + 1] * invc, v[q + 2] * invc, v[q + 3] * invc);
+      }
     }
-    tc::cp_async_wait_all();
+  };
+
+  for (int c = 0; c < nch; ++c) {
+    // B(c) landed (only chunk c+1's group may still be in flight... it is issued below)
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     tc::fence_async_shared();
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     if (tid == 0) {
+      const int ncol = chunk_cols(c);
       const uint32_t idesc = tc::idesc_bf16_f32(128, ncol, false, true);
-      const uint32_t a0 = tc::smem_u32(sA), b0 = tc::smem_u32(sB);
+      const uint32_t a0 = tc::smem_u32(sA), b0 = tc::smem_u32(sB + (c & 1) * (kKtMax * 128));
+      const uint32_t dst = c < nd ? tbase + (uint32_t)((c & 1) * 64) : tS + (uint32_t)(64 * (c - nd));
       for (int s = 0; s < ktp / 16; ++s) {
         const uint64_t ad = tc::smem_desc_sw128(a0 + (s >> 2) * kTile * 128 + (s & 3) * 32, 16, 1024);
         const uint64_t bd = tc::smem_desc_sw128(b0 + s * 2048, ktp * 128, 1024);
-        tc::mma_bf16(is_s ? tS : tD, ad, bd, idesc, s > 0 ? 1u : 0u);
+        tc::mma_bf16(dst, ad, bd, idesc, s > 0 ? 1u : 0u);
       }
-      tc::mma_commit(&mbar);
+      tc::mma_commit(&mbar[c & 1]);
     }
-    tc::mbar_wait(&mbar, phase);
-    phase ^= 1u;
-    tc::fence_after_sync();
-    if (!is_s) {
-#pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        float v[32];
-        tc::tmem_ld32(tD + t_lane + c0, v);
-#pragma unroll
-        for (int q = 0; q < 32; ++q) ss = fmaf(v[q], v[q], ss);
-        if (P.features && valid) {
-          float* dst = P.features + (int64_t)i * P.d + c * 128 + c0;
-#pragma unroll
-          for (int q = 0; q < 32; q += 4)
-            *reinterpret_cast<float4*>(dst + q) =
-                make_float4(v[q] * invc, v[q + 1] * invc, v[q + 2] * invc, v[q + 3] * invc);
-        }
-      }
-      tc::fence_before_sync();
-      __syncthreads();
+    if (c >= 1) {
+      tc::mbar_wait(&mbar[(c - 1) & 1], ((c - 1) >> 1) & 1);
       tc::fence_after_sync();
+      if (c - 1 < nd) drain(c - 1);
     }
+    // stage (c+1)&1 was read by MMA c-1, which has completed (waited above by every thread)
+    if (c + 1 < nch) issue_load(c + 1);
   }
+  tc::mbar_wait(&mbar[(nch - 1) & 1], ((nch - 1) >> 1) & 1);
+  tc::fence_after_sync();
+  if (nch - 1 < nd) drain(nch - 1);
 
   // ---- epilogue: thread = point; S row in TMEM -----------------------------------------------------
   const bool featured = valid && count > 0;
   const float inv = ss > 0.f ? 1.f / sqrtf(ss) : 0.f;
-  const float it = P.inv_temp;
-  float m = -INFINITY;
+  const float sc = inv * P.inv_temp * 1.4426950408889634f;  // log2(e) * inv / T
+  float m2 = -INFINITY;                                      // max of s * log2(e) / T
   bool nan = false;
   for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
     float v[32];
     tc::tmem_ld32(tS + t_lane + c0, v);
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
+      const float x = v[q] * sc;
       if (c0 + q < P.k) {
-        const float s = v[q] * inv;
-        nan |= isnan(s);
-        m = fmaxf(m, s * it);
+        nan |= isnan(x);
+        m2 = fmaxf(m2, x);
       }
     }
   }
   if (featured && nan) atomicOr(P.status, 1);
   float se = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f, pl3 = 0.f, pml = 0.f;
+  const float4* sv4 = reinterpret_cast<const float4*>(svals);
   for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
     float v[32];
     tc::tmem_ld32(tS + t_lane + c0, v);
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
       const int kk = c0 + q;
-      if (kk < P.k) {
-        const float e = expf(v[q] * inv * it - m);
-        se += e;
-        pl0 = fmaf(e, svals[kk * 4 + 0], pl0);
-        pl1 = fmaf(e, svals[kk * 4 + 1], pl1);
-        pl2 = fmaf(e, svals[kk * 4 + 2], pl2);
-        pl3 = fmaf(e, svals[kk * 4 + 3], pl3);
-        pml = fmaf(e, smt[kk], pml);
-      }
+      const float e = kk < P.k ? exp2f(v[q] * sc - m2) : 0.f;
+      se += e;
+      const float4 y = sv4[kk];
+      pl0 = fmaf(e, y.x, pl0);
+      pl1 = fmaf(e, y.y, pl1);
+      pl2 = fmaf(e, y.z, pl2);
+      pl3 = fmaf(e, y.w, pl3);
+      pml = fmaf(e, smt[kk], pml);
+      sRed[tid * kRedStride + kk] = e;
     }
   }
   const float rs = featured ? 1.f / se : 0.f;
-  // third pass: normalised weights -> reduction buffer (+ optional validation outputs)
-  for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
-    float v[32];
-    tc::tmem_ld32(tS + t_lane + c0, v);
-#pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const int kk = c0 + q;
-      const float s = v[q] * inv;
-      const float wgt = (kk < P.k && featured) ? expf(s * it - m) * rs : 0.f;
-      sRed[tid * kRedStride + kk] = wgt;
-      if (kk < P.k && valid) {
-        if (P.sims) P.sims[(int64_t)i * P.k + kk] = featured ? s : 0.f;
-        if (P.weights) P.weights[(int64_t)i * P.k + kk] = wgt;
+  srs[tid] = rs;
+  if (P.sims || P.weights) {  // validation outputs (uniform branch)
+    for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
+      float v[32];
+      tc::tmem_ld32(tS + t_lane + c0, v);
+      if (valid) {
+        for (int q = 0; q < 32 && c0 + q < P.k; ++q) {
+          if (P.sims) P.sims[(int64_t)i * P.k + c0 + q] = featured ? v[q] * inv : 0.f;
+          if (P.weights) P.weights[(int64_t)i * P.k + c0 + q] = sRed[tid * kRedStride + c0 + q] * rs;
+        }
       }
     }
   }
@@ -524,7 +579,7 @@ __global__ void __launch_bounds__(kTile, 2) k_tile_mma(TileParams P) {
       atomicAdd(P.grid_partials + P.cells3 + code, 1.0f);
     }
   }
-  // block partials: weight totals by column sums, scalars by warp + block reduction
+  // block partials: weight totals = column sums of e * rs, scalars by warp + block reduction
   float r6[6] = {pm, pm * p.x, pm * p.y, pm * p.z, featured ? 1.f : 0.f, (float)count};
 #pragma unroll
   for (int q = 0; q < 6; ++q) r6[q] = warp_sum(r6[q]);
@@ -536,12 +591,14 @@ __global__ void __launch_bounds__(kTile, 2) k_tile_mma(TileParams P) {
   float* out = P.tile_part + tile * (int64_t)(P.k + 6);
   for (int kk = tid; kk < P.k; kk += kTile) {
     float acc = 0.f;
-    for (int r = 0; r < kTile; ++r) acc += sRed[r * kRedStride + kk];
+#pragma unroll 8
+    for (int r = 0; r < kTile; ++r) acc = fmaf(sRed[r * kRedStride + kk], srs[r], acc);
     out[kk] = acc;
   }
   if (tid < 6) out[P.k + tid] = sred6[0][tid] + sred6[1][tid] + sred6[2][tid] + sred6[3][tid];
   if (warp == 0) tc::tmem_dealloc(tbase, ncols);
 }
+
 
 __global__ void k_tile_partials(const float* __restrict__ tile_part, int64_t ntiles, int ncol,
                                 double* __restrict__ partials) {
