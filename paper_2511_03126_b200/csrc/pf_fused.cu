@@ -427,9 +427,14 @@ static int kpl_of(int k) { return (k + 31) / 32; }
 // views, feature grids <= 255 per side and <= 128 padded materials.
 static bool tile_path_ok(const pf_fuse_args_t* a) {
   if (a->fmap_dtype != PF_BF16 || a->d % 128 != 0 || a->nviews > tile::kMaxViewsTC) return false;
-  if (32 * kpl_of(a->k) > tile::kMaxKpadTC || (a->flags & PF_FUSE_FORCE_SIMT)) return false;
-  for (int j = 0; j < a->nviews; ++j)
-    if (a->views_host[j].Hf > 255 || a->views_host[j].Wf > 255) return false;
+  if (((a->k + 63) / 64) * 64 > tile::kMaxKpadTC || (a->flags & PF_FUSE_FORCE_SIMT)) return false;
+  // uniform, contiguously packed views (the TMA tensor maps address them as one [V*Hf][Wf][D] block)
+  const pf_view_t& v0 = a->views_host[0];
+  if (v0.Hf > 255 || v0.Wf > 255) return false;
+  for (int j = 0; j < a->nviews; ++j) {
+    const pf_view_t& v = a->views_host[j];
+    if (v.Hf != v0.Hf || v.Wf != v0.Wf || v.fmap_offset != (int64_t)j * v0.Hf * v0.Wf * a->d) return false;
+  }
   return true;
 }
 
@@ -442,7 +447,7 @@ uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* a) {
   if (!a || !a->views_host || a->d <= 0 || a->k <= 0) return 0;
   uint64_t bytes = g_bytes(a);
   if (tile_path_ok(a))
-    bytes += tile::tile_layout(a->n, a->nviews, total_cells(a), 32 * kpl_of(a->k)).bytes;
+    bytes += tile::tile_layout(a->n, a->nviews, total_cells(a), ((a->k + 63) / 64) * 64).bytes;
   return bytes;
 }
 
@@ -517,7 +522,7 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
   const int d = a->d;
   if (tile_path_ok(a)) {
     const int64_t cells = total_cells(a);
-    const int kpadg = kpad;
+    const int kpadg = ((a->k + 63) / 64) * 64;  // S chunks are 64 columns wide
     unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
     const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg);
     tile::TileParams T{};
@@ -543,7 +548,9 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     uint32_t cols = 32;
     while (cols < (uint32_t)(128 + kpadg)) cols <<= 1;
     T.tmem_cols = cols;
-    if (int rc = tile::run_tile_path(T, L, ws, a->points, a->n, cells, G, kpad, st)) return rc;
+    if (int rc = tile::run_tile_path(T, L, ws, a->points, a->n, cells, G, kpad, a->views_host[0].Hf,
+                                     a->views_host[0].Wf, st))
+      return rc;
     // overflow tiles (more taps than fit in shared memory) run through the SIMT kernel
     prm.list = T.ovf_list;
     prm.list_len = T.ovf_count;

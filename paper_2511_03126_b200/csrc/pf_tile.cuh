@@ -77,7 +77,8 @@ struct TileLayout {
 TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg);
 size_t tile_smem_bytes();
 int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const float* points,
-                  int64_t n, int64_t cells, const float* G, int kpad, cudaStream_t st);
+                  int64_t n, int64_t cells, const float* G, int kpad, int hf, int wf, cudaStream_t st);
+int run_tile_ws(const TileParams& P, int hf, int wf, int nv, cudaStream_t st);
 
 }  // namespace tile
 }  // namespace pf

@@ -1,0 +1,474 @@
+// Persistent, warp-specialised tcgen05 tile kernel of the bf16 fused query (see pf_tile.cu for the
+// formulation). One CTA per SM loops over tiles of 128 sorted points; roles:
+//
+//   warp 0      TMA producer: for every 64-column chunk of a tile (D/64 feature chunks, then the
+//               G-table chunks) it loads each visible view's tap window — a (64 ch, w, h) box of the
+//               channel-last map — with one cp.async.bulk.tensor into a 4-stage ring of B buffers
+//               (N-major, 128-byte swizzle), completing on the stage's mbarrier (expect_tx);
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=64, K=16) over the
+//               tile's taps into a TMEM double buffer (feature chunks) or the S columns (G chunks);
+//               tcgen05.commit frees the B stage / A buffer and signals the accumulator;
+//   warps 2-5   accumulator warps: drain each feature chunk from TMEM (|F|^2, optional mean
+//               features), then the epilogue: softmax over K, property regression, voxel atomics,
+//               integrate partials accumulated in registers across all tiles of the CTA;
+//   warps 6-9   A builders: build the next tile's W (bilinear weights, bf16, K-major 128-B swizzle)
+//               in one of two A buffers while the current tile's MMAs run.
+// Synchronisation is mbarrier-only (full/empty pairs for A, B stages, TMEM D buffers and S).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <climits>
+#include <cstring>
+#include <mutex>
+
+#include "pf_common.cuh"
+#include "pf_tc.cuh"
+#include "pf_tile.cuh"
+#include "pf_tile_dev.cuh"
+
+namespace pf {
+namespace tile {
+namespace {
+
+constexpr int kWsThreads = 320;        // 10 warps
+constexpr int kStages = 4;             // B ring depth
+constexpr int kKtWs = 160;             // taps per tile held in one A buffer / B stage
+constexpr int kStageBytes = kKtWs * 128;
+constexpr int kABytes = kTile * kKtWs * 2;
+constexpr int kMaxBox = 4;             // TMA window boxes up to 4 x 4 cells
+
+struct TMaps {
+  CUtensorMap fm[kMaxBox * kMaxBox];
+  CUtensorMap g[kMaxBox * kMaxBox];
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+struct WsShared {
+  uint64_t a_full[2], a_empty[2];
+  uint64_t b_full[kStages], b_empty[kStages];
+  uint64_t d_full[2], d_empty[2];
+  uint64_t s_full, s_empty;
+  uint32_t tmem_base;
+  int pad;
+  uint2 desc_a[2][kMaxViewsTC];  // A builders' copy of the tile windows, per A buffer
+  ViewF sv[kMaxViewsTC];
+  float svals[kMaxKpadTC * 4];
+  float smt[kMaxKpadTC];
+  double red[kMaxKpadTC + 8];
+};
+
+__device__ __forceinline__ int tile_ktp(const TileParams& P, int64_t tile, bool& ok) {
+  const int kt = P.tile_kt[tile];
+  const int ktp = (kt + 15) & ~15;
+  ok = kt > 0 && ktp <= kKtWs;
+  return ktp;
+}
+
+__device__ __forceinline__ uint16_t f2bf16(float f) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+__global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant__ TileParams P,
+                                                           const __grid_constant__ TMaps M) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = smem;                     // 2 x [128 rows x kKtWs] bf16
+  unsigned char* sB = smem + 2 * kABytes;       // kStages x [kKtWs rows x 128 B]
+  __shared__ WsShared S;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nd = P.d >> 6, ns = P.kpadg >> 6, nch = nd + ns;
+  const int64_t ntiles = (P.n + kTile - 1) / kTile;
+
+  // ---- setup ------------------------------------------------------------------------------------------
+  for (int j = tid; j < P.nv; j += kWsThreads) S.sv[j] = make_viewf(P.views[j], P.d);
+  for (int j = tid; j < P.kpadg * 4; j += kWsThreads) {
+    const int kk = j >> 2, pp = j & 3;
+    S.svals[j] = (kk < P.k && pp < P.p) ? P.values[kk * P.p + pp] : 0.f;
+  }
+  for (int j = tid; j < P.kpadg; j += kWsThreads) S.smt[j] = j < P.k ? P.mid_theta[j] : 0.f;
+  for (int j = tid; j < kMaxKpadTC + 8; j += kWsThreads) S.red[j] = 0.0;
+  {  // B pad rows must hold finite values: zero every stage once
+    uint4* b4 = reinterpret_cast<uint4*>(sB);
+    for (int e = tid; e < kStages * kStageBytes / 16; e += kWsThreads) b4[e] = make_uint4(0, 0, 0, 0);
+  }
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&S.a_full[b], 128);
+      tc::mbar_init(&S.a_empty[b], 1);
+      tc::mbar_init(&S.d_full[b], 1);
+      tc::mbar_init(&S.d_empty[b], 128);
+    }
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&S.b_full[s], 1);
+      tc::mbar_init(&S.b_empty[s], 1);
+    }
+    tc::mbar_init(&S.s_full, 1);
+    tc::mbar_init(&S.s_empty, 128);
+  }
+  if (warp == 2) tc::tmem_alloc(&S.tmem_base, 256);
+  tc::fence_async_shared();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = S.tmem_base;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      bool ok;
+      tile_ktp(P, tile, ok);
+      if (!ok) continue;
+      const uint2* desc = P.tile_desc + tile * P.nv;
+      const uint2 d0 = lane < P.nv ? desc[lane] : make_uint2(0, 0);
+      const uint2 d1 = lane + 32 < P.nv ? desc[lane + 32] : make_uint2(0, 0);
+      const int kt = P.tile_kt[tile];
+      const int hf = S.sv[0].Hf;
+      for (int c = 0; c < nch; ++c) {
+        tc::mbar_wait(&S.b_empty[stage], phase ^ 1u);
+        if (lane == 0) mbar_expect_tx(&S.b_full[stage], (uint32_t)kt * 128u);
+        __syncwarp();
+        const uint32_t dst0 = tc::smem_u32(sB + stage * kStageBytes);
+        const int col = c < nd ? c * 64 : (c - nd) * 64;
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int v = lane + 32 * h2;
+          const uint2 ds = h2 ? d1 : d0;
+          const int w = ds.y & 0xff, h = (ds.y >> 8) & 0xff;
+          if (v < P.nv && w > 0) {
+            const int base = ds.x & 0xffff, x0 = (ds.x >> 16) & 0xff, y0 = ds.x >> 24;
+            const CUtensorMap* map = c < nd ? &M.fm[(h - 1) * kMaxBox + (w - 1)] : &M.g[(h - 1) * kMaxBox + (w - 1)];
+            tma_load_3d(dst0 + base * 128, map, col, x0, v * hf + y0, &S.b_full[stage]);
+          }
+        }
+        if (++stage == kStages) { stage = 0; phase ^= 1u; }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t dcount = 0;  // feature chunks issued so far (selects the TMEM D buffer)
+    uint32_t t_local = 0, s_phase = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      bool ok;
+      const int ktp = tile_ktp(P, tile, ok);
+      if (!ok) continue;
+      const int ab = t_local & 1;
+      tc::mbar_wait(&S.a_full[ab], (t_local >> 1) & 1u);
+      tc::fence_after_sync();
+      const uint32_t a0 = tc::smem_u32(sA + ab * kABytes);
+      const uint32_t idesc = tc::idesc_bf16_f32(128, 64, false, true);
+      for (int c = 0; c < nch; ++c) {
+        tc::mbar_wait(&S.b_full[stage], phase);
+        uint32_t dst;
+        int db = 0;
+        if (c < nd) {
+          db = dcount & 1;
+          tc::mbar_wait(&S.d_empty[db], ((dcount >> 1) & 1u) ^ 1u);
+          dst = tbase + (uint32_t)(db * 64);
+        } else {
+          if (c == nd) tc::mbar_wait(&S.s_empty, s_phase ^ 1u);
+          dst = tbase + 128u + (uint32_t)(64 * (c - nd));
+        }
+        tc::fence_after_sync();
+        if (lane == 0) {
+          const uint32_t b0 = tc::smem_u32(sB + stage * kStageBytes);
+          for (int s = 0; s < ktp / 16; ++s) {
+            const uint64_t ad = tc::smem_desc_sw128(a0 + (s >> 2) * kTile * 128 + (s & 3) * 32, 16, 1024);
+            const uint64_t bd = tc::smem_desc_sw128(b0 + s * 2048, kKtWs * 128, 1024);
+            tc::mma_bf16(dst, ad, bd, idesc, s > 0 ? 1u : 0u);
+          }
+          tc::mma_commit(&S.b_empty[stage]);
+          if (c < nd) tc::mma_commit(&S.d_full[db]);
+          if (c == nch - 1) {
+            tc::mma_commit(&S.s_full);
+            tc::mma_commit(&S.a_empty[ab]);
+          }
+        }
+        __syncwarp();
+        if (c < nd) ++dcount;
+        if (++stage == kStages) { stage = 0; phase ^= 1u; }
+      }
+      s_phase ^= 1u;
+      ++t_local;
+    }
+  } else if (warp >= 6) {
+    // ================= A builders (thread = tile row) =================
+    const int row = tid - 192;  // 0..127
+    uint32_t t_local = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      bool ok;
+      const int ktp = tile_ktp(P, tile, ok);
+      if (!ok) continue;
+      const int ab = t_local & 1;
+      tc::mbar_wait(&S.a_empty[ab], ((t_local >> 1) & 1u) ^ 1u);
+      uint2* sdesc = S.desc_a[ab];
+      for (int v = row; v < P.nv; v += 128) sdesc[v] = P.tile_desc[tile * P.nv + v];
+      unsigned char* A = sA + ab * kABytes;
+      uint4* a4 = reinterpret_cast<uint4*>(A);
+      for (int e = row; e < ((ktp + 63) >> 6) * kTile * 8; e += 128) a4[e] = make_uint4(0, 0, 0, 0);
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // builders only: zeros + windows visible
+      const int64_t jpt = tile * kTile + row;
+      if (jpt < P.n) {
+        const int32_t i = P.perm[jpt];
+        const float4 p = P.spts[jpt];
+        for (int w = 0; w < P.nwords; ++w) {
+          uint32_t bits = P.mask_bits[(int64_t)i * P.nwords + w];
+          while (bits) {
+            const int v = w * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            const ProjF q = project_f32(S.sv[v], p.x, p.y, p.z);
+            const TapF t = taps_f32(S.sv[v], q.u, q.v);
+            float w00 = (1.f - t.wy) * (1.f - t.wx), w01 = (1.f - t.wy) * t.wx;
+            float w10 = t.wy * (1.f - t.wx), w11 = t.wy * t.wx;
+            if (!t.dx) { w00 += w01; w10 += w11; }
+            if (!t.dy) { w00 += w10; w01 += w11; }
+            const uint2 ds = sdesc[v];
+            const int base = ds.x & 0xffff, x0 = (ds.x >> 16) & 0xff, y0 = ds.x >> 24;
+            const int ww = ds.y & 0xff;
+            const int c00 = base + (t.y0 - y0) * ww + (t.x0 - x0);
+            *reinterpret_cast<uint16_t*>(A + tc::a_off(row, c00, kTile)) = f2bf16(w00);
+            if (t.dx) *reinterpret_cast<uint16_t*>(A + tc::a_off(row, c00 + 1, kTile)) = f2bf16(w01);
+            if (t.dy) *reinterpret_cast<uint16_t*>(A + tc::a_off(row, c00 + ww, kTile)) = f2bf16(w10);
+            if (t.dx && t.dy) *reinterpret_cast<uint16_t*>(A + tc::a_off(row, c00 + ww + 1, kTile)) = f2bf16(w11);
+          }
+        }
+      }
+      tc::fence_async_shared();
+      mbar_arrive(&S.a_full[ab]);
+      ++t_local;
+    }
+  } else {
+    // ================= accumulator warps 2-5: drain + epilogue =================
+    const int row = 32 * (warp & 3) + lane;  // TMEM lane group of this warp
+    const uint32_t t_lane = (uint32_t)(32 * (warp & 3)) << 16;
+    const uint32_t tS = tbase + 128u;
+    uint32_t dcount = 0, s_phase = 0;
+    float wt[kMaxKpadTC / 32] = {0.f, 0.f, 0.f, 0.f};
+    double pm_sum = 0.0, pmx = 0.0, pmy = 0.0, pmz = 0.0, featured_n = 0.0, pairs = 0.0;
+    const float4* sv4 = reinterpret_cast<const float4*>(S.svals);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      bool ok;
+      tile_ktp(P, tile, ok);
+      const int64_t jpt = tile * kTile + row;
+      const bool valid = jpt < P.n;
+      const int32_t i = valid ? P.perm[jpt] : 0;
+      if (!ok) {
+        if (valid) P.ovf_list[atomicAdd(P.ovf_count, 1)] = i;
+        continue;
+      }
+      const int count = valid ? P.counts[i] : 0;
+      const float invc = count > 0 ? 1.f / (float)count : 0.f;
+      float ss = 0.f;
+      for (int c = 0; c < nd; ++c) {
+        const int db = dcount & 1;
+        tc::mbar_wait(&S.d_full[db], (dcount >> 1) & 1u);
+        tc::fence_after_sync();
+        const uint32_t tD = tbase + (uint32_t)(db * 64);
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(tD + t_lane + c0, v);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) ss = fmaf(v[q], v[q], ss);
+          if (P.features && valid) {
+            float* dst = P.features + (int64_t)i * P.d + c * 64 + c0;
+#pragma unroll
+            for (int q = 0; q < 32; q += 4)
+              *reinterpret_cast<float4*>(dst + q) =
+                  make_float4(v[q] * invc, v[q + 1] * invc, v[q + 2] * invc, v[q + 3] * invc);
+          }
+        }
+        tc::fence_before_sync();
+        mbar_arrive(&S.d_empty[db]);
+        ++dcount;
+      }
+      // ---- epilogue on S ------------------------------------------------------------------------------
+      tc::mbar_wait(&S.s_full, s_phase);
+      s_phase ^= 1u;
+      tc::fence_after_sync();
+      const bool featured = valid && count > 0;
+      const float inv = ss > 0.f ? 1.f / sqrtf(ss) : 0.f;
+      const float sc = inv * P.inv_temp * 1.4426950408889634f;
+      float m2 = -INFINITY;
+      bool nan = false;
+      for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
+        float v[32];
+        tc::tmem_ld32(tS + t_lane + c0, v);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const float x = v[q] * sc;
+          if (c0 + q < P.k) {
+            nan |= isnan(x);
+            m2 = fmaxf(m2, x);
+          }
+        }
+      }
+      if (featured && nan) atomicOr(P.status, 1);
+      float se = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f, pl3 = 0.f, pml = 0.f;
+      for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
+        float v[32];
+        tc::tmem_ld32(tS + t_lane + c0, v);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int kk = c0 + q;
+          const float e = kk < P.k ? exp2f(v[q] * sc - m2) : 0.f;
+          se += e;
+          const float4 y = sv4[kk];
+          pl0 = fmaf(e, y.x, pl0);
+          pl1 = fmaf(e, y.y, pl1);
+          pl2 = fmaf(e, y.z, pl2);
+          pl3 = fmaf(e, y.w, pl3);
+          pml = fmaf(e, S.smt[kk], pml);
+        }
+      }
+      const float rs = featured ? 1.f / se : 0.f;
+      // third pass: normalised weights -> column sums across the warp (butterfly) -> wt registers
+#pragma unroll
+      for (int g = 0; g < kMaxKpadTC / 32; ++g) {
+        if (g * 32 < P.kpadg) {
+          float v[32];
+          tc::tmem_ld32(tS + t_lane + g * 32, v);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const int kk = g * 32 + q;
+            const float s = v[q] * inv;
+            const float wgt = (kk < P.k && featured) ? exp2f(v[q] * sc - m2) * rs : 0.f;
+            if (valid && kk < P.k) {
+              if (P.sims) P.sims[(int64_t)i * P.k + kk] = featured ? s : 0.f;
+              if (P.weights) P.weights[(int64_t)i * P.k + kk] = wgt;
+            }
+            v[q] = wgt;
+          }
+          // reduce-scatter: after 5 steps lane l holds the warp's sum of column g*32 + l
+#pragma unroll
+          for (int half = 16; half >= 1; half >>= 1) {
+            const bool upper = (lane & half) != 0;
+#pragma unroll
+            for (int q = 0; q < half; ++q) {
+              const float send = upper ? v[q] : v[q + half];
+              const float keep = upper ? v[q + half] : v[q];
+              v[q] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+            }
+          }
+          wt[g] += v[0];
+        }
+      }
+      tc::fence_before_sync();
+      mbar_arrive(&S.s_empty);
+      const float prop[4] = {pl0 * rs, pl1 * rs, pl2 * rs, pl3 * rs};
+      const float pm = pml * rs;
+      if (valid) {
+        const float4 p = P.spts[jpt];
+        for (int pp = 0; pp < P.p; ++pp) P.props[(int64_t)i * P.p + pp] = prop[pp];
+        if (P.grid_partials) {
+          const int32_t code = P.codes[i];
+          float rho = prop[0];
+#pragma unroll
+          for (int pp = 1; pp < 4; ++pp) rho = P.density_col == pp ? prop[pp] : rho;
+          atomicAdd(P.grid_partials + code, rho);
+          atomicAdd(P.grid_partials + P.cells3 + code, 1.0f);
+        }
+        pm_sum += pm;
+        pmx += (double)pm * p.x;
+        pmy += (double)pm * p.y;
+        pmz += (double)pm * p.z;
+        featured_n += featured ? 1.0 : 0.0;
+        pairs += count;
+      }
+    }
+    // flush this CTA's partials (integrate.py:133-155) once
+#pragma unroll
+    for (int g = 0; g < kMaxKpadTC / 32; ++g)
+      if (g * 32 + lane < P.k) atomicAdd(&S.red[g * 32 + lane], (double)wt[g]);
+    double r6[6] = {pm_sum, pmx, pmy, pmz, featured_n, pairs};
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      r6[q] = warp_sum(r6[q]);
+      if (lane == 0) atomicAdd(&S.red[P.k + q], r6[q]);
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    for (int j = row; j < P.k + 6; j += 128)
+      if (S.red[j] != 0.0) atomicAdd(P.partials + j, S.red[j]);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 2) tc::tmem_dealloc(tbase, 256);
+}
+
+// ---- host: tensor maps --------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool encode_window_map(CUtensorMap* m, const void* base, int cols, int wf, int rows_total, int bw, int bh) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)wf, (cuuint64_t)rows_total};
+  const cuuint64_t strides[2] = {(cuuint64_t)cols * 2, (cuuint64_t)cols * 2 * wf};
+  const cuuint32_t box[3] = {64u, (cuuint32_t)bw, (cuuint32_t)bh};
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+int ws_kt_max() { return kKtWs; }
+
+size_t ws_smem_bytes() { return 2 * (size_t)kABytes + (size_t)kStages * kStageBytes + 1024; }
+
+// Launch the persistent kernel; returns PF_OK, or -1 when TMA maps cannot be built (caller falls
+// back to k_tile_mma).
+int run_tile_ws(const TileParams& P, int hf, int wf, int nv, cudaStream_t st) {
+  if (!encode_fn()) return -1;
+  if (P.kpadg % 64 != 0) return -1;
+  TMaps M;
+  std::memset(&M, 0, sizeof(M));
+  for (int h = 1; h <= kMaxBox; ++h)
+    for (int w = 1; w <= kMaxBox; ++w) {
+      if (!encode_window_map(&M.fm[(h - 1) * kMaxBox + (w - 1)], P.fmap, P.d, wf, hf * nv, w, h)) return -1;
+      if (!encode_window_map(&M.g[(h - 1) * kMaxBox + (w - 1)], P.Gbf, P.kpadg, wf, hf * nv, w, h)) return -1;
+    }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = ws_smem_bytes();
+  cudaFuncSetAttribute(k_tile_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t ntiles = (P.n + kTile - 1) / kTile;
+  const int grid = (int)(ntiles < sms ? ntiles : sms);
+  k_tile_ws<<<grid, kWsThreads, smem, st>>>(P, M);
+  return check_launch("tile_ws");
+}
+
+}  // namespace tile
+}  // namespace pf
