@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -34,7 +35,7 @@ constexpr int kWsThreads = 320;        // 10 warps
 constexpr int kStages = 4;             // B ring depth
 constexpr int kKtWs = 160;             // taps per tile held in one A buffer / B stage
 constexpr int kStageBytes = kKtWs * 128;
-constexpr int kABytes = kTile * kKtWs * 2;
+constexpr int kABytes = kTile * ((kKtWs + 63) / 64) * 64 * 2;  // whole 64-column swizzle atoms
 constexpr int kMaxBox = 4;             // TMA window boxes up to 4 x 4 cells
 
 struct TMaps {
@@ -67,7 +68,7 @@ struct WsShared {
   int pad;
   uint2 desc_a[2][kMaxViewsTC];  // A builders' copy of the tile windows, per A buffer
   ViewF sv[kMaxViewsTC];
-  float svals[kMaxKpadTC * 4];
+  alignas(16) float svals[kMaxKpadTC * 4];  // read as float4
   float smt[kMaxKpadTC];
   double red[kMaxKpadTC + 8];
 };
@@ -83,8 +84,9 @@ __device__ __forceinline__ uint16_t f2bf16(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
 
-__global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant__ TileParams P,
-                                                           const __grid_constant__ TMaps M) {
+// the tensor maps come first: TMA needs them 64-byte aligned in the parameter space
+__global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant__ TMaps M,
+                                                           const __grid_constant__ TileParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -465,10 +467,50 @@ int run_tile_ws(const TileParams& P, int hf, int wf, int nv, cudaStream_t st) {
   const size_t smem = ws_smem_bytes();
   cudaFuncSetAttribute(k_tile_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = (P.n + kTile - 1) / kTile;
-  const int grid = (int)(ntiles < sms ? ntiles : sms);
-  k_tile_ws<<<grid, kWsThreads, smem, st>>>(P, M);
+  int grid = (int)(ntiles < sms ? ntiles : sms);
+  if (const char* g = getenv("PF_WS_GRID")) grid = (int)(ntiles < atoi(g) ? ntiles : atoi(g));  // debug knob
+  k_tile_ws<<<grid, kWsThreads, smem, st>>>(M, P);
   return check_launch("tile_ws");
 }
 
 }  // namespace tile
 }  // namespace pf
+
+// ---- diagnostic: TMA window load at an arbitrary 128-byte row offset ---------------------------------
+namespace pf {
+namespace tile {
+namespace {
+__global__ void k_tma_selftest(const __grid_constant__ CUtensorMap map, int x0, int y0, int row_off,
+                               int rows, uint16_t* __restrict__ out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, (uint32_t)rows * 128u);
+    tma_load_3d(tc::smem_u32(smem) + row_off * 128, &map, 0, x0, y0, &bar);
+  }
+  __syncthreads();
+  tc::mbar_wait(&bar, 0);
+  // un-swizzle by the absolute-address rule (chunk c of row r stored at chunk c ^ (r & 7))
+  for (int e = threadIdx.x; e < rows * 64; e += blockDim.x) {
+    const int r = row_off + e / 64, n = e % 64;
+    const uint32_t off = r * 128 + ((((n >> 3) ^ (r & 7)) & 7) << 4) + (n & 7) * 2;
+    out[e] = *reinterpret_cast<const uint16_t*>(smem + off);
+  }
+}
+}  // namespace
+}  // namespace tile
+}  // namespace pf
+
+extern "C" int pf_selftest_tma(const void* src_bf16, int32_t hf, int32_t wf, int32_t x0, int32_t y0,
+                               int32_t bw, int32_t bh, int32_t row_off, void* out, void* stream) {
+  using namespace pf::tile;
+  CUtensorMap m;
+  if (!encode_window_map(&m, src_bf16, 64, wf, hf, bw, bh))
+    return pf::set_error(PF_ERR_CUDA, "selftest_tma: tensor map encode failed");
+  k_tma_selftest<<<1, 128, 8 * 1024 + 1024, reinterpret_cast<cudaStream_t>(stream)>>>(
+      m, x0, y0, row_off, bw * bh, reinterpret_cast<uint16_t*>(out));
+  return pf::check_launch("selftest_tma");
+}
