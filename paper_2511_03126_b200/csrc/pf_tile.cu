@@ -207,7 +207,6 @@ __global__ void __launch_bounds__(kTile) k_tile_prep(TileParams P) {
   __syncthreads();
   if (tid == 0) {
     int base = 0;
-    bool big = false;  // a window wider than the 4x4 TMA boxes -> SIMT overflow
     uint2* desc = P.tile_desc + tile * P.nv;
     for (int v = 0; v < P.nv; ++v) {
       int w = 0, h = 0;
@@ -219,9 +218,9 @@ __global__ void __launch_bounds__(kTile) k_tile_prep(TileParams P) {
       desc[v] = make_uint2((uint32_t)min(base, 65535) | ((uint32_t)x0 << 16) | ((uint32_t)y0 << 24),
                            (uint32_t)w | ((uint32_t)h << 8));
       base += w * h;
-      big |= w > 4 || h > 4;
+
     }
-    P.tile_kt[tile] = big ? base + (1 << 20) : base;
+    P.tile_kt[tile] = base;
   }
 }
 

@@ -1,17 +1,20 @@
 // Persistent, warp-specialised tcgen05 tile kernel of the bf16 fused query (see pf_tile.cu for the
-// formulation). One CTA per SM loops over tiles of 128 sorted points; roles:
+// formulation). One CTA per SM loops over tiles of 128 sorted points; roles (13 warps):
 //
-//   warp 0      TMA producer: for every 64-column chunk of a tile (D/64 feature chunks, then the
-//               G-table chunks) it loads each visible view's tap window — a (64 ch, w, h) box of the
-//               channel-last map — with one cp.async.bulk.tensor into a 4-stage ring of B buffers
-//               (N-major, 128-byte swizzle), completing on the stage's mbarrier (expect_tx);
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=64, K=16) over the
+//   warps 0-3   B loaders: for every 64-channel chunk of a tile (D/64 feature chunks, then the
+//               G-table chunks) they copy each tap's 128-byte row piece with cp.async (16 B per
+//               lane op, 8 lanes per row) into a 4-stage ring of B buffers (N-major, 128-byte
+//               swizzle), keeping three chunks in flight; after cp.async.wait_group the writer
+//               fences the generic->async proxy and arrives on the stage's full barrier.
+//               (Per-window TMA boxes were measured first: ~460 tiny TMA ops per tile made the TMA
+//               unit the bottleneck, profiles/r01_notes.md.)
+//   warp 4      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=64, K=16) over the
 //               tile's taps into a TMEM double buffer (feature chunks) or the S columns (G chunks);
-//               tcgen05.commit frees the B stage / A buffer and signals the accumulator;
-//   warps 2-5   accumulator warps: drain each feature chunk from TMEM (|F|^2, optional mean
+//               tcgen05.commit frees the B stage / A buffer and signals the accumulators;
+//   warps 5-8   accumulator warps: drain each feature chunk from TMEM (|F|^2, optional mean
 //               features), then the epilogue: softmax over K, property regression, voxel atomics,
 //               integrate partials accumulated in registers across all tiles of the CTA;
-//   warps 6-9   A builders: build the next tile's W (bilinear weights, bf16, K-major 128-B swizzle)
+//   warps 9-12  A builders: build the next tile's W (bilinear weights, bf16, K-major 128-B swizzle)
 //               in one of two A buffers while the current tile's MMAs run.
 // Synchronisation is mbarrier-only (full/empty pairs for A, B stages, TMEM D buffers and S).
 #include <cuda.h>
@@ -31,9 +34,9 @@ namespace pf {
 namespace tile {
 namespace {
 
-constexpr int kWsThreads = 320;        // 10 warps
+constexpr int kWsThreads = 416;        // 13 warps
 constexpr int kStages = 4;             // B ring depth
-constexpr int kKtWs = 160;             // taps per tile held in one A buffer / B stage
+constexpr int kKtWs = 192;             // taps per tile held in one A buffer / B stage
 constexpr int kStageBytes = kKtWs * 128;
 constexpr int kABytes = kTile * ((kKtWs + 63) / 64) * 64 * 2;  // whole 64-column swizzle atoms
 constexpr int kMaxBox = 4;             // TMA window boxes up to 4 x 4 cells
@@ -67,6 +70,7 @@ struct WsShared {
   uint32_t tmem_base;
   int pad;
   uint2 desc_a[2][kMaxViewsTC];  // A builders' copy of the tile windows, per A buffer
+  int32_t cell[2][kKtWs];        // loaders: tap row -> global cell, per tile (ring of 2)
   ViewF sv[kMaxViewsTC];
   alignas(16) float svals[kMaxKpadTC * 4];  // read as float4
   float smt[kMaxKpadTC];
@@ -84,9 +88,7 @@ __device__ __forceinline__ uint16_t f2bf16(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
 
-// the tensor maps come first: TMA needs them 64-byte aligned in the parameter space
-__global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant__ TMaps M,
-                                                           const __grid_constant__ TileParams P) {
+__global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant__ TileParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -106,10 +108,6 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   }
   for (int j = tid; j < P.kpadg; j += kWsThreads) S.smt[j] = j < P.k ? P.mid_theta[j] : 0.f;
   for (int j = tid; j < kMaxKpadTC + 8; j += kWsThreads) S.red[j] = 0.0;
-  {  // B pad rows must hold finite values: zero every stage once
-    uint4* b4 = reinterpret_cast<uint4*>(sB);
-    for (int e = tid; e < kStages * kStageBytes / 16; e += kWsThreads) b4[e] = make_uint4(0, 0, 0, 0);
-  }
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.a_full[b], 128);
@@ -118,67 +116,91 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       tc::mbar_init(&S.d_empty[b], 128);
     }
     for (int s = 0; s < kStages; ++s) {
-      tc::mbar_init(&S.b_full[s], 1);
+      tc::mbar_init(&S.b_full[s], 128);
       tc::mbar_init(&S.b_empty[s], 1);
     }
     tc::mbar_init(&S.s_full, 1);
     tc::mbar_init(&S.s_empty, 128);
   }
-  if (warp == 2) tc::tmem_alloc(&S.tmem_base, 256);
-  tc::fence_async_shared();
+  if (warp == 5) tc::tmem_alloc(&S.tmem_base, 256);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = S.tmem_base;
 
-  if (warp == 0) {
-    // ================= TMA producer =================
+  if (warp < 4) {
+    // ================= B loaders (128 threads) =================
+    // thread -> 16-byte column q of every row r = r0, r0 + 16, ...; pad rows repeat row 0's cell
+    const int q = tid & 7, r0 = tid >> 3;
     int stage = 0;
     uint32_t phase = 0;
+    int pending[3];  // stages whose cp.async groups are still in flight (oldest first)
+    int npend = 0;
+    uint32_t t_local = 0;
+    auto retire_oldest = [&](int keep) {
+      if (keep == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+      else if (keep == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      tc::fence_async_shared();
+      mbar_arrive(&S.b_full[pending[0]]);
+      pending[0] = pending[1];
+      pending[1] = pending[2];
+      --npend;
+    };
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       bool ok;
-      tile_ktp(P, tile, ok);
+      const int ktp = tile_ktp(P, tile, ok);
       if (!ok) continue;
-      const uint2* desc = P.tile_desc + tile * P.nv;
-      const uint2 d0 = lane < P.nv ? desc[lane] : make_uint2(0, 0);
-      const uint2 d1 = lane + 32 < P.nv ? desc[lane + 32] : make_uint2(0, 0);
+      // row -> cell table for this tile (ring of 2: at most one older tile is still being loaded)
+      int32_t* cell = S.cell[t_local & 1];
+      asm volatile("bar.sync 3, 128;" ::: "memory");  // previous users of this slot are done
+      if (tid < P.nv) {
+        const uint2 ds = P.tile_desc[tile * P.nv + tid];
+        const int base = ds.x & 0xffff, x0 = (ds.x >> 16) & 0xff, y0 = ds.x >> 24;
+        const int w = ds.y & 0xff, h = (ds.y >> 8) & 0xff;
+        const ViewF& vw = S.sv[tid];
+        for (int a = 0; a < w * h; ++a) cell[base + a] = vw.cell_base + (y0 + a / w) * vw.Wf + x0 + a % w;
+      }
+      asm volatile("bar.sync 3, 128;" ::: "memory");
       const int kt = P.tile_kt[tile];
-      const int hf = S.sv[0].Hf;
+      for (int r = kt + tid; r < ktp; r += 128) cell[r] = cell[0];
+      asm volatile("bar.sync 3, 128;" ::: "memory");
       for (int c = 0; c < nch; ++c) {
         tc::mbar_wait(&S.b_empty[stage], phase ^ 1u);
-        if (lane == 0) mbar_expect_tx(&S.b_full[stage], (uint32_t)kt * 128u);
-        __syncwarp();
-        const uint32_t dst0 = tc::smem_u32(sB + stage * kStageBytes);
-        const int col = c < nd ? c * 64 : (c - nd) * 64;
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int v = lane + 32 * h2;
-          const uint2 ds = h2 ? d1 : d0;
-          const int w = ds.y & 0xff, h = (ds.y >> 8) & 0xff;
-          if (v < P.nv && w > 0) {
-            const int base = ds.x & 0xffff, x0 = (ds.x >> 16) & 0xff, y0 = ds.x >> 24;
-            const CUtensorMap* map = c < nd ? &M.fm[(h - 1) * kMaxBox + (w - 1)] : &M.g[(h - 1) * kMaxBox + (w - 1)];
-            tma_load_3d(dst0 + base * 128, map, col, x0, v * hf + y0, &S.b_full[stage]);
-          }
+        const uint32_t sb = tc::smem_u32(sB + stage * kStageBytes);
+        const uint16_t* src;
+        int64_t rowlen;
+        if (c < nd) {
+          src = reinterpret_cast<const uint16_t*>(P.fmap) + c * 64 + q * 8;
+          rowlen = P.d;
+        } else {
+          src = P.Gbf + (c - nd) * 64 + q * 8;
+          rowlen = P.kpadg;
         }
+        for (int r = r0; r < ktp; r += 16)
+          tc::cp_async16(sb + tc::b_chunk_off(r, q, kKtWs), src + (int64_t)cell[r] * rowlen);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        pending[npend++] = stage;
+        if (npend == 3) retire_oldest(2);
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
       }
+      ++t_local;
     }
-  } else if (warp == 1) {
+    while (npend > 0) retire_oldest(npend - 1);
+  } else if (warp == 4) {
     // ================= MMA issuer =================
     int stage = 0;
     uint32_t phase = 0;
     uint32_t dcount = 0;  // feature chunks issued so far (selects the TMEM D buffer)
     uint32_t t_local = 0, s_phase = 0;
+    const uint32_t idesc = tc::idesc_bf16_f32(128, 64, false, true);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       bool ok;
       const int ktp = tile_ktp(P, tile, ok);
       if (!ok) continue;
       const int ab = t_local & 1;
       tc::mbar_wait(&S.a_full[ab], (t_local >> 1) & 1u);
-      tc::fence_after_sync();
       const uint32_t a0 = tc::smem_u32(sA + ab * kABytes);
-      const uint32_t idesc = tc::idesc_bf16_f32(128, 64, false, true);
       for (int c = 0; c < nch; ++c) {
         tc::mbar_wait(&S.b_full[stage], phase);
         uint32_t dst;
@@ -193,6 +215,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         }
         tc::fence_after_sync();
         if (lane == 0) {
+          tc::fence_async_shared();
           const uint32_t b0 = tc::smem_u32(sB + stage * kStageBytes);
           for (int s = 0; s < ktp / 16; ++s) {
             const uint64_t ad = tc::smem_desc_sw128(a0 + (s >> 2) * kTile * 128 + (s & 3) * 32, 16, 1024);
@@ -213,9 +236,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       s_phase ^= 1u;
       ++t_local;
     }
-  } else if (warp >= 6) {
+  } else if (warp >= 9) {
     // ================= A builders (thread = tile row) =================
-    const int row = tid - 192;  // 0..127
+    const int row = tid - 288;  // 0..127
     uint32_t t_local = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       bool ok;
@@ -260,7 +283,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       ++t_local;
     }
   } else {
-    // ================= accumulator warps 2-5: drain + epilogue =================
+    // ================= accumulator warps 5-8: drain + epilogue =================
     const int row = 32 * (warp & 3) + lane;  // TMEM lane group of this warp
     const uint32_t t_lane = (uint32_t)(32 * (warp & 3)) << 16;
     const uint32_t tS = tbase + 128u;
@@ -268,6 +291,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     float wt[kMaxKpadTC / 32] = {0.f, 0.f, 0.f, 0.f};
     double pm_sum = 0.0, pmx = 0.0, pmy = 0.0, pmz = 0.0, featured_n = 0.0, pairs = 0.0;
     const float4* sv4 = reinterpret_cast<const float4*>(S.svals);
+    const bool outs = P.sims || P.weights;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       bool ok;
       tile_ktp(P, tile, ok);
@@ -280,30 +304,41 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       }
       const int count = valid ? P.counts[i] : 0;
       const float invc = count > 0 ? 1.f / (float)count : 0.f;
-      float ss = 0.f;
+      float ss0 = 0.f, ss1 = 0.f, ss2 = 0.f, ss3 = 0.f;
       for (int c = 0; c < nd; ++c) {
         const int db = dcount & 1;
         tc::mbar_wait(&S.d_full[db], (dcount >> 1) & 1u);
         tc::fence_after_sync();
         const uint32_t tD = tbase + (uint32_t)(db * 64);
+        float v[32], u[32];
+        tc::tmem_ld32(tD + t_lane, v);
+        tc::tmem_ld32(tD + t_lane + 32, u);
+        tc::fence_before_sync();
+        mbar_arrive(&S.d_empty[db]);  // data is in registers: release the buffer early
 #pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          float v[32];
-          tc::tmem_ld32(tD + t_lane + c0, v);
+        for (int q = 0; q < 32; q += 4) {
+          ss0 = fmaf(v[q], v[q], ss0);
+          ss1 = fmaf(v[q + 1], v[q + 1], ss1);
+          ss2 = fmaf(v[q + 2], v[q + 2], ss2);
+          ss3 = fmaf(v[q + 3], v[q + 3], ss3);
+          ss0 = fmaf(u[q], u[q], ss0);
+          ss1 = fmaf(u[q + 1], u[q + 1], ss1);
+          ss2 = fmaf(u[q + 2], u[q + 2], ss2);
+          ss3 = fmaf(u[q + 3], u[q + 3], ss3);
+        }
+        if (P.features && valid) {
+          float* dst = P.features + (int64_t)i * P.d + c * 64;
 #pragma unroll
-          for (int q = 0; q < 32; ++q) ss = fmaf(v[q], v[q], ss);
-          if (P.features && valid) {
-            float* dst = P.features + (int64_t)i * P.d + c * 64 + c0;
-#pragma unroll
-            for (int q = 0; q < 32; q += 4)
-              *reinterpret_cast<float4*>(dst + q) =
-                  make_float4(v[q] * invc, v[q + 1] * invc, v[q + 2] * invc, v[q + 3] * invc);
+          for (int q = 0; q < 32; q += 4) {
+            *reinterpret_cast<float4*>(dst + q) =
+                make_float4(v[q] * invc, v[q + 1] * invc, v[q + 2] * invc, v[q + 3] * invc);
+            *reinterpret_cast<float4*>(dst + 32 + q) =
+                make_float4(u[q] * invc, u[q + 1] * invc, u[q + 2] * invc, u[q + 3] * invc);
           }
         }
-        tc::fence_before_sync();
-        mbar_arrive(&S.d_empty[db]);
         ++dcount;
       }
+      const float ss = (ss0 + ss1) + (ss2 + ss3);
       // ---- epilogue on S ------------------------------------------------------------------------------
       tc::mbar_wait(&S.s_full, s_phase);
       s_phase ^= 1u;
@@ -311,21 +346,27 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const bool featured = valid && count > 0;
       const float inv = ss > 0.f ? 1.f / sqrtf(ss) : 0.f;
       const float sc = inv * P.inv_temp * 1.4426950408889634f;
-      float m2 = -INFINITY;
+      float m2a = -INFINITY, m2b = -INFINITY;
       bool nan = false;
       for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
         float v[32];
         tc::tmem_ld32(tS + t_lane + c0, v);
+        if (c0 + 32 <= P.k) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const float x = v[q] * sc;
-          if (c0 + q < P.k) {
-            nan |= isnan(x);
-            m2 = fmaxf(m2, x);
+          for (int q = 0; q < 32; q += 2) {
+            m2a = fmaxf(m2a, v[q] * sc);
+            m2b = fmaxf(m2b, v[q + 1] * sc);
+            nan |= isnan(v[q]) | isnan(v[q + 1]);
+          }
+        } else {
+          for (int q = 0; c0 + q < P.k; ++q) {
+            m2a = fmaxf(m2a, v[q] * sc);
+            nan |= isnan(v[q]);
           }
         }
       }
-      if (featured && nan) atomicOr(P.status, 1);
+      const float m2 = fmaxf(m2a, m2b);
+      if (featured && (nan || isnan(sc))) atomicOr(P.status, 1);
       float se = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f, pl3 = 0.f, pml = 0.f;
       for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
         float v[32];
@@ -350,16 +391,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         if (g * 32 < P.kpadg) {
           float v[32];
           tc::tmem_ld32(tS + t_lane + g * 32, v);
+          if (outs && valid) {
+            for (int q = 0; q < 32 && g * 32 + q < P.k; ++q) {
+              const int kk = g * 32 + q;
+              if (P.sims) P.sims[(int64_t)i * P.k + kk] = featured ? v[q] * inv : 0.f;
+              if (P.weights) P.weights[(int64_t)i * P.k + kk] = featured ? exp2f(v[q] * sc - m2) * rs : 0.f;
+            }
+          }
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
             const int kk = g * 32 + q;
-            const float s = v[q] * inv;
-            const float wgt = (kk < P.k && featured) ? exp2f(v[q] * sc - m2) * rs : 0.f;
-            if (valid && kk < P.k) {
-              if (P.sims) P.sims[(int64_t)i * P.k + kk] = featured ? s : 0.f;
-              if (P.weights) P.weights[(int64_t)i * P.k + kk] = wgt;
-            }
-            v[q] = wgt;
+            v[q] = (kk < P.k && featured) ? exp2f(v[q] * sc - m2) * rs : 0.f;
           }
           // reduce-scatter: after 5 steps lane l holds the warp's sum of column g*32 + l
 #pragma unroll
@@ -414,7 +456,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 2) tc::tmem_dealloc(tbase, 256);
+  if (warp == 5) tc::tmem_dealloc(tbase, 256);
 }
 
 // ---- host: tensor maps --------------------------------------------------------------------------------
@@ -449,18 +491,12 @@ int ws_kt_max() { return kKtWs; }
 
 size_t ws_smem_bytes() { return 2 * (size_t)kABytes + (size_t)kStages * kStageBytes + 1024; }
 
-// Launch the persistent kernel; returns PF_OK, or -1 when TMA maps cannot be built (caller falls
-// back to k_tile_mma).
+// Launch the persistent kernel (one CTA per SM).
 int run_tile_ws(const TileParams& P, int hf, int wf, int nv, cudaStream_t st) {
-  if (!encode_fn()) return -1;
+  (void)hf;
+  (void)wf;
+  (void)nv;
   if (P.kpadg % 64 != 0) return -1;
-  TMaps M;
-  std::memset(&M, 0, sizeof(M));
-  for (int h = 1; h <= kMaxBox; ++h)
-    for (int w = 1; w <= kMaxBox; ++w) {
-      if (!encode_window_map(&M.fm[(h - 1) * kMaxBox + (w - 1)], P.fmap, P.d, wf, hf * nv, w, h)) return -1;
-      if (!encode_window_map(&M.g[(h - 1) * kMaxBox + (w - 1)], P.Gbf, P.kpadg, wf, hf * nv, w, h)) return -1;
-    }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -469,7 +505,7 @@ int run_tile_ws(const TileParams& P, int hf, int wf, int nv, cudaStream_t st) {
   const int64_t ntiles = (P.n + kTile - 1) / kTile;
   int grid = (int)(ntiles < sms ? ntiles : sms);
   if (const char* g = getenv("PF_WS_GRID")) grid = (int)(ntiles < atoi(g) ? ntiles : atoi(g));  // debug knob
-  k_tile_ws<<<grid, kWsThreads, smem, st>>>(M, P);
+  k_tile_ws<<<grid, kWsThreads, smem, st>>>(P);
   return check_launch("tile_ws");
 }
 
