@@ -65,6 +65,7 @@ struct TileParams {
   float* tile_part;
   int32_t* ovf_list;
   int32_t* ovf_count;
+  unsigned long long* dbg;  // optional per-CTA wait-cycle counters (PF_WS_DEBUG)
   double* partials;
   uint32_t tmem_cols;
 };

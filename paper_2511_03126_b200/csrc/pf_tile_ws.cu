@@ -1,26 +1,27 @@
 // Persistent, warp-specialised tcgen05 tile kernel of the bf16 fused query (see pf_tile.cu for the
-// formulation). One CTA per SM loops over tiles of 128 sorted points; roles (13 warps):
+// formulation). One CTA per SM loops over tiles of 128 sorted points; roles (15 warps):
 //
-//   warps 0-3   B loaders: for every 64-channel chunk of a tile (D/64 feature chunks, then the
+//   warps 0-1   B loaders: for every 64-channel chunk of a tile (D/64 feature chunks, then the
 //               G-table chunks) they copy each tap's 128-byte row piece with cp.async (16 B per
 //               lane op, 8 lanes per row) into a 4-stage ring of B buffers (N-major, 128-byte
 //               swizzle), keeping three chunks in flight; after cp.async.wait_group the writer
 //               fences the generic->async proxy and arrives on the stage's full barrier.
 //               (Per-window TMA boxes were measured first: ~460 tiny TMA ops per tile made the TMA
 //               unit the bottleneck, profiles/r01_notes.md.)
-//   warp 4      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=64, K=16) over the
-//               tile's taps into a TMEM double buffer (feature chunks) or the S columns (G chunks);
+//   warp 2      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=64, K=16) over the
+//               tile's taps into 4 TMEM buffers (feature chunks) or the S columns (G chunks);
 //               tcgen05.commit frees the B stage / A buffer and signals the accumulators;
-//   warps 5-8   accumulator warps: drain each feature chunk from TMEM (|F|^2, optional mean
+//   warps 3-10  accumulator warps (two per TMEM lane group, each half of the columns): drain each feature chunk from TMEM (|F|^2, optional mean
 //               features), then the epilogue: softmax over K, property regression, voxel atomics,
 //               integrate partials accumulated in registers across all tiles of the CTA;
-//   warps 9-12  A builders: build the next tile's W (bilinear weights, bf16, K-major 128-B swizzle)
+//   warps 11-14 A builders: build the next tile's W (bilinear weights, bf16, K-major 128-B swizzle)
 //               in one of two A buffers while the current tile's MMAs run.
 // Synchronisation is mbarrier-only (full/empty pairs for A, B stages, TMEM D buffers and S).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -34,7 +35,14 @@ namespace pf {
 namespace tile {
 namespace {
 
-constexpr int kWsThreads = 416;        // 13 warps
+constexpr int kLoadWarps = 2;          // warps 0-1: B loaders
+constexpr int kLoadThreads = 32 * kLoadWarps;
+constexpr int kMmaWarp = 2;            // warp 2: MMA issuer
+constexpr int kAccWarp0 = 3;           // warps 3-10: accumulators (2 per TMEM lane group)
+constexpr int kAccThreads = 256;
+constexpr int kBuildWarp0 = 11;        // warps 11-14: A builders
+constexpr int kWsThreads = 480;        // 15 warps
+constexpr int kDBufs = 4;              // TMEM feature-chunk buffers (64 columns each)
 constexpr int kStages = 4;             // B ring depth
 constexpr int kKtWs = 192;             // taps per tile held in one A buffer / B stage
 constexpr int kStageBytes = kKtWs * 128;
@@ -65,7 +73,7 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 struct WsShared {
   uint64_t a_full[2], a_empty[2];
   uint64_t b_full[kStages], b_empty[kStages];
-  uint64_t d_full[2], d_empty[2];
+  uint64_t d_full[kDBufs], d_empty[kDBufs];
   uint64_t s_full, s_empty;
   uint32_t tmem_base;
   int pad;
@@ -74,6 +82,9 @@ struct WsShared {
   ViewF sv[kMaxViewsTC];
   alignas(16) float svals[kMaxKpadTC * 4];  // read as float4
   float smt[kMaxKpadTC];
+  float xss[2][kTile];           // accumulator halves: partial |F|^2
+  float xm[2][kTile];            //                     partial max
+  float xsum[2][6][kTile];       //                     partial softmax sums
   double red[kMaxKpadTC + 8];
 };
 
@@ -88,6 +99,12 @@ __device__ __forceinline__ uint16_t f2bf16(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant__ TileParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -99,6 +116,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nd = P.d >> 6, ns = P.kpadg >> 6, nch = nd + ns;
   const int64_t ntiles = (P.n + kTile - 1) / kTile;
+  long long wait_cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_start = clock64();
+#define WS_WAIT(bar, par, slot)            \
+  do {                                     \
+    const long long t0_ = clock64();       \
+    tc::mbar_wait(bar, par);               \
+    wait_cyc[slot] += clock64() - t0_;     \
+  } while (0)
 
   // ---- setup ------------------------------------------------------------------------------------------
   for (int j = tid; j < P.nv; j += kWsThreads) S.sv[j] = make_viewf(P.views[j], P.d);
@@ -112,25 +137,28 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.a_full[b], 128);
       tc::mbar_init(&S.a_empty[b], 1);
+    }
+    for (int b = 0; b < kDBufs; ++b) {
       tc::mbar_init(&S.d_full[b], 1);
-      tc::mbar_init(&S.d_empty[b], 128);
+      tc::mbar_init(&S.d_empty[b], kAccThreads);
     }
     for (int s = 0; s < kStages; ++s) {
-      tc::mbar_init(&S.b_full[s], 128);
+      tc::mbar_init(&S.b_full[s], kLoadThreads);
       tc::mbar_init(&S.b_empty[s], 1);
     }
     tc::mbar_init(&S.s_full, 1);
-    tc::mbar_init(&S.s_empty, 128);
+    tc::mbar_init(&S.s_empty, kAccThreads);
   }
-  if (warp == 5) tc::tmem_alloc(&S.tmem_base, 256);
+  if (warp == kAccWarp0) tc::tmem_alloc(&S.tmem_base, 512);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = S.tmem_base;
+  const uint32_t tS = tbase + 64u * kDBufs;
 
-  if (warp < 4) {
-    // ================= B loaders (128 threads) =================
-    // thread -> 16-byte column q of every row r = r0, r0 + 16, ...; pad rows repeat row 0's cell
+  if (warp < kLoadWarps) {
+    // ================= B loaders =================
+    // thread -> 16-byte column q of rows r0, r0 + 8, ...; pad rows repeat row 0's cell
     const int q = tid & 7, r0 = tid >> 3;
     int stage = 0;
     uint32_t phase = 0;
@@ -151,22 +179,22 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       bool ok;
       const int ktp = tile_ktp(P, tile, ok);
       if (!ok) continue;
-      // row -> cell table for this tile (ring of 2: at most one older tile is still being loaded)
+      // row -> cell table for this tile (ring of 2: the older slot's copies were all issued)
       int32_t* cell = S.cell[t_local & 1];
-      asm volatile("bar.sync 3, 128;" ::: "memory");  // previous users of this slot are done
-      if (tid < P.nv) {
-        const uint2 ds = P.tile_desc[tile * P.nv + tid];
+      asm volatile("bar.sync 3, %0;" ::"n"(kLoadThreads) : "memory");
+      for (int v = tid; v < P.nv; v += kLoadThreads) {
+        const uint2 ds = P.tile_desc[tile * P.nv + v];
         const int base = ds.x & 0xffff, x0 = (ds.x >> 16) & 0xff, y0 = ds.x >> 24;
         const int w = ds.y & 0xff, h = (ds.y >> 8) & 0xff;
-        const ViewF& vw = S.sv[tid];
+        const ViewF& vw = S.sv[v];
         for (int a = 0; a < w * h; ++a) cell[base + a] = vw.cell_base + (y0 + a / w) * vw.Wf + x0 + a % w;
       }
-      asm volatile("bar.sync 3, 128;" ::: "memory");
+      asm volatile("bar.sync 3, %0;" ::"n"(kLoadThreads) : "memory");
       const int kt = P.tile_kt[tile];
-      for (int r = kt + tid; r < ktp; r += 128) cell[r] = cell[0];
-      asm volatile("bar.sync 3, 128;" ::: "memory");
+      for (int r = kt + tid; r < ktp; r += kLoadThreads) cell[r] = cell[0];
+      asm volatile("bar.sync 3, %0;" ::"n"(kLoadThreads) : "memory");
       for (int c = 0; c < nch; ++c) {
-        tc::mbar_wait(&S.b_empty[stage], phase ^ 1u);
+        WS_WAIT(&S.b_empty[stage], phase ^ 1u, 0);
         const uint32_t sb = tc::smem_u32(sB + stage * kStageBytes);
         const uint16_t* src;
         int64_t rowlen;
@@ -177,7 +205,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           src = P.Gbf + (c - nd) * 64 + q * 8;
           rowlen = P.kpadg;
         }
-        for (int r = r0; r < ktp; r += 16)
+        for (int r = r0; r < ktp; r += kLoadThreads / 8)
           tc::cp_async16(sb + tc::b_chunk_off(r, q, kKtWs), src + (int64_t)cell[r] * rowlen);
         asm volatile("cp.async.commit_group;" ::: "memory");
         pending[npend++] = stage;
@@ -187,7 +215,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       ++t_local;
     }
     while (npend > 0) retire_oldest(npend - 1);
-  } else if (warp == 4) {
+  } else if (warp == kMmaWarp) {
     // ================= MMA issuer =================
     int stage = 0;
     uint32_t phase = 0;
@@ -199,19 +227,19 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const int ktp = tile_ktp(P, tile, ok);
       if (!ok) continue;
       const int ab = t_local & 1;
-      tc::mbar_wait(&S.a_full[ab], (t_local >> 1) & 1u);
+      WS_WAIT(&S.a_full[ab], (t_local >> 1) & 1u, 1);
       const uint32_t a0 = tc::smem_u32(sA + ab * kABytes);
       for (int c = 0; c < nch; ++c) {
-        tc::mbar_wait(&S.b_full[stage], phase);
+        WS_WAIT(&S.b_full[stage], phase, 2);
         uint32_t dst;
         int db = 0;
         if (c < nd) {
-          db = dcount & 1;
-          tc::mbar_wait(&S.d_empty[db], ((dcount >> 1) & 1u) ^ 1u);
+          db = dcount % kDBufs;
+          WS_WAIT(&S.d_empty[db], ((dcount / kDBufs) & 1u) ^ 1u, 3);
           dst = tbase + (uint32_t)(db * 64);
         } else {
-          if (c == nd) tc::mbar_wait(&S.s_empty, s_phase ^ 1u);
-          dst = tbase + 128u + (uint32_t)(64 * (c - nd));
+          if (c == nd) WS_WAIT(&S.s_empty, s_phase ^ 1u, 4);
+          dst = tS + (uint32_t)(64 * (c - nd));
         }
         tc::fence_after_sync();
         if (lane == 0) {
@@ -236,16 +264,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       s_phase ^= 1u;
       ++t_local;
     }
-  } else if (warp >= 9) {
+  } else if (warp >= kBuildWarp0) {
     // ================= A builders (thread = tile row) =================
-    const int row = tid - 288;  // 0..127
+    const int row = tid - kBuildWarp0 * 32;  // 0..127
     uint32_t t_local = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       bool ok;
       const int ktp = tile_ktp(P, tile, ok);
       if (!ok) continue;
       const int ab = t_local & 1;
-      tc::mbar_wait(&S.a_empty[ab], ((t_local >> 1) & 1u) ^ 1u);
+      WS_WAIT(&S.a_empty[ab], ((t_local >> 1) & 1u) ^ 1u, 5);
       uint2* sdesc = S.desc_a[ab];
       for (int v = row; v < P.nv; v += 128) sdesc[v] = P.tile_desc[tile * P.nv + v];
       unsigned char* A = sA + ab * kABytes;
@@ -283,15 +311,18 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       ++t_local;
     }
   } else {
-    // ================= accumulator warps 5-8: drain + epilogue =================
-    const int row = 32 * (warp & 3) + lane;  // TMEM lane group of this warp
+    // ================= accumulator warps: two per TMEM lane group, split by columns =================
+    const int half = (warp - kAccWarp0) >> 2;          // 0 / 1
+    const int row = 32 * (warp & 3) + lane;            // TMEM lane = tile row
     const uint32_t t_lane = (uint32_t)(32 * (warp & 3)) << 16;
-    const uint32_t tS = tbase + 128u;
+    const int kh = P.kpadg >> 1;                       // materials per half (32 or 64)
+    const int k0 = half * kh;
     uint32_t dcount = 0, s_phase = 0;
-    float wt[kMaxKpadTC / 32] = {0.f, 0.f, 0.f, 0.f};
+    float wt[2] = {0.f, 0.f};
     double pm_sum = 0.0, pmx = 0.0, pmy = 0.0, pmz = 0.0, featured_n = 0.0, pairs = 0.0;
     const float4* sv4 = reinterpret_cast<const float4*>(S.svals);
     const bool outs = P.sims || P.weights;
+    const int p_n = P.p;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       bool ok;
       tile_ktp(P, tile, ok);
@@ -299,20 +330,18 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const bool valid = jpt < P.n;
       const int32_t i = valid ? P.perm[jpt] : 0;
       if (!ok) {
-        if (valid) P.ovf_list[atomicAdd(P.ovf_count, 1)] = i;
+        if (valid && half == 0) P.ovf_list[atomicAdd(P.ovf_count, 1)] = i;
         continue;
       }
       const int count = valid ? P.counts[i] : 0;
       const float invc = count > 0 ? 1.f / (float)count : 0.f;
       float ss0 = 0.f, ss1 = 0.f, ss2 = 0.f, ss3 = 0.f;
       for (int c = 0; c < nd; ++c) {
-        const int db = dcount & 1;
-        tc::mbar_wait(&S.d_full[db], (dcount >> 1) & 1u);
+        const int db = dcount % kDBufs;
+        WS_WAIT(&S.d_full[db], (dcount / kDBufs) & 1u, 6);
         tc::fence_after_sync();
-        const uint32_t tD = tbase + (uint32_t)(db * 64);
-        float v[32], u[32];
-        tc::tmem_ld32(tD + t_lane, v);
-        tc::tmem_ld32(tD + t_lane + 32, u);
+        float v[32];
+        tc::tmem_ld32(tbase + (uint32_t)(db * 64 + half * 32) + t_lane, v);
         tc::fence_before_sync();
         mbar_arrive(&S.d_empty[db]);  // data is in registers: release the buffer early
 #pragma unroll
@@ -321,97 +350,100 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           ss1 = fmaf(v[q + 1], v[q + 1], ss1);
           ss2 = fmaf(v[q + 2], v[q + 2], ss2);
           ss3 = fmaf(v[q + 3], v[q + 3], ss3);
-          ss0 = fmaf(u[q], u[q], ss0);
-          ss1 = fmaf(u[q + 1], u[q + 1], ss1);
-          ss2 = fmaf(u[q + 2], u[q + 2], ss2);
-          ss3 = fmaf(u[q + 3], u[q + 3], ss3);
         }
         if (P.features && valid) {
-          float* dst = P.features + (int64_t)i * P.d + c * 64;
+          float* dst = P.features + (int64_t)i * P.d + c * 64 + half * 32;
 #pragma unroll
-          for (int q = 0; q < 32; q += 4) {
+          for (int q = 0; q < 32; q += 4)
             *reinterpret_cast<float4*>(dst + q) =
                 make_float4(v[q] * invc, v[q + 1] * invc, v[q + 2] * invc, v[q + 3] * invc);
-            *reinterpret_cast<float4*>(dst + 32 + q) =
-                make_float4(u[q] * invc, u[q + 1] * invc, u[q + 2] * invc, u[q + 3] * invc);
-          }
         }
         ++dcount;
       }
-      const float ss = (ss0 + ss1) + (ss2 + ss3);
-      // ---- epilogue on S ------------------------------------------------------------------------------
-      tc::mbar_wait(&S.s_full, s_phase);
+      S.xss[half][row] = (ss0 + ss1) + (ss2 + ss3);
+      // ---- epilogue on S (this half's materials) ----------------------------------------------------
+      WS_WAIT(&S.s_full, s_phase, 7);
       s_phase ^= 1u;
       tc::fence_after_sync();
-      const bool featured = valid && count > 0;
-      const float inv = ss > 0.f ? 1.f / sqrtf(ss) : 0.f;
-      const float sc = inv * P.inv_temp * 1.4426950408889634f;
-      float m2a = -INFINITY, m2b = -INFINITY;
+      float mx = -INFINITY;
       bool nan = false;
-      for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
+      for (int c0 = 0; c0 < kh; c0 += 32) {
         float v[32];
-        tc::tmem_ld32(tS + t_lane + c0, v);
-        if (c0 + 32 <= P.k) {
+        tc::tmem_ld32(tS + (uint32_t)(k0 + c0) + t_lane, v);
+        if (k0 + c0 + 32 <= P.k) {
 #pragma unroll
-          for (int q = 0; q < 32; q += 2) {
-            m2a = fmaxf(m2a, v[q] * sc);
-            m2b = fmaxf(m2b, v[q + 1] * sc);
-            nan |= isnan(v[q]) | isnan(v[q + 1]);
+          for (int q = 0; q < 32; ++q) {
+            mx = fmaxf(mx, v[q]);
+            nan |= isnan(v[q]);
           }
         } else {
-          for (int q = 0; c0 + q < P.k; ++q) {
-            m2a = fmaxf(m2a, v[q] * sc);
+          for (int q = 0; k0 + c0 + q < P.k; ++q) {
+            mx = fmaxf(mx, v[q]);
             nan |= isnan(v[q]);
           }
         }
       }
-      const float m2 = fmaxf(m2a, m2b);
+      S.xm[half][row] = mx;
+      asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
+      const float ss = S.xss[0][row] + S.xss[1][row];
+      const bool featured = valid && count > 0;
+      const float inv = ss > 0.f ? 1.f / sqrtf(ss) : 0.f;
+      const float sc = inv * P.inv_temp * 1.4426950408889634f;  // > 0 (or 0 when featureless)
+      const float m2 = fmaxf(S.xm[0][row], S.xm[1][row]) * sc;
       if (featured && (nan || isnan(sc))) atomicOr(P.status, 1);
       float se = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f, pl3 = 0.f, pml = 0.f;
-      for (int c0 = 0; c0 < P.kpadg; c0 += 32) {
+      for (int c0 = 0; c0 < kh; c0 += 32) {
         float v[32];
-        tc::tmem_ld32(tS + t_lane + c0, v);
+        tc::tmem_ld32(tS + (uint32_t)(k0 + c0) + t_lane, v);
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
-          const int kk = c0 + q;
-          const float e = kk < P.k ? exp2f(v[q] * sc - m2) : 0.f;
+          const int kk = k0 + c0 + q;
+          const float e = kk < P.k ? ex2(fmaf(v[q], sc, -m2)) : 0.f;
           se += e;
           const float4 y = sv4[kk];
           pl0 = fmaf(e, y.x, pl0);
           pl1 = fmaf(e, y.y, pl1);
-          pl2 = fmaf(e, y.z, pl2);
-          pl3 = fmaf(e, y.w, pl3);
+          if (p_n > 2) {
+            pl2 = fmaf(e, y.z, pl2);
+            pl3 = fmaf(e, y.w, pl3);
+          }
           pml = fmaf(e, S.smt[kk], pml);
         }
       }
-      const float rs = featured ? 1.f / se : 0.f;
-      // third pass: normalised weights -> column sums across the warp (butterfly) -> wt registers
+      S.xsum[half][0][row] = se;
+      S.xsum[half][1][row] = pl0;
+      S.xsum[half][2][row] = pl1;
+      S.xsum[half][3][row] = pl2;
+      S.xsum[half][4][row] = pl3;
+      S.xsum[half][5][row] = pml;
+      asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
+      const float se_t = S.xsum[0][0][row] + S.xsum[1][0][row];
+      const float rs = featured ? 1.f / se_t : 0.f;
+      // normalised weights of this half -> column sums across the warp (butterfly) -> wt registers
 #pragma unroll
-      for (int g = 0; g < kMaxKpadTC / 32; ++g) {
-        if (g * 32 < P.kpadg) {
+      for (int g = 0; g < 2; ++g) {
+        if (g * 32 < kh) {
           float v[32];
-          tc::tmem_ld32(tS + t_lane + g * 32, v);
-          if (outs && valid) {
-            for (int q = 0; q < 32 && g * 32 + q < P.k; ++q) {
-              const int kk = g * 32 + q;
-              if (P.sims) P.sims[(int64_t)i * P.k + kk] = featured ? v[q] * inv : 0.f;
-              if (P.weights) P.weights[(int64_t)i * P.k + kk] = featured ? exp2f(v[q] * sc - m2) * rs : 0.f;
-            }
-          }
+          tc::tmem_ld32(tS + (uint32_t)(k0 + g * 32) + t_lane, v);
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
-            const int kk = g * 32 + q;
-            v[q] = (kk < P.k && featured) ? exp2f(v[q] * sc - m2) * rs : 0.f;
+            const int kk = k0 + g * 32 + q;
+            const float wv = (kk < P.k && featured) ? ex2(fmaf(v[q], sc, -m2)) * rs : 0.f;
+            if (outs && valid && kk < P.k) {
+              if (P.sims) P.sims[(int64_t)i * P.k + kk] = featured ? v[q] * inv : 0.f;
+              if (P.weights) P.weights[(int64_t)i * P.k + kk] = wv;
+            }
+            v[q] = wv;
           }
-          // reduce-scatter: after 5 steps lane l holds the warp's sum of column g*32 + l
+          // reduce-scatter: after 5 steps lane l holds the warp's sum of column k0 + g*32 + l
 #pragma unroll
-          for (int half = 16; half >= 1; half >>= 1) {
-            const bool upper = (lane & half) != 0;
+          for (int hb = 16; hb >= 1; hb >>= 1) {
+            const bool upper = (lane & hb) != 0;
 #pragma unroll
-            for (int q = 0; q < half; ++q) {
-              const float send = upper ? v[q] : v[q + half];
-              const float keep = upper ? v[q + half] : v[q];
-              v[q] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+            for (int q = 0; q < hb; ++q) {
+              const float send = upper ? v[q] : v[q + hb];
+              const float keep = upper ? v[q + hb] : v[q];
+              v[q] = keep + __shfl_xor_sync(0xffffffffu, send, hb);
             }
           }
           wt[g] += v[0];
@@ -419,11 +451,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       }
       tc::fence_before_sync();
       mbar_arrive(&S.s_empty);
-      const float prop[4] = {pl0 * rs, pl1 * rs, pl2 * rs, pl3 * rs};
-      const float pm = pml * rs;
-      if (valid) {
+      if (valid && half == 0) {
+        float prop[4];
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) prop[pp] = (S.xsum[0][1 + pp][row] + S.xsum[1][1 + pp][row]) * rs;
+        const float pm = (S.xsum[0][5][row] + S.xsum[1][5][row]) * rs;
         const float4 p = P.spts[jpt];
-        for (int pp = 0; pp < P.p; ++pp) P.props[(int64_t)i * P.p + pp] = prop[pp];
+        for (int pp = 0; pp < p_n; ++pp) P.props[(int64_t)i * p_n + pp] = prop[pp];
         if (P.grid_partials) {
           const int32_t code = P.codes[i];
           float rho = prop[0];
@@ -442,21 +476,28 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     }
     // flush this CTA's partials (integrate.py:133-155) once
 #pragma unroll
-    for (int g = 0; g < kMaxKpadTC / 32; ++g)
-      if (g * 32 + lane < P.k) atomicAdd(&S.red[g * 32 + lane], (double)wt[g]);
+    for (int g = 0; g < 2; ++g)
+      if (g * 32 < kh && k0 + g * 32 + lane < P.k) atomicAdd(&S.red[k0 + g * 32 + lane], (double)wt[g]);
     double r6[6] = {pm_sum, pmx, pmy, pmz, featured_n, pairs};
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
       r6[q] = warp_sum(r6[q]);
       if (lane == 0) atomicAdd(&S.red[P.k + q], r6[q]);
     }
-    asm volatile("bar.sync 2, 128;" ::: "memory");
-    for (int j = row; j < P.k + 6; j += 128)
+    asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
+    for (int j = tid - kAccWarp0 * 32; j < P.k + 6; j += kAccThreads)
       if (S.red[j] != 0.0) atomicAdd(P.partials + j, S.red[j]);
   }
+  if (P.dbg && lane == 0 && (warp == 0 || warp == kMmaWarp || warp == kAccWarp0 || warp == kBuildWarp0)) {
+    unsigned long long* d = P.dbg + blockIdx.x * 16;
+    for (int q = 0; q < 8; ++q)
+      if (wait_cyc[q]) d[q] = (unsigned long long)wait_cyc[q];
+    if (warp == kMmaWarp) d[8] = (unsigned long long)(clock64() - t_start);
+  }
+#undef WS_WAIT
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 5) tc::tmem_dealloc(tbase, 256);
+  if (warp == kAccWarp0) tc::tmem_dealloc(tbase, 512);
 }
 
 // ---- host: tensor maps --------------------------------------------------------------------------------
@@ -505,8 +546,31 @@ int run_tile_ws(const TileParams& P, int hf, int wf, int nv, cudaStream_t st) {
   const int64_t ntiles = (P.n + kTile - 1) / kTile;
   int grid = (int)(ntiles < sms ? ntiles : sms);
   if (const char* g = getenv("PF_WS_GRID")) grid = (int)(ntiles < atoi(g) ? ntiles : atoi(g));  // debug knob
-  k_tile_ws<<<grid, kWsThreads, smem, st>>>(P);
-  return check_launch("tile_ws");
+  static unsigned long long* dbg = nullptr;
+  TileParams Q = P;
+  const bool debug = getenv("PF_WS_DEBUG") != nullptr;
+  if (debug) {
+    if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 16 * 1024);
+    cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 16 * 1024, st);
+    Q.dbg = dbg;
+  }
+  k_tile_ws<<<grid, kWsThreads, smem, st>>>(Q);
+  const int rc = check_launch("tile_ws");
+  if (debug && rc == PF_OK) {
+    static unsigned long long h[16 * 1024];
+    cudaMemcpyAsync(h, dbg, sizeof(unsigned long long) * 16 * grid, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const char* names[9] = {"load:b_empty", "mma:a_full", "mma:b_full", "mma:d_empty", "mma:s_empty",
+                            "build:a_empty", "acc:d_full", "acc:s_full", "total"};
+    fprintf(stderr, "[ws debug] mean cycles per CTA over %d CTAs:", grid);
+    for (int q = 0; q < 9; ++q) {
+      double sum = 0;
+      for (int b = 0; b < grid; ++b) sum += (double)h[b * 16 + q];
+      fprintf(stderr, " %s=%.3g", names[q], sum / grid);
+    }
+    fprintf(stderr, "\n");
+  }
+  return rc;
 }
 
 }  // namespace tile
