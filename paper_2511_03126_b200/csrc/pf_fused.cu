@@ -488,12 +488,24 @@ int pf_fuse_prepare(const pf_fuse_args_t* a, void* stream) {
   const int kpad = 32 * kpl_of(a->k);
   const int64_t cells = total_cells(a);
   float* G = reinterpret_cast<float*>(a->workspace);
+  uint16_t* Gbf = nullptr;
+  int kpadg = 0;
+  if (tile_path_ok(a)) {
+    kpadg = ((a->k + 63) / 64) * 64;
+    unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
+    Gbf = reinterpret_cast<uint16_t*>(ws + tile::tile_layout(a->n, a->nviews, cells, kpadg).gbf);
+    // bf16 maps: G on the tensor cores (bf16 text), fp32 copy for the SIMT overflow tiles
+    const int rc = tile::run_gproj_tc(a->fmap, cells, a->d, a->text, a->k, kpadg, kpad, Gbf, G, st);
+    if (rc >= 0) return rc;
+  }
   dim3 grid((unsigned)((cells + TP_CELLS - 1) / TP_CELLS), (unsigned)(kpad / TP_MATS));
   if (a->fmap_dtype == PF_F32)
     k_text_proj<PF_F32><<<grid, 256, 0, st>>>(a->fmap, cells, a->d, a->text, a->k, kpad, G);
   else
     k_text_proj<PF_BF16><<<grid, 256, 0, st>>>(a->fmap, cells, a->d, a->text, a->k, kpad, G);
-  return check_launch("text_proj");
+  if (int rc = check_launch("text_proj")) return rc;
+  if (Gbf) return tile::run_g_bf16(G, cells, kpad, kpadg, Gbf, st);
+  return PF_OK;
 }
 
 int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {

@@ -1,0 +1,131 @@
+// G = fmap @ text^T on the tensor cores for the bf16 tile path (the per-object table behind the
+// similarity-by-associativity, see pf_tile.cu): one CTA per 128 feature cells, K = D streamed in
+// 64-channel chunks through a 2-stage cp.async ring, tcgen05.mma (M=128, N=kpadg, K=16) into TMEM,
+// epilogue writes G in bf16 (cells x kpadg, the tile kernel's S operand) and fp32 (cells x kpad,
+// the SIMT overflow path). Text rows are rounded to bf16 on the fly (bf16-feature mode bar 1e-2).
+#include <cuda_bf16.h>
+
+#include "pf_common.cuh"
+#include "pf_tc.cuh"
+#include "pf_tile.cuh"
+
+namespace pf {
+namespace tile {
+namespace {
+
+constexpr int kGM = 128;  // cells per CTA
+
+__global__ void __launch_bounds__(128, 1) k_gproj_tc(const uint16_t* __restrict__ fmap, int64_t cells, int d,
+                                                     const float* __restrict__ text, int k, int kpadg,
+                                                     int kpad, uint16_t* __restrict__ Gbf,
+                                                     float* __restrict__ G32) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // stage s: A [128 rows x 64 ch] (16 KB, K-major SW128) then B [kpadg rows x 64 ch] (K-major SW128)
+  const int b_bytes = kpadg * 128;
+  const int stage_bytes = 16384 + b_bytes;
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * kGM;
+  const int nchunk = d / 64;
+
+  auto load = [&](int ch, int st) {
+    unsigned char* sa = smem + st * stage_bytes;
+    unsigned char* sb = sa + 16384;
+    // A: row r, 16-byte piece q (8 channels): K-major SW128, one 64-channel atom column
+    for (int e = tid; e < kGM * 8; e += 128) {
+      const int r = e >> 3, q = e & 7;
+      const int64_t cell = c0 + r < cells ? c0 + r : cells - 1;
+      const uint32_t off = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + (((q ^ (r & 7)) & 7) << 4));
+      tc::cp_async16(tc::smem_u32(sa + off), fmap + cell * d + ch * 64 + q * 8);
+    }
+    // B: material n, channels ch*64 .. +64 rounded to bf16 (K-major SW128)
+    for (int e = tid; e < kpadg * 8; e += 128) {
+      const int n = e >> 3, q = e & 7;
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+      if (n < k) {
+        const float4 x0 = *reinterpret_cast<const float4*>(text + (int64_t)n * d + ch * 64 + q * 8);
+        const float4 x1 = *reinterpret_cast<const float4*>(text + (int64_t)n * d + ch * 64 + q * 8 + 4);
+        const __nv_bfloat162 p0 = __floats2bfloat162_rn(x0.x, x0.y), p1 = __floats2bfloat162_rn(x0.z, x0.w);
+        const __nv_bfloat162 p2 = __floats2bfloat162_rn(x1.x, x1.y), p3 = __floats2bfloat162_rn(x1.z, x1.w);
+        w[0] = *reinterpret_cast<const uint32_t*>(&p0);
+        w[1] = *reinterpret_cast<const uint32_t*>(&p1);
+        w[2] = *reinterpret_cast<const uint32_t*>(&p2);
+        w[3] = *reinterpret_cast<const uint32_t*>(&p3);
+      }
+      const uint32_t off = (uint32_t)((n >> 3) * 1024 + (n & 7) * 128 + (((q ^ (n & 7)) & 7) << 4));
+      *reinterpret_cast<uint4*>(sb + off) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  if (tid == 0) tc::mbar_init(&mbar, 1);
+  uint32_t ncols = 32;
+  while (ncols < (uint32_t)kpadg) ncols <<= 1;
+  if (warp == 0) tc::tmem_alloc(&tmem_base_s, ncols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = tmem_base_s;
+  const uint32_t idesc = tc::idesc_bf16_f32(128, kpadg, false, false);
+
+  load(0, 0);
+  uint32_t phase = 0;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int st = ch & 1;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    tc::fence_async_shared();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    if (tid == 0) {
+      const uint32_t a0 = tc::smem_u32(smem + st * stage_bytes), b0 = a0 + 16384;
+      for (int s = 0; s < 4; ++s) {
+        const uint64_t ad = tc::smem_desc_sw128(a0 + s * 32, 16, 1024);
+        const uint64_t bd = tc::smem_desc_sw128(b0 + s * 32, 16, 1024);
+        tc::mma_bf16(tbase, ad, bd, idesc, (ch | s) ? 1u : 0u);
+      }
+      tc::mma_commit(&mbar);
+    }
+    // stage st^1 was read by the MMAs of chunk ch-1, which completed (waited below last iteration)
+    if (ch + 1 < nchunk) load(ch + 1, st ^ 1);
+    tc::mbar_wait(&mbar, phase);
+    phase ^= 1u;
+  }
+  tc::fence_after_sync();
+  const int64_t cell = c0 + tid;
+  for (int cc = 0; cc < kpadg; cc += 32) {
+    float v[32];
+    tc::tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + cc, v);
+    if (cell < cells) {
+#pragma unroll
+      for (int q = 0; q < 32; q += 2) {
+        const __nv_bfloat162 b = __floats2bfloat162_rn(v[q], v[q + 1]);
+        *reinterpret_cast<__nv_bfloat162*>(Gbf + cell * kpadg + cc + q) = b;
+      }
+      if (G32)
+        for (int q = 0; q < 32 && cc + q < kpad; ++q) G32[cell * kpad + cc + q] = cc + q < k ? v[q] : 0.f;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tbase, ncols);
+}
+
+}  // namespace
+
+int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int k, int kpadg, int kpad,
+                 uint16_t* Gbf, float* G32, cudaStream_t st) {
+  if (d % 64 != 0 || kpadg % 16 != 0 || kpadg > 256) return -1;
+  const size_t smem = 2 * (16384 + (size_t)kpadg * 128) + 1024;
+  cudaFuncSetAttribute(k_gproj_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned grid = (unsigned)((cells + kGM - 1) / kGM);
+  k_gproj_tc<<<grid, 128, smem, st>>>(reinterpret_cast<const uint16_t*>(fmap), cells, d, text, k, kpadg, kpad,
+                                      Gbf, G32);
+  return check_launch("gproj_tc");
+}
+
+}  // namespace tile
+}  // namespace pf

@@ -554,6 +554,11 @@ size_t tile_smem_bytes() {
   return (ab > red ? ab : red) + 1024;
 }
 
+int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf, cudaStream_t st) {
+  k_g_bf16<<<grid_for(cells * kpadg, 256), 256, 0, st>>>(G, cells, kpad, kpadg, Gbf);
+  return check_launch("g_bf16");
+}
+
 int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const float* points,
                   int64_t n, int64_t cells, const float* G, int kpad, int hf, int wf, cudaStream_t st) {
   uint32_t* keys = reinterpret_cast<uint32_t*>(ws + L.keys);
@@ -572,9 +577,6 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   k_sort_scatter<<<grid_for(n, 256), 256, 0, st>>>(points, n, keys, hist, const_cast<int32_t*>(P.perm),
                                                    const_cast<float4*>(P.spts));
   if (int rc = check_launch("sort_scatter")) return rc;
-  k_g_bf16<<<grid_for(cells * P.kpadg, 256), 256, 0, st>>>(G, cells, kpad, P.kpadg,
-                                                          const_cast<uint16_t*>(P.Gbf));
-  if (int rc = check_launch("g_bf16")) return rc;
   k_tile_prep<<<(unsigned)L.ntiles, kTile, 0, st>>>(P);
   if (int rc = check_launch("tile_prep")) return rc;
   // persistent warp-specialised TMA kernel (pf_tile_ws.cu); k_tile_mma when TMA maps are unavailable

@@ -80,6 +80,9 @@ size_t tile_smem_bytes();
 int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const float* points,
                   int64_t n, int64_t cells, const float* G, int kpad, int hf, int wf, cudaStream_t st);
 int run_tile_ws(const TileParams& P, int hf, int wf, int nv, cudaStream_t st);
+int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf, cudaStream_t st);
+int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int k, int kpadg, int kpad,
+                 uint16_t* Gbf, float* G32, cudaStream_t st);
 
 }  // namespace tile
 }  // namespace pf
