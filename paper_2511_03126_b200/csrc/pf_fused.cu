@@ -447,7 +447,7 @@ uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* a) {
   if (!a || !a->views_host || a->d <= 0 || a->k <= 0) return 0;
   uint64_t bytes = g_bytes(a);
   if (tile_path_ok(a))
-    bytes += tile::tile_layout(a->n, a->nviews, total_cells(a), ((a->k + 63) / 64) * 64).bytes;
+    bytes += tile::tile_layout(a->n, a->nviews, total_cells(a), tile::kMaxKpadTC).bytes;
   return bytes;
 }
 
@@ -491,7 +491,7 @@ int pf_fuse_prepare(const pf_fuse_args_t* a, void* stream) {
   uint16_t* Gbf = nullptr;
   int kpadg = 0;
   if (tile_path_ok(a)) {
-    kpadg = ((a->k + 63) / 64) * 64;
+    kpadg = tile::kMaxKpadTC;  // S operand is always one 128-column chunk pair
     unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
     Gbf = reinterpret_cast<uint16_t*>(ws + tile::tile_layout(a->n, a->nviews, cells, kpadg).gbf);
     // bf16 maps: G on the tensor cores (bf16 text), fp32 copy for the SIMT overflow tiles
@@ -534,7 +534,7 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
   const int d = a->d;
   if (tile_path_ok(a)) {
     const int64_t cells = total_cells(a);
-    const int kpadg = ((a->k + 63) / 64) * 64;  // S chunks are 64 columns wide
+    const int kpadg = tile::kMaxKpadTC;  // S operand is always one 128-column chunk pair
     unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
     const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg);
     tile::TileParams T{};

@@ -1,20 +1,20 @@
 // Persistent, warp-specialised tcgen05 tile kernel of the bf16 fused query (see pf_tile.cu for the
-// formulation). One CTA per SM loops over tiles of 128 sorted points; roles (15 warps):
+// formulation). One CTA per SM loops over tiles of 128 sorted points; roles (17 warps):
 //
-//   warps 0-1   B loaders: for every 64-channel chunk of a tile (D/64 feature chunks, then the
+//   warps 0-3   B loaders: for every 64-channel chunk of a tile (D/64 feature chunks, then the
 //               G-table chunks) they copy each tap's 128-byte row piece with cp.async (16 B per
 //               lane op, 8 lanes per row) into a 4-stage ring of B buffers (N-major, 128-byte
 //               swizzle), keeping three chunks in flight; after cp.async.wait_group the writer
 //               fences the generic->async proxy and arrives on the stage's full barrier.
 //               (Per-window TMA boxes were measured first: ~460 tiny TMA ops per tile made the TMA
 //               unit the bottleneck, profiles/r01_notes.md.)
-//   warp 2      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=64, K=16) over the
+//   warp 4      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=64, K=16) over the
 //               tile's taps into 4 TMEM buffers (feature chunks) or the S columns (G chunks);
 //               tcgen05.commit frees the B stage / A buffer and signals the accumulators;
-//   warps 3-10  accumulator warps (two per TMEM lane group, each half of the columns): drain each feature chunk from TMEM (|F|^2, optional mean
+//   warps 5-12  accumulator warps (two per TMEM lane group, each half of the columns): drain each feature chunk from TMEM (|F|^2, optional mean
 //               features), then the epilogue: softmax over K, property regression, voxel atomics,
 //               integrate partials accumulated in registers across all tiles of the CTA;
-//   warps 11-14 A builders: build the next tile's W (bilinear weights, bf16, K-major 128-B swizzle)
+//   warps 13-16 A builders: build the next tile's W (bilinear weights, bf16, K-major 128-B swizzle)
 //               in one of two A buffers while the current tile's MMAs run.
 // Synchronisation is mbarrier-only (full/empty pairs for A, B stages, TMEM D buffers and S).
 #include <cuda.h>
@@ -35,14 +35,14 @@ namespace pf {
 namespace tile {
 namespace {
 
-constexpr int kLoadWarps = 2;          // warps 0-1: B loaders
+constexpr int kLoadWarps = 4;          // warps 0-3: B loaders
 constexpr int kLoadThreads = 32 * kLoadWarps;
-constexpr int kMmaWarp = 2;            // warp 2: MMA issuer
-constexpr int kAccWarp0 = 3;           // warps 3-10: accumulators (2 per TMEM lane group)
+constexpr int kMmaWarp = 4;            // warp 4: MMA issuer
+constexpr int kAccWarp0 = 5;           // warps 5-12: accumulators (2 per TMEM lane group)
 constexpr int kAccThreads = 256;
-constexpr int kBuildWarp0 = 11;        // warps 11-14: A builders
-constexpr int kWsThreads = 480;        // 15 warps
-constexpr int kDBufs = 4;              // TMEM feature-chunk buffers (64 columns each)
+constexpr int kBuildWarp0 = 13;        // warps 13-16: A builders
+constexpr int kWsThreads = 544;        // 17 warps
+constexpr int kDBufs = 2;              // TMEM feature buffers (128 columns = 2 chunks each)
 constexpr int kStages = 4;             // B ring depth
 constexpr int kKtWs = 192;             // taps per tile held in one A buffer / B stage
 constexpr int kStageBytes = kKtWs * 128;
@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nd = P.d >> 6, ns = P.kpadg >> 6, nch = nd + ns;
   const int64_t ntiles = (P.n + kTile - 1) / kTile;
-  long long wait_cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long wait_cyc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long issue_cyc = 0;
   const long long t_start = clock64();
 #define WS_WAIT(bar, par, slot)            \
   do {                                     \
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = S.tmem_base;
-  const uint32_t tS = tbase + 64u * kDBufs;
+  const uint32_t tS = tbase + 128u * kDBufs;
 
   if (warp < kLoadWarps) {
     // ================= B loaders =================
@@ -166,9 +167,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     int npend = 0;
     uint32_t t_local = 0;
     auto retire_oldest = [&](int keep) {
+      const long long tr0 = clock64();
       if (keep == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
       else if (keep == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
       else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      wait_cyc[10] += clock64() - tr0;
       tc::fence_async_shared();
       mbar_arrive(&S.b_full[pending[0]]);
       pending[0] = pending[1];
@@ -205,9 +208,18 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           src = P.Gbf + (c - nd) * 64 + q * 8;
           rowlen = P.kpadg;
         }
-        for (int r = r0; r < ktp; r += kLoadThreads / 8)
-          tc::cp_async16(sb + tc::b_chunk_off(r, q, kKtWs), src + (int64_t)cell[r] * rowlen);
+        // rows r0, r0 + 8, ...: r & 7 is fixed per thread, so the swizzled destination just
+        // advances by one 1024-byte row group per step (tc::b_chunk_off with the constant hoisted)
+        static_assert(kLoadWarps % 2 == 0, "rows step by a multiple of 8");
+        constexpr int kRowStep = kLoadThreads / 8;
+        const uint32_t dst0 = sb + (uint32_t)((r0 >> 3) * 1024 + (r0 & 7) * 128 + (((q ^ (r0 & 7)) & 7) << 4));
+        const int nrow = (ktp - r0 + kRowStep - 1) / kRowStep;
+        const long long tl0 = clock64();
+#pragma unroll 4
+        for (int j = 0; j < nrow; ++j)
+          tc::cp_async16(dst0 + (uint32_t)j * (kRowStep / 8 * 1024u), src + (int64_t)cell[r0 + kRowStep * j] * rowlen);
         asm volatile("cp.async.commit_group;" ::: "memory");
+        wait_cyc[11] += clock64() - tl0;
         pending[npend++] = stage;
         if (npend == 3) retire_oldest(2);
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
@@ -217,11 +229,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     while (npend > 0) retire_oldest(npend - 1);
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer =================
+    // chunks are issued in pairs: two consecutive 64-column B chunks sit in adjacent ring stages
+    // (the pair always starts on an even stage: D/64 and the 2 G chunks are even), so one MMA
+    // covers N = 128 with LBO = stage stride — half the A re-reads of N = 64 MMAs.
     int stage = 0;
     uint32_t phase = 0;
-    uint32_t dcount = 0;  // feature chunks issued so far (selects the TMEM D buffer)
+    uint32_t dcount = 0;  // feature chunk pairs issued so far (selects the TMEM D buffer)
     uint32_t t_local = 0, s_phase = 0;
-    const uint32_t idesc = tc::idesc_bf16_f32(128, 64, false, true);
+    const uint32_t idesc = tc::idesc_bf16_f32(128, 128, false, true);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       bool ok;
       const int ktp = tile_ktp(P, tile, ok);
@@ -229,37 +244,42 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const int ab = t_local & 1;
       WS_WAIT(&S.a_full[ab], (t_local >> 1) & 1u, 1);
       const uint32_t a0 = tc::smem_u32(sA + ab * kABytes);
-      for (int c = 0; c < nch; ++c) {
+      for (int c = 0; c < nch; c += 2) {
         WS_WAIT(&S.b_full[stage], phase, 2);
+        WS_WAIT(&S.b_full[stage + 1], phase, 2);
         uint32_t dst;
         int db = 0;
         if (c < nd) {
           db = dcount % kDBufs;
           WS_WAIT(&S.d_empty[db], ((dcount / kDBufs) & 1u) ^ 1u, 3);
-          dst = tbase + (uint32_t)(db * 64);
+          dst = tbase + (uint32_t)(db * 128);
         } else {
-          if (c == nd) WS_WAIT(&S.s_empty, s_phase ^ 1u, 4);
-          dst = tS + (uint32_t)(64 * (c - nd));
+          WS_WAIT(&S.s_empty, s_phase ^ 1u, 4);
+          dst = tS;
         }
         tc::fence_after_sync();
+        const long long ti0 = clock64();
         if (lane == 0) {
-          tc::fence_async_shared();
+          // (loaders and builders fence their generic-proxy writes before arriving)
           const uint32_t b0 = tc::smem_u32(sB + stage * kStageBytes);
           for (int s = 0; s < ktp / 16; ++s) {
             const uint64_t ad = tc::smem_desc_sw128(a0 + (s >> 2) * kTile * 128 + (s & 3) * 32, 16, 1024);
-            const uint64_t bd = tc::smem_desc_sw128(b0 + s * 2048, kKtWs * 128, 1024);
+            const uint64_t bd = tc::smem_desc_sw128(b0 + s * 2048, kStageBytes, 1024);
             tc::mma_bf16(dst, ad, bd, idesc, s > 0 ? 1u : 0u);
           }
           tc::mma_commit(&S.b_empty[stage]);
+          tc::mma_commit(&S.b_empty[stage + 1]);
           if (c < nd) tc::mma_commit(&S.d_full[db]);
-          if (c == nch - 1) {
+          if (c + 2 >= nch) {
             tc::mma_commit(&S.s_full);
             tc::mma_commit(&S.a_empty[ab]);
           }
         }
         __syncwarp();
+        issue_cyc += clock64() - ti0;
         if (c < nd) ++dcount;
-        if (++stage == kStages) { stage = 0; phase ^= 1u; }
+        stage += 2;
+        if (stage == kStages) { stage = 0; phase ^= 1u; }
       }
       s_phase ^= 1u;
       ++t_local;
@@ -336,27 +356,31 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const int count = valid ? P.counts[i] : 0;
       const float invc = count > 0 ? 1.f / (float)count : 0.f;
       float ss0 = 0.f, ss1 = 0.f, ss2 = 0.f, ss3 = 0.f;
-      for (int c = 0; c < nd; ++c) {
+      for (int c = 0; c < nd; c += 2) {  // 128-column pair: this half drains 64 columns
         const int db = dcount % kDBufs;
         WS_WAIT(&S.d_full[db], (dcount / kDBufs) & 1u, 6);
         tc::fence_after_sync();
-        float v[32];
-        tc::tmem_ld32(tbase + (uint32_t)(db * 64 + half * 32) + t_lane, v);
+        float v[32], u[32];
+        tc::tmem_ld32(tbase + (uint32_t)(db * 128 + half * 64) + t_lane, v);
+        tc::tmem_ld32(tbase + (uint32_t)(db * 128 + half * 64 + 32) + t_lane, u);
         tc::fence_before_sync();
         mbar_arrive(&S.d_empty[db]);  // data is in registers: release the buffer early
 #pragma unroll
-        for (int q = 0; q < 32; q += 4) {
+        for (int q = 0; q < 32; q += 2) {
           ss0 = fmaf(v[q], v[q], ss0);
           ss1 = fmaf(v[q + 1], v[q + 1], ss1);
-          ss2 = fmaf(v[q + 2], v[q + 2], ss2);
-          ss3 = fmaf(v[q + 3], v[q + 3], ss3);
+          ss2 = fmaf(u[q], u[q], ss2);
+          ss3 = fmaf(u[q + 1], u[q + 1], ss3);
         }
         if (P.features && valid) {
-          float* dst = P.features + (int64_t)i * P.d + c * 64 + half * 32;
+          float* dst = P.features + (int64_t)i * P.d + c * 64 + half * 64;
 #pragma unroll
-          for (int q = 0; q < 32; q += 4)
+          for (int q = 0; q < 32; q += 4) {
             *reinterpret_cast<float4*>(dst + q) =
                 make_float4(v[q] * invc, v[q + 1] * invc, v[q + 2] * invc, v[q + 3] * invc);
+            *reinterpret_cast<float4*>(dst + 32 + q) =
+                make_float4(u[q] * invc, u[q + 1] * invc, u[q + 2] * invc, u[q + 3] * invc);
+          }
         }
         ++dcount;
       }
@@ -492,7 +516,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     unsigned long long* d = P.dbg + blockIdx.x * 16;
     for (int q = 0; q < 8; ++q)
       if (wait_cyc[q]) d[q] = (unsigned long long)wait_cyc[q];
-    if (warp == kMmaWarp) d[8] = (unsigned long long)(clock64() - t_start);
+    if (warp == 0) {
+      d[10] = (unsigned long long)wait_cyc[10];
+      d[11] = (unsigned long long)wait_cyc[11];
+    }
+    if (warp == kMmaWarp) {
+      d[8] = (unsigned long long)(clock64() - t_start);
+      d[9] = (unsigned long long)issue_cyc;
+    }
   }
 #undef WS_WAIT
   tc::fence_before_sync();
@@ -560,10 +591,11 @@ int run_tile_ws(const TileParams& P, int hf, int wf, int nv, cudaStream_t st) {
     static unsigned long long h[16 * 1024];
     cudaMemcpyAsync(h, dbg, sizeof(unsigned long long) * 16 * grid, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    const char* names[9] = {"load:b_empty", "mma:a_full", "mma:b_full", "mma:d_empty", "mma:s_empty",
-                            "build:a_empty", "acc:d_full", "acc:s_full", "total"};
+    const char* names[12] = {"load:b_empty", "mma:a_full", "mma:b_full", "mma:d_empty", "mma:s_empty",
+                             "build:a_empty", "acc:d_full", "acc:s_full", "total", "mma:issue",
+                             "load:retire", "load:issue"};
     fprintf(stderr, "[ws debug] mean cycles per CTA over %d CTAs:", grid);
-    for (int q = 0; q < 9; ++q) {
+    for (int q = 0; q < 12; ++q) {
       double sum = 0;
       for (int b = 0; b < grid; ++b) sum += (double)h[b * 16 + q];
       fprintf(stderr, " %s=%.3g", names[q], sum / grid);
