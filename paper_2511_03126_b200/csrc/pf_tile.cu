@@ -123,15 +123,60 @@ __global__ void k_sort_scatter(const float* __restrict__ p, int64_t n, const uin
   }
 }
 
+// Per-view constant error bounds over the object's bbox (all points lie inside it): the camera
+// coordinates are affine in p, so their extremes over the box are attained at its corners. When
+// the whole box is safely in front of the camera the per-sample bound of classify() is replaced by
+// one constant per view (same formulas with the worst-case |X|, |Y|, 1/z), which removes the
+// per-sample bound arithmetic from the hot loop.
+__device__ float4 view_bound(const ViewF& w, const pf_view_t& v, const double* lo_hi) {
+  double zmin = 1e300, xmax = 0.0, ymax = 0.0, p1 = 0.0;
+  for (int c = 0; c < 8; ++c) {
+    const double px = (c & 1) ? lo_hi[3] : lo_hi[0];
+    const double py = (c & 2) ? lo_hi[4] : lo_hi[1];
+    const double pz = (c & 4) ? lo_hi[5] : lo_hi[2];
+    const double X = v.R[0] * px + v.R[1] * py + v.R[2] * pz + v.t[0];
+    const double Y = v.R[3] * px + v.R[4] * py + v.R[5] * pz + v.t[1];
+    const double Z = v.R[6] * px + v.R[7] * py + v.R[8] * pz + v.t[2];
+    zmin = fmin(zmin, Z);
+    xmax = fmax(xmax, fabs(X));
+    ymax = fmax(ymax, fabs(Y));
+    p1 = fmax(p1, fabs(px) + fabs(py) + fabs(pz));
+  }
+  const double e = (p1 + (double)w.tmax) * 9.5367431640625e-07 * 1.001;
+  if (!(zmin > 8.0 * e)) return make_float4(0.f, 0.f, 0.f, 0.f);
+  const double zl = zmin - e;  // lower bound of |z| as computed in fp32
+  auto err = [&](double f, double c, double num) {
+    const double a = (num + e) / zl;
+    const double da = e / zl + 2.0 * e * (num + e) / (zl * zl) + 1.2e-7 * a;
+    return 2.0 * (fabs(f) * da + 1.2e-7 * (fabs(f) * a + fabs(c)) + 1e-6);
+  };
+  const double eu = err(w.fx, w.cx, xmax), ev = err(w.fy, w.cy, ymax);
+  if (eu >= 0.25 || ev >= 0.25) return make_float4(0.f, 0.f, 0.f, 0.f);
+  return make_float4((float)(eu * 1.001), (float)(ev * 1.001), (float)e, 1.f);
+}
+
+// classify() with the per-view constant bounds (z > 0 and finite u, v are guaranteed)
+__device__ __forceinline__ int classify_fast(const ViewF& w, const float4& b, const ProjF& q,
+                                             int64_t& didx) {
+  const float du = fabsf(q.u - floorf(q.u) - 0.5f), dv = fabsf(q.v - floorf(q.v) - 0.5f);
+  if (du <= b.x || dv <= b.y) return kAmbiguous;
+  const float ru = rintf(q.u), rv = rintf(q.v);
+  if (!(ru >= 0.f && ru < (float)w.W && rv >= 0.f && rv < (float)w.H)) return kInvisible;
+  didx = w.depth_off + (int64_t)rv * w.W + (int64_t)ru;
+  return kNeedDepth;
+}
+
 // ---- k_tile_prep ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kTile) k_tile_prep(TileParams P) {
   __shared__ ViewF sv[kMaxViewsTC];
   __shared__ pf_view_t sv64[kMaxViewsTC];
   __shared__ int wx0[kMaxViewsTC], wx1[kMaxViewsTC], wy0[kMaxViewsTC], wy1[kMaxViewsTC];
+  __shared__ float4 sbound[kMaxViewsTC];  // per-view constant bounds: eu, ev, e, fast
   const int tid = threadIdx.x, lane = tid & 31;
   for (int j = tid; j < P.nv; j += kTile) {
     sv64[j] = P.views[j];
     sv[j] = make_viewf(P.views[j], P.d);
+    sbound[j] = view_bound(sv[j], P.views[j], P.lo_hi);
     wx0[j] = INT_MAX;
     wy0[j] = INT_MAX;
     wx1[j] = -1;
@@ -163,7 +208,8 @@ __global__ void __launch_bounds__(kTile) k_tile_prep(TileParams P) {
       if (valid && v < P.nv) {
         q[u] = project_f32(sv[v], p.x, p.y, p.z);
         int64_t didx = 0;
-        st[u] = classify(sv[v], q[u], didx);
+        const float4 b = sbound[v];
+        st[u] = b.w > 0.f ? classify_fast(sv[v], b, q[u], didx) : classify(sv[v], q[u], didx);
         if (st[u] == kNeedDepth) stored[u] = __ldg(P.depth + didx);
       }
     }
