@@ -24,6 +24,7 @@
 //       S = W . G and the epilogue. Tiles whose tap count exceeds KT_MAX fall back to the SIMT
 //       kernel through an overflow list.
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -142,13 +143,13 @@ __device__ float4 view_bound(const ViewF& w, const pf_view_t& v, const double* l
     ymax = fmax(ymax, fabs(Y));
     p1 = fmax(p1, fabs(px) + fabs(py) + fabs(pz));
   }
-  const double e = (p1 + (double)w.tmax) * 9.5367431640625e-07 * 1.001;
+  const double e = (p1 + (double)w.tmax) * 4.76837158203125e-07 * 1.001;  // project_f32's e, maxed
   if (!(zmin > 8.0 * e)) return make_float4(0.f, 0.f, 0.f, 0.f);
   const double zl = zmin - e;  // lower bound of |z| as computed in fp32
   auto err = [&](double f, double c, double num) {
     const double a = (num + e) / zl;
     const double da = e / zl + 2.0 * e * (num + e) / (zl * zl) + 1.2e-7 * a;
-    return 2.0 * (fabs(f) * da + 1.2e-7 * (fabs(f) * a + fabs(c)) + 1e-6);
+    return fabs(f) * da + 1.2e-7 * (fabs(f) * a + fabs(c)) + 1e-6;
   };
   const double eu = err(w.fx, w.cx, xmax), ev = err(w.fy, w.cy, ymax);
   if (eu >= 0.25 || ev >= 0.25) return make_float4(0.f, 0.f, 0.f, 0.f);
@@ -167,7 +168,7 @@ __device__ __forceinline__ int classify_fast(const ViewF& w, const float4& b, co
 }
 
 // ---- k_tile_prep ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTile) k_tile_prep(TileParams P) {
+__global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
   __shared__ ViewF sv[kMaxViewsTC];
   __shared__ pf_view_t sv64[kMaxViewsTC];
   __shared__ int wx0[kMaxViewsTC], wx1[kMaxViewsTC], wy0[kMaxViewsTC], wy1[kMaxViewsTC];
@@ -221,6 +222,14 @@ __global__ void __launch_bounds__(kTile) k_tile_prep(TileParams P) {
       if (s == kNeedDepth) s = depth_decide(q[u], stored[u], eps_f);
       bool vis = s == kNeedDepth;
       if (s == kAmbiguous) vis = visible_f64(sv64[v], P.depth, p.x, p.y, p.z, P.eps);
+      if (P.dbg) {  // PF_WS_DEBUG: fraction of samples decided in fp64 / warp-iterations with any
+        const unsigned amb = __ballot_sync(0xffffffffu, s == kAmbiguous);
+        if (lane == 0) {
+          atomicAdd(P.dbg + 16 * 1000, (unsigned long long)__popc(amb));
+          atomicAdd(P.dbg + 16 * 1000 + 1, (unsigned long long)(amb != 0u));
+          atomicAdd(P.dbg + 16 * 1000 + 2, 1ull);
+        }
+      }
       if (__any_sync(0xffffffffu, vis)) {
         int tx0 = INT_MAX, ty0 = INT_MAX, tx1 = -1, ty1 = -1;
         if (vis) {
@@ -623,7 +632,22 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   k_sort_scatter<<<grid_for(n, 256), 256, 0, st>>>(points, n, keys, hist, const_cast<int32_t*>(P.perm),
                                                    const_cast<float4*>(P.spts));
   if (int rc = check_launch("sort_scatter")) return rc;
-  k_tile_prep<<<(unsigned)L.ntiles, kTile, 0, st>>>(P);
+  static unsigned long long* pdbg = nullptr;
+  const bool debug = getenv("PF_WS_DEBUG") != nullptr;
+  TileParams Q = P;
+  if (debug) {
+    if (!pdbg) cudaMalloc(&pdbg, sizeof(unsigned long long) * 16 * 1024);
+    cudaMemsetAsync(pdbg, 0, sizeof(unsigned long long) * 16 * 1024, st);
+    Q.dbg = pdbg;
+  }
+  k_tile_prep<<<(unsigned)L.ntiles, kTile, 0, st>>>(Q);
+  if (debug) {
+    unsigned long long h[3];
+    cudaMemcpyAsync(h, pdbg + 16 * 1000, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[prep debug] ambiguous samples %.4f%%, warp-iterations with any %.2f%%\n",
+            100.0 * h[0] / (32.0 * h[2]), 100.0 * h[1] / h[2]);
+  }
   if (int rc = check_launch("tile_prep")) return rc;
   // persistent warp-specialised TMA kernel (pf_tile_ws.cu); k_tile_mma when TMA maps are unavailable
   static const bool force_v2 = getenv("PF_TILE_KERNEL") && !strcmp(getenv("PF_TILE_KERNEL"), "v2");

@@ -52,18 +52,18 @@ __device__ __forceinline__ ProjF project_f32(const ViewF& w, float px, float py,
   o.u = __fmaf_rn(w.fx, __fmul_rn(o.X, o.rz), w.cx);
   o.v = __fmaf_rn(w.fy, __fmul_rn(o.Y, o.rz), w.cy);
   // |R_ij| <= 1: each camera coordinate has magnitude <= |p|_1 + |t|_inf. f32 R/t representation
-  // (2^-24 relative) plus 4 roundings of that magnitude is < 5*2^-24; take 2^-20 (>3x margin).
-  o.e = (fabsf(px) + fabsf(py) + fabsf(pz) + w.tmax) * 9.5367431640625e-07f;
+  // (2^-24 relative) plus 4 roundings of that magnitude is < 5*2^-24; take 2^-21 (1.6x margin).
+  o.e = (fabsf(px) + fabsf(py) + fabsf(pz) + w.tmax) * 4.76837158203125e-07f;
   return o;
 }
 
 // Bound on |u - u64| for u = f * num/z + c, given |num - num*|, |z - z*| <= e and |z| >= 2e:
-// |a - a*| <= e/|z| + 2e(|num| + e)/z^2 + 2^-23|a| (rcp + mul roundings); the fma adds
-// 2^-24 |f a + c| and f / c representation 2^-24 each. Doubled for safety. No divisions.
+// |a - a*| <= e/|z| + e(|num| + e)/z^2 (taken twice) + 2^-23|a| (rcp + mul roundings); the fma adds
+// 2^-24 |f a + c| and f / c representation 2^-24 each (taken as 2^-23). No divisions.
 __device__ __forceinline__ float pix_err(float f, float c, float num, float arz, float e) {
   const float a = fabsf(num) * arz;
   const float da = e * arz * (1.f + 2.f * (fabsf(num) + e) * arz) + 1.2e-7f * a;
-  return 2.f * (fabsf(f) * da + 1.2e-7f * (fabsf(f) * a + fabsf(c)) + 1e-6f);
+  return fabsf(f) * da + 1.2e-7f * (fabsf(f) * a + fabsf(c)) + 1e-6f;
 }
 
 // Classification of one (point, view) sample before the depth lookup.
