@@ -208,26 +208,47 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_prep(TileParams P) {
   const float eps_f = (float)P.eps;
   double lo[3];
   const double edge = voxel_edge(P.lo_hi, P.grid, lo);
-  for (int pt = warp * 32; pt < warp * 32 + 32; ++pt) {
-    const int64_t jpt = tile * kTile + pt;
-    if (jpt >= P.n) break;  // warp-uniform
-    const float4 p = spts_s[pt];
-    const int32_t i = sperm[pt];
-    int cnt = 0;
+  // two points per iteration: four independent depth loads per lane in flight
+  for (int pt0 = warp * 32; pt0 < warp * 32 + 32; pt0 += 2) {
+    if (tile * kTile + pt0 >= P.n) break;  // warp-uniform
+    ProjF q[2][2];
+    int st[2][2];
+    float stored[2][2];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      if (r >= nround) break;
-      const int v = lane + 32 * r;
-      bool vis = false;
-      if (v < P.nv) {
-        const ProjF q = project_f32(vw[r], p.x, p.y, p.z);
-        int64_t didx = 0;
-        int s = vb[r].w > 0.f ? classify_fast(vw[r], vb[r], q, didx) : classify(vw[r], q, didx);
-        if (s == kNeedDepth) s = depth_decide(q, __ldg(P.depth + didx), eps_f);
-        vis = s == kNeedDepth;
+    for (int a = 0; a < 2; ++a) {
+      const int64_t jpt = tile * kTile + pt0 + a;
+      const float4 p = spts_s[pt0 + a];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int v = lane + 32 * r;
+        st[a][r] = kInvisible;
+        stored[a][r] = 0.f;
+        if (jpt < P.n && r < nround && v < P.nv) {
+          q[a][r] = project_f32(vw[r], p.x, p.y, p.z);
+          int64_t didx = 0;
+          st[a][r] = vb[r].w > 0.f ? classify_fast(vw[r], vb[r], q[a][r], didx) : classify(vw[r], q[a][r], didx);
+          if (st[a][r] == kNeedDepth) stored[a][r] = __ldg(P.depth + didx);
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int pt = pt0 + a;
+      const int64_t jpt = tile * kTile + pt;
+      if (jpt >= P.n) break;  // warp-uniform
+      const float4 p = spts_s[pt];
+      const int32_t i = sperm[pt];
+      int cnt = 0;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (r >= nround) break;
+        const int v = lane + 32 * r;
+        int s = st[a][r];
+        if (s == kNeedDepth) s = depth_decide(q[a][r], stored[a][r], eps_f);
+        bool vis = s == kNeedDepth;
         if (s == kAmbiguous) vis = visible_f64(P.views[v], P.depth, p.x, p.y, p.z, P.eps);  // rare
         if (P.dbg) {  // PF_WS_DEBUG: fraction of samples decided in fp64 / warp-iterations with any
-          const unsigned amb = __ballot_sync(__activemask(), s == kAmbiguous);
+          const unsigned amb = __ballot_sync(0xffffffffu, s == kAmbiguous);
           if (lane == 0) {
             atomicAdd(P.dbg + 16 * 1000, (unsigned long long)__popc(amb));
             atomicAdd(P.dbg + 16 * 1000 + 1, (unsigned long long)(amb != 0u));
@@ -235,20 +256,20 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_prep(TileParams P) {
           }
         }
         if (vis) {
-          const TapF t = taps_f32(vw[r], q.u, q.v);
+          const TapF t = taps_f32(vw[r], q[a][r].u, q[a][r].v);
           mx0[r] = min(mx0[r], t.x0);
           my0[r] = min(my0[r], t.y0);
           mx1[r] = max(mx1[r], t.x0 + t.dx);
           my1[r] = max(my1[r], t.y0 + t.dy);
         }
+        const uint32_t bits = __ballot_sync(0xffffffffu, vis);
+        cnt += __popc(bits);
+        if (lane == 0) P.mask_bits[(int64_t)i * P.nwords + r] = bits;
       }
-      const uint32_t bits = __ballot_sync(0xffffffffu, vis);
-      cnt += __popc(bits);
-      if (lane == 0) P.mask_bits[(int64_t)i * P.nwords + r] = bits;
-    }
-    if (lane == 0) {
-      P.counts[i] = cnt;
-      P.codes[i] = voxel_code(p.x, p.y, p.z, lo, edge, P.grid);
+      if (lane == 0) {
+        P.counts[i] = cnt;
+        P.codes[i] = voxel_code(p.x, p.y, p.z, lo, edge, P.grid);
+      }
     }
   }
 #pragma unroll
