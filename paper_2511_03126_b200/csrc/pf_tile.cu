@@ -208,6 +208,8 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_prep(TileParams P) {
   const float eps_f = (float)P.eps;
   double lo[3];
   const double edge = voxel_edge(P.lo_hi, P.grid, lo);
+  uint32_t my_bits[2] = {0u, 0u};
+  int my_cnt = 0;
   // two points per iteration: four independent depth loads per lane in flight
   for (int pt0 = warp * 32; pt0 < warp * 32 + 32; pt0 += 2) {
     if (tile * kTile + pt0 >= P.n) break;  // warp-uniform
@@ -264,12 +266,22 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_prep(TileParams P) {
         }
         const uint32_t bits = __ballot_sync(0xffffffffu, vis);
         cnt += __popc(bits);
-        if (lane == 0) P.mask_bits[(int64_t)i * P.nwords + r] = bits;
+        if (lane == pt - warp * 32) my_bits[r] = bits;
       }
-      if (lane == 0) {
-        P.counts[i] = cnt;
-        P.codes[i] = voxel_code(p.x, p.y, p.z, lo, edge, P.grid);
-      }
+      if (lane == pt - warp * 32) my_cnt = cnt;
+      (void)i;
+      (void)p;
+    }
+  }
+  {  // per-point outputs: lane l owns the warp's l-th point (coalesced-ish, and the fp64 voxel
+     // code runs on all 32 lanes instead of lane 0)
+    const int pt = warp * 32 + lane;
+    if (tile * kTile + pt < P.n) {
+      const int32_t i = sperm[pt];
+      const float4 p = spts_s[pt];
+      for (int r = 0; r < nround; ++r) P.mask_bits[(int64_t)i * P.nwords + r] = my_bits[r];
+      P.counts[i] = my_cnt;
+      P.codes[i] = voxel_code(p.x, p.y, p.z, lo, edge, P.grid);
     }
   }
 #pragma unroll
