@@ -168,131 +168,96 @@ __device__ __forceinline__ int classify_fast(const ViewF& w, const float4& b, co
 }
 
 // ---- k_tile_prep ---------------------------------------------------------------------------------------
-// One CTA per tile of 128 sorted points, 4 warps; each warp takes 32 of the tile's points in turn
-// and its lanes take the views (lane = view, two rounds for 33..64 views), so every lane keeps its
-// view's camera, bounds and tap window in registers: no per-sample shared-memory reads of view
-// parameters and no per-sample warp reductions. The visibility bitset word of a point is one ballot.
-__global__ void __launch_bounds__(kTile, 4) k_tile_prep(TileParams P) {
+__global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
+  __shared__ ViewF sv[kMaxViewsTC];
+  __shared__ pf_view_t sv64[kMaxViewsTC];
   __shared__ int wx0[kMaxViewsTC], wx1[kMaxViewsTC], wy0[kMaxViewsTC], wy1[kMaxViewsTC];
-  __shared__ float4 spts_s[kTile];
-  __shared__ int32_t sperm[kTile];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t tile = blockIdx.x;
+  __shared__ float4 sbound[kMaxViewsTC];  // per-view constant bounds: eu, ev, e, fast
+  const int tid = threadIdx.x, lane = tid & 31;
   for (int j = tid; j < P.nv; j += kTile) {
+    sv64[j] = P.views[j];
+    sv[j] = make_viewf(P.views[j], P.d);
+    sbound[j] = view_bound(sv[j], P.views[j], P.lo_hi);
     wx0[j] = INT_MAX;
     wy0[j] = INT_MAX;
     wx1[j] = -1;
     wy1[j] = -1;
   }
-  {
-    const int64_t jpt = tile * kTile + tid;
-    if (jpt < P.n) {
-      spts_s[tid] = P.spts[jpt];
-      sperm[tid] = P.perm[jpt];
-    }
-  }
-  // this lane's views: v0 = lane, v1 = lane + 32 (when present)
-  const int nround = P.nwords;  // 1 or 2
-  ViewF vw[2];
-  float4 vb[2];
-  int mx0[2] = {INT_MAX, INT_MAX}, my0[2] = {INT_MAX, INT_MAX}, mx1[2] = {-1, -1}, my1[2] = {-1, -1};
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int v = lane + 32 * r;
-    if (r < nround && v < P.nv) {
-      vw[r] = make_viewf(P.views[v], P.d);
-      vb[r] = view_bound(vw[r], P.views[v], P.lo_hi);
-    }
-  }
   __syncthreads();
+  const int64_t tile = blockIdx.x;
+  const int64_t jpt = tile * kTile + tid;
+  const bool valid = jpt < P.n;
+  float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+  int32_t i = 0;
+  if (valid) {
+    p = P.spts[jpt];
+    i = P.perm[jpt];
+  }
   const float eps_f = (float)P.eps;
-  double lo[3];
-  const double edge = voxel_edge(P.lo_hi, P.grid, lo);
-  uint32_t my_bits[2] = {0u, 0u};
-  int my_cnt = 0;
-  // two points per iteration: four independent depth loads per lane in flight
-  for (int pt0 = warp * 32; pt0 < warp * 32 + 32; pt0 += 2) {
-    if (tile * kTile + pt0 >= P.n) break;  // warp-uniform
-    ProjF q[2][2];
-    int st[2][2];
-    float stored[2][2];
+  uint32_t words[kMaxViewsTC / 32] = {0u, 0u};
+  int cnt = 0;
+  constexpr int U = 4;  // views in flight per thread (independent depth loads)
+  for (int v0 = 0; v0 < P.nv; v0 += U) {
+    ProjF q[U];
+    int st[U];
+    float stored[U];
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const int64_t jpt = tile * kTile + pt0 + a;
-      const float4 p = spts_s[pt0 + a];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int v = lane + 32 * r;
-        st[a][r] = kInvisible;
-        stored[a][r] = 0.f;
-        if (jpt < P.n && r < nround && v < P.nv) {
-          q[a][r] = project_f32(vw[r], p.x, p.y, p.z);
-          int64_t didx = 0;
-          st[a][r] = vb[r].w > 0.f ? classify_fast(vw[r], vb[r], q[a][r], didx) : classify(vw[r], q[a][r], didx);
-          if (st[a][r] == kNeedDepth) stored[a][r] = __ldg(P.depth + didx);
-        }
+    for (int u = 0; u < U; ++u) {
+      st[u] = kInvisible;
+      stored[u] = 0.f;
+      const int v = v0 + u;
+      if (valid && v < P.nv) {
+        q[u] = project_f32(sv[v], p.x, p.y, p.z);
+        int64_t didx = 0;
+        const float4 b = sbound[v];
+        st[u] = b.w > 0.f ? classify_fast(sv[v], b, q[u], didx) : classify(sv[v], q[u], didx);
+        if (st[u] == kNeedDepth) stored[u] = __ldg(P.depth + didx);
       }
     }
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const int pt = pt0 + a;
-      const int64_t jpt = tile * kTile + pt;
-      if (jpt >= P.n) break;  // warp-uniform
-      const float4 p = spts_s[pt];
-      const int32_t i = sperm[pt];
-      int cnt = 0;
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        if (r >= nround) break;
-        const int v = lane + 32 * r;
-        int s = st[a][r];
-        if (s == kNeedDepth) s = depth_decide(q[a][r], stored[a][r], eps_f);
-        bool vis = s == kNeedDepth;
-        if (s == kAmbiguous) vis = visible_f64(P.views[v], P.depth, p.x, p.y, p.z, P.eps);  // rare
-        if (P.dbg) {  // PF_WS_DEBUG: fraction of samples decided in fp64 / warp-iterations with any
-          const unsigned amb = __ballot_sync(0xffffffffu, s == kAmbiguous);
-          if (lane == 0) {
-            atomicAdd(P.dbg + 16 * 1000, (unsigned long long)__popc(amb));
-            atomicAdd(P.dbg + 16 * 1000 + 1, (unsigned long long)(amb != 0u));
-            atomicAdd(P.dbg + 16 * 1000 + 2, 1ull);
-          }
+    for (int u = 0; u < U; ++u) {
+      const int v = v0 + u;
+      if (v >= P.nv) break;
+      int s = st[u];
+      if (s == kNeedDepth) s = depth_decide(q[u], stored[u], eps_f);
+      bool vis = s == kNeedDepth;
+      if (s == kAmbiguous) vis = visible_f64(sv64[v], P.depth, p.x, p.y, p.z, P.eps);
+      if (P.dbg) {  // PF_WS_DEBUG: fraction of samples decided in fp64 / warp-iterations with any
+        const unsigned amb = __ballot_sync(0xffffffffu, s == kAmbiguous);
+        if (lane == 0) {
+          atomicAdd(P.dbg + 16 * 1000, (unsigned long long)__popc(amb));
+          atomicAdd(P.dbg + 16 * 1000 + 1, (unsigned long long)(amb != 0u));
+          atomicAdd(P.dbg + 16 * 1000 + 2, 1ull);
         }
+      }
+      if (__any_sync(0xffffffffu, vis)) {
+        int tx0 = INT_MAX, ty0 = INT_MAX, tx1 = -1, ty1 = -1;
         if (vis) {
-          const TapF t = taps_f32(vw[r], q[a][r].u, q[a][r].v);
-          mx0[r] = min(mx0[r], t.x0);
-          my0[r] = min(my0[r], t.y0);
-          mx1[r] = max(mx1[r], t.x0 + t.dx);
-          my1[r] = max(my1[r], t.y0 + t.dy);
+          const TapF t = taps_f32(sv[v], q[u].u, q[u].v);
+          tx0 = t.x0;
+          ty0 = t.y0;
+          tx1 = t.x0 + t.dx;
+          ty1 = t.y0 + t.dy;
+          words[v >> 5] |= 1u << (v & 31);
+          ++cnt;
         }
-        const uint32_t bits = __ballot_sync(0xffffffffu, vis);
-        cnt += __popc(bits);
-        if (lane == pt - warp * 32) my_bits[r] = bits;
+        const int ax0 = __reduce_min_sync(0xffffffffu, tx0), ay0 = __reduce_min_sync(0xffffffffu, ty0);
+        const int ax1 = __reduce_max_sync(0xffffffffu, tx1), ay1 = __reduce_max_sync(0xffffffffu, ty1);
+        if (lane == 0) {
+          atomicMin(wx0 + v, ax0);
+          atomicMin(wy0 + v, ay0);
+          atomicMax(wx1 + v, ax1);
+          atomicMax(wy1 + v, ay1);
+        }
       }
-      if (lane == pt - warp * 32) my_cnt = cnt;
-      (void)i;
-      (void)p;
     }
   }
-  {  // per-point outputs: lane l owns the warp's l-th point (coalesced-ish, and the fp64 voxel
-     // code runs on all 32 lanes instead of lane 0)
-    const int pt = warp * 32 + lane;
-    if (tile * kTile + pt < P.n) {
-      const int32_t i = sperm[pt];
-      const float4 p = spts_s[pt];
-      for (int r = 0; r < nround; ++r) P.mask_bits[(int64_t)i * P.nwords + r] = my_bits[r];
-      P.counts[i] = my_cnt;
-      P.codes[i] = voxel_code(p.x, p.y, p.z, lo, edge, P.grid);
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int v = lane + 32 * r;
-    if (r < nround && v < P.nv && mx1[r] >= 0) {
-      atomicMin(wx0 + v, mx0[r]);
-      atomicMin(wy0 + v, my0[r]);
-      atomicMax(wx1 + v, mx1[r]);
-      atomicMax(wy1 + v, my1[r]);
-    }
+  if (valid) {
+    for (int w = 0; w < P.nwords; ++w) P.mask_bits[(int64_t)i * P.nwords + w] = words[w];
+    P.counts[i] = cnt;
+    double lo[3];
+    const double edge = voxel_edge(P.lo_hi, P.grid, lo);
+    P.codes[i] = voxel_code(p.x, p.y, p.z, lo, edge, P.grid);
   }
   __syncthreads();
   if (tid == 0) {
@@ -308,6 +273,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_prep(TileParams P) {
       desc[v] = make_uint2((uint32_t)min(base, 65535) | ((uint32_t)x0 << 16) | ((uint32_t)y0 << 24),
                            (uint32_t)w | ((uint32_t)h << 8));
       base += w * h;
+
     }
     P.tile_kt[tile] = base;
   }
