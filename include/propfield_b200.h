@@ -208,9 +208,10 @@ int pf_fuse_query(const pf_fuse_args_t* args, void* stream);
  * ------------------------------------------------------------------------------------------- */
 
 /* C (128,n) f32 = A (128,k) bf16 row-major @ B (k,n) bf16 row-major through the tile kernel's
- * tcgen05 operand layouts / descriptors / TMEM read-back. k % 64 == 0 (<= 256), n % 16 == 0. */
+ * tcgen05 operand layouts / descriptors / TMEM read-back. k % 64 == 0 (<= 256), n % 16 == 0.
+ * ts != 0: A is first copied to TMEM with tcgen05.cp and the MMAs read A from TMEM. */
 int pf_selftest_umma(const void* a_bf16, const void* b_bf16, float* c, int32_t k, int32_t n,
-                     void* stream);
+                     int32_t ts, void* stream);
 
 /* TMA window load diagnostic: a (64 ch, bw, bh) box of an (hf, wf, 64) bf16 map at (x0, y0) is
  * loaded with the tile kernel's tensor-map settings (128-B swizzle) into shared memory at

@@ -113,7 +113,7 @@ SIGNATURES = {
     "pf_fuse_workspace_bytes": ([C.POINTER(FuseArgs)], C.c_uint64),
     "pf_fuse_prepare": ([C.POINTER(FuseArgs), _P], C.c_int),
     "pf_fuse_query": ([C.POINTER(FuseArgs), _P], C.c_int),
-    "pf_selftest_umma": ([_P, _P, _P, _I32, _I32, _P], C.c_int),
+    "pf_selftest_umma": ([_P, _P, _P, _I32, _I32, _I32, _P], C.c_int),
     "pf_selftest_tma": ([_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P], C.c_int),
 }
 

@@ -151,11 +151,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     tc::mbar_init(&S.s_empty, kAccThreads);
   }
   if (warp == kAccWarp0) tc::tmem_alloc(&S.tmem_base, 512);
+  static_assert(2 * 128 + 128 + kKtWs / 2 <= 512, "TMEM: D buffers + S + A");
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = S.tmem_base;
-  const uint32_t tS = tbase + 128u * kDBufs;
+  const uint32_t tS = tbase + 128u * kDBufs;            // S: 128 columns
+  const uint32_t tA = tS + 128u;                        // A (bf16 pairs): kKtWs / 2 columns
 
   if (warp < kLoadWarps) {
     // ================= B loaders =================
@@ -244,6 +246,18 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const int ab = t_local & 1;
       WS_WAIT(&S.a_full[ab], (t_local >> 1) & 1u, 1);
       const uint32_t a0 = tc::smem_u32(sA + ab * kABytes);
+      // A (the tile's bilinear weights) into TMEM once per tile (tcgen05.cp, 128 rows x 16 k per
+      // op); the MMAs then read A from TMEM and only B from shared memory. The copies execute in
+      // issue order after the previous tile's MMAs, so one TMEM A region suffices; the commit
+      // releases the shared-memory A buffer to the builders as soon as the copies are done.
+      tc::fence_after_sync();
+      if (lane == 0) {
+        for (int s = 0; s < ktp / 16; ++s)
+          tc::tmem_cp_128x256b(tA + (uint32_t)(s * 8),
+                               tc::smem_desc_sw128(a0 + (s >> 2) * kTile * 128 + (s & 3) * 32, 16, 1024));
+        tc::mma_commit(&S.a_empty[ab]);
+      }
+      __syncwarp();
       for (int c = 0; c < nch; c += 2) {
         WS_WAIT(&S.b_full[stage], phase, 2);
         WS_WAIT(&S.b_full[stage + 1], phase, 2);
@@ -263,17 +277,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           // (loaders and builders fence their generic-proxy writes before arriving)
           const uint32_t b0 = tc::smem_u32(sB + stage * kStageBytes);
           for (int s = 0; s < ktp / 16; ++s) {
-            const uint64_t ad = tc::smem_desc_sw128(a0 + (s >> 2) * kTile * 128 + (s & 3) * 32, 16, 1024);
             const uint64_t bd = tc::smem_desc_sw128(b0 + s * 2048, kStageBytes, 1024);
-            tc::mma_bf16(dst, ad, bd, idesc, s > 0 ? 1u : 0u);
+            tc::mma_bf16_ts(dst, tA + (uint32_t)(s * 8), bd, idesc, s > 0 ? 1u : 0u);
           }
           tc::mma_commit(&S.b_empty[stage]);
           tc::mma_commit(&S.b_empty[stage + 1]);
           if (c < nd) tc::mma_commit(&S.d_full[db]);
-          if (c + 2 >= nch) {
-            tc::mma_commit(&S.s_full);
-            tc::mma_commit(&S.a_empty[ab]);
-          }
+          if (c + 2 >= nch) tc::mma_commit(&S.s_full);
         }
         __syncwarp();
         issue_cyc += clock64() - ti0;

@@ -213,8 +213,9 @@ class TestVoxelMass:
 
 
 class TestTensorCorePlumbing:
-    @pytest.mark.parametrize("k,n", [(64, 128), (128, 128), (256, 64), (192, 256), (64, 16)])
-    def test_umma_selftest_matches_matmul(self, cuda, k, n):
+    @pytest.mark.parametrize("ts", [0, 1])
+    @pytest.mark.parametrize("k,n", [(64, 128), (128, 128), (256, 64), (192, 128), (64, 16)])
+    def test_umma_selftest_matches_matmul(self, cuda, k, n, ts):
         import torch
 
         from paper_2511_03126_b200 import _lib
@@ -223,7 +224,7 @@ class TestTensorCorePlumbing:
         a = torch.randn(128, k, device="cuda", generator=g).to(torch.bfloat16)
         b = torch.randn(k, n, device="cuda", generator=g).to(torch.bfloat16)
         c = torch.empty(128, n, device="cuda", dtype=torch.float32)
-        _lib.call("pf_selftest_umma", a.data_ptr(), b.data_ptr(), c.data_ptr(), k, n,
+        _lib.call("pf_selftest_umma", a.data_ptr(), b.data_ptr(), c.data_ptr(), k, n, ts,
                   torch.cuda.current_stream().cuda_stream)
         ref = a.float() @ b.float()
         torch.testing.assert_close(c, ref, rtol=1e-5, atol=1e-4)
