@@ -42,8 +42,10 @@ constexpr int kAccWarp0 = 5;           // warps 5-12: accumulators (2 per TMEM l
 constexpr int kAccThreads = 256;
 constexpr int kBuildWarp0 = 13;        // warps 13-16: A builders
 constexpr int kWsThreads = 544;        // 17 warps
-constexpr int kDBufs = 2;              // TMEM feature buffers (128 columns = 2 chunks each)
-constexpr int kStages = 4;             // B ring depth
+constexpr int kCG = 2;                 // 64-column B chunks per MMA group (N = 64 * kCG)
+constexpr int kDCols = 64 * kCG;       // TMEM columns of one feature buffer
+constexpr int kDBufs = 256 / kDCols;   // TMEM feature buffers (256 columns in total)
+constexpr int kStages = 6;             // B ring depth (3 chunk groups)
 constexpr int kKtWs = 192;             // taps per tile held in one A buffer / B stage
 constexpr int kStageBytes = kKtWs * 128;
 constexpr int kABytes = kTile * ((kKtWs + 63) / 64) * 64 * 2;  // whole 64-column swizzle atoms
@@ -110,7 +112,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* sA = smem;                     // 2 x [128 rows x kKtWs] bf16
-  unsigned char* sB = smem + 2 * kABytes;       // kStages x [kKtWs rows x 128 B]
+  unsigned char* sB = smem + kABytes;           // kStages x [kKtWs rows x 128 B]
   __shared__ WsShared S;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -151,12 +153,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     tc::mbar_init(&S.s_empty, kAccThreads);
   }
   if (warp == kAccWarp0) tc::tmem_alloc(&S.tmem_base, 512);
-  static_assert(2 * 128 + 128 + kKtWs / 2 <= 512, "TMEM: D buffers + S + A");
+  static_assert(256 + 128 + kKtWs / 2 <= 512, "TMEM: D buffers + S + A");
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = S.tmem_base;
-  const uint32_t tS = tbase + 128u * kDBufs;            // S: 128 columns
+  const uint32_t tS = tbase + 256u;                     // S: 128 columns
   const uint32_t tA = tS + 128u;                        // A (bf16 pairs): kKtWs / 2 columns
 
   if (warp < kLoadWarps) {
@@ -238,13 +240,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     uint32_t phase = 0;
     uint32_t dcount = 0;  // feature chunk pairs issued so far (selects the TMEM D buffer)
     uint32_t t_local = 0, s_phase = 0;
-    const uint32_t idesc = tc::idesc_bf16_f32(128, 128, false, true);
+    const uint32_t idesc = tc::idesc_bf16_f32(128, kDCols, false, true);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       bool ok;
       const int ktp = tile_ktp(P, tile, ok);
       if (!ok) continue;
-      const int ab = t_local & 1;
-      WS_WAIT(&S.a_full[ab], (t_local >> 1) & 1u, 1);
+      const int ab = 0;  // one shared-memory A buffer: it is free once the tcgen05.cp to TMEM is done
+      WS_WAIT(&S.a_full[ab], t_local & 1u, 1);
       const uint32_t a0 = tc::smem_u32(sA + ab * kABytes);
       // A (the tile's bilinear weights) into TMEM once per tile (tcgen05.cp, 128 rows x 16 k per
       // op); the MMAs then read A from TMEM and only B from shared memory. The copies execute in
@@ -258,18 +260,18 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         tc::mma_commit(&S.a_empty[ab]);
       }
       __syncwarp();
-      for (int c = 0; c < nch; c += 2) {
-        WS_WAIT(&S.b_full[stage], phase, 2);
-        WS_WAIT(&S.b_full[stage + 1], phase, 2);
+      for (int c = 0; c < nch; c += kCG) {
+#pragma unroll
+        for (int g = 0; g < kCG; ++g) WS_WAIT(&S.b_full[stage + g], phase, 2);
         uint32_t dst;
         int db = 0;
         if (c < nd) {
           db = dcount % kDBufs;
           WS_WAIT(&S.d_empty[db], ((dcount / kDBufs) & 1u) ^ 1u, 3);
-          dst = tbase + (uint32_t)(db * 128);
+          dst = tbase + (uint32_t)(db * kDCols);
         } else {
-          WS_WAIT(&S.s_empty, s_phase ^ 1u, 4);
-          dst = tS;
+          if (c == nd) WS_WAIT(&S.s_empty, s_phase ^ 1u, 4);
+          dst = tS + (uint32_t)(64 * (c - nd));
         }
         tc::fence_after_sync();
         const long long ti0 = clock64();
@@ -280,15 +282,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
             const uint64_t bd = tc::smem_desc_sw128(b0 + s * 2048, kStageBytes, 1024);
             tc::mma_bf16_ts(dst, tA + (uint32_t)(s * 8), bd, idesc, s > 0 ? 1u : 0u);
           }
-          tc::mma_commit(&S.b_empty[stage]);
-          tc::mma_commit(&S.b_empty[stage + 1]);
+#pragma unroll
+          for (int g = 0; g < kCG; ++g) tc::mma_commit(&S.b_empty[stage + g]);
           if (c < nd) tc::mma_commit(&S.d_full[db]);
-          if (c + 2 >= nch) tc::mma_commit(&S.s_full);
+          if (c + kCG >= nch) tc::mma_commit(&S.s_full);
         }
         __syncwarp();
         issue_cyc += clock64() - ti0;
         if (c < nd) ++dcount;
-        stage += 2;
+        stage += kCG;
         if (stage == kStages) { stage = 0; phase ^= 1u; }
       }
       s_phase ^= 1u;
@@ -302,8 +304,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       bool ok;
       const int ktp = tile_ktp(P, tile, ok);
       if (!ok) continue;
-      const int ab = t_local & 1;
-      WS_WAIT(&S.a_empty[ab], ((t_local >> 1) & 1u) ^ 1u, 5);
+      const int ab = 0;
+      WS_WAIT(&S.a_empty[ab], (t_local & 1u) ^ 1u, 5);
       uint2* sdesc = S.desc_a[ab];
       for (int v = row; v < P.nv; v += 128) sdesc[v] = P.tile_desc[tile * P.nv + v];
       unsigned char* A = sA + ab * kABytes;
@@ -366,30 +368,31 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const int count = valid ? P.counts[i] : 0;
       const float invc = count > 0 ? 1.f / (float)count : 0.f;
       float ss0 = 0.f, ss1 = 0.f, ss2 = 0.f, ss3 = 0.f;
-      for (int c = 0; c < nd; c += 2) {  // 128-column pair: this half drains 64 columns
+      for (int c = 0; c < nd; c += kCG) {  // kCG chunks: this half drains kDCols / 2 columns
         const int db = dcount % kDBufs;
         WS_WAIT(&S.d_full[db], (dcount / kDBufs) & 1u, 6);
         tc::fence_after_sync();
-        float v[32], u[32];
-        tc::tmem_ld32(tbase + (uint32_t)(db * 128 + half * 64) + t_lane, v);
-        tc::tmem_ld32(tbase + (uint32_t)(db * 128 + half * 64 + 32) + t_lane, u);
+        float v[kCG][32];
+#pragma unroll
+        for (int g = 0; g < kCG; ++g)
+          tc::tmem_ld32(tbase + (uint32_t)(db * kDCols + half * (kDCols / 2) + 32 * g) + t_lane, v[g]);
         tc::fence_before_sync();
         mbar_arrive(&S.d_empty[db]);  // data is in registers: release the buffer early
 #pragma unroll
-        for (int q = 0; q < 32; q += 2) {
-          ss0 = fmaf(v[q], v[q], ss0);
-          ss1 = fmaf(v[q + 1], v[q + 1], ss1);
-          ss2 = fmaf(u[q], u[q], ss2);
-          ss3 = fmaf(u[q + 1], u[q + 1], ss3);
-        }
-        if (P.features && valid) {
-          float* dst = P.features + (int64_t)i * P.d + c * 64 + half * 64;
+        for (int g = 0; g < kCG; ++g) {
 #pragma unroll
           for (int q = 0; q < 32; q += 4) {
-            *reinterpret_cast<float4*>(dst + q) =
-                make_float4(v[q] * invc, v[q + 1] * invc, v[q + 2] * invc, v[q + 3] * invc);
-            *reinterpret_cast<float4*>(dst + 32 + q) =
-                make_float4(u[q] * invc, u[q + 1] * invc, u[q + 2] * invc, u[q + 3] * invc);
+            ss0 = fmaf(v[g][q], v[g][q], ss0);
+            ss1 = fmaf(v[g][q + 1], v[g][q + 1], ss1);
+            ss2 = fmaf(v[g][q + 2], v[g][q + 2], ss2);
+            ss3 = fmaf(v[g][q + 3], v[g][q + 3], ss3);
+          }
+          if (P.features && valid) {
+            float* dst = P.features + (int64_t)i * P.d + c * 64 + half * (kDCols / 2) + 32 * g;
+#pragma unroll
+            for (int q = 0; q < 32; q += 4)
+              *reinterpret_cast<float4*>(dst + q) =
+                  make_float4(v[g][q] * invc, v[g][q + 1] * invc, v[g][q + 2] * invc, v[g][q + 3] * invc);
           }
         }
         ++dcount;
@@ -571,7 +574,7 @@ bool encode_window_map(CUtensorMap* m, const void* base, int cols, int wf, int r
 
 int ws_kt_max() { return kKtWs; }
 
-size_t ws_smem_bytes() { return 2 * (size_t)kABytes + (size_t)kStages * kStageBytes + 1024; }
+size_t ws_smem_bytes() { return (size_t)kABytes + (size_t)kStages * kStageBytes + 1024; }
 
 // Launch the persistent kernel (one CTA per SM).
 int run_tile_ws(const TileParams& P, int hf, int wf, int nv, cudaStream_t st) {
