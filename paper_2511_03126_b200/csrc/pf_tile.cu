@@ -167,6 +167,42 @@ __device__ __forceinline__ int classify_fast(const ViewF& w, const float4& b, co
   return kNeedDepth;
 }
 
+// Tile-level occlusion cull for one view (exact): the tile's points lie in the box [lo, hi]; their
+// camera depth is >= the minimum over the box corners (z is affine) and their pixels fall inside
+// the projected corners' bounding rectangle (perspective maps a box in front of the camera into
+// the convex hull of its projected corners). If every stored depth in that rectangle (+1 px) plus
+// eps is below the box's minimum depth, no point of the tile can pass the depth test in this view
+// (out-of-image and invalid pixels fail it anyway), so the per-point work is skipped.
+__device__ bool tile_occluded(const pf_view_t& v, const float* __restrict__ depth, const float* lo,
+                              const float* hi, double eps) {
+  double zmin = 1e300, umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300;
+  for (int c = 0; c < 8; ++c) {
+    const double px = (c & 1) ? hi[0] : lo[0];
+    const double py = (c & 2) ? hi[1] : lo[1];
+    const double pz = (c & 4) ? hi[2] : lo[2];
+    const double X = v.R[0] * px + v.R[1] * py + v.R[2] * pz + v.t[0];
+    const double Y = v.R[3] * px + v.R[4] * py + v.R[5] * pz + v.t[1];
+    const double Z = v.R[6] * px + v.R[7] * py + v.R[8] * pz + v.t[2];
+    if (!(Z > 1e-6)) return false;
+    zmin = fmin(zmin, Z);
+    const double u = v.fx * X / Z + v.cx, w = v.fy * Y / Z + v.cy;
+    umin = fmin(umin, u);
+    umax = fmax(umax, u);
+    vmin = fmin(vmin, w);
+    vmax = fmax(vmax, w);
+  }
+  const int x0 = (int)fmax(floor(umin) - 1.0, 0.0), x1 = (int)fmin(ceil(umax) + 1.0, (double)(v.W - 1));
+  const int y0 = (int)fmax(floor(vmin) - 1.0, 0.0), y1 = (int)fmin(ceil(vmax) + 1.0, (double)(v.H - 1));
+  if (umax < -1.0 || vmax < -1.0 || umin > (double)v.W || vmin > (double)v.H) return true;  // off-image
+  if (x1 < x0 || y1 < y0) return true;
+  if ((x1 - x0 + 1) * (y1 - y0 + 1) > 256) return false;
+  const float* d = depth + v.depth_offset;
+  float dmax = 0.f;
+  for (int y = y0; y <= y1; ++y)
+    for (int x = x0; x <= x1; ++x) dmax = fmaxf(dmax, __ldg(d + (int64_t)y * v.W + x));
+  return zmin > (double)dmax + eps + 1e-7;
+}
+
 // ---- k_tile_prep ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
   __shared__ ViewF sv[kMaxViewsTC];
@@ -194,10 +230,49 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     i = P.perm[jpt];
   }
   const float eps_f = (float)P.eps;
+  // tile bbox -> per-view occlusion cull -> compact list of views that need per-point tests
+  __shared__ float sbb[kTile / 32][6];
+  __shared__ int s_views_list[kMaxViewsTC];
+  __shared__ int s_nlist;
+  {
+    float b[6] = {valid ? p.x : INFINITY, valid ? p.y : INFINITY, valid ? p.z : INFINITY,
+                  valid ? p.x : -INFINITY, valid ? p.y : -INFINITY, valid ? p.z : -INFINITY};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        b[a] = fminf(b[a], __shfl_xor_sync(0xffffffffu, b[a], o));
+        b[a + 3] = fmaxf(b[a + 3], __shfl_xor_sync(0xffffffffu, b[a + 3], o));
+      }
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int a = 0; a < 6; ++a) sbb[tid >> 5][a] = b[a];
+  }
+  __syncthreads();
+  __shared__ unsigned char s_keep[kMaxViewsTC];
+  if (tid < P.nv) {
+    float lo[3], hi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = fminf(fminf(sbb[0][a], sbb[1][a]), fminf(sbb[2][a], sbb[3][a]));
+      hi[a] = fmaxf(fmaxf(sbb[0][a + 3], sbb[1][a + 3]), fmaxf(sbb[2][a + 3], sbb[3][a + 3]));
+    }
+    s_keep[tid] = tile_occluded(sv64[tid], P.depth, lo, hi, P.eps) ? 0 : 1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int n = 0;
+    for (int v = 0; v < P.nv; ++v)
+      if (s_keep[v]) s_views_list[n++] = v;
+    s_nlist = n;
+  }
+  __syncthreads();
+  const int nlist = s_nlist;
   uint32_t words[kMaxViewsTC / 32] = {0u, 0u};
   int cnt = 0;
   constexpr int U = 4;  // views in flight per thread (independent depth loads)
-  for (int v0 = 0; v0 < P.nv; v0 += U) {
+  for (int l0 = 0; l0 < nlist; l0 += U) {
     ProjF q[U];
     int st[U];
     float stored[U];
@@ -205,8 +280,8 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     for (int u = 0; u < U; ++u) {
       st[u] = kInvisible;
       stored[u] = 0.f;
-      const int v = v0 + u;
-      if (valid && v < P.nv) {
+      const int v = l0 + u < nlist ? s_views_list[l0 + u] : 0;
+      if (valid && l0 + u < nlist) {
         q[u] = project_f32(sv[v], p.x, p.y, p.z);
         int64_t didx = 0;
         const float4 b = sbound[v];
@@ -216,8 +291,8 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int v = v0 + u;
-      if (v >= P.nv) break;
+      if (l0 + u >= nlist) break;
+      const int v = s_views_list[l0 + u];
       int s = st[u];
       if (s == kNeedDepth) s = depth_decide(q[u], stored[u], eps_f);
       bool vis = s == kNeedDepth;
