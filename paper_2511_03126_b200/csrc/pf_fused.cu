@@ -554,6 +554,8 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.tile_desc = reinterpret_cast<uint2*>(ws + L.desc);
     T.tile_kt = reinterpret_cast<int32_t*>(ws + L.kt);
     T.tile_part = reinterpret_cast<float*>(ws + L.part);
+    T.viewf = reinterpret_cast<tile::ViewF*>(ws + L.viewf);
+    T.vbound = reinterpret_cast<float4*>(ws + L.vbound);
     T.ovf_list = reinterpret_cast<int32_t*>(ws + L.ovf) + 1;
     T.ovf_count = reinterpret_cast<int32_t*>(ws + L.ovf);
     T.partials = a->partials;

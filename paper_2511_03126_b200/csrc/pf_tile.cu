@@ -173,47 +173,59 @@ __device__ __forceinline__ int classify_fast(const ViewF& w, const float4& b, co
 // the convex hull of its projected corners). If every stored depth in that rectangle (+1 px) plus
 // eps is below the box's minimum depth, no point of the tile can pass the depth test in this view
 // (out-of-image and invalid pixels fail it anyway), so the per-point work is skipped.
-__device__ bool tile_occluded(const pf_view_t& v, const float* __restrict__ depth, const float* lo,
-                              const float* hi, double eps) {
-  double zmin = 1e300, umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300;
+__device__ bool tile_occluded(const ViewF& v, const float* __restrict__ depth, const float* lo,
+                              const float* hi, float eps) {
+  // fp32 with explicit slack: depths / pixels of the box corners are only used as conservative
+  // bounds (+1e-5 m on the depth comparison, +1 px on the window), never as a visibility decision
+  float zmin = 1e30f, umin = 1e30f, umax = -1e30f, vmin = 1e30f, vmax = -1e30f;
+#pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const double px = (c & 1) ? hi[0] : lo[0];
-    const double py = (c & 2) ? hi[1] : lo[1];
-    const double pz = (c & 4) ? hi[2] : lo[2];
-    const double X = v.R[0] * px + v.R[1] * py + v.R[2] * pz + v.t[0];
-    const double Y = v.R[3] * px + v.R[4] * py + v.R[5] * pz + v.t[1];
-    const double Z = v.R[6] * px + v.R[7] * py + v.R[8] * pz + v.t[2];
-    if (!(Z > 1e-6)) return false;
-    zmin = fmin(zmin, Z);
-    const double u = v.fx * X / Z + v.cx, w = v.fy * Y / Z + v.cy;
-    umin = fmin(umin, u);
-    umax = fmax(umax, u);
-    vmin = fmin(vmin, w);
-    vmax = fmax(vmax, w);
+    const float px = (c & 1) ? hi[0] : lo[0];
+    const float py = (c & 2) ? hi[1] : lo[1];
+    const float pz = (c & 4) ? hi[2] : lo[2];
+    const float X = fmaf(v.R[2], pz, fmaf(v.R[1], py, v.R[0] * px)) + v.t[0];
+    const float Y = fmaf(v.R[5], pz, fmaf(v.R[4], py, v.R[3] * px)) + v.t[1];
+    const float Z = fmaf(v.R[8], pz, fmaf(v.R[7], py, v.R[6] * px)) + v.t[2];
+    zmin = fminf(zmin, Z);
+    const float rz = 1.f / Z;
+    const float u = fmaf(v.fx, X * rz, v.cx), w = fmaf(v.fy, Y * rz, v.cy);
+    umin = fminf(umin, u);
+    umax = fmaxf(umax, u);
+    vmin = fminf(vmin, w);
+    vmax = fmaxf(vmax, w);
   }
-  const int x0 = (int)fmax(floor(umin) - 1.0, 0.0), x1 = (int)fmin(ceil(umax) + 1.0, (double)(v.W - 1));
-  const int y0 = (int)fmax(floor(vmin) - 1.0, 0.0), y1 = (int)fmin(ceil(vmax) + 1.0, (double)(v.H - 1));
-  if (umax < -1.0 || vmax < -1.0 || umin > (double)v.W || vmin > (double)v.H) return true;  // off-image
+  if (!(zmin > 1e-3f)) return false;
+  if (umax < -2.f || vmax < -2.f || umin > (float)v.W + 1.f || vmin > (float)v.H + 1.f) return true;  // off-image
+  const int x0 = max((int)floorf(umin) - 1, 0), x1 = min((int)ceilf(umax) + 1, v.W - 1);
+  const int y0 = max((int)floorf(vmin) - 1, 0), y1 = min((int)ceilf(vmax) + 1, v.H - 1);
   if (x1 < x0 || y1 < y0) return true;
-  if ((x1 - x0 + 1) * (y1 - y0 + 1) > 256) return false;
-  const float* d = depth + v.depth_offset;
+  const int ww = x1 - x0 + 1, n = ww * (y1 - y0 + 1);
+  if (n > 64) return false;
+  const float* d = depth + v.depth_off + (int64_t)y0 * v.W + x0;
   float dmax = 0.f;
-  for (int y = y0; y <= y1; ++y)
-    for (int x = x0; x <= x1; ++x) dmax = fmaxf(dmax, __ldg(d + (int64_t)y * v.W + x));
-  return zmin > (double)dmax + eps + 1e-7;
+#pragma unroll 8
+  for (int e = 0; e < n; ++e) dmax = fmaxf(dmax, __ldg(d + (int64_t)(e / ww) * v.W + (e % ww)));
+  return zmin - 1e-5f > dmax + eps + 1e-5f;
+}
+
+__global__ void k_view_setup(TileParams P) {
+  const int j = threadIdx.x;
+  if (j < P.nv) {
+    const ViewF w = make_viewf(P.views[j], P.d);
+    P.viewf[j] = w;
+    P.vbound[j] = view_bound(w, P.views[j], P.lo_hi);
+  }
 }
 
 // ---- k_tile_prep ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
   __shared__ ViewF sv[kMaxViewsTC];
-  __shared__ pf_view_t sv64[kMaxViewsTC];
   __shared__ int wx0[kMaxViewsTC], wx1[kMaxViewsTC], wy0[kMaxViewsTC], wy1[kMaxViewsTC];
   __shared__ float4 sbound[kMaxViewsTC];  // per-view constant bounds: eu, ev, e, fast
   const int tid = threadIdx.x, lane = tid & 31;
   for (int j = tid; j < P.nv; j += kTile) {
-    sv64[j] = P.views[j];
-    sv[j] = make_viewf(P.views[j], P.d);
-    sbound[j] = view_bound(sv[j], P.views[j], P.lo_hi);
+    sv[j] = P.viewf[j];     // per-view fp32 camera + bounds computed once (k_view_setup)
+    sbound[j] = P.vbound[j];
     wx0[j] = INT_MAX;
     wy0[j] = INT_MAX;
     wx1[j] = -1;
@@ -258,7 +270,7 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
       lo[a] = fminf(fminf(sbb[0][a], sbb[1][a]), fminf(sbb[2][a], sbb[3][a]));
       hi[a] = fmaxf(fmaxf(sbb[0][a + 3], sbb[1][a + 3]), fmaxf(sbb[2][a + 3], sbb[3][a + 3]));
     }
-    s_keep[tid] = tile_occluded(sv64[tid], P.depth, lo, hi, P.eps) ? 0 : 1;
+    s_keep[tid] = tile_occluded(sv[tid], P.depth, lo, hi, eps_f) ? 0 : 1;
   }
   __syncthreads();
   if (tid == 0) {
@@ -266,6 +278,10 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     for (int v = 0; v < P.nv; ++v)
       if (s_keep[v]) s_views_list[n++] = v;
     s_nlist = n;
+    if (P.dbg) {
+      atomicAdd(P.dbg + 16 * 1000 + 3, (unsigned long long)n);
+      atomicAdd(P.dbg + 16 * 1000 + 4, (unsigned long long)P.nv);
+    }
   }
   __syncthreads();
   const int nlist = s_nlist;
@@ -296,7 +312,7 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
       int s = st[u];
       if (s == kNeedDepth) s = depth_decide(q[u], stored[u], eps_f);
       bool vis = s == kNeedDepth;
-      if (s == kAmbiguous) vis = visible_f64(sv64[v], P.depth, p.x, p.y, p.z, P.eps);
+      if (s == kAmbiguous) vis = visible_f64(P.views[v], P.depth, p.x, p.y, p.z, P.eps);  // rare
       if (P.dbg) {  // PF_WS_DEBUG: fraction of samples decided in fp64 / warp-iterations with any
         const unsigned amb = __ballot_sync(0xffffffffu, s == kAmbiguous);
         if (lane == 0) {
@@ -672,6 +688,8 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg) {
   L.desc = take(sizeof(uint2) * (size_t)ntiles * nv);
   L.kt = take(sizeof(int32_t) * (size_t)ntiles);
   L.part = take(sizeof(float) * (size_t)ntiles * (kMaxKpadTC + 6));
+  L.viewf = take(sizeof(ViewF) * kMaxViewsTC);
+  L.vbound = take(sizeof(float4) * kMaxViewsTC);
   L.ovf = take(sizeof(int32_t) * (size_t)(n + 1));
   L.gbf = take(sizeof(uint16_t) * (size_t)cells * kpadg);
   L.bytes = off;
@@ -715,13 +733,16 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
     cudaMemsetAsync(pdbg, 0, sizeof(unsigned long long) * 16 * 1024, st);
     Q.dbg = pdbg;
   }
+  k_view_setup<<<1, kMaxViewsTC, 0, st>>>(Q);
+  if (int rc = check_launch("view_setup")) return rc;
   k_tile_prep<<<(unsigned)L.ntiles, kTile, 0, st>>>(Q);
   if (debug) {
-    unsigned long long h[3];
+    unsigned long long h[5];
     cudaMemcpyAsync(h, pdbg + 16 * 1000, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    fprintf(stderr, "[prep debug] ambiguous samples %.4f%%, warp-iterations with any %.2f%%\n",
-            100.0 * h[0] / (32.0 * h[2]), 100.0 * h[1] / h[2]);
+    fprintf(stderr, "[prep debug] ambiguous samples %.4f%%, warp-iterations with any %.2f%%, views kept "
+            "after the tile cull %.1f%%\n", 100.0 * h[0] / (32.0 * h[2]), 100.0 * h[1] / h[2],
+            100.0 * h[3] / h[4]);
   }
   if (int rc = check_launch("tile_prep")) return rc;
   // persistent warp-specialised TMA kernel (pf_tile_ws.cu); k_tile_mma when TMA maps are unavailable

@@ -63,6 +63,8 @@ struct TileParams {
   uint2* tile_desc;
   int32_t* tile_kt;
   float* tile_part;
+  ViewF* viewf;   // per-view fp32 camera (k_view_setup)
+  float4* vbound; // per-view constant error bounds over the bbox (k_view_setup)
   int32_t* ovf_list;
   int32_t* ovf_count;
   unsigned long long* dbg;  // optional per-CTA wait-cycle counters (PF_WS_DEBUG)
@@ -72,7 +74,7 @@ struct TileParams {
 
 struct TileLayout {
   int64_t ntiles;
-  size_t keys, hist, totals, perm, spts, desc, kt, part, ovf, gbf, bytes;
+  size_t keys, hist, totals, perm, spts, desc, kt, part, ovf, gbf, viewf, vbound, bytes;
 };
 
 TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg);
