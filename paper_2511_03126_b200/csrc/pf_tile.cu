@@ -199,13 +199,18 @@ __device__ bool tile_occluded(const ViewF& v, const float* __restrict__ depth, c
   const int x0 = max((int)floorf(umin) - 1, 0), x1 = min((int)ceilf(umax) + 1, v.W - 1);
   const int y0 = max((int)floorf(vmin) - 1, 0), y1 = min((int)ceilf(vmax) + 1, v.H - 1);
   if (x1 < x0 || y1 < y0) return true;
-  const int ww = x1 - x0 + 1, n = ww * (y1 - y0 + 1);
-  if (n > 64) return false;
+  if ((x1 - x0 + 1) * (y1 - y0 + 1) > 64) return false;
   const float* d = depth + v.depth_off + (int64_t)y0 * v.W + x0;
-  float dmax = 0.f;
-#pragma unroll 8
-  for (int e = 0; e < n; ++e) dmax = fmaxf(dmax, __ldg(d + (int64_t)(e / ww) * v.W + (e % ww)));
-  return zmin - 1e-5f > dmax + eps + 1e-5f;
+  float dmax0 = 0.f, dmax1 = 0.f;
+  for (int y = 0; y <= y1 - y0; ++y, d += v.W) {
+    int x = 0;
+    for (; x + 1 <= x1 - x0; x += 2) {
+      dmax0 = fmaxf(dmax0, __ldg(d + x));
+      dmax1 = fmaxf(dmax1, __ldg(d + x + 1));
+    }
+    if (x <= x1 - x0) dmax0 = fmaxf(dmax0, __ldg(d + x));
+  }
+  return zmin - 1e-5f > fmaxf(dmax0, dmax1) + eps + 1e-5f;
 }
 
 __global__ void k_view_setup(TileParams P) {
@@ -273,12 +278,15 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     s_keep[tid] = tile_occluded(sv[tid], P.depth, lo, hi, eps_f) ? 0 : 1;
   }
   __syncthreads();
-  if (tid == 0) {
-    int n = 0;
-    for (int v = 0; v < P.nv; ++v)
-      if (s_keep[v]) s_views_list[n++] = v;
-    s_nlist = n;
-    if (P.dbg) {
+  if (tid < 32) {  // ballot compaction of the kept views (<= 64: two per lane)
+    const bool k0 = lane < P.nv && s_keep[lane], k1 = lane + 32 < P.nv && s_keep[lane + 32];
+    const uint32_t b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
+    const uint32_t below = (1u << lane) - 1u;
+    if (k0) s_views_list[__popc(b0 & below)] = lane;
+    if (k1) s_views_list[__popc(b0) + __popc(b1 & below)] = lane + 32;
+    const int n = __popc(b0) + __popc(b1);
+    if (lane == 0) s_nlist = n;
+    if (P.dbg && lane == 0) {
       atomicAdd(P.dbg + 16 * 1000 + 3, (unsigned long long)n);
       atomicAdd(P.dbg + 16 * 1000 + 4, (unsigned long long)P.nv);
     }
@@ -351,22 +359,41 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     P.codes[i] = voxel_code(p.x, p.y, p.z, lo, edge, P.grid);
   }
   __syncthreads();
-  if (tid == 0) {
-    int base = 0;
-    uint2* desc = P.tile_desc + tile * P.nv;
-    for (int v = 0; v < P.nv; ++v) {
-      int w = 0, h = 0;
-      if (wx1[v] >= 0) {
-        w = wx1[v] - wx0[v] + 1;
-        h = wy1[v] - wy0[v] + 1;
+  if (tid < 32) {  // windows -> descriptors: exclusive prefix of window sizes over views (2 per lane)
+    int w[2], h[2], x0[2], y0[2], sz[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int v = lane + 32 * r;
+      w[r] = h[r] = 0;
+      if (v < P.nv && wx1[v] >= 0) {
+        w[r] = wx1[v] - wx0[v] + 1;
+        h[r] = wy1[v] - wy0[v] + 1;
       }
-      const int x0 = w ? wx0[v] : 0, y0 = h ? wy0[v] : 0;
-      desc[v] = make_uint2((uint32_t)min(base, 65535) | ((uint32_t)x0 << 16) | ((uint32_t)y0 << 24),
-                           (uint32_t)w | ((uint32_t)h << 8));
-      base += w * h;
-
+      x0[r] = w[r] ? wx0[v] : 0;
+      y0[r] = h[r] ? wy0[v] : 0;
+      sz[r] = w[r] * h[r];
     }
-    P.tile_kt[tile] = base;
+    int incl0 = sz[0], incl1 = sz[1];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t0 = __shfl_up_sync(0xffffffffu, incl0, o), t1 = __shfl_up_sync(0xffffffffu, incl1, o);
+      if (lane >= o) {
+        incl0 += t0;
+        incl1 += t1;
+      }
+    }
+    const int tot0 = __shfl_sync(0xffffffffu, incl0, 31);
+    const int base0 = incl0 - sz[0], base1 = tot0 + incl1 - sz[1];
+    uint2* desc = P.tile_desc + tile * P.nv;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int v = lane + 32 * r;
+      const int base = r ? base1 : base0;
+      if (v < P.nv)
+        desc[v] = make_uint2((uint32_t)min(base, 65535) | ((uint32_t)x0[r] << 16) | ((uint32_t)y0[r] << 24),
+                             (uint32_t)w[r] | ((uint32_t)h[r] << 8));
+    }
+    if (lane == 31) P.tile_kt[tile] = tot0 + incl1;
   }
 }
 
