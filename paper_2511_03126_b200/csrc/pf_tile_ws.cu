@@ -35,16 +35,16 @@ namespace pf {
 namespace tile {
 namespace {
 
-constexpr int kLoadWarps = 4;          // warps 0-3: B loaders
+constexpr int kLoadWarps = 6;          // warps 0-5: B loaders
 constexpr int kLoadThreads = 32 * kLoadWarps;
-constexpr int kMmaWarp = 4;            // warp 4: MMA issuer
-constexpr int kAccWarp0 = 5;           // warps 5-12: accumulators (2 per TMEM lane group)
+constexpr int kMmaWarp = 6;            // warp 6: MMA issuer
+constexpr int kAccWarp0 = 7;           // warps 7-14: accumulators (2 per TMEM lane group)
 constexpr int kAccThreads = 256;
-constexpr int kBuildWarp0 = 13;        // warps 13-16: A builders
-constexpr int kWsThreads = 544;        // 17 warps
+constexpr int kBuildWarp0 = 15;        // warps 15-18: A builders
+constexpr int kWsThreads = 608;        // 19 warps
 constexpr int kCG = 2;                 // 64-column B chunks per MMA group (N = 64 * kCG)
 constexpr int kDCols = 64 * kCG;       // TMEM columns of one feature buffer
-constexpr int kDBufs = 256 / kDCols;   // TMEM feature buffers (256 columns in total)
+constexpr int kDBufs = 3;              // TMEM accumulator slots (feature groups and the S group rotate)
 constexpr int kStages = 6;             // B ring depth (3 chunk groups)
 constexpr int kKtWs = 192;             // taps per tile held in one A buffer / B stage
 constexpr int kStageBytes = kKtWs * 128;
@@ -153,13 +153,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     tc::mbar_init(&S.s_empty, kAccThreads);
   }
   if (warp == kAccWarp0) tc::tmem_alloc(&S.tmem_base, 512);
-  static_assert(256 + 128 + kKtWs / 2 <= 512, "TMEM: D buffers + S + A");
+  static_assert(kDBufs * kDCols + kKtWs / 2 <= 512, "TMEM: accumulator slots + A");
+  static_assert(kDCols == kMaxKpadTC, "the S group fills one accumulator slot");
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = S.tmem_base;
-  const uint32_t tS = tbase + 256u;                     // S: 128 columns
-  const uint32_t tA = tS + 128u;                        // A (bf16 pairs): kKtWs / 2 columns
+  const uint32_t tA = tbase + kDBufs * kDCols;          // A (bf16 pairs): kKtWs / 2 columns
 
   if (warp < kLoadWarps) {
     // ================= B loaders =================
@@ -265,14 +265,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         for (int g = 0; g < kCG; ++g) WS_WAIT(&S.b_full[stage + g], phase, 2);
         uint32_t dst;
         int db = 0;
-        if (c < nd) {
-          db = dcount % kDBufs;
-          WS_WAIT(&S.d_empty[db], ((dcount / kDBufs) & 1u) ^ 1u, 3);
-          dst = tbase + (uint32_t)(db * kDCols);
-        } else {
-          if (c == nd) WS_WAIT(&S.s_empty, s_phase ^ 1u, 4);
-          dst = tS + (uint32_t)(64 * (c - nd));
-        }
+        db = dcount % kDBufs;  // feature groups and the final S group share the slot rotation
+        if (c < nd) WS_WAIT(&S.d_empty[db], ((dcount / kDBufs) & 1u) ^ 1u, 3);
+        else WS_WAIT(&S.d_empty[db], ((dcount / kDBufs) & 1u) ^ 1u, 4);
+        dst = tbase + (uint32_t)(db * kDCols);
         tc::fence_after_sync();
         const long long ti0 = clock64();
         if (lane == 0) {
@@ -284,12 +280,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           }
 #pragma unroll
           for (int g = 0; g < kCG; ++g) tc::mma_commit(&S.b_empty[stage + g]);
-          if (c < nd) tc::mma_commit(&S.d_full[db]);
-          if (c + kCG >= nch) tc::mma_commit(&S.s_full);
+          tc::mma_commit(&S.d_full[db]);
         }
         __syncwarp();
         issue_cyc += clock64() - ti0;
-        if (c < nd) ++dcount;
+        ++dcount;
         stage += kCG;
         if (stage == kStages) { stage = 0; phase ^= 1u; }
       }
@@ -399,8 +394,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       }
       S.xss[half][row] = (ss0 + ss1) + (ss2 + ss3);
       // ---- epilogue on S (this half's materials) ----------------------------------------------------
-      WS_WAIT(&S.s_full, s_phase, 7);
-      s_phase ^= 1u;
+      const int sslot = dcount % kDBufs;
+      WS_WAIT(&S.d_full[sslot], (dcount / kDBufs) & 1u, 7);
+      const uint32_t tS = tbase + (uint32_t)(sslot * kDCols);
       tc::fence_after_sync();
       float mx = -INFINITY;
       bool nan = false;
@@ -487,7 +483,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         }
       }
       tc::fence_before_sync();
-      mbar_arrive(&S.s_empty);
+      mbar_arrive(&S.d_empty[sslot]);
+      ++dcount;
       if (valid && half == 0) {
         float prop[4];
 #pragma unroll
