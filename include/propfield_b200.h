@@ -213,13 +213,6 @@ int pf_fuse_query(const pf_fuse_args_t* args, void* stream);
 int pf_selftest_umma(const void* a_bf16, const void* b_bf16, float* c, int32_t k, int32_t n,
                      int32_t ts, void* stream);
 
-/* TMA window load diagnostic: a (64 ch, bw, bh) box of an (hf, wf, 64) bf16 map at (x0, y0) is
- * loaded with the tile kernel's tensor-map settings (128-B swizzle) into shared memory at
- * 128-byte row `row_off`, un-swizzled by the absolute-address rule, and written to out
- * (bw*bh, 64) bf16. */
-int pf_selftest_tma(const void* src_bf16, int32_t hf, int32_t wf, int32_t x0, int32_t y0,
-                    int32_t bw, int32_t bh, int32_t row_off, void* out, void* stream);
-
 #ifdef __cplusplus
 }
 #endif

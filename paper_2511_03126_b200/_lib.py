@@ -114,7 +114,6 @@ SIGNATURES = {
     "pf_fuse_prepare": ([C.POINTER(FuseArgs), _P], C.c_int),
     "pf_fuse_query": ([C.POINTER(FuseArgs), _P], C.c_int),
     "pf_selftest_umma": ([_P, _P, _P, _I32, _I32, _I32, _P], C.c_int),
-    "pf_selftest_tma": ([_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P], C.c_int),
 }
 
 _lock = threading.Lock()

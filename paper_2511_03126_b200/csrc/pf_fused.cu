@@ -539,7 +539,8 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg);
     tile::TileParams T{};
     T.spts = reinterpret_cast<const float4*>(ws + L.spts);
-    T.perm = reinterpret_cast<const int32_t*>(ws + L.perm);
+    T.inv = reinterpret_cast<const int32_t*>(ws + L.inv);
+    T.srec = reinterpret_cast<tile::SRec*>(ws + L.srec);
     T.n = a->n; T.views = a->views; T.nv = a->nviews; T.nwords = (a->nviews + 31) / 32; T.d = d;
     T.depth = a->depth; T.fmap = a->fmap; T.Gbf = reinterpret_cast<const uint16_t*>(ws + L.gbf);
     T.kpadg = kpadg; T.k = a->k; T.p = a->p; T.density_col = a->density_col;
@@ -553,18 +554,15 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.status = a->status;
     T.tile_desc = reinterpret_cast<uint2*>(ws + L.desc);
     T.tile_kt = reinterpret_cast<int32_t*>(ws + L.kt);
-    T.tile_part = reinterpret_cast<float*>(ws + L.part);
     T.viewf = reinterpret_cast<tile::ViewF*>(ws + L.viewf);
     T.vbound = reinterpret_cast<float4*>(ws + L.vbound);
     T.ovf_list = reinterpret_cast<int32_t*>(ws + L.ovf) + 1;
     T.ovf_count = reinterpret_cast<int32_t*>(ws + L.ovf);
     T.partials = a->partials;
-    uint32_t cols = 32;
-    while (cols < (uint32_t)(128 + kpadg)) cols <<= 1;
-    T.tmem_cols = cols;
-    if (int rc = tile::run_tile_path(T, L, ws, a->points, a->n, cells, G, kpad, a->views_host[0].Hf,
-                                     a->views_host[0].Wf, st))
-      return rc;
+    if (int rc = tile::run_tile_path(T, L, ws, a->points, a->n, st)) return rc;
+    // sorted records -> caller's order; then the overflow points (tiles with more taps than fit in
+    // shared memory) run through the SIMT kernel, which writes their outputs directly
+    if (int rc = tile::run_unsort(T, st)) return rc;
     // overflow tiles (more taps than fit in shared memory) run through the SIMT kernel
     prm.list = T.ovf_list;
     prm.list_len = T.ovf_count;

@@ -139,10 +139,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred done;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
       "@!done bra WAIT_%=;\n\t"
       "}" ::"r"(a),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 

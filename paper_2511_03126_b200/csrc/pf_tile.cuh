@@ -1,4 +1,12 @@
-// Shared declarations of the tensor-core tile path (pf_tile.cu) and its host orchestration.
+// Shared declarations of the tensor-core tile path (pf_tile.cu, pf_tile_ws.cu) and its host
+// orchestration.
+//
+// Data flow (all per-point intermediates live in SORTED order, so every pass over them is
+// coalesced; the original order is touched once, by a gather in k_unsort):
+//   k_sort_scatter : spts[j] = {x, y, z, bits(i)}, inv[i] = j          (j = Morton-sorted slot)
+//   k_tile_prep    : srec[j].{mask, count, code}, per-tile tap windows
+//   k_tile_ws      : srec[j].prop, voxel + integrate partials
+//   k_unsort       : outputs[i] <- srec[inv[i]]  (one 32-byte sector read per point)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -10,10 +18,8 @@ namespace pf {
 namespace tile {
 
 constexpr int kTile = 128;             // points per tile = tcgen05 M
-constexpr int kKtMax = 192;            // taps per tile held in shared memory
 constexpr int kMaxViewsTC = 64;        // views supported by the tile path (2 bitset words)
-constexpr int kMaxKpadTC = 128;        // padded materials (MMA N of the S chunk; B tile <= 2 halves)
-constexpr int kRedStride = kMaxKpadTC + 1;
+constexpr int kMaxKpadTC = 128;        // padded materials (MMA N of the S chunk pair)
 constexpr int kSortBits = 7;           // Morton grid 128^3 over the bbox
 constexpr int kSortCells = 1 << kSortBits;
 constexpr int kSortBins = 1 << (3 * kSortBits);
@@ -34,9 +40,18 @@ struct TapF {
   float wx, wy;
 };
 
+// one point's record in sorted order (32 bytes = one DRAM sector)
+struct __align__(32) SRec {
+  uint32_t m0, m1;  // visibility bitset (views 0-31, 32-63)
+  int32_t count;    // visible views
+  int32_t code;     // voxel code
+  float prop[4];    // regressed properties (P <= 4)
+};
+
 struct TileParams {
-  const float4* spts;   // sorted points
-  const int32_t* perm;  // sorted slot -> original index
+  const float4* spts;   // sorted points, .w = original index (int bits)
+  const int32_t* inv;   // original index -> sorted slot
+  SRec* srec;           // sorted per-point records
   int64_t n;
   const pf_view_t* views;
   int nv, nwords, d;
@@ -51,40 +66,39 @@ struct TileParams {
   int grid;
   int64_t cells3;
   const double* lo_hi;
-  uint32_t* mask_bits;
+  uint32_t* mask_bits;   // outputs in original order (k_unsort)
   int32_t* counts;
   int32_t* codes;
   float* props;
   float* grid_partials;  // nullptr: skip voxels
-  float* features;
+  float* features;       // optional validation outputs, original order
   float* sims;
   float* weights;
   int32_t* status;
   uint2* tile_desc;
   int32_t* tile_kt;
-  float* tile_part;
   ViewF* viewf;   // per-view fp32 camera (k_view_setup)
   float4* vbound; // per-view constant error bounds over the bbox (k_view_setup)
   int32_t* ovf_list;
   int32_t* ovf_count;
-  unsigned long long* dbg;  // optional per-CTA wait-cycle counters (PF_WS_DEBUG)
+  unsigned long long* dbg;  // optional counters (PF_WS_DEBUG)
   double* partials;
-  uint32_t tmem_cols;
 };
 
 struct TileLayout {
   int64_t ntiles;
-  size_t keys, hist, totals, perm, spts, desc, kt, part, ovf, gbf, viewf, vbound, bytes;
+  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, gbf, viewf, vbound, bytes;
 };
 
 TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg);
-size_t tile_smem_bytes();
 int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const float* points,
-                  int64_t n, int64_t cells, const float* G, int kpad, int hf, int wf, cudaStream_t st);
-int run_tile_ws(const TileParams& P, int hf, int wf, int nv, cudaStream_t st);
+                  int64_t n, cudaStream_t st);
+int run_unsort(const TileParams& P, cudaStream_t st);
+int run_tile_ws(const TileParams& P, cudaStream_t st);
 int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf, cudaStream_t st);
 int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int k, int kpadg, int kpad,
                  uint16_t* Gbf, float* G32, cudaStream_t st);
+int ws_kt_max();
 
 }  // namespace tile
 }  // namespace pf
