@@ -270,6 +270,7 @@ def run_ours(args, cfg):
     launches0 = _lib.launch_count()
     barrier()
     torch.cuda.synchronize()
+    _lib.stage_timing(True)  # CUDA events at the tile path's stage boundaries (same stream)
     for i in range(args.steps):
         if flush:
             scratch.fill_(float(i))  # L2 flush between steps (outside the step's events)
@@ -280,6 +281,9 @@ def run_ours(args, cfg):
     barrier()
     clocks = clk.stop()
     launches = _lib.launch_count() - launches0
+    st_calls, st_ms = _lib.stage_times()
+    _lib.stage_timing(False)
+    stage_avg = {k: v / st_calls for k, v in st_ms.items()} if st_calls else {}
     step_ms = [starts[i].elapsed_time(evs[i][3]) for i in range(args.steps)]
     kern_ms = [evs[i][1].elapsed_time(evs[i][2]) for i in range(args.steps)]
     prep_ms = [evs[i][0].elapsed_time(evs[i][1]) for i in range(args.steps)]
@@ -351,16 +355,34 @@ def run_ours(args, cfg):
     except Exception:
         peak_src = "fallback"
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    tc_peak = float(peaks.get("bf16_tflops_sustained", 1400.0))
     cells = nv * cfg.fmap[0] * cfg.fmap[1]
     kpad = 32 * ((cfg.k + 31) // 32)
     algo = algorithmic_bytes(cfg, n, nv, cfg.k, tables.p, cfg.d, 2 if cfg.bf16 else 4, cells, kpad)
-    achieved = algo / (t_kern * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
-        traffic = json.load(open(tf)).get(cfg.name, {}).get("fuse_bytes_per_launch")
+        traffic = json.load(open(tf)).get(cfg.name, {}).get("dram_bytes_per_launch")
     vis_pairs = part["visible_pairs"]
-    fma_flop = 2.0 * vis_pairs / max(1, world) * 4 * (cfg.d + kpad)  # gather + G-table taps
+    # SURVEY §8d algorithmic FLOPs: bilinear gather 8*D per visible sample + similarity 2*N*D*K
+    algo_flop = 8.0 * cfg.d * vis_pairs / max(1, world) + 2.0 * n * cfg.d * cfg.k
+    tile_path = bool(stage_avg) and stage_avg.get("tile_kernel", 0.0) > 0.0
+    if tile_path:
+        t_dom = stage_avg["tile_kernel"]
+        ach = algo_flop / (t_dom * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s",
+                    "frac": ach / tc_peak, "traffic": traffic, "peak_source": f"{peak_src} (bf16 sustained)",
+                    "kernel": "k_tile_ws", "kernel_ms": t_dom,
+                    "algorithmic_flop_per_launch": algo_flop,
+                    "hbm": {"algorithmic_bytes_per_launch": algo,
+                            "achieved_gbs": algo / (t_dom * 1e-3) / 1e9, "peak_gbs": hbm_peak}}
+    else:
+        ach = algo / (t_kern * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": ach / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                    "kernel": "k_fuse_simt", "kernel_ms": t_kern, "algorithmic_bytes_per_launch": algo,
+                    "simt": {"fma_tflops": algo_flop / (t_kern * 1e-3) / 1e12,
+                             "peak_tflops_nominal": SIMT_FP32_PEAK_TFLOPS}}
     line = {
         "metric": "point-view samples/sec",
         "value": n_total * nv / (t_step * 1e-3),
@@ -373,17 +395,14 @@ def run_ours(args, cfg):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f32",
+        "dtype": "bf16" if tile_path else "f32",
         "data": "synthetic",
         "config": {**config_desc(cfg), "parallelism": f"point-range x{world}",
                    "l2": ("inputs larger than L2" if not flush else "L2 flushed between steps")},
-        "stages_ms": {"fuse_kernel": t_kern, "prepare_G": sum(prep_ms) / args.steps,
+        "stages_ms": {"fuse_query": t_kern, **{k: v for k, v in stage_avg.items()},
+                      "prepare_G": sum(prep_ms) / args.steps,
                       "rest(bbox,zero,voxel-mass,allreduce)": t_step - t_kern - sum(prep_ms) / args.steps},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "k_fuse_simt", "algorithmic_bytes_per_launch": algo,
-                     "compute": {"simt_fma_tflops": fma_flop / (t_kern * 1e-3) / 1e12,
-                                 "simt_peak_tflops_nominal": SIMT_FP32_PEAK_TFLOPS}},
+        "roofline": roofline,
         "gpu_launches": int(launches),
         "clocks": clocks,
         "result": {"mass_kg": mass, "featured": part["featured"], "visible_pairs": vis_pairs,

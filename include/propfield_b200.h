@@ -207,6 +207,14 @@ int pf_fuse_query(const pf_fuse_args_t* args, void* stream);
  * Diagnostics (no reference twin).
  * ------------------------------------------------------------------------------------------- */
 
+/* Stage timer of the tensor-core tile path: enable (1) / disable (0) CUDA-event marks at the stage
+ * boundaries of every following pf_fuse_query (resets the record). pf_stage_times then fills
+ * ms[0..4] with the summed device time of sort, prep, tile kernel, unsort and SIMT overflow over
+ * the recorded calls (synchronising on their events) and returns the number of calls (<= 64), or
+ * minus a PF_ERR_* status. */
+int pf_stage_timing(int32_t enable);
+int pf_stage_times(float* ms, int32_t n);
+
 /* C (128,n) f32 = A (128,k) bf16 row-major @ B (k,n) bf16 row-major through the tile kernel's
  * tcgen05 operand layouts / descriptors / TMEM read-back. k % 64 == 0 (<= 256), n % 16 == 0.
  * ts != 0: A is first copied to TMEM with tcgen05.cp and the MMAs read A from TMEM. */

@@ -113,6 +113,8 @@ SIGNATURES = {
     "pf_fuse_workspace_bytes": ([C.POINTER(FuseArgs)], C.c_uint64),
     "pf_fuse_prepare": ([C.POINTER(FuseArgs), _P], C.c_int),
     "pf_fuse_query": ([C.POINTER(FuseArgs), _P], C.c_int),
+    "pf_stage_timing": ([_I32], C.c_int),
+    "pf_stage_times": ([_P, _I32], C.c_int),
     "pf_selftest_umma": ([_P, _P, _P, _I32, _I32, _I32, _P], C.c_int),
 }
 
@@ -163,3 +165,20 @@ def call(name: str, *args) -> None:
 
 def launch_count() -> int:
     return int(load().pf_launch_count())
+
+
+STAGES = ("sort", "prep", "tile_kernel", "unsort", "overflow_simt")
+
+
+def stage_timing(enable: bool) -> None:
+    """Start (True) / stop recording CUDA-event stage marks in every following pf_fuse_query."""
+    check(load().pf_stage_timing(1 if enable else 0))
+
+
+def stage_times() -> tuple[int, dict]:
+    """(calls, {stage: summed device ms}) over the calls recorded since stage_timing(True)."""
+    buf = (C.c_float * len(STAGES))()
+    n = int(load().pf_stage_times(buf, len(STAGES)))
+    if n < 0:
+        check(-n)
+    return n, {k: float(buf[i]) for i, k in enumerate(STAGES)}

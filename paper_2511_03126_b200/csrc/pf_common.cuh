@@ -21,6 +21,10 @@ constexpr int kWarp = 32;
 int set_error(int status, const char* fmt, ...);
 int check_launch(const char* what);
 void note_launch();
+// stage timer marks of the tile path: 0 start, 1 sorted, 2 prepped, 3 tile kernel, 4 unsorted,
+// 5 overflow done (pf_stage_timing / pf_stage_times)
+constexpr int kStageMarks = 6;
+void stage_mark(int mark, cudaStream_t st);
 
 // ---- fp64 projection matching numpy ------------------------------------------------------------
 struct Proj {

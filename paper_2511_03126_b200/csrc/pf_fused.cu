@@ -567,20 +567,23 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     prm.list = T.ovf_list;
     prm.list_len = T.ovf_count;
   }
+  int rc;
   if (a->fmap_dtype == PF_F32) {
-    if (d == 128) return launch_fuse<PF_F32, 4, 1>(prm, smem, st);
-    if (d == 256) return launch_fuse<PF_F32, 4, 2>(prm, smem, st);
-    if (d == 512) return launch_fuse<PF_F32, 4, 4>(prm, smem, st);
-    if (d == 768) return launch_fuse<PF_F32, 4, 6>(prm, smem, st);
-    if (d == 1024) return launch_fuse<PF_F32, 4, 8>(prm, smem, st);
-    return launch_fuse<PF_F32, 1, 32>(prm, smem, st);
+    if (d == 128) rc = launch_fuse<PF_F32, 4, 1>(prm, smem, st);
+    else if (d == 256) rc = launch_fuse<PF_F32, 4, 2>(prm, smem, st);
+    else if (d == 512) rc = launch_fuse<PF_F32, 4, 4>(prm, smem, st);
+    else if (d == 768) rc = launch_fuse<PF_F32, 4, 6>(prm, smem, st);
+    else if (d == 1024) rc = launch_fuse<PF_F32, 4, 8>(prm, smem, st);
+    else rc = launch_fuse<PF_F32, 1, 32>(prm, smem, st);
   } else {
-    if (d == 256) return launch_fuse<PF_BF16, 8, 1>(prm, smem, st);
-    if (d == 512) return launch_fuse<PF_BF16, 8, 2>(prm, smem, st);
-    if (d == 768) return launch_fuse<PF_BF16, 8, 3>(prm, smem, st);
-    if (d == 1024) return launch_fuse<PF_BF16, 8, 4>(prm, smem, st);
-    return launch_fuse<PF_BF16, 1, 32>(prm, smem, st);
+    if (d == 256) rc = launch_fuse<PF_BF16, 8, 1>(prm, smem, st);
+    else if (d == 512) rc = launch_fuse<PF_BF16, 8, 2>(prm, smem, st);
+    else if (d == 768) rc = launch_fuse<PF_BF16, 8, 3>(prm, smem, st);
+    else if (d == 1024) rc = launch_fuse<PF_BF16, 8, 4>(prm, smem, st);
+    else rc = launch_fuse<PF_BF16, 1, 32>(prm, smem, st);
   }
+  if (prm.list) stage_mark(5, st);
+  return rc;
 }
 
 }  // extern "C"

@@ -14,6 +14,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <cstdio>
 
 namespace pf {
 namespace tc {
@@ -144,6 +145,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}" ::"r"(a),
       "r"(parity), "r"(0x989680u)
       : "memory");
+}
+
+// debug variant: gives up after ~2 s (a pipeline deadlock) with a message and a trap, so a hang
+// becomes a launch error instead of a stuck GPU
+__device__ __forceinline__ void mbar_wait_or_trap(uint64_t* bar, uint32_t parity, int tag) {
+  const uint32_t a = smem_u32(bar);
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t"
+        "}"
+        : "=r"(done)
+        : "r"(a), "r"(parity), "r"(1000000u)
+        : "memory");
+    if (done) return;
+    if (clock64() - t0 > 4000000000ll) {
+      printf("mbarrier wait timeout: block %d thread %d tag %d parity %u\n", blockIdx.x, threadIdx.x, tag,
+             parity);
+      __trap();
+    }
+  }
 }
 
 // ---- cp.async 16 B --------------------------------------------------------------------------------

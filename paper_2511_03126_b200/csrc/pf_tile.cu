@@ -16,9 +16,9 @@
 // Kernels (this file; the tensor-core tile kernel is pf_tile_ws.cu):
 //   k_sort_keys / k_scan_* / k_sort_scatter — counting sort of the points by a 21-bit Morton key of
 //       a 128^3 grid over the bbox (spatial coherence of tiles; no library sort);
-//   k_tile_prep — per tile: each view is first classified for the whole tile box (OFF: occluded or
-//       off-image for every point; FULL: visible for every point; MIXED), rigorously, from the
-//       box corners and the stored depths under the box's pixel footprint. Only MIXED views get the
+//   k_tile_prep — per tile: each view is first classified for the box of every 32 points (OFF:
+//       occluded or off-image for every point; FULL: visible for every point; MIXED), rigorously,
+//       from the box corners and the stored depths under the box's pixel footprint. Only MIXED views get the
 //       exact per-point test (fp32 projection with a rigorous error bound, fp64 fallback near any
 //       decision boundary -> bit-identical masks). Writes the sorted records (mask, count, voxel
 //       code) and each view's tap window of the tile;
@@ -219,12 +219,20 @@ __device__ int classify_tile_view(const ViewF& v, const float* __restrict__ dept
   if (bw * bh > kScanMax) return kViewMixed;
   const float* d = depth + v.depth_off + (int64_t)cy0 * v.W + cx0;
   float dmax = 0.f, dmin = 1e30f;
-  for (int y = 0; y < bh; ++y, d += v.W)
-    for (int x = 0; x < bw; ++x) {
-      const float s = __ldg(d + x);
-      dmax = fmaxf(dmax, s);
-      dmin = fminf(dmin, s);
+  const int npx = bw * bh;
+  for (int k = 0; k < npx; k += 4) {  // four independent loads in flight
+    float s[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int kk = min(k + u, npx - 1), yy = kk / bw;
+      s[u] = __ldg(d + (int64_t)yy * v.W + (kk - yy * bw));
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      dmax = fmaxf(dmax, s[u]);
+      dmin = fminf(dmin, s[u]);
+    }
+  }
   if (zmin - 1e-5f > dmax + eps + 1e-5f) return kViewOff;
   const bool inside = x0 >= 0 && y0 >= 0 && x1 < v.W && y1 < v.H;
   if (!(inside && dmin > 0.f && zmax + 2e-5f < dmin + eps)) return kViewMixed;
@@ -265,135 +273,118 @@ __device__ __forceinline__ bool point_visible(const ViewF& v, const float4& b, c
 }
 
 // ---- k_tile_prep ---------------------------------------------------------------------------------------
+// One warp's 32 consecutive sorted points form the classification box (a ~2 mm patch at C5: small
+// enough that most views are decided for all 32 points at once); lane l classifies views l and
+// l + 32. FULL views set their bit for the whole warp and widen the tile's tap window by the box
+// window; MIXED views run the exact per-point test and widen it by the visible points' taps.
+__device__ __forceinline__ void window_reduce(bool vis, const TapF& t, int* wx0, int* wy0, int* wx1, int* wy1,
+                                              int v, int lane) {
+  if (__any_sync(0xffffffffu, vis)) {
+    const int ax0 = __reduce_min_sync(0xffffffffu, vis ? t.x0 : INT_MAX);
+    const int ay0 = __reduce_min_sync(0xffffffffu, vis ? t.y0 : INT_MAX);
+    const int ax1 = __reduce_max_sync(0xffffffffu, vis ? t.x0 + t.dx : -1);
+    const int ay1 = __reduce_max_sync(0xffffffffu, vis ? t.y0 + t.dy : -1);
+    if (lane == 0) {
+      atomicMin(wx0 + v, ax0);
+      atomicMin(wy0 + v, ay0);
+      atomicMax(wx1 + v, ax1);
+      atomicMax(wy1 + v, ay1);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
+  constexpr int kWarps = kTile / 32;
   __shared__ ViewF sv[kMaxViewsTC];
   __shared__ float4 sbound[kMaxViewsTC];
   __shared__ int wx0[kMaxViewsTC], wx1[kMaxViewsTC], wy0[kMaxViewsTC], wy1[kMaxViewsTC];
-  __shared__ unsigned char s_cls[kMaxViewsTC];
-  __shared__ int s_mixed[kMaxViewsTC];
-  __shared__ uint32_t s_full[2];
-  __shared__ int s_nmixed;
-  __shared__ float sbb[kTile / 32][6];
-  const int tid = threadIdx.x, lane = tid & 31;
+  __shared__ unsigned char s_mixed[kWarps][kMaxViewsTC];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t tile = blockIdx.x;
   const int64_t jpt = tile * kTile + tid;
   const bool valid = jpt < P.n;
   const float4 p = valid ? P.spts[jpt] : make_float4(0.f, 0.f, 0.f, 0.f);
-  {
-    float b[6] = {valid ? p.x : INFINITY, valid ? p.y : INFINITY, valid ? p.z : INFINITY,
-                  valid ? p.x : -INFINITY, valid ? p.y : -INFINITY, valid ? p.z : -INFINITY};
+  for (int j = tid; j < P.nv; j += kTile) {
+    sv[j] = P.viewf[j];  // per-view fp32 camera + constant error bounds (k_view_setup)
+    sbound[j] = P.vbound[j];
+    wx0[j] = INT_MAX;
+    wy0[j] = INT_MAX;
+    wx1[j] = -1;
+    wy1[j] = -1;
+  }
+  float lo[3] = {valid ? p.x : INFINITY, valid ? p.y : INFINITY, valid ? p.z : INFINITY};
+  float hi[3] = {valid ? p.x : -INFINITY, valid ? p.y : -INFINITY, valid ? p.z : -INFINITY};
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+  for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        b[a] = fminf(b[a], __shfl_xor_sync(0xffffffffu, b[a], o));
-        b[a + 3] = fmaxf(b[a + 3], __shfl_xor_sync(0xffffffffu, b[a + 3], o));
-      }
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
     }
-    if (lane == 0)
-#pragma unroll
-      for (int a = 0; a < 6; ++a) sbb[tid >> 5][a] = b[a];
   }
   __syncthreads();
   const float eps_f = (float)P.eps;
-  if (tid < P.nv) {
-    const ViewF v = P.viewf[tid];  // per-view fp32 camera (k_view_setup)
-    float lo[3], hi[3];
+  const bool any_point = lo[0] <= hi[0];
+  uint32_t fb[2], mb[2];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      lo[a] = fminf(fminf(sbb[0][a], sbb[1][a]), fminf(sbb[2][a], sbb[3][a]));
-      hi[a] = fmaxf(fmaxf(sbb[0][a + 3], sbb[1][a + 3]), fmaxf(sbb[2][a + 3], sbb[3][a + 3]));
-    }
-    int4 win = make_int4(INT_MAX, INT_MAX, -1, -1);
-    const int cls = classify_tile_view(v, P.depth, lo, hi, eps_f, win);
-    s_cls[tid] = (unsigned char)cls;
-    wx0[tid] = win.x;
-    wy0[tid] = win.y;
-    wx1[tid] = win.z;
-    wy1[tid] = win.w;
-    if (cls == kViewMixed) {
-      sv[tid] = v;
-      sbound[tid] = P.vbound[tid];
-    }
-  }
-  __syncthreads();
-  if (tid < 32) {  // ballot compaction: FULL bitmask, MIXED list (<= 64 views: two per lane)
-    const bool m0 = lane < P.nv && s_cls[lane] == kViewMixed;
-    const bool m1 = lane + 32 < P.nv && s_cls[lane + 32] == kViewMixed;
-    const uint32_t b0 = __ballot_sync(0xffffffffu, m0), b1 = __ballot_sync(0xffffffffu, m1);
-    const uint32_t f0 = __ballot_sync(0xffffffffu, lane < P.nv && s_cls[lane] == kViewFull);
-    const uint32_t f1 = __ballot_sync(0xffffffffu, lane + 32 < P.nv && s_cls[lane + 32] == kViewFull);
-    const uint32_t below = (1u << lane) - 1u;
-    if (m0) s_mixed[__popc(b0 & below)] = lane;
-    if (m1) s_mixed[__popc(b0) + __popc(b1 & below)] = lane + 32;
-    if (lane == 0) {
-      s_nmixed = __popc(b0) + __popc(b1);
-      s_full[0] = f0;
-      s_full[1] = f1;
-      if (P.dbg) {
-        atomicAdd(P.dbg + 16 * 1000 + 3, (unsigned long long)(__popc(f0) + __popc(f1)));
-        atomicAdd(P.dbg + 16 * 1000 + 4, (unsigned long long)(__popc(b0) + __popc(b1)));
-        atomicAdd(P.dbg + 16 * 1000 + 5, (unsigned long long)P.nv);
+  for (int r = 0; r < 2; ++r) {
+    const int v = lane + 32 * r;
+    int cls = kViewOff;
+    if (any_point && v < P.nv) {
+      int4 win = make_int4(INT_MAX, INT_MAX, -1, -1);
+      cls = classify_tile_view(sv[v], P.depth, lo, hi, eps_f, win);
+      if (cls == kViewFull) {
+        atomicMin(wx0 + v, win.x);
+        atomicMin(wy0 + v, win.y);
+        atomicMax(wx1 + v, win.z);
+        atomicMax(wy1 + v, win.w);
       }
     }
+    fb[r] = __ballot_sync(0xffffffffu, cls == kViewFull);
+    mb[r] = __ballot_sync(0xffffffffu, cls == kViewMixed);
+    const uint32_t below = (1u << lane) - 1u;
+    if (cls == kViewMixed) s_mixed[wid][(r ? __popc(mb[0]) : 0) + __popc(mb[r] & below)] = (unsigned char)v;
   }
-  __syncthreads();
-  const int nmixed = s_nmixed;
-  uint32_t w0 = s_full[0], w1 = s_full[1];
+  __syncwarp();
+  if (P.dbg && lane == 0) {
+    atomicAdd(P.dbg + 16 * 1000 + 3, (unsigned long long)(__popc(fb[0]) + __popc(fb[1])));
+    atomicAdd(P.dbg + 16 * 1000 + 4, (unsigned long long)(__popc(mb[0]) + __popc(mb[1])));
+    atomicAdd(P.dbg + 16 * 1000 + 5, (unsigned long long)P.nv);
+  }
+  const int nmixed = __popc(mb[0]) + __popc(mb[1]);
+  const unsigned char* mixed = s_mixed[wid];
+  uint32_t w0 = fb[0], w1 = fb[1];
   int l = 0;
   for (; l + 1 < nmixed; l += 2) {  // two MIXED views in flight (independent depth loads)
-    const int va = s_mixed[l], vb = s_mixed[l + 1];
+    const int va = mixed[l], vb = mixed[l + 1];
     TapF ta, tb;
     const bool visa = valid && point_visible(sv[va], sbound[va], P.views[va], P.depth, p, P.eps, eps_f, ta);
     const bool visb = valid && point_visible(sv[vb], sbound[vb], P.views[vb], P.depth, p, P.eps, eps_f, tb);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const bool vis = h ? visb : visa;
-      const int v = h ? vb : va;
-      const TapF& t = h ? tb : ta;
-      if (vis) {
-        if (v < 32) w0 |= 1u << v;
-        else w1 |= 1u << (v - 32);
-      }
-      if (__any_sync(0xffffffffu, vis)) {
-        const int ax0 = __reduce_min_sync(0xffffffffu, vis ? t.x0 : INT_MAX);
-        const int ay0 = __reduce_min_sync(0xffffffffu, vis ? t.y0 : INT_MAX);
-        const int ax1 = __reduce_max_sync(0xffffffffu, vis ? t.x0 + t.dx : -1);
-        const int ay1 = __reduce_max_sync(0xffffffffu, vis ? t.y0 + t.dy : -1);
-        if (lane == 0) {
-          atomicMin(wx0 + v, ax0);
-          atomicMin(wy0 + v, ay0);
-          atomicMax(wx1 + v, ax1);
-          atomicMax(wy1 + v, ay1);
-        }
-      }
+    if (visa) {
+      if (va < 32) w0 |= 1u << va;
+      else w1 |= 1u << (va - 32);
     }
+    if (visb) {
+      if (vb < 32) w0 |= 1u << vb;
+      else w1 |= 1u << (vb - 32);
+    }
+    window_reduce(visa, ta, wx0, wy0, wx1, wy1, va, lane);
+    window_reduce(visb, tb, wx0, wy0, wx1, wy1, vb, lane);
   }
   if (l < nmixed) {
-    const int v = s_mixed[l];
+    const int v = mixed[l];
     TapF t;
     const bool vis = valid && point_visible(sv[v], sbound[v], P.views[v], P.depth, p, P.eps, eps_f, t);
     if (vis) {
       if (v < 32) w0 |= 1u << v;
       else w1 |= 1u << (v - 32);
     }
-    if (__any_sync(0xffffffffu, vis)) {
-      const int ax0 = __reduce_min_sync(0xffffffffu, vis ? t.x0 : INT_MAX);
-      const int ay0 = __reduce_min_sync(0xffffffffu, vis ? t.y0 : INT_MAX);
-      const int ax1 = __reduce_max_sync(0xffffffffu, vis ? t.x0 + t.dx : -1);
-      const int ay1 = __reduce_max_sync(0xffffffffu, vis ? t.y0 + t.dy : -1);
-      if (lane == 0) {
-        atomicMin(wx0 + v, ax0);
-        atomicMin(wy0 + v, ay0);
-        atomicMax(wx1 + v, ax1);
-        atomicMax(wy1 + v, ay1);
-      }
-    }
+    window_reduce(vis, t, wx0, wy0, wx1, wy1, v, lane);
   }
   if (valid) {
-    double lo[3];
-    const double edge = voxel_edge(P.lo_hi, P.grid, lo);
-    const int32_t code = voxel_code(p.x, p.y, p.z, lo, edge, P.grid);
+    double dlo[3];
+    const double edge = voxel_edge(P.lo_hi, P.grid, dlo);
+    const int32_t code = voxel_code(p.x, p.y, p.z, dlo, edge, P.grid);
     *reinterpret_cast<uint4*>(P.srec + jpt) =
         make_uint4(w0, w1, (uint32_t)(__popc(w0) + __popc(w1)), (uint32_t)code);
   }
@@ -516,7 +507,9 @@ int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf
 int run_unsort(const TileParams& P, cudaStream_t st) {
   k_unsort<<<grid_for(P.n, 256), 256, 0, st>>>(P.srec, P.inv, P.n, P.nwords, P.p, P.mask_bits, P.counts,
                                               P.codes, P.props);
-  return check_launch("unsort");
+  const int rc = check_launch("unsort");
+  stage_mark(4, st);
+  return rc;
 }
 
 int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const float* points,
@@ -524,6 +517,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   uint32_t* keys = reinterpret_cast<uint32_t*>(ws + L.keys);
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
   uint32_t* totals = reinterpret_cast<uint32_t*>(ws + L.totals);
+  stage_mark(0, st);
   cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kSortBins, st);
   cudaMemsetAsync(P.ovf_count, 0, sizeof(int32_t), st);
   k_sort_keys<<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist);
@@ -537,6 +531,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   k_sort_scatter<<<grid_for(n, 256), 256, 0, st>>>(points, n, keys, hist, const_cast<int32_t*>(P.inv),
                                                    const_cast<float4*>(P.spts));
   if (int rc = check_launch("sort_scatter")) return rc;
+  stage_mark(1, st);
   static unsigned long long* pdbg = nullptr;
   const bool debug = getenv("PF_WS_DEBUG") != nullptr;
   TileParams Q = P;
@@ -549,6 +544,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   if (int rc = check_launch("view_setup")) return rc;
   k_tile_prep<<<(unsigned)L.ntiles, kTile, 0, st>>>(Q);
   if (int rc = check_launch("tile_prep")) return rc;
+  stage_mark(2, st);
   if (debug) {
     unsigned long long h[6];
     cudaMemcpyAsync(h, pdbg + 16 * 1000, sizeof(h), cudaMemcpyDeviceToHost, st);
@@ -567,7 +563,9 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
             100.0 * (h[5] - h[3] - h[4]) / h[5], ksum / kt.size(), (long long)kmax, (long long)over,
             (long long)kt.size());
   }
-  return run_tile_ws(P, st);
+  const int rc = run_tile_ws(P, st);
+  stage_mark(3, st);
+  return rc;
 }
 
 }  // namespace tile

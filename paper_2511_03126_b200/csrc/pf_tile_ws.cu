@@ -1,5 +1,5 @@
 // Persistent, warp-specialised tcgen05 tile kernel of the bf16 fused query (see pf_tile.cu for the
-// formulation). One CTA per SM loops over tiles of 128 sorted points. Roles (20 warps, 5 warp
+// formulation). One CTA per SM loops over tiles of 128 sorted points. Roles (24 warps, 6 warp
 // groups; setmaxnreg moves registers from the producer groups to the accumulator groups):
 //
 //   warps 0-5   B loaders: for every 64-channel chunk of a tile (D/64 feature chunks, then the two
@@ -19,8 +19,9 @@
 //               columns for softmax sums and property regression and a second for the weight
 //               totals, which stay in registers across all tiles of the CTA; voxel atomics; the
 //               regressed properties go to the sorted records.
-//   warps 16-19 A builders: build the next tile's W (bilinear weights, bf16, K-major 128-B swizzle)
-//               while the current tile's MMAs run.
+//   warps 16-23 A builders (two threads per tile row, alternating over the row's visible views):
+//               build the next tile's W (bilinear weights, bf16, K-major 128-B swizzle) while the
+//               current tile's MMAs run.
 // Synchronisation is mbarrier-only (full/empty pairs for A, B stages and TMEM accumulator slots).
 #include <climits>
 #include <cstdio>
@@ -41,9 +42,10 @@ constexpr int kLoadThreads = 32 * kLoadWarps;
 constexpr int kMmaWarp = 6;            // warp 6: MMA issuer (warp 7 idle)
 constexpr int kAccWarp0 = 8;           // warps 8-15: accumulators (2 per TMEM lane group)
 constexpr int kAccThreads = 256;
-constexpr int kBuildWarp0 = 16;        // warps 16-19: A builders
-constexpr int kBuildWarps = 4;
-constexpr int kWsThreads = 640;        // 20 warps = 5 warp groups
+constexpr int kBuildWarp0 = 16;        // warps 16-23: A builders (two per tile row)
+constexpr int kBuildWarps = 8;
+constexpr int kBuildThreads = 32 * kBuildWarps;
+constexpr int kWsThreads = 768;        // 24 warps = 6 warp groups
 constexpr int kCG = 2;                 // 64-column B chunks per MMA group (N = 64 * kCG)
 constexpr int kDCols = 64 * kCG;       // TMEM columns of one accumulator slot
 constexpr int kDBufs = 3;              // TMEM accumulator slots (feature groups and the S group rotate)
@@ -54,8 +56,9 @@ constexpr int kABytes = kTile * ((kKtWs + 63) / 64) * 64 * 2;  // whole 64-colum
 constexpr int kRowStep = kLoadThreads / 8;                      // rows between one thread's copies
 constexpr int kRowsPer = kKtWs / kRowStep;                      // copies per thread per chunk
 constexpr int kHalfK = kMaxKpadTC / 2;                          // materials per accumulator half
-constexpr int kRegProducer = 64, kRegAcc = 144;                 // setmaxnreg budgets (5 x 128 threads)
-static_assert(3 * 128 * kRegProducer + 2 * 128 * kRegAcc <= 65536, "register file");
+constexpr int kRegLaunch = 80;                                  // 65536 / 768, rounded down to 8
+constexpr int kRegProducer = 48, kRegAcc = 136;                 // setmaxnreg budgets (6 x 128 threads)
+static_assert(4 * 128 * kRegProducer + 2 * 128 * kRegAcc <= kWsThreads * kRegLaunch, "register pool");
 static_assert(kRowStep % 8 == 0, "a thread's rows keep their swizzle phase");
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   do {                                             \
     if constexpr (PROF) {                          \
       const long long t0_ = clock64();             \
-      tc::mbar_wait(bar, par);                     \
+      tc::mbar_wait_or_trap(bar, par, slot);       \
       wait_cyc[slot] += clock64() - t0_;           \
     } else {                                       \
       tc::mbar_wait(bar, par);                     \
@@ -292,9 +295,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   } else if (warp < kAccWarp0) {
     reg_dealloc<kRegProducer>();  // idle warp of the second group
   } else if (warp >= kBuildWarp0) {
-    // ================= A builders (thread = tile row) =================
+    // ================= A builders (two threads per tile row) =================
     reg_dealloc<kRegProducer>();
-    const int row = tid - kBuildWarp0 * 32;  // 0..127
+    const int bt = tid - kBuildWarp0 * 32;   // 0..255
+    const int row = bt & (kTile - 1), hb = bt >> 7;
     uint32_t t_local = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       bool ok;
@@ -302,20 +306,22 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       if (!ok) continue;
       WS_WAIT(&S.a_empty, (t_local & 1u) ^ 1u, 5);
       uint2* sdesc = S.desc_a;
-      for (int v = row; v < P.nv; v += 128) sdesc[v] = P.tile_desc[tile * P.nv + v];
+      for (int v = bt; v < P.nv; v += kBuildThreads) sdesc[v] = P.tile_desc[tile * P.nv + v];
       uint4* a4 = reinterpret_cast<uint4*>(sA);
-      for (int e = row; e < ((ktp + 63) >> 6) * kTile * 8; e += 128) a4[e] = make_uint4(0, 0, 0, 0);
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // builders only: zeros + windows visible
+      for (int e = bt; e < ((ktp + 63) >> 6) * kTile * 8; e += kBuildThreads) a4[e] = make_uint4(0, 0, 0, 0);
+      asm volatile("bar.sync 1, %0;" ::"n"(kBuildThreads) : "memory");  // zeros + windows visible
       const int64_t jpt = tile * kTile + row;
       if (jpt < P.n) {
         const float4 p = P.spts[jpt];
         const uint2 mw = *reinterpret_cast<const uint2*>(P.srec + jpt);
+        int nth = 0;
 #pragma unroll
         for (int w = 0; w < 2; ++w) {
           uint32_t bits = w ? mw.y : mw.x;
           while (bits) {
             const int v = w * 32 + __ffs(bits) - 1;
             bits &= bits - 1;
+            if ((nth++ & 1) != hb) continue;  // the row's other thread takes this view
             const ProjF q = project_f32(S.sv[v], p.x, p.y, p.z);
             const TapF t = taps_f32(S.sv[v], q.u, q.v);
             float w00 = (1.f - t.wy) * (1.f - t.wx), w01 = (1.f - t.wy) * t.wx;
@@ -466,12 +472,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         float v[32];
         tc::tmem_ld32(tS + (uint32_t)c0, v);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const float wv = ex2(fmaf(v[q], sc, -m2)) * rs;
-          wacc[c0 + q] += wv;
-          if (outs && valid && k0 + c0 + q < P.k) {
+        for (int q = 0; q < 32; ++q) wacc[c0 + q] = fmaf(ex2(fmaf(v[q], sc, -m2)), rs, wacc[c0 + q]);
+      }
+      if (outs) {  // validation outputs (similarities, softmax weights), caller's order
+        for (int c0 = 0; c0 < kHalfK; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(tS + (uint32_t)c0, v);  // warp-collective: every lane, valid or not
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            if (!valid || k0 + c0 + q >= P.k) continue;
             if (P.sims) P.sims[(int64_t)i * P.k + k0 + c0 + q] = featured ? v[q] * inv : 0.f;
-            if (P.weights) P.weights[(int64_t)i * P.k + k0 + c0 + q] = wv;
+            if (P.weights) P.weights[(int64_t)i * P.k + k0 + c0 + q] = ex2(fmaf(v[q], sc, -m2)) * rs;
           }
         }
       }
