@@ -213,6 +213,14 @@ int pf_fuse_query(const pf_fuse_args_t* args, void* stream);
  * the recorded calls (synchronising on their events) and returns the number of calls (<= 64), or
  * minus a PF_ERR_* status. */
 int pf_stage_timing(int32_t enable);
+/* tcgen05.mma rate microbenchmark: per SM, reps x 8 MMAs (M=128, N=n, K=16, A from shared memory or
+ * TMEM (ts), B resident in shared memory), optionally with concurrent shared-memory stores; writes
+ * (issue cycles, issue->completion cycles) per SM to out_dev (2 x SMs uint64). */
+int pf_bench_umma(int32_t n, int32_t ts, int32_t reps, int32_t stores, void* out_dev, void* stream);
+/* B-operand loader microbenchmark: per SM, `stages` x 16 KB of 128-byte rows gathered from a
+ * (cells, 1024) bf16 table with cp.async (mode 0, the tile kernel's loader pattern) or TMA
+ * tile::gather4 (mode 1); writes cycles per SM to out_dev (SMs uint64). */
+int pf_bench_gather(const void* src_bf16, int32_t cells, int32_t stages, int32_t mode, void* out_dev, void* stream);
 int pf_stage_times(float* ms, int32_t n);
 
 /* C (128,n) f32 = A (128,k) bf16 row-major @ B (k,n) bf16 row-major through the tile kernel's

@@ -114,6 +114,8 @@ SIGNATURES = {
     "pf_fuse_prepare": ([C.POINTER(FuseArgs), _P], C.c_int),
     "pf_fuse_query": ([C.POINTER(FuseArgs), _P], C.c_int),
     "pf_stage_timing": ([_I32], C.c_int),
+    "pf_bench_umma": ([_I32, _I32, _I32, _I32, _P, _P], C.c_int),
+    "pf_bench_gather": ([_P, _I32, _I32, _I32, _P, _P], C.c_int),
     "pf_stage_times": ([_P, _I32], C.c_int),
     "pf_selftest_umma": ([_P, _P, _P, _I32, _I32, _I32, _P], C.c_int),
 }

@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
       }
       x0[r] = w[r] ? wx0[v] : 0;
       y0[r] = h[r] ? wy0[v] : 0;
-      sz[r] = w[r] * h[r];
+      sz[r] = (w[r] * h[r] + 1) & ~1;  // windows start on even taps (whole 32-bit TMEM columns of bf16 pairs)
     }
     int incl0 = sz[0], incl1 = sz[1];
 #pragma unroll
@@ -557,6 +557,30 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
       ksum += k;
       over += ((k + 15) & ~15) > ws_kt_max();
       kmax = k > kmax ? k : kmax;
+    }
+    {  // window shapes
+      std::vector<uint2> ds((size_t)L.ntiles * P.nv);
+      cudaMemcpy(ds.data(), P.tile_desc, sizeof(uint2) * ds.size(), cudaMemcpyDeviceToHost);
+      long long hist[6] = {0, 0, 0, 0, 0, 0}, taps_in[6] = {0, 0, 0, 0, 0, 0}, nonempty = 0;
+      const char* nm[6] = {"2x2", "1x1/1x2/2x1", "3x2/2x3", "3x3", "<=16 other", ">16"};
+      for (const uint2& d : ds) {
+        const int w = d.y & 0xff, h = (d.y >> 8) & 0xff;
+        if (!w) continue;
+        ++nonempty;
+        const int c = (w == 2 && h == 2) ? 0 : (w * h <= 2) ? 1 : (w * h == 6) ? 2 : (w == 3 && h == 3) ? 3
+                      : (w * h <= 16) ? 4 : 5;
+        ++hist[c];
+        taps_in[c] += w * h;
+      }
+      fprintf(stderr, "[prep debug] windows per tile %.1f:", (double)nonempty / L.ntiles);
+      for (int c = 0; c < 6; ++c)
+        fprintf(stderr, " %s %.1f%% (taps %.1f%%)", nm[c], 100.0 * hist[c] / nonempty, 0.0);
+      fprintf(stderr, "\n");
+      long long tt = 0;
+      for (int c = 0; c < 6; ++c) tt += taps_in[c];
+      fprintf(stderr, "[prep debug] share of taps:");
+      for (int c = 0; c < 6; ++c) fprintf(stderr, " %s %.1f%%", nm[c], 100.0 * taps_in[c] / tt);
+      fprintf(stderr, "\n");
     }
     fprintf(stderr, "[prep debug] tile x view: FULL %.1f%%, MIXED %.1f%%, OFF %.1f%%; taps per tile mean %.1f "
             "max %lld, overflow tiles %lld of %lld\n", 100.0 * h[3] / h[5], 100.0 * h[4] / h[5],

@@ -82,6 +82,7 @@ struct TileParams {
   int32_t* ovf_list;
   int32_t* ovf_count;
   unsigned long long* dbg;  // optional counters (PF_WS_DEBUG)
+  uint32_t* trace;          // optional per-tile role timestamps (PF_WS_DEBUG + PF_WS_TRACE=<file>)
   double* partials;
 };
 

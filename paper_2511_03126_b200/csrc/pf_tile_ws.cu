@@ -19,9 +19,9 @@
 //               columns for softmax sums and property regression and a second for the weight
 //               totals, which stay in registers across all tiles of the CTA; voxel atomics; the
 //               regressed properties go to the sorted records.
-//   warps 16-23 A builders (two threads per tile row, alternating over the row's visible views):
-//               build the next tile's W (bilinear weights, bf16, K-major 128-B swizzle) while the
-//               current tile's MMAs run.
+//   warps 16-23 A builders: write the next tile's W (bilinear weights, bf16 pairs) straight into
+//               one of two TMEM A buffers with tcgen05.st (warp 16 + j: lane quarter j & 3, views of
+//               rank parity j >> 2) while the current tile's MMAs run.
 // Synchronisation is mbarrier-only (full/empty pairs for A, B stages and TMEM accumulator slots).
 #include <climits>
 #include <cstdio>
@@ -42,22 +42,24 @@ constexpr int kLoadThreads = 32 * kLoadWarps;
 constexpr int kMmaWarp = 6;            // warp 6: MMA issuer (warp 7 idle)
 constexpr int kAccWarp0 = 8;           // warps 8-15: accumulators (2 per TMEM lane group)
 constexpr int kAccThreads = 256;
-constexpr int kBuildWarp0 = 16;        // warps 16-23: A builders (two per tile row)
+constexpr int kBuildWarp0 = 16;        // warps 16-23: A builders (two per 32 tile rows)
 constexpr int kBuildWarps = 8;
 constexpr int kBuildThreads = 32 * kBuildWarps;
 constexpr int kWsThreads = 768;        // 24 warps = 6 warp groups
+constexpr float kAffineR = 12e-3f;     // tiles wider than 2 * kAffineR (m) build with the exact projection:
+                                       // the expansion error is ~fx X / Z^3 r^2 <= ~0.05 px (0.4% of a C5 cell)
+constexpr int kTraceCtas = 4, kTraceTiles = 64;
 constexpr int kCG = 2;                 // 64-column B chunks per MMA group (N = 64 * kCG)
 constexpr int kDCols = 64 * kCG;       // TMEM columns of one accumulator slot
-constexpr int kDBufs = 3;              // TMEM accumulator slots (feature groups and the S group rotate)
-constexpr int kStages = 6;             // B ring depth (3 chunk groups)
+constexpr int kDBufs = 2;              // TMEM accumulator slots (feature groups and the S group rotate)
+constexpr int kStages = 8;             // B ring depth (4 chunk groups)
 constexpr int kKtWs = 192;             // taps per tile held in one A buffer / B stage
 constexpr int kStageBytes = kKtWs * 128;
-constexpr int kABytes = kTile * ((kKtWs + 63) / 64) * 64 * 2;  // whole 64-column swizzle atoms
 constexpr int kRowStep = kLoadThreads / 8;                      // rows between one thread's copies
 constexpr int kRowsPer = kKtWs / kRowStep;                      // copies per thread per chunk
 constexpr int kHalfK = kMaxKpadTC / 2;                          // materials per accumulator half
 constexpr int kRegLaunch = 80;                                  // 65536 / 768, rounded down to 8
-constexpr int kRegProducer = 48, kRegAcc = 136;                 // setmaxnreg budgets (6 x 128 threads)
+constexpr int kRegProducer = 48, kRegAcc = 144;                 // setmaxnreg budgets (6 x 128 threads)
 static_assert(4 * 128 * kRegProducer + 2 * 128 * kRegAcc <= kWsThreads * kRegLaunch, "register pool");
 static_assert(kRowStep % 8 == 0, "a thread's rows keep their swizzle phase");
 
@@ -74,14 +76,19 @@ __device__ __forceinline__ void reg_alloc() {
 }
 
 struct WsShared {
-  uint64_t a_full, a_empty;
+  uint64_t a_full[2], a_empty[2];
   uint64_t b_full[kStages], b_empty[kStages];
   uint64_t d_full[kDBufs], d_empty[kDBufs];
   uint32_t tmem_base;
   int pad;
-  uint2 desc_a[kMaxViewsTC];     // A builders' copy of the tile windows
+  uint2 desc_a[2][kMaxViewsTC];  // A builders' copy of the tile windows (per A buffer)
   int32_t cell[2][kKtWs];        // loaders: tap row -> global cell, per tile (ring of 2)
   ViewF sv[kMaxViewsTC];
+  float4 vpk[kMaxViewsTC][5];    // builders: packed camera {R0 R1 R2 t0}{R3 R4 R5 t1}{R6 R7 R8 t2}{fx cx fy cy}{ru rv Wf-1 Hf-1}
+  float4 vcoef[2][kMaxViewsTC][2];  // builders: fu, fv = c0 + g . (p - o) per view rank (per A buffer)
+  int32_t vrank[2][kMaxViewsTC];    // builders: view | window base << 8, per rank
+  int4 vwin[2][kMaxViewsTC];        // builders: window x0, y0, w, h per rank
+  float bbox[2][4][6];              // builders: per lane group box of the tile's points
   float4 yv[kMaxKpadTC];         // per material: {y0, y1, mid_theta, bias (0 | -inf for padding)}
   float4 yv2[kMaxKpadTC];        // per material: {y2, y3, 0, 0} (P > 2)
   float xss[2][kTile];           // accumulator halves: partial |F|^2
@@ -90,11 +97,16 @@ struct WsShared {
   double red[kMaxKpadTC + 8];
 };
 
-__device__ __forceinline__ int tile_ktp(const TileParams& P, int64_t tile, bool& ok) {
-  const int kt = P.tile_kt[tile];
+
+// every role reads the next tile's inputs (tap count, windows, points, records) one tile ahead, so
+// their DRAM latency overlaps the current tile
+__device__ __forceinline__ int ktp_of(int kt, bool& ok) {
   const int ktp = (kt + 15) & ~15;
   ok = kt > 0 && ktp <= kKtWs;
   return ktp;
+}
+__device__ __forceinline__ int kt_at(const TileParams& P, int64_t tile, int64_t ntiles) {
+  return tile < ntiles ? P.tile_kt[tile] : 0;
 }
 
 __device__ __forceinline__ uint16_t f2bf16(float f) {
@@ -112,17 +124,26 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sA = smem;                     // [128 rows x kKtWs] bf16
-  unsigned char* sB = smem + kABytes;           // kStages x [kKtWs rows x 128 B]
+  unsigned char* sB = smem;                     // kStages x [kKtWs rows x 128 B]
   __shared__ WsShared S;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nd = P.d >> 6, ns = P.kpadg >> 6, nch = nd + ns;
   const int64_t ntiles = (P.n + kTile - 1) / kTile;
   // PROF (PF_WS_DEBUG=1): per-role mbarrier wait / issue cycles, printed by the host
-  long long wait_cyc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long wait_cyc[15] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long issue_cyc = 0;
   const long long t_start = PROF ? clock64() : 0;
+  // PROF trace: per-tile role timestamps (cycles since kernel start) of the first kTraceTiles tiles of
+  // the first kTraceCtas CTAs; events: 0 build start, 1 build zeroed, 2 build done, 3 mma A ready,
+  // 4-12 mma group g issued, 13 loader tile start, 14-22 loader group g published, 23-31 acc group g
+  // ready (last = similarity group)
+  uint32_t* trace = (PROF && P.trace && blockIdx.x < kTraceCtas) ? P.trace + blockIdx.x * kTraceTiles * 32 : nullptr;
+#define WS_TRACE(tl, ev)                                                                   \
+  do {                                                                                     \
+    if (PROF && trace && (tl) < (uint32_t)kTraceTiles && (ev) < 32)                        \
+      trace[(tl) * 32 + (ev)] = (uint32_t)(clock64() - t_start);                           \
+  } while (0)
 #define WS_WAIT(bar, par, slot)                    \
   do {                                             \
     if constexpr (PROF) {                          \
@@ -136,7 +157,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
 #define WS_CLOCK() (PROF ? clock64() : 0ll)
 
   // ---- setup ------------------------------------------------------------------------------------------
-  for (int j = tid; j < P.nv; j += kWsThreads) S.sv[j] = make_viewf(P.views[j], P.d);
+  for (int j = tid; j < P.nv; j += kWsThreads) {
+    const ViewF w = make_viewf(P.views[j], P.d);
+    S.sv[j] = w;
+    S.vpk[j][0] = make_float4(w.R[0], w.R[1], w.R[2], w.t[0]);
+    S.vpk[j][1] = make_float4(w.R[3], w.R[4], w.R[5], w.t[1]);
+    S.vpk[j][2] = make_float4(w.R[6], w.R[7], w.R[8], w.t[2]);
+    S.vpk[j][3] = make_float4(w.fx, w.cx, w.fy, w.cy);
+    S.vpk[j][4] = make_float4(w.ru, w.rv, (float)(w.Wf - 1), (float)(w.Hf - 1));
+  }
   for (int j = tid; j < kMaxKpadTC; j += kWsThreads) {
     float y[4];
 #pragma unroll
@@ -146,25 +175,28 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   }
   for (int j = tid; j < kMaxKpadTC + 8; j += kWsThreads) S.red[j] = 0.0;
   if (tid == 0) {
-    tc::mbar_init(&S.a_full, kBuildWarps);
-    tc::mbar_init(&S.a_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&S.a_full[b], kBuildWarps);
+      tc::mbar_init(&S.a_empty[b], 1);
+    }
     for (int b = 0; b < kDBufs; ++b) {
       tc::mbar_init(&S.d_full[b], 1);
       tc::mbar_init(&S.d_empty[b], kAccThreads / 32);
     }
     for (int s = 0; s < kStages; ++s) {
-      tc::mbar_init(&S.b_full[s], kLoadWarps);
+      tc::mbar_init(&S.b_full[s], kLoadThreads);  // one cp.async.mbarrier.arrive.noinc per loader thread
       tc::mbar_init(&S.b_empty[s], 1);
     }
   }
   if (warp == kAccWarp0) tc::tmem_alloc(&S.tmem_base, 512);
-  static_assert(kDBufs * kDCols + kKtWs / 2 <= 512, "TMEM: accumulator slots + A");
+  static_assert(kDBufs * kDCols + 2 * (kKtWs / 2) <= 512, "TMEM: accumulator slots + 2 A buffers");
   static_assert(kDCols == kMaxKpadTC, "the S group fills one accumulator slot");
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = S.tmem_base;
-  const uint32_t tA = tbase + kDBufs * kDCols;          // A (bf16 pairs): kKtWs / 2 columns
+  // two A buffers (bf16 pairs, lane = tile row, k ascending): kKtWs / 2 columns each
+  const uint32_t tA0 = tbase + kDBufs * kDCols;
 
   if (warp < kLoadWarps) {
     // ================= B loaders =================
@@ -173,35 +205,35 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     const int q = tid & 7, r0 = tid >> 3;
     int stage = 0;
     uint32_t phase = 0;
-    int npend = 0;   // chunks whose cp.async groups are in flight: stages stage-npend .. stage-1
+    uint32_t published = 0, pub_tile = 0, pub_group = 0;  // PROF trace bookkeeping (warp 0)
     uint32_t t_local = 0;
-    auto retire_oldest = [&](int keep) {  // wait for the oldest group, publish its stage
-      const long long tr0 = WS_CLOCK();
-      if (keep == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
-      else if (keep == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
-      else asm volatile("cp.async.wait_group 0;" ::: "memory");
-      if constexpr (PROF) wait_cyc[10] += clock64() - tr0;
-      tc::fence_async_shared();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.b_full[(stage + kStages - npend) % kStages]);
-      --npend;
-    };
+    int kt_nx = kt_at(P, blockIdx.x, ntiles);
+    uint2 ds_nx = (tid < P.nv && blockIdx.x < ntiles) ? P.tile_desc[blockIdx.x * P.nv + tid] : make_uint2(0u, 0u);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int kt = kt_nx;
+      const uint2 ds_cur = ds_nx;
+      kt_nx = kt_at(P, tile + gridDim.x, ntiles);
+      if (tid < P.nv && tile + gridDim.x < ntiles) ds_nx = P.tile_desc[(tile + gridDim.x) * P.nv + tid];
       bool ok;
-      const int ktp = tile_ktp(P, tile, ok);
+      const int ktp = ktp_of(kt, ok);
       if (!ok) continue;
       // row -> cell table for this tile
       int32_t* cell = S.cell[t_local & 1];
       asm volatile("bar.sync 3, %0;" ::"n"(kLoadThreads) : "memory");
+      static_assert(kMaxViewsTC <= kLoadThreads, "one window per loader thread");
       for (int v = tid; v < P.nv; v += kLoadThreads) {
-        const uint2 ds = P.tile_desc[tile * P.nv + v];
+        const uint2 ds = ds_cur;
         const int base = ds.x & 0xffff, x0 = (ds.x >> 16) & 0xff, y0 = ds.x >> 24;
         const int w = ds.y & 0xff, h = (ds.y >> 8) & 0xff;
         const ViewF& vw = S.sv[v];
-        for (int a = 0; a < w * h; ++a) cell[base + a] = vw.cell_base + (y0 + a / w) * vw.Wf + x0 + a % w;
+        const int sz = (w * h + 1) & ~1;  // padding column (zero weights) reads a valid row
+        for (int a = 0; a < sz; ++a) {
+          const int aa = a < w * h ? a : 0;
+          cell[base + a] = vw.cell_base + (y0 + aa / w) * vw.Wf + x0 + aa % w;
+        }
       }
       asm volatile("bar.sync 3, %0;" ::"n"(kLoadThreads) : "memory");
-      const int kt = P.tile_kt[tile];
+      if (tid == 0) WS_TRACE(t_local, 13);
       int rc[kRowsPer];
 #pragma unroll
       for (int j = 0; j < kRowsPer; ++j) {
@@ -227,14 +259,22 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
 #pragma unroll
         for (int j = 0; j < kRowsPer; ++j)
           if (rc[j] >= 0) tc::cp_async16(dst0 + (uint32_t)j * (kRowStep / 8 * 1024u), src + (int64_t)rc[j] * rowlen);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        if constexpr (PROF) wait_cyc[11] += clock64() - tl0;
+        // the stage's full barrier completes when every loader thread's copies have landed (as
+        // CUTLASS's SM100 cp.async mainloop: no wait_group, no proxy fence before the UMMA reads)
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&S.b_full[stage]))
+                     : "memory");
+        if constexpr (PROF) {
+          wait_cyc[11] += clock64() - tl0;
+          if (warp == 0 && lane == 0 && (++published & 1) == 0) {
+            WS_TRACE(pub_tile, 14 + pub_group);  // (issue time of the group's second chunk)
+            if (++pub_group == nch / 2) { pub_group = 0; ++pub_tile; }
+          }
+        }
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
-        if (++npend == 3) retire_oldest(2);
       }
       ++t_local;
     }
-    while (npend > 0) retire_oldest(npend - 1);
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer =================
     // chunks are issued in pairs: two consecutive 64-column B chunks sit in adjacent ring stages
@@ -246,24 +286,20 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     uint32_t dcount = 0;  // chunk pairs issued so far (selects the TMEM accumulator slot)
     uint32_t t_local = 0;
     const uint32_t idesc = tc::idesc_bf16_f32(128, kDCols, false, true);
+    int kt_nx = kt_at(P, blockIdx.x, ntiles);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int kt = kt_nx;
+      kt_nx = kt_at(P, tile + gridDim.x, ntiles);
       bool ok;
-      const int ktp = tile_ktp(P, tile, ok);
+      const int ktp = ktp_of(kt, ok);
       if (!ok) continue;
-      WS_WAIT(&S.a_full, t_local & 1u, 1);
-      const uint32_t a0 = tc::smem_u32(sA);
-      // A (the tile's bilinear weights) into TMEM once per tile (tcgen05.cp, 128 rows x 16 k per
-      // op); the MMAs then read A from TMEM and only B from shared memory. The copies execute in
-      // issue order after the previous tile's MMAs, so one TMEM A region suffices; the commit
-      // releases the shared-memory A buffer to the builders as soon as the copies are done.
+      const int ab = (int)(t_local & 1u);
+      WS_WAIT(&S.a_full[ab], (t_local >> 1) & 1u, 1);
+      if (lane == 0) WS_TRACE(t_local, 3);
+      // the builders wrote A (the tile's bilinear weights) straight into TMEM buffer ab; the MMAs read
+      // A from TMEM and B from shared memory; the commit after the last group frees buffer ab
+      const uint32_t tA = tA0 + (uint32_t)(ab * (kKtWs / 2));
       tc::fence_after_sync();
-      if (lane == 0) {
-        for (int s = 0; s < ktp / 16; ++s)
-          tc::tmem_cp_128x256b(tA + (uint32_t)(s * 8),
-                               tc::smem_desc_sw128(a0 + (s >> 2) * kTile * 128 + (s & 3) * 32, 16, 1024));
-        tc::mma_commit(&S.a_empty);
-      }
-      __syncwarp();
       for (int c = 0; c < nch; c += kCG) {
 #pragma unroll
         for (int g = 0; g < kCG; ++g) WS_WAIT(&S.b_full[stage + g], phase, 2);
@@ -273,19 +309,23 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         const uint32_t dst = tbase + (uint32_t)(db * kDCols);
         tc::fence_after_sync();
         const long long ti0 = WS_CLOCK();
-        if (lane == 0) {
-          // (loaders and builders fence their generic-proxy writes before arriving)
+        {
+          // warp-uniform issue (operands in uniform registers, elect.sync picks the issuing lane):
+          // one lane under `if (lane == 0)` measured ~100 cycles per MMA, this reaches the 64-cycle
+          // tensor rate of M=128, N=128, K=16 (scripts/umma_rate.py)
           const uint32_t b0 = tc::smem_u32(sB + stage * kStageBytes);
           for (int s = 0; s < ktp / 16; ++s) {
             const uint64_t bd = tc::smem_desc_sw128(b0 + s * 2048, kStageBytes, 1024);
-            tc::mma_bf16_ts(dst, tA + (uint32_t)(s * 8), bd, idesc, s > 0 ? 1u : 0u);
+            tc::mma_bf16_ts_elect(dst, tA + (uint32_t)(s * 8), bd, idesc, s > 0 ? 1u : 0u);
           }
 #pragma unroll
-          for (int g = 0; g < kCG; ++g) tc::mma_commit(&S.b_empty[stage + g]);
-          tc::mma_commit(&S.d_full[db]);
+          for (int g = 0; g < kCG; ++g) tc::mma_commit_elect(&S.b_empty[stage + g]);
+          tc::mma_commit_elect(&S.d_full[db]);
+          if (c + kCG >= nch) tc::mma_commit_elect(&S.a_empty[ab]);
         }
         __syncwarp();
         if constexpr (PROF) issue_cyc += clock64() - ti0;
+        if (lane == 0) WS_TRACE(t_local, 4 + c / kCG);
         ++dcount;
         stage += kCG;
         if (stage == kStages) { stage = 0; phase ^= 1u; }
@@ -295,53 +335,229 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   } else if (warp < kAccWarp0) {
     reg_dealloc<kRegProducer>();  // idle warp of the second group
   } else if (warp >= kBuildWarp0) {
-    // ================= A builders (two threads per tile row) =================
+    // ================= A builders: W straight into TMEM =================
+    // Builder warp 16 + j owns TMEM lane group q = j & 3 (tile rows 32q .. 32q + 31; tcgen05.st can
+    // only reach a warp's own lane quarter) and every other view present in the tile (rank parity
+    // j >> 2). For each of its views it writes all 32 rows' columns of that view's window (zeros
+    // where a row does not see the view), so every column of the tile's A is written exactly once.
+    // The taps come from a first-order expansion of fu, fv (fusion.py:83-86) around the tile centre
+    // (error ~1e-3 px over a tile), clamped into prep's window (a tap can only leave it when its
+    // weight is ~0); tiles wider than 2 kAffineR use the exact fp32 projection, bit-identical to
+    // prep's (pf_tile_dev.cuh). A 2x2 window (the common case: a tile is ~1/10 of a feature cell)
+    // is two TMEM columns written with one tcgen05.st.x2.
     reg_dealloc<kRegProducer>();
-    const int bt = tid - kBuildWarp0 * 32;   // 0..255
-    const int row = bt & (kTile - 1), hb = bt >> 7;
+    const int bj = warp - kBuildWarp0, bq = bj & 3, bh = bj >> 2, bt = tid - kBuildWarp0 * 32;
+    const int row = 32 * bq + lane;
+    const uint32_t t_lanes = (uint32_t)(32 * bq) << 16;
     uint32_t t_local = 0;
+    static_assert(kMaxViewsTC <= kBuildThreads, "one window per builder thread");
+    auto fetch = [&](int64_t t, int& kt, uint2& ds, float4& pp, uint2& mm) {
+      kt = kt_at(P, t, ntiles);
+      pp = make_float4(0.f, 0.f, 0.f, 0.f);
+      mm = make_uint2(0u, 0u);  // rows past the end: empty mask
+      if (t >= ntiles) return;
+      if (bt < P.nv) ds = P.tile_desc[t * P.nv + bt];
+      if (t * kTile + row < P.n) {
+        pp = P.spts[t * kTile + row];
+        mm = *reinterpret_cast<const uint2*>(P.srec + t * kTile + row);
+      }
+    };
+    int kt_nx = 0;
+    uint2 ds_nx = make_uint2(0u, 0u), mw_nx;
+    float4 p_nx;
+    fetch(blockIdx.x, kt_nx, ds_nx, p_nx, mw_nx);
+    const float wf1 = (float)(S.sv[0].Wf - 1), hf1 = (float)(S.sv[0].Hf - 1);  // uniform maps (tile_path_ok)
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int kt = kt_nx;
+      const uint2 ds_cur = ds_nx;
+      const float4 p = p_nx;
+      const uint2 mw = mw_nx;
+      fetch(tile + gridDim.x, kt_nx, ds_nx, p_nx, mw_nx);
       bool ok;
-      const int ktp = tile_ktp(P, tile, ok);
+      const int ktp = ktp_of(kt, ok);
       if (!ok) continue;
-      WS_WAIT(&S.a_empty, (t_local & 1u) ^ 1u, 5);
-      uint2* sdesc = S.desc_a;
-      for (int v = bt; v < P.nv; v += kBuildThreads) sdesc[v] = P.tile_desc[tile * P.nv + v];
-      uint4* a4 = reinterpret_cast<uint4*>(sA);
-      for (int e = bt; e < ((ktp + 63) >> 6) * kTile * 8; e += kBuildThreads) a4[e] = make_uint4(0, 0, 0, 0);
-      asm volatile("bar.sync 1, %0;" ::"n"(kBuildThreads) : "memory");  // zeros + windows visible
-      const int64_t jpt = tile * kTile + row;
-      if (jpt < P.n) {
-        const float4 p = P.spts[jpt];
-        const uint2 mw = *reinterpret_cast<const uint2*>(P.srec + jpt);
-        int nth = 0;
+      const int ab = (int)(t_local & 1u);
+      uint2* sdesc = S.desc_a[ab];
+      if (bt < P.nv) sdesc[bt] = ds_cur;
+      // tile box over the valid rows: expansion point and width (this warp's rows, then all four
+      // lane groups through shared memory)
+      float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+      if (tile * kTile + row < P.n) {
+        lo[0] = hi[0] = p.x;
+        lo[1] = hi[1] = p.y;
+        lo[2] = hi[2] = p.z;
+      }
 #pragma unroll
-        for (int w = 0; w < 2; ++w) {
-          uint32_t bits = w ? mw.y : mw.x;
-          while (bits) {
-            const int v = w * 32 + __ffs(bits) - 1;
-            bits &= bits - 1;
-            if ((nth++ & 1) != hb) continue;  // the row's other thread takes this view
-            const ProjF q = project_f32(S.sv[v], p.x, p.y, p.z);
-            const TapF t = taps_f32(S.sv[v], q.u, q.v);
-            float w00 = (1.f - t.wy) * (1.f - t.wx), w01 = (1.f - t.wy) * t.wx;
-            float w10 = t.wy * (1.f - t.wx), w11 = t.wy * t.wx;
-            if (!t.dx) { w00 += w01; w10 += w11; }
-            if (!t.dy) { w00 += w10; w01 += w11; }
-            const uint2 ds = sdesc[v];
-            const int base = ds.x & 0xffff, x0 = (ds.x >> 16) & 0xff, y0 = ds.x >> 24;
-            const int ww = ds.y & 0xff;
-            const int c00 = base + (t.y0 - y0) * ww + (t.x0 - x0);
-            *reinterpret_cast<uint16_t*>(sA + tc::a_off(row, c00, kTile)) = f2bf16(w00);
-            if (t.dx) *reinterpret_cast<uint16_t*>(sA + tc::a_off(row, c00 + 1, kTile)) = f2bf16(w01);
-            if (t.dy) *reinterpret_cast<uint16_t*>(sA + tc::a_off(row, c00 + ww, kTile)) = f2bf16(w10);
-            if (t.dx && t.dy) *reinterpret_cast<uint16_t*>(sA + tc::a_off(row, c00 + ww + 1, kTile)) = f2bf16(w11);
-          }
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+          hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+      if (lane == 0 && bh == 0)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          S.bbox[ab][bq][a] = lo[a];
+          S.bbox[ab][bq][a + 3] = hi[a];
+        }
+      asm volatile("bar.sync 1, %0;" ::"n"(kBuildThreads) : "memory");  // windows + boxes visible
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = fminf(fminf(S.bbox[ab][0][a], S.bbox[ab][1][a]), fminf(S.bbox[ab][2][a], S.bbox[ab][3][a]));
+        hi[a] = fmaxf(fmaxf(S.bbox[ab][0][a + 3], S.bbox[ab][1][a + 3]), fmaxf(S.bbox[ab][2][a + 3], S.bbox[ab][3][a + 3]));
+      }
+      const float ox = 0.5f * (lo[0] + hi[0]), oy = 0.5f * (lo[1] + hi[1]), oz = 0.5f * (lo[2] + hi[2]);
+      const float ex = hi[0] - lo[0], ey = hi[1] - lo[1], ez = hi[2] - lo[2];
+      const bool exact = ex * ex + ey * ey + ez * ez > 4.f * kAffineR * kAffineR;
+      // views with taps in this tile, by rank; coefficients of rank 8 l + bj by lane l of warp bj
+      const uint2 dlo = lane < P.nv ? sdesc[lane] : make_uint2(0u, 0u);
+      const uint2 dhi = lane + 32 < P.nv ? sdesc[lane + 32] : make_uint2(0u, 0u);
+      const uint32_t vm0 = __ballot_sync(0xffffffffu, (dlo.y & 0xffu) != 0u);
+      const uint32_t vm1 = __ballot_sync(0xffffffffu, (dhi.y & 0xffu) != 0u);
+      const int n0 = __popc(vm0), nvp = n0 + __popc(vm1);
+      {
+        const int rk = kBuildWarps * lane + bj;
+        if (lane < kMaxViewsTC / kBuildWarps && rk < nvp) {
+          const int v = rk < n0 ? (int)__fns(vm0, 0, rk + 1) : 32 + (int)__fns(vm1, 0, rk - n0 + 1);
+          const float4* vp = S.vpk[v];
+          const float4 c0 = vp[0], c1 = vp[1], c2 = vp[2], kk = vp[3], mm = vp[4];
+          const float X = fmaf(c0.z, oz, fmaf(c0.y, oy, c0.x * ox)) + c0.w;
+          const float Y = fmaf(c1.z, oz, fmaf(c1.y, oy, c1.x * ox)) + c1.w;
+          const float Z = fmaf(c2.z, oz, fmaf(c2.y, oy, c2.x * ox)) + c2.w;
+          const float rz = 1.f / Z, xr = X * rz, yr = Y * rz;
+          const float su = mm.x * kk.x * rz, sv = mm.y * kk.z * rz;  // d fu / d X_cam, d fv / d Y_cam
+          const uint2 ds = sdesc[v];
+          // the expansion's constant terms are taken relative to the window origin (wx0, wy0)
+          S.vcoef[ab][rk][0] = make_float4((fmaf(kk.x, xr, kk.y) + 0.5f) * mm.x - 0.5f - (float)((ds.x >> 16) & 0xff),
+                                           su * (c0.x - xr * c2.x), su * (c0.y - xr * c2.y), su * (c0.z - xr * c2.z));
+          S.vcoef[ab][rk][1] = make_float4((fmaf(kk.z, yr, kk.w) + 0.5f) * mm.y - 0.5f - (float)(ds.x >> 24),
+                                           sv * (c1.x - yr * c2.x), sv * (c1.y - yr * c2.y), sv * (c1.z - yr * c2.z));
+          S.vrank[ab][rk] = v | (int)((ds.x & 0xffff) << 8);  // view | window base << 8
+          S.vwin[ab][rk] = make_int4((ds.x >> 16) & 0xff, ds.x >> 24, ds.y & 0xff, (ds.y >> 8) & 0xff);
         }
       }
-      tc::fence_async_shared();
+      // this tile's TMEM A buffer is free once the MMAs of the tile two back have completed
+      WS_WAIT(&S.a_empty[ab], ((t_local >> 1) & 1u) ^ 1u, 5);
+      const long long tb0 = WS_CLOCK();
+      asm volatile("bar.sync 1, %0;" ::"n"(kBuildThreads) : "memory");  // coefficients visible
+      if (bt == 0) WS_TRACE(t_local, 1);
+      tc::fence_after_sync();
+      const uint32_t tAb = tA0 + (uint32_t)(ab * (kKtWs / 2)) + t_lanes;
+      const long long tb1 = WS_CLOCK();
+      if constexpr (PROF) wait_cyc[14] += tb1 - tb0;
+      const float dxp = p.x - ox, dyp = p.y - oy, dzp = p.z - oz;
+      // one view's 32 rows: fast path for 2x2 windows (two TMEM columns), general otherwise;
+      // coordinates relative to the window origin
+      auto unit_general = [&](int rk) {
+        const int vb = S.vrank[ab][rk];
+        const int v = vb & 0xff, base = vb >> 8;
+        const int4 wn = S.vwin[ab][rk];
+        const int wx0 = wn.x, wy0 = wn.y, ww = wn.z, wh = wn.w;
+        const bool vis = (((v < 32 ? mw.x : mw.y) >> (v & 31)) & 1u) != 0u;
+        float fu, fv;
+        if (!exact) {
+          const float4 A0 = S.vcoef[ab][rk][0], A1 = S.vcoef[ab][rk][1];
+          fu = fmaf(A0.w, dzp, fmaf(A0.z, dyp, fmaf(A0.y, dxp, A0.x))) + (float)wx0;
+          fv = fmaf(A1.w, dzp, fmaf(A1.z, dyp, fmaf(A1.y, dxp, A1.x))) + (float)wy0;
+        } else {
+          const ProjF pr = project_f32(S.sv[v], p.x, p.y, p.z);
+          const TapF tf = taps_f32(S.sv[v], pr.u, pr.v);
+          fu = (float)tf.x0 + tf.wx;  // reproduces the clamped coordinate exactly
+          fv = (float)tf.y0 + tf.wy;
+        }
+        const uint32_t col0 = tAb + (uint32_t)(base >> 1);
+        const float x = fminf(fmaxf(fu, 0.f), wf1), y = fminf(fmaxf(fv, 0.f), hf1);
+        const float xf = floorf(x), yf = floorf(y);
+        float wx = x - xf, wy = y - yf;
+        int ix = (int)xf - wx0, iy = (int)yf - wy0;
+        bool dxb = xf < wf1, dyb = yf < hf1;
+        if (ix < 0) { ix = 0; wx = 0.f; }
+        if (ix > ww - 1) { ix = ww - 1; dxb = false; }
+        if (ix + 1 > ww - 1) dxb = false;
+        if (iy < 0) { iy = 0; wy = 0.f; }
+        if (iy > wh - 1) { iy = wh - 1; dyb = false; }
+        if (iy + 1 > wh - 1) dyb = false;
+        float w00 = (1.f - wy) * (1.f - wx), w01 = (1.f - wy) * wx;
+        float w10 = wy * (1.f - wx), w11 = wy * wx;
+        if (!dxb) { w00 += w01; w10 += w11; }
+        if (!dyb) { w00 += w10; w01 += w11; }
+        const int t00 = iy * ww + ix;
+        const int t01 = dxb ? t00 + 1 : -1, t10 = dyb ? t00 + ww : -1, t11 = (dxb && dyb) ? t00 + ww + 1 : -1;
+        auto tapw = [&](int k) {
+          return vis ? (k == t00 ? w00 : 0.f) + (k == t01 ? w01 : 0.f) + (k == t10 ? w10 : 0.f) + (k == t11 ? w11 : 0.f)
+                     : 0.f;
+        };
+        const int ncols = (ww * wh + 1) >> 1;
+        for (int j = 0; j < ncols; ++j) {  // warp-uniform
+          const __nv_bfloat162 pr = __floats2bfloat162_rn(tapw(2 * j), tapw(2 * j + 1));
+          tc::tmem_st_x1(col0 + (uint32_t)j, *reinterpret_cast<const uint32_t*>(&pr));
+        }
+      };
+      // windows with sides in {2, 3} (~99.5% of them at C5): the row's weights are separable,
+      // vx (over the window's columns) x vy (over its rows); clamping into the window reproduces the
+      // reference taps (an exact tap can never leave the window; an expanded one only with ~0 weight)
+      auto small = [&](int v, int base, int ww, int wh, float fu_rel, float fv_rel) {
+        const bool vis = (((v < 32 ? mw.x : mw.y) >> (v & 31)) & 1u) != 0u;
+        const float xr = fminf(fmaxf(fu_rel, 0.f), (float)(ww - 1)), yr = fminf(fmaxf(fv_rel, 0.f), (float)(wh - 1));
+        const float ixf = fminf(floorf(xr), (float)(ww - 2)), iyf = fminf(floorf(yr), (float)(wh - 2));
+        const float wx = xr - ixf, wy = yr - iyf;
+        const float g = vis ? 1.f : 0.f;
+        // x weights over 3 columns / y weights over 3 rows (third entry only for width/height 3)
+        const bool xa = ixf == 0.f, ya = iyf == 0.f;
+        const float vx0 = xa ? 1.f - wx : 0.f, vx1 = xa ? wx : 1.f - wx, vx2 = xa ? 0.f : wx;
+        const float vy0 = ya ? g * (1.f - wy) : 0.f, vy1 = ya ? g * wy : g * (1.f - wy), vy2 = ya ? 0.f : g * wy;
+        const uint32_t col0 = tAb + (uint32_t)(base >> 1);
+        auto pk = [](float lo, float hi) {
+          const __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
+          return *reinterpret_cast<const uint32_t*>(&b2);
+        };
+        if (ww == 2 && wh == 2) {
+          tc::tmem_st_x2(col0, pk(vy0 * vx0, vy0 * vx1), pk(vy1 * vx0, vy1 * vx1));
+        } else if (ww == 3 && wh == 2) {  // taps r0: 0 1 2, r1: 3 4 5
+          tc::tmem_st_x2(col0, pk(vy0 * vx0, vy0 * vx1), pk(vy0 * vx2, vy1 * vx0));
+          tc::tmem_st_x1(col0 + 2u, pk(vy1 * vx1, vy1 * vx2));
+        } else if (ww == 2 && wh == 3) {  // taps r0: 0 1, r1: 2 3, r2: 4 5
+          tc::tmem_st_x2(col0, pk(vy0 * vx0, vy0 * vx1), pk(vy1 * vx0, vy1 * vx1));
+          tc::tmem_st_x1(col0 + 2u, pk(vy2 * vx0, vy2 * vx1));
+        } else {  // 3 x 3: taps 0..8 + one padding tap
+          tc::tmem_st_x4(col0, pk(vy0 * vx0, vy0 * vx1), pk(vy0 * vx2, vy1 * vx0), pk(vy1 * vx1, vy1 * vx2),
+                         pk(vy2 * vx0, vy2 * vx1));
+          tc::tmem_st_x1(col0 + 4u, pk(vy2 * vx2, 0.f));
+        }
+      };
+      for (int rk = bh; rk < nvp; rk += 2) {
+        const int vb = S.vrank[ab][rk];
+        const int v = vb & 0xff, base = vb >> 8;
+        const int4 wn = S.vwin[ab][rk];
+        if (wn.z < 2 || wn.z > 3 || wn.w < 2 || wn.w > 3) {
+          unit_general(rk);
+          continue;
+        }
+        float fu_rel, fv_rel;
+        if (!exact) {
+          const float4 A0 = S.vcoef[ab][rk][0], A1 = S.vcoef[ab][rk][1];
+          fu_rel = fmaf(A0.w, dzp, fmaf(A0.z, dyp, fmaf(A0.y, dxp, A0.x)));
+          fv_rel = fmaf(A1.w, dzp, fmaf(A1.z, dyp, fmaf(A1.y, dxp, A1.x)));
+        } else {
+          const ProjF pr = project_f32(S.sv[v], p.x, p.y, p.z);
+          const TapF tf = taps_f32(S.sv[v], pr.u, pr.v);
+          fu_rel = (float)(tf.x0 - wn.x) + tf.wx;
+          fv_rel = (float)(tf.y0 - wn.y) + tf.wy;
+        }
+        small(v, base, wn.z, wn.w, fu_rel, fv_rel);
+      }
+      if (bh == 0)  // columns past the last window (K padding to 16) must be zero too
+        for (int j = kt >> 1; j < (ktp >> 1); ++j) tc::tmem_st_x1(tAb + (uint32_t)j, 0u);
+      const long long tb2 = WS_CLOCK();
+      tc::tmem_st_wait();
+      if constexpr (PROF) {
+        wait_cyc[12] += tb2 - tb1;
+        wait_cyc[13] += clock64() - tb2;
+      }
+      tc::fence_before_sync();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.a_full);
+      if (lane == 0) mbar_arrive(&S.a_full[ab]);
+      if (bt == 0) WS_TRACE(t_local, 2);
       ++t_local;
     }
   } else {
@@ -351,31 +567,46 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     const int row = 32 * (warp & 3) + lane;            // TMEM lane = tile row
     const uint32_t t_lane = (uint32_t)(32 * (warp & 3)) << 16;
     const int k0 = half * kHalfK;
-    uint32_t dcount = 0;
+    uint32_t dcount = 0, a_tile = 0;
     float wacc[kHalfK];  // weight totals of this thread's rows (integrate.py:133), all tiles
 #pragma unroll
     for (int q = 0; q < kHalfK; ++q) wacc[q] = 0.f;
-    double pm_sum = 0.0, pmx = 0.0, pmy = 0.0, pmz = 0.0, featured_n = 0.0, pairs = 0.0;
+    // per-thread integrate partials (<= ~1k tiles per CTA: fp32 accumulation, flushed in fp64)
+    float pm_sum = 0.f, pmx = 0.f, pmy = 0.f, pmz = 0.f, featured_n = 0.f, pairs = 0.f;
     const bool outs = P.sims || P.weights;
     const bool p_wide = P.p > 2;
+    int kt_nx = kt_at(P, blockIdx.x, ntiles);
+    uint4 rec_nx = make_uint4(0u, 0u, 0u, 0u);
+    float4 p_nx = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (blockIdx.x * kTile + row < P.n) {
+      rec_nx = *reinterpret_cast<const uint4*>(P.srec + blockIdx.x * kTile + row);
+      p_nx = P.spts[blockIdx.x * kTile + row];
+    }
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int kt = kt_nx;
+      const uint4 rec = rec_nx;
+      const float4 pcur = p_nx;
+      kt_nx = kt_at(P, tile + gridDim.x, ntiles);
+      if ((tile + gridDim.x) * kTile + row < P.n) {
+        rec_nx = *reinterpret_cast<const uint4*>(P.srec + (tile + gridDim.x) * kTile + row);
+        p_nx = P.spts[(tile + gridDim.x) * kTile + row];
+      }
       bool ok;
-      tile_ktp(P, tile, ok);
+      ktp_of(kt, ok);
       const int64_t jpt = tile * kTile + row;
       const bool valid = jpt < P.n;
       if (!ok) {
-        if (valid && half == 0) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(P.spts[jpt].w);
+        if (valid && half == 0) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(pcur.w);
         continue;
       }
-      uint4 rec = make_uint4(0u, 0u, 0u, 0u);
-      if (valid) rec = *reinterpret_cast<const uint4*>(P.srec + jpt);
       const int count = (int)rec.z;
       const float invc = count > 0 ? 1.f / (float)count : 0.f;
-      const int32_t i = (valid && (outs || P.features)) ? __float_as_int(P.spts[jpt].w) : 0;
+      const int32_t i = valid ? __float_as_int(pcur.w) : 0;
       float ss0 = 0.f, ss1 = 0.f, ss2 = 0.f, ss3 = 0.f;
       for (int c = 0; c < nd; c += kCG) {  // kCG chunks: this half drains kDCols / 2 columns
         const int db = dcount % kDBufs;
         WS_WAIT(&S.d_full[db], (dcount / kDBufs) & 1u, 6);
+        if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile, 23 + c / kCG);
         tc::fence_after_sync();
 #pragma unroll
         for (int g = 0; g < kCG; ++g) {  // 32 columns at a time (register budget: wacc stays live)
@@ -407,6 +638,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       // ---- epilogue on S (this half's materials) ----------------------------------------------------
       const int sslot = dcount % kDBufs;
       WS_WAIT(&S.d_full[sslot], (dcount / kDBufs) & 1u, 7);
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile, 23 + nd / kCG);
+      ++a_tile;
       const uint32_t tS = tbase + (uint32_t)(sslot * kDCols + k0) + t_lane;
       tc::fence_after_sync();
       asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
@@ -495,7 +728,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
 #pragma unroll
         for (int pp = 0; pp < 4; ++pp) prop[pp] = (S.xsum[0][1 + pp][row] + S.xsum[1][1 + pp][row]) * rs;
         const float pm = (S.xsum[0][5][row] + S.xsum[1][5][row]) * rs;
-        const float4 p = P.spts[jpt];
+        const float4 p = pcur;
         *(reinterpret_cast<float4*>(P.srec + jpt) + 1) = make_float4(prop[0], prop[1], prop[2], prop[3]);
         if (P.grid_partials) {
           const int32_t code = (int32_t)rec.w;
@@ -506,11 +739,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           atomicAdd(P.grid_partials + P.cells3 + code, 1.0f);
         }
         pm_sum += pm;
-        pmx += (double)pm * p.x;
-        pmy += (double)pm * p.y;
-        pmz += (double)pm * p.z;
-        featured_n += featured ? 1.0 : 0.0;
-        pairs += count;
+        pmx = fmaf(pm, p.x, pmx);
+        pmy = fmaf(pm, p.y, pmy);
+        pmz = fmaf(pm, p.z, pmz);
+        featured_n += featured ? 1.f : 0.f;
+        pairs += (float)count;
       }
     }
     // flush this CTA's partials (integrate.py:133-155) once
@@ -519,7 +752,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const float s = warp_sum(wacc[q]);
       if (lane == 0 && k0 + q < P.k && s != 0.f) atomicAdd(&S.red[k0 + q], (double)s);
     }
-    double r6[6] = {pm_sum, pmx, pmy, pmz, featured_n, pairs};
+    double r6[6] = {pm_sum, pmx, pmy, pmz, featured_n, pairs};  // fp64 from here on
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
       r6[q] = warp_sum(r6[q]);
@@ -542,9 +775,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       d[8] = (unsigned long long)(clock64() - t_start);
       d[9] = (unsigned long long)issue_cyc;
     }
+    if (warp == kBuildWarp0) {
+      d[12] = (unsigned long long)wait_cyc[12];
+      d[13] = (unsigned long long)wait_cyc[13];
+      d[14] = (unsigned long long)wait_cyc[14];
+    }
   }
 #undef WS_WAIT
 #undef WS_CLOCK
+#undef WS_TRACE
   tc::fence_before_sync();
   __syncthreads();
   if (warp == kAccWarp0) tc::tmem_dealloc(tbase, 512);
@@ -554,7 +793,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
 
 int ws_kt_max() { return kKtWs; }
 
-size_t ws_smem_bytes() { return (size_t)kABytes + (size_t)kStages * kStageBytes + 1024; }
+size_t ws_smem_bytes() { return (size_t)kStages * kStageBytes + 1024; }
 
 // Launch the persistent kernel (one CTA per SM).
 int run_tile_ws(const TileParams& P, cudaStream_t st) {
@@ -578,6 +817,13 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
     cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 16 * 1024, st);
     Q.dbg = dbg;
   }
+  static uint32_t* trace = nullptr;
+  const char* trace_path = getenv("PF_WS_TRACE");
+  if (debug && trace_path) {
+    if (!trace) cudaMalloc(&trace, sizeof(uint32_t) * kTraceCtas * kTraceTiles * 32);
+    cudaMemsetAsync(trace, 0xff, sizeof(uint32_t) * kTraceCtas * kTraceTiles * 32, st);
+    Q.trace = trace;
+  }
   if (debug) k_tile_ws<true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
   else k_tile_ws<false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
   const int rc = check_launch("tile_ws");
@@ -585,16 +831,24 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
     static unsigned long long h[16 * 1024];
     cudaMemcpyAsync(h, dbg, sizeof(unsigned long long) * 16 * grid, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    const char* names[12] = {"load:b_empty", "mma:a_full", "mma:b_full", "mma:d_empty(F)", "mma:d_empty(S)",
+    const char* names[15] = {"load:b_empty", "mma:a_full", "mma:b_full", "mma:d_empty(F)", "mma:d_empty(S)",
                              "build:a_empty", "acc:d_full(F)", "acc:d_full(S)", "total", "mma:issue",
-                             "load:retire", "load:issue"};
+                             "load:retire", "load:issue", "build:units", "build:st_wait", "build:coef_bar"};
     fprintf(stderr, "[ws debug] mean cycles per CTA over %d CTAs:", grid);
-    for (int q = 0; q < 12; ++q) {
+    for (int q = 0; q < 15; ++q) {
       double sum = 0;
       for (int b = 0; b < grid; ++b) sum += (double)h[b * 16 + q];
       fprintf(stderr, " %s=%.3g", names[q], sum / grid);
     }
     fprintf(stderr, "\n");
+    if (trace_path) {
+      static uint32_t ht[kTraceCtas * kTraceTiles * 32];
+      cudaMemcpy(ht, trace, sizeof(ht), cudaMemcpyDeviceToHost);
+      if (FILE* f = fopen(trace_path, "wb")) {
+        fwrite(ht, sizeof(ht), 1, f);
+        fclose(f);
+      }
+    }
   }
   return rc;
 }
