@@ -558,6 +558,9 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.vbound = reinterpret_cast<float4*>(ws + L.vbound);
     T.ovf_list = reinterpret_cast<int32_t*>(ws + L.ovf) + 1;
     T.ovf_count = reinterpret_cast<int32_t*>(ws + L.ovf);
+    T.sub_count = reinterpret_cast<int32_t*>(ws + L.sub);
+    T.sub_tiles = T.sub_count + 1;
+    T.max_sub_tiles = L.max_sub_tiles;
     T.partials = a->partials;
     if (int rc = tile::run_tile_path(T, L, ws, a->points, a->n, st)) return rc;
     // sorted records -> caller's order; then the overflow points (tiles with more taps than fit in

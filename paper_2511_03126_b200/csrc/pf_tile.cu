@@ -14,7 +14,7 @@
 // integrate.py:133-155).
 //
 // Kernels (this file; the tensor-core tile kernel is pf_tile_ws.cu):
-//   k_sort_keys / k_scan_* / k_sort_scatter — counting sort of the points by a 21-bit Morton key of
+//   k_sort_keys / k_scan_* / k_sort_scatter — counting sort of the points by a 21-bit Hilbert key of
 //       a 128^3 grid over the bbox (spatial coherence of tiles; no library sort);
 //   k_tile_prep — per tile: each view is first classified for the box of every 32 points (OFF:
 //       occluded or off-image for every point; FULL: visible for every point; MIXED), rigorously,
@@ -37,14 +37,42 @@
 namespace pf {
 namespace tile {
 
-// ---- counting sort by a coarse Morton key --------------------------------------------------------------
-__device__ __forceinline__ uint32_t spread3(uint32_t x) {
-  x &= 0x3ffu;
-  x = (x | (x << 16)) & 0x030000ffu;
-  x = (x | (x << 8)) & 0x0300f00fu;
-  x = (x | (x << 4)) & 0x030c30c3u;
-  x = (x | (x << 2)) & 0x09249249u;
-  return x;
+// ---- counting sort by a coarse space-filling-curve key ------------------------------------------------
+
+// 3-D Hilbert index of a cell of the 2^kSortBits grid (Skilling's transpose algorithm): consecutive
+// keys are face-adjacent cells, so a run of consecutive sorted points (a tile) stays one compact
+// surface patch far more often than along a Morton (Z) curve, which jumps across the object.
+__device__ __forceinline__ uint32_t hilbert3(uint32_t x, uint32_t y, uint32_t z) {
+  uint32_t X[3] = {x, y, z};
+  const uint32_t M = 1u << (kSortBits - 1);
+#pragma unroll
+  for (uint32_t Q = M; Q > 1; Q >>= 1) {  // inverse undo
+    const uint32_t Pm = Q - 1;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (X[i] & Q) {
+        X[0] ^= Pm;
+      } else {
+        const uint32_t t = (X[0] ^ X[i]) & Pm;
+        X[0] ^= t;
+        X[i] ^= t;
+      }
+    }
+  }
+  X[1] ^= X[0];  // Gray encode
+  X[2] ^= X[1];
+  uint32_t t = 0;
+#pragma unroll
+  for (uint32_t Q = M; Q > 1; Q >>= 1)
+    if (X[2] & Q) t ^= Q - 1;
+  X[0] ^= t;
+  X[1] ^= t;
+  X[2] ^= t;
+  uint32_t key = 0;
+#pragma unroll
+  for (int b = kSortBits - 1; b >= 0; --b)
+    key = (key << 3) | (((X[0] >> b) & 1u) << 2) | (((X[1] >> b) & 1u) << 1) | ((X[2] >> b) & 1u);
+  return key;
 }
 
 __global__ void k_sort_keys(const float* __restrict__ p, int64_t n, const double* __restrict__ lo_hi,
@@ -58,7 +86,7 @@ __global__ void k_sort_keys(const float* __restrict__ p, int64_t n, const double
     const int cx = min(max((int)((__ldg(p + 3 * i) - lx) * inv), 0), kSortCells - 1);
     const int cy = min(max((int)((__ldg(p + 3 * i + 1) - ly) * inv), 0), kSortCells - 1);
     const int cz = min(max((int)((__ldg(p + 3 * i + 2) - lz) * inv), 0), kSortCells - 1);
-    const uint32_t key = spread3(cx) | (spread3(cy) << 1) | (spread3(cz) << 2);
+    const uint32_t key = hilbert3((uint32_t)cx, (uint32_t)cy, (uint32_t)cz);
     keys[i] = key;
     atomicAdd(hist + key, 1u);
   }
@@ -172,8 +200,17 @@ __device__ __forceinline__ int classify_fast(const ViewF& w, const float4& b, co
 }
 
 // ---- tile x view classification ----------------------------------------------------------------------
-enum : int { kViewOff = 0, kViewFull = 1, kViewMixed = 2 };
+enum : int { kViewOff = 0, kViewFull = 1, kViewMixed = 2, kViewExact = 3 };
 constexpr int kScanMax = 64;  // pixels of depth scanned per (tile, view) at most
+
+// Per-(tile, view) affine model of a MIXED view: u, v, z = c0 + g . (p - o) with rigorous bounds
+// eu, ev, ez on |model - numpy's fp64 value| over the tile box (see classify_tile_view).
+struct ViewAff {
+  float4 u, v, z;        // {value at o, gradient}
+  float eu, ev, ez, pad;
+  int W, H;
+  int64_t depth_off;
+};
 
 // Decide one view for every point of a tile at once. The points lie in the box [lo, hi] (exact:
 // min / max of their f32 coordinates). Camera coordinates are affine in p, so the camera depth over
@@ -186,11 +223,19 @@ constexpr int kScanMax = 64;  // pixels of depth scanned per (tile, view) at mos
 //          -> no point passes z <= stored + eps (numpy_impl.py:31-40);
 //   FULL : the rectangle is inside the image, every stored depth in it is > 0 and
 //          zmax < (min stored depth) + eps -> every point passes;
-//   MIXED: anything else (per-point exact test).
-// FULL views also get their tap window here: fu = (u + 0.5) * Wf/W - 0.5 is computed by the same
-// monotone fp32 ops as taps_f32 on the widened pixel range, which bounds every point's taps.
-__device__ int classify_tile_view(const ViewF& v, const float* __restrict__ depth, const float* lo,
-                                  const float* hi, float eps, int4& win) {
+//   MIXED: per-point test against the affine model (below);
+//   EXACT: the box reaches the camera plane or covers > kScanMax pixels: per-point exact test.
+// FULL and MIXED views get the box's tap window: fu = (u + 0.5) * Wf/W - 0.5 computed by the same
+// monotone fp32 ops as taps_f32 on the widened pixel range bounds every point's taps.
+//
+// MIXED model: o = box centre, d = p - o, |d| <= r. z is affine in p, so z = Z(o) + R2 . d exactly;
+// u = fx X/Z + cx with X = X(o) + a, Z = Z(o) + b (a = R0 . d, b = R2 . d, |a|, |b| <= r):
+//   X/Z - [X0/Z0 + a/Z0 - X0 b/Z0^2] = b (X0 b - a Z0) / (Z0^2 Z)
+// so the first-order model is within fx r^2 (|X0| + Z0) / (Z0^2 zmin) of the exact value. On top:
+// the fp32 error of u(o) (the view's constant project_f32 bound), 3 fma roundings of a ~|u| value
+// and the gradient's relative error.
+__device__ int classify_tile_view(const ViewF& v, const float4& vb, const float* __restrict__ depth,
+                                  const float* lo, const float* hi, float eps, int4& win, ViewAff& aff) {
   float zmin = 1e30f, zmax = -1e30f, umin = 1e30f, umax = -1e30f, vmin = 1e30f, vmax = -1e30f;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -209,14 +254,14 @@ __device__ int classify_tile_view(const ViewF& v, const float* __restrict__ dept
     vmin = fminf(vmin, w);
     vmax = fmaxf(vmax, w);
   }
-  if (!(zmin > 1e-3f)) return kViewMixed;  // the box reaches the camera plane
+  if (!(zmin > 1e-3f)) return kViewExact;  // the box reaches the camera plane
   const float ulo = fmaxf(umin - 0.01f, -1e6f), uhi = fminf(umax + 0.01f, 1e6f);
   const float vlo = fmaxf(vmin - 0.01f, -1e6f), vhi = fminf(vmax + 0.01f, 1e6f);
   const int x0 = (int)rintf(ulo), x1 = (int)rintf(uhi), y0 = (int)rintf(vlo), y1 = (int)rintf(vhi);
   const int cx0 = max(x0, 0), cx1 = min(x1, v.W - 1), cy0 = max(y0, 0), cy1 = min(y1, v.H - 1);
   if (cx1 < cx0 || cy1 < cy0) return kViewOff;
   const int bw = cx1 - cx0 + 1, bh = cy1 - cy0 + 1;
-  if (bw * bh > kScanMax) return kViewMixed;
+  if (bw * bh > kScanMax) return kViewExact;
   const float* d = depth + v.depth_off + (int64_t)cy0 * v.W + cx0;
   float dmax = 0.f, dmin = 1e30f;
   const int npx = bw * bh;
@@ -234,8 +279,6 @@ __device__ int classify_tile_view(const ViewF& v, const float* __restrict__ dept
     }
   }
   if (zmin - 1e-5f > dmax + eps + 1e-5f) return kViewOff;
-  const bool inside = x0 >= 0 && y0 >= 0 && x1 < v.W && y1 < v.H;
-  if (!(inside && dmin > 0.f && zmax + 2e-5f < dmin + eps)) return kViewMixed;
   // tap window of every point (taps_f32 on the widened range; fu is monotone in u)
   const float fu0 = __fsub_rn(__fmul_rn(__fadd_rn(ulo, 0.5f), v.ru), 0.5f);
   const float fu1 = __fsub_rn(__fmul_rn(__fadd_rn(uhi, 0.5f), v.ru), 0.5f);
@@ -246,7 +289,30 @@ __device__ int classify_tile_view(const ViewF& v, const float* __restrict__ dept
   win.y = (int)floorf(fminf(fmaxf(fv0, 0.f), hmax));
   win.z = min((int)floorf(fminf(fmaxf(fu1, 0.f), wmax)) + 1, v.Wf - 1);
   win.w = min((int)floorf(fminf(fmaxf(fv1, 0.f), hmax)) + 1, v.Hf - 1);
-  return kViewFull;
+  const bool inside = x0 >= 0 && y0 >= 0 && x1 < v.W && y1 < v.H;
+  if (inside && dmin > 0.f && zmax + 2e-5f < dmin + eps) return kViewFull;
+  if (!(vb.w > 0.f)) return kViewExact;  // no constant fp32 bound for this view
+  // MIXED: affine model around the box centre
+  const float ox = 0.5f * (lo[0] + hi[0]), oy = 0.5f * (lo[1] + hi[1]), oz = 0.5f * (lo[2] + hi[2]);
+  const float hx = 0.5f * (hi[0] - lo[0]), hy = 0.5f * (hi[1] - lo[1]), hz = 0.5f * (hi[2] - lo[2]);
+  const float r = sqrtf(hx * hx + hy * hy + hz * hz) * 1.0001f + 1e-7f;
+  const ProjF q = project_f32(v, ox, oy, oz);  // |q.u - u64(o)| <= vb.x (o lies in the object box)
+  const float xr = q.X * q.rz, yr = q.Y * q.rz;
+  const float su = v.fx * q.rz, sv = v.fy * q.rz;
+  aff.u = make_float4(q.u, su * (v.R[0] - xr * v.R[6]), su * (v.R[1] - xr * v.R[7]), su * (v.R[2] - xr * v.R[8]));
+  aff.v = make_float4(q.v, sv * (v.R[3] - yr * v.R[6]), sv * (v.R[4] - yr * v.R[7]), sv * (v.R[5] - yr * v.R[8]));
+  aff.z = make_float4(q.z, v.R[6], v.R[7], v.R[8]);
+  const float z0 = q.z, rem = r * r / (z0 * z0 * zmin) * 1.05f;
+  const float gmax_u = fabsf(aff.u.y) + fabsf(aff.u.z) + fabsf(aff.u.w);
+  const float gmax_v = fabsf(aff.v.y) + fabsf(aff.v.z) + fabsf(aff.v.w);
+  aff.eu = vb.x + fabsf(v.fx) * (fabsf(q.X) + z0) * rem + 4e-7f * (fabsf(q.u) + gmax_u * r) + 1e-5f * gmax_u * r + 1e-5f;
+  aff.ev = vb.y + fabsf(v.fy) * (fabsf(q.Y) + z0) * rem + 4e-7f * (fabsf(q.v) + gmax_v * r) + 1e-5f * gmax_v * r + 1e-5f;
+  aff.ez = q.e + 4e-7f * (fabsf(z0) + 2.f * r) + 1e-7f;  // z is exactly affine: rounding only
+  aff.W = v.W;
+  aff.H = v.H;
+  aff.depth_off = v.depth_off;
+  if (!(aff.eu < 0.25f && aff.ev < 0.25f)) return kViewExact;
+  return kViewMixed;
 }
 
 __global__ void k_view_setup(TileParams P) {
@@ -258,7 +324,7 @@ __global__ void k_view_setup(TileParams P) {
   }
 }
 
-// exact per-point decision for one (point, MIXED view) sample; fills the taps when visible
+// exact per-point decision for one (point, view) sample; fills the taps when visible
 __device__ __forceinline__ bool point_visible(const ViewF& v, const float4& b, const pf_view_t& v64,
                                               const float* __restrict__ depth, const float4& p,
                                               double eps, float eps_f, TapF& t) {
@@ -272,11 +338,26 @@ __device__ __forceinline__ bool point_visible(const ViewF& v, const float4& b, c
   return vis;
 }
 
+// MIXED-view decision through the affine model; kAmbiguous sends the sample to point_visible
+__device__ __forceinline__ int affine_visible(const ViewAff& a, const float* __restrict__ depth, float dx,
+                                              float dy, float dz, float eps_f) {
+  const float u = fmaf(a.u.w, dz, fmaf(a.u.z, dy, fmaf(a.u.y, dx, a.u.x)));
+  const float v = fmaf(a.v.w, dz, fmaf(a.v.z, dy, fmaf(a.v.y, dx, a.v.x)));
+  const float du = fabsf(u - floorf(u) - 0.5f), dv = fabsf(v - floorf(v) - 0.5f);
+  if (du <= a.eu || dv <= a.ev) return kAmbiguous;
+  const float ru = rintf(u), rv = rintf(v);
+  if (!(ru >= 0.f && ru < (float)a.W && rv >= 0.f && rv < (float)a.H)) return kInvisible;
+  const float stored = __ldg(depth + a.depth_off + (int64_t)rv * a.W + (int64_t)ru);
+  if (!(stored > 0.f)) return kInvisible;
+  const float z = fmaf(a.z.w, dz, fmaf(a.z.z, dy, fmaf(a.z.y, dx, a.z.x)));
+  const float thr = __fadd_rn(stored, eps_f);
+  const float m = a.ez + 2.4e-7f * fabsf(thr) + 1e-9f;
+  if (z + m < thr) return kNeedDepth;  // visible
+  if (z - m > thr) return kInvisible;
+  return kAmbiguous;
+}
+
 // ---- k_tile_prep ---------------------------------------------------------------------------------------
-// One warp's 32 consecutive sorted points form the classification box (a ~2 mm patch at C5: small
-// enough that most views are decided for all 32 points at once); lane l classifies views l and
-// l + 32. FULL views set their bit for the whole warp and widen the tile's tap window by the box
-// window; MIXED views run the exact per-point test and widen it by the visible points' taps.
 __device__ __forceinline__ void window_reduce(bool vis, const TapF& t, int* wx0, int* wy0, int* wx1, int* wy1,
                                               int v, int lane) {
   if (__any_sync(0xffffffffu, vis)) {
@@ -294,85 +375,135 @@ __device__ __forceinline__ void window_reduce(bool vis, const TapF& t, int* wx0,
 }
 
 __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
-  constexpr int kWarps = kTile / 32;
   __shared__ ViewF sv[kMaxViewsTC];
+  __shared__ ViewAff saff[kMaxViewsTC];
   __shared__ float4 sbound[kMaxViewsTC];
   __shared__ int wx0[kMaxViewsTC], wx1[kMaxViewsTC], wy0[kMaxViewsTC], wy1[kMaxViewsTC];
-  __shared__ unsigned char s_mixed[kWarps][kMaxViewsTC];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  __shared__ unsigned char s_cls[kMaxViewsTC];
+  __shared__ unsigned char s_list[kMaxViewsTC];  // MIXED views, then EXACT views
+  __shared__ uint32_t s_full[2], s_seen[2];
+  __shared__ int s_nmixed, s_nexact;
+  __shared__ float sbb[kTile / 32][6];
+  const int tid = threadIdx.x, lane = tid & 31;
   const int64_t tile = blockIdx.x;
   const int64_t jpt = tile * kTile + tid;
   const bool valid = jpt < P.n;
   const float4 p = valid ? P.spts[jpt] : make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int j = tid; j < P.nv; j += kTile) {
-    sv[j] = P.viewf[j];  // per-view fp32 camera + constant error bounds (k_view_setup)
-    sbound[j] = P.vbound[j];
-    wx0[j] = INT_MAX;
-    wy0[j] = INT_MAX;
-    wx1[j] = -1;
-    wy1[j] = -1;
+  {
+    float b[6] = {valid ? p.x : INFINITY, valid ? p.y : INFINITY, valid ? p.z : INFINITY,
+                  valid ? p.x : -INFINITY, valid ? p.y : -INFINITY, valid ? p.z : -INFINITY};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        b[a] = fminf(b[a], __shfl_xor_sync(0xffffffffu, b[a], o));
+        b[a + 3] = fmaxf(b[a + 3], __shfl_xor_sync(0xffffffffu, b[a + 3], o));
+      }
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int a = 0; a < 6; ++a) sbb[tid >> 5][a] = b[a];
   }
-  float lo[3] = {valid ? p.x : INFINITY, valid ? p.y : INFINITY, valid ? p.z : INFINITY};
-  float hi[3] = {valid ? p.x : -INFINITY, valid ? p.y : -INFINITY, valid ? p.z : -INFINITY};
+  if (tid < 2) s_seen[tid] = 0u;
+  __syncthreads();
+  float lo[3], hi[3];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
-      hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = fminf(fminf(sbb[0][a], sbb[1][a]), fminf(sbb[2][a], sbb[3][a]));
+    hi[a] = fmaxf(fmaxf(sbb[0][a + 3], sbb[1][a + 3]), fmaxf(sbb[2][a + 3], sbb[3][a + 3]));
+  }
+  const float eps_f = (float)P.eps;
+  if (tid < P.nv) {
+    const ViewF v = P.viewf[tid];  // per-view fp32 camera + constant error bounds (k_view_setup)
+    const float4 vb = P.vbound[tid];
+    int4 win = make_int4(INT_MAX, INT_MAX, -1, -1);
+    ViewAff aff;
+    const int cls = classify_tile_view(v, vb, P.depth, lo, hi, eps_f, win, aff);
+    s_cls[tid] = (unsigned char)cls;
+    // FULL: box window now; MIXED: box window once a point is seen visible; EXACT: per-point union
+    const bool boxwin = cls == kViewFull;
+    wx0[tid] = boxwin ? win.x : INT_MAX;
+    wy0[tid] = boxwin ? win.y : INT_MAX;
+    wx1[tid] = boxwin ? win.z : -1;
+    wy1[tid] = boxwin ? win.w : -1;
+    if (cls == kViewMixed) saff[tid] = aff;
+    if (cls == kViewMixed || cls == kViewExact) {
+      sv[tid] = v;
+      sbound[tid] = vb;
+    }
+    // stash the MIXED box window in the EXACT-only slots until visibility is known
+    if (cls == kViewMixed) saff[tid].pad = __int_as_float(win.x | (win.y << 8) | (win.z << 16) | (win.w << 24));
+  }
+  __syncthreads();
+  if (tid < 32) {  // ballot compaction: FULL bitmask, MIXED then EXACT list (<= 64 views: two per lane)
+    const bool m0 = lane < P.nv && s_cls[lane] == kViewMixed;
+    const bool m1 = lane + 32 < P.nv && s_cls[lane + 32] == kViewMixed;
+    const bool e0 = lane < P.nv && s_cls[lane] == kViewExact;
+    const bool e1 = lane + 32 < P.nv && s_cls[lane + 32] == kViewExact;
+    const uint32_t b0 = __ballot_sync(0xffffffffu, m0), b1 = __ballot_sync(0xffffffffu, m1);
+    const uint32_t x0 = __ballot_sync(0xffffffffu, e0), x1 = __ballot_sync(0xffffffffu, e1);
+    const uint32_t f0 = __ballot_sync(0xffffffffu, lane < P.nv && s_cls[lane] == kViewFull);
+    const uint32_t f1 = __ballot_sync(0xffffffffu, lane + 32 < P.nv && s_cls[lane + 32] == kViewFull);
+    const uint32_t below = (1u << lane) - 1u;
+    const int nm = __popc(b0) + __popc(b1);
+    if (m0) s_list[__popc(b0 & below)] = (unsigned char)lane;
+    if (m1) s_list[__popc(b0) + __popc(b1 & below)] = (unsigned char)(lane + 32);
+    if (e0) s_list[nm + __popc(x0 & below)] = (unsigned char)lane;
+    if (e1) s_list[nm + __popc(x0) + __popc(x1 & below)] = (unsigned char)(lane + 32);
+    if (lane == 0) {
+      s_nmixed = nm;
+      s_nexact = __popc(x0) + __popc(x1);
+      s_full[0] = f0;
+      s_full[1] = f1;
+      if (P.dbg) {
+        atomicAdd(P.dbg + 16 * 1000 + 3, (unsigned long long)(__popc(f0) + __popc(f1)));
+        atomicAdd(P.dbg + 16 * 1000 + 4, (unsigned long long)nm);
+        atomicAdd(P.dbg + 16 * 1000 + 5, (unsigned long long)P.nv);
+        atomicAdd(P.dbg + 16 * 1000 + 6, (unsigned long long)(__popc(x0) + __popc(x1)));
+      }
     }
   }
   __syncthreads();
-  const float eps_f = (float)P.eps;
-  const bool any_point = lo[0] <= hi[0];
-  uint32_t fb[2], mb[2];
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int v = lane + 32 * r;
-    int cls = kViewOff;
-    if (any_point && v < P.nv) {
-      int4 win = make_int4(INT_MAX, INT_MAX, -1, -1);
-      cls = classify_tile_view(sv[v], P.depth, lo, hi, eps_f, win);
-      if (cls == kViewFull) {
-        atomicMin(wx0 + v, win.x);
-        atomicMin(wy0 + v, win.y);
-        atomicMax(wx1 + v, win.z);
-        atomicMax(wy1 + v, win.w);
+  const int nmixed = s_nmixed, nexact = s_nexact;
+  uint32_t w0 = s_full[0], w1 = s_full[1];
+  const float dx = p.x - 0.5f * (lo[0] + hi[0]), dy = p.y - 0.5f * (lo[1] + hi[1]), dz = p.z - 0.5f * (lo[2] + hi[2]);
+  uint32_t seen0 = 0u, seen1 = 0u;  // MIXED views this warp saw visible somewhere
+  for (int l = 0; l < nmixed; ++l) {
+    const int v = s_list[l];
+    bool vis = false;
+    if (valid) {
+      int s = affine_visible(saff[v], P.depth, dx, dy, dz, eps_f);
+      if (P.dbg) {
+        atomicAdd(P.dbg + 16 * 1000 + 7, 1ull);
+        if (s == kAmbiguous) atomicAdd(P.dbg + 16 * 1000 + 8, 1ull);
+        if (tid == 0) {  // mean bounds
+          atomicAdd(P.dbg + 16 * 1000 + 9, (unsigned long long)(saff[v].eu * 1e6f));
+          atomicAdd(P.dbg + 16 * 1000 + 10, 1ull);
+        }
+      }
+      if (s == kAmbiguous) {
+        TapF t;
+        vis = point_visible(sv[v], sbound[v], P.views[v], P.depth, p, P.eps, eps_f, t);
+      } else {
+        vis = s == kNeedDepth;
       }
     }
-    fb[r] = __ballot_sync(0xffffffffu, cls == kViewFull);
-    mb[r] = __ballot_sync(0xffffffffu, cls == kViewMixed);
-    const uint32_t below = (1u << lane) - 1u;
-    if (cls == kViewMixed) s_mixed[wid][(r ? __popc(mb[0]) : 0) + __popc(mb[r] & below)] = (unsigned char)v;
-  }
-  __syncwarp();
-  if (P.dbg && lane == 0) {
-    atomicAdd(P.dbg + 16 * 1000 + 3, (unsigned long long)(__popc(fb[0]) + __popc(fb[1])));
-    atomicAdd(P.dbg + 16 * 1000 + 4, (unsigned long long)(__popc(mb[0]) + __popc(mb[1])));
-    atomicAdd(P.dbg + 16 * 1000 + 5, (unsigned long long)P.nv);
-  }
-  const int nmixed = __popc(mb[0]) + __popc(mb[1]);
-  const unsigned char* mixed = s_mixed[wid];
-  uint32_t w0 = fb[0], w1 = fb[1];
-  int l = 0;
-  for (; l + 1 < nmixed; l += 2) {  // two MIXED views in flight (independent depth loads)
-    const int va = mixed[l], vb = mixed[l + 1];
-    TapF ta, tb;
-    const bool visa = valid && point_visible(sv[va], sbound[va], P.views[va], P.depth, p, P.eps, eps_f, ta);
-    const bool visb = valid && point_visible(sv[vb], sbound[vb], P.views[vb], P.depth, p, P.eps, eps_f, tb);
-    if (visa) {
-      if (va < 32) w0 |= 1u << va;
-      else w1 |= 1u << (va - 32);
+    const bool any = __any_sync(0xffffffffu, vis);
+    if (vis) {
+      if (v < 32) w0 |= 1u << v;
+      else w1 |= 1u << (v - 32);
     }
-    if (visb) {
-      if (vb < 32) w0 |= 1u << vb;
-      else w1 |= 1u << (vb - 32);
+    if (any) {
+      if (v < 32) seen0 |= 1u << v;
+      else seen1 |= 1u << (v - 32);
     }
-    window_reduce(visa, ta, wx0, wy0, wx1, wy1, va, lane);
-    window_reduce(visb, tb, wx0, wy0, wx1, wy1, vb, lane);
   }
-  if (l < nmixed) {
-    const int v = mixed[l];
+  if (lane == 0 && (seen0 | seen1)) {
+    atomicOr(&s_seen[0], seen0);
+    atomicOr(&s_seen[1], seen1);
+  }
+  for (int l = nmixed; l < nmixed + nexact; ++l) {
+    const int v = s_list[l];
     TapF t;
     const bool vis = valid && point_visible(sv[v], sbound[v], P.views[v], P.depth, p, P.eps, eps_f, t);
     if (vis) {
@@ -387,6 +518,14 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     const int32_t code = voxel_code(p.x, p.y, p.z, dlo, edge, P.grid);
     *reinterpret_cast<uint4*>(P.srec + jpt) =
         make_uint4(w0, w1, (uint32_t)(__popc(w0) + __popc(w1)), (uint32_t)code);
+  }
+  __syncthreads();
+  if (tid < P.nv && s_cls[tid] == kViewMixed && ((s_seen[tid >> 5] >> (tid & 31)) & 1u)) {
+    const uint32_t w = __float_as_uint(saff[tid].pad);  // the box window (every visible point's taps)
+    wx0[tid] = (int)(w & 0xff);
+    wy0[tid] = (int)((w >> 8) & 0xff);
+    wx1[tid] = (int)((w >> 16) & 0xff);
+    wy1[tid] = (int)(w >> 24);
   }
   __syncthreads();
   if (tid < 32) {  // windows -> descriptors: exclusive prefix of window sizes over views (2 per lane)
@@ -425,6 +564,69 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     }
     if (lane == 31) P.tile_kt[tile] = tot0 + incl1;
   }
+}
+
+// ---- overflow tiles -> sub-tiles ----------------------------------------------------------------------
+// A tile whose windows need more taps than one A buffer holds (it straddles a jump of the Hilbert
+// order: two distant surface patches) is re-run as four sub-tiles of 32 consecutive sorted points,
+// each with the exact union of its visible points' taps; the original tile is marked -1 (skipped).
+__global__ void k_find_overflow(TileParams P, int64_t ntiles, int kt_max) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+    const int kt = P.tile_kt[t];
+    if (((kt + 15) & ~15) <= kt_max) continue;
+    const int b = atomicAdd(P.sub_count, 1);
+    if (b < P.max_sub_tiles) {
+      P.sub_tiles[b] = (int32_t)t;
+      P.tile_kt[t] = -1;
+    }
+  }
+}
+
+// one block per overflow tile, warp q = sub-tile q (rows 32q .. 32q + 31)
+__global__ void __launch_bounds__(kTile) k_subtile_prep(TileParams P, int64_t ntiles) {
+  __shared__ ViewF sv[kMaxViewsTC];
+  const int b = blockIdx.x;
+  const int nsub = min(*P.sub_count, P.max_sub_tiles);
+  if (b >= nsub) return;
+  for (int j = threadIdx.x; j < P.nv; j += kTile) sv[j] = P.viewf[j];
+  __syncthreads();
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tile = P.sub_tiles[b];
+  const int64_t item = ntiles + 4 * (int64_t)b + q;
+  const int64_t jpt = tile * kTile + kSubRows * q + lane;
+  const bool valid = jpt < P.n;
+  float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint2 mw = make_uint2(0u, 0u);
+  if (valid) {
+    p = P.spts[jpt];
+    mw = *reinterpret_cast<const uint2*>(P.srec + jpt);
+  }
+  uint2* desc = P.tile_desc + item * P.nv;
+  int running = 0;
+  for (int v = 0; v < P.nv; ++v) {  // views in order: exclusive prefix of (even-padded) window sizes
+    const bool vis = (((v < 32 ? mw.x : mw.y) >> (v & 31)) & 1u) != 0u;
+    int x0 = INT_MAX, y0 = INT_MAX, x1 = -1, y1 = -1;
+    if (__any_sync(0xffffffffu, vis)) {
+      if (vis) {
+        const ProjF pr = project_f32(sv[v], p.x, p.y, p.z);
+        const TapF t = taps_f32(sv[v], pr.u, pr.v);
+        x0 = t.x0;
+        y0 = t.y0;
+        x1 = t.x0 + t.dx;
+        y1 = t.y0 + t.dy;
+      }
+      x0 = __reduce_min_sync(0xffffffffu, x0);
+      y0 = __reduce_min_sync(0xffffffffu, y0);
+      x1 = __reduce_max_sync(0xffffffffu, x1);
+      y1 = __reduce_max_sync(0xffffffffu, y1);
+    }
+    const int w = x1 >= 0 ? x1 - x0 + 1 : 0, h = x1 >= 0 ? y1 - y0 + 1 : 0;
+    if (lane == 0)
+      desc[v] = make_uint2((uint32_t)min(running, 65535) | ((uint32_t)(w ? x0 : 0) << 16) | ((uint32_t)(h ? y0 : 0) << 24),
+                           (uint32_t)w | ((uint32_t)h << 8));
+    running += (w * h + 1) & ~1;
+  }
+  if (lane == 0) P.tile_kt[item] = running;
 }
 
 // ---- sorted records -> caller's point order (gather: one 32-byte record read per point) -----------------
@@ -489,8 +691,11 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg) {
   L.inv = take(sizeof(int32_t) * (size_t)n);
   L.spts = take(sizeof(float4) * (size_t)ntiles * kTile);
   L.srec = take(sizeof(SRec) * (size_t)ntiles * kTile);
-  L.desc = take(sizeof(uint2) * (size_t)ntiles * nv);
-  L.kt = take(sizeof(int32_t) * (size_t)ntiles);
+  L.max_sub_tiles = (int32_t)(ntiles < 1024 + ntiles / 32 ? ntiles : 1024 + ntiles / 32);
+  const int64_t items = ntiles + 4 * (int64_t)L.max_sub_tiles;
+  L.desc = take(sizeof(uint2) * (size_t)items * nv);
+  L.kt = take(sizeof(int32_t) * (size_t)items);
+  L.sub = take(sizeof(int32_t) * ((size_t)L.max_sub_tiles + 1));
   L.viewf = take(sizeof(ViewF) * kMaxViewsTC);
   L.vbound = take(sizeof(float4) * kMaxViewsTC);
   L.ovf = take(sizeof(int32_t) * (size_t)(n + 1));
@@ -544,16 +749,34 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   if (int rc = check_launch("view_setup")) return rc;
   k_tile_prep<<<(unsigned)L.ntiles, kTile, 0, st>>>(Q);
   if (int rc = check_launch("tile_prep")) return rc;
+  // overflow tiles -> sub-tile work items (appended after the tiles)
+  cudaMemsetAsync(P.sub_count, 0, sizeof(int32_t), st);
+  k_find_overflow<<<grid_for(L.ntiles, 256), 256, 0, st>>>(P, L.ntiles, ws_kt_max());
+  if (int rc = check_launch("find_overflow")) return rc;
+  k_subtile_prep<<<(unsigned)L.max_sub_tiles, kTile, 0, st>>>(P, L.ntiles);
+  if (int rc = check_launch("subtile_prep")) return rc;
   stage_mark(2, st);
   if (debug) {
-    unsigned long long h[6];
+    unsigned long long h[11];
     cudaMemcpyAsync(h, pdbg + 16 * 1000, sizeof(h), cudaMemcpyDeviceToHost, st);
     std::vector<int32_t> kt((size_t)L.ntiles);
     cudaMemcpyAsync(kt.data(), P.tile_kt, sizeof(int32_t) * kt.size(), cudaMemcpyDeviceToHost, st);
+    int32_t nsub_tiles = 0;
+    cudaMemcpyAsync(&nsub_tiles, P.sub_count, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
+    {
+      const int nsi = 4 * (nsub_tiles < L.max_sub_tiles ? nsub_tiles : L.max_sub_tiles);
+      std::vector<int32_t> skt(nsi > 0 ? nsi : 1);
+      if (nsi) cudaMemcpy(skt.data(), P.tile_kt + L.ntiles, sizeof(int32_t) * nsi, cudaMemcpyDeviceToHost);
+      int over2 = 0;
+      for (int k = 0; k < nsi; ++k) over2 += ((skt[k] + 15) & ~15) > ws_kt_max();
+      fprintf(stderr, "[prep debug] overflow tiles %d -> %d sub-tiles, %d of them still over %d taps\n", nsub_tiles,
+              nsi, over2, ws_kt_max());
+    }
     double ksum = 0;
     int64_t over = 0, kmax = 0;
     for (int32_t k : kt) {
+      if (k < 0) { ++over; continue; }
       ksum += k;
       over += ((k + 15) & ~15) > ws_kt_max();
       kmax = k > kmax ? k : kmax;
@@ -582,10 +805,12 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
       for (int c = 0; c < 6; ++c) fprintf(stderr, " %s %.1f%%", nm[c], 100.0 * taps_in[c] / tt);
       fprintf(stderr, "\n");
     }
-    fprintf(stderr, "[prep debug] tile x view: FULL %.1f%%, MIXED %.1f%%, OFF %.1f%%; taps per tile mean %.1f "
-            "max %lld, overflow tiles %lld of %lld\n", 100.0 * h[3] / h[5], 100.0 * h[4] / h[5],
-            100.0 * (h[5] - h[3] - h[4]) / h[5], ksum / kt.size(), (long long)kmax, (long long)over,
-            (long long)kt.size());
+    fprintf(stderr, "[prep debug] tile x view: FULL %.1f%%, MIXED %.1f%%, EXACT %.1f%%, OFF %.1f%%; taps per tile "
+            "mean %.1f max %lld, overflow tiles %lld of %lld\n", 100.0 * h[3] / h[5], 100.0 * h[4] / h[5],
+            100.0 * h[6] / h[5], 100.0 * (h[5] - h[3] - h[4] - h[6]) / h[5], ksum / kt.size(), (long long)kmax,
+            (long long)over, (long long)kt.size());
+    fprintf(stderr, "[prep debug] MIXED samples ambiguous under the affine model: %.2f%%, mean eu %.4f px\n",
+            100.0 * h[8] / (double)(h[7] ? h[7] : 1), 1e-6 * h[9] / (double)(h[10] ? h[10] : 1));
   }
   const int rc = run_tile_ws(P, st);
   stage_mark(3, st);

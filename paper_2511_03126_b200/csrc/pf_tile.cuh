@@ -3,7 +3,7 @@
 //
 // Data flow (all per-point intermediates live in SORTED order, so every pass over them is
 // coalesced; the original order is touched once, by a gather in k_unsort):
-//   k_sort_scatter : spts[j] = {x, y, z, bits(i)}, inv[i] = j          (j = Morton-sorted slot)
+//   k_sort_scatter : spts[j] = {x, y, z, bits(i)}, inv[i] = j          (j = Hilbert-sorted slot)
 //   k_tile_prep    : srec[j].{mask, count, code}, per-tile tap windows
 //   k_tile_ws      : srec[j].prop, voxel + integrate partials
 //   k_unsort       : outputs[i] <- srec[inv[i]]  (one 32-byte sector read per point)
@@ -20,7 +20,7 @@ namespace tile {
 constexpr int kTile = 128;             // points per tile = tcgen05 M
 constexpr int kMaxViewsTC = 64;        // views supported by the tile path (2 bitset words)
 constexpr int kMaxKpadTC = 128;        // padded materials (MMA N of the S chunk pair)
-constexpr int kSortBits = 7;           // Morton grid 128^3 over the bbox
+constexpr int kSortBits = 7;           // Hilbert curve over a 128^3 grid over the bbox
 constexpr int kSortCells = 1 << kSortBits;
 constexpr int kSortBins = 1 << (3 * kSortBits);
 
@@ -81,6 +81,11 @@ struct TileParams {
   float4* vbound; // per-view constant error bounds over the bbox (k_view_setup)
   int32_t* ovf_list;
   int32_t* ovf_count;
+  // overflow tiles (more taps than one A buffer) are re-run as 4 sub-tiles of 32 rows: work items
+  // ntiles + 4 b + q (b < min(*sub_count, max_sub_tiles)) cover rows 32q.. of tile sub_tiles[b]
+  int32_t* sub_tiles;
+  int32_t* sub_count;
+  int32_t max_sub_tiles;
   unsigned long long* dbg;  // optional counters (PF_WS_DEBUG)
   uint32_t* trace;          // optional per-tile role timestamps (PF_WS_DEBUG + PF_WS_TRACE=<file>)
   double* partials;
@@ -88,7 +93,8 @@ struct TileParams {
 
 struct TileLayout {
   int64_t ntiles;
-  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, gbf, viewf, vbound, bytes;
+  int32_t max_sub_tiles;
+  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, gbf, viewf, vbound, bytes;
 };
 
 TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg);
@@ -100,6 +106,7 @@ int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf
 int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int k, int kpadg, int kpad,
                  uint16_t* Gbf, float* G32, cudaStream_t st);
 int ws_kt_max();
+constexpr int kSubRows = 32;  // rows of a sub-tile
 
 }  // namespace tile
 }  // namespace pf

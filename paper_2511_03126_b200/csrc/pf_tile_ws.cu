@@ -109,6 +109,26 @@ __device__ __forceinline__ int kt_at(const TileParams& P, int64_t tile, int64_t 
   return tile < ntiles ? P.tile_kt[tile] : 0;
 }
 
+// work item t -> (tile, first row, row count): tiles first, then the sub-tiles of overflow tiles
+__device__ __forceinline__ int64_t item_tile(const TileParams& P, int64_t t, int64_t ntiles, int& rlo, int& rhi) {
+  if (t < ntiles) {
+    rlo = 0;
+    rhi = kTile;
+    return t;
+  }
+  const int64_t b = (t - ntiles) >> 2;
+  rlo = kSubRows * (int)((t - ntiles) & 3);
+  rhi = rlo + kSubRows;
+  return P.sub_tiles[b];
+}
+// does work item t cover tile row `row` (and is the point real)?
+__device__ __forceinline__ bool item_row(const TileParams& P, int64_t t, int64_t ntiles, int row, int64_t& jpt) {
+  int rlo, rhi;
+  const int64_t tl = item_tile(P, t, ntiles, rlo, rhi);
+  jpt = tl * kTile + row;
+  return row >= rlo && row < rhi && jpt < P.n;
+}
+
 __device__ __forceinline__ uint16_t f2bf16(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
@@ -130,6 +150,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nd = P.d >> 6, ns = P.kpadg >> 6, nch = nd + ns;
   const int64_t ntiles = (P.n + kTile - 1) / kTile;
+  const int64_t nitems = ntiles + 4 * (int64_t)min(*P.sub_count, P.max_sub_tiles);
   // PROF (PF_WS_DEBUG=1): per-role mbarrier wait / issue cycles, printed by the host
   long long wait_cyc[15] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long issue_cyc = 0;
@@ -207,13 +228,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     uint32_t phase = 0;
     uint32_t published = 0, pub_tile = 0, pub_group = 0;  // PROF trace bookkeeping (warp 0)
     uint32_t t_local = 0;
-    int kt_nx = kt_at(P, blockIdx.x, ntiles);
-    uint2 ds_nx = (tid < P.nv && blockIdx.x < ntiles) ? P.tile_desc[blockIdx.x * P.nv + tid] : make_uint2(0u, 0u);
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int kt_nx = kt_at(P, blockIdx.x, nitems);
+    uint2 ds_nx = (tid < P.nv && blockIdx.x < nitems) ? P.tile_desc[blockIdx.x * P.nv + tid] : make_uint2(0u, 0u);
+    for (int64_t tile = blockIdx.x; tile < nitems; tile += gridDim.x) {
       const int kt = kt_nx;
       const uint2 ds_cur = ds_nx;
-      kt_nx = kt_at(P, tile + gridDim.x, ntiles);
-      if (tid < P.nv && tile + gridDim.x < ntiles) ds_nx = P.tile_desc[(tile + gridDim.x) * P.nv + tid];
+      kt_nx = kt_at(P, tile + gridDim.x, nitems);
+      if (tid < P.nv && tile + gridDim.x < nitems) ds_nx = P.tile_desc[(tile + gridDim.x) * P.nv + tid];
       bool ok;
       const int ktp = ktp_of(kt, ok);
       if (!ok) continue;
@@ -286,10 +307,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     uint32_t dcount = 0;  // chunk pairs issued so far (selects the TMEM accumulator slot)
     uint32_t t_local = 0;
     const uint32_t idesc = tc::idesc_bf16_f32(128, kDCols, false, true);
-    int kt_nx = kt_at(P, blockIdx.x, ntiles);
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int kt_nx = kt_at(P, blockIdx.x, nitems);
+    for (int64_t tile = blockIdx.x; tile < nitems; tile += gridDim.x) {
       const int kt = kt_nx;
-      kt_nx = kt_at(P, tile + gridDim.x, ntiles);
+      kt_nx = kt_at(P, tile + gridDim.x, nitems);
       bool ok;
       const int ktp = ktp_of(kt, ok);
       if (!ok) continue;
@@ -352,14 +373,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     uint32_t t_local = 0;
     static_assert(kMaxViewsTC <= kBuildThreads, "one window per builder thread");
     auto fetch = [&](int64_t t, int& kt, uint2& ds, float4& pp, uint2& mm) {
-      kt = kt_at(P, t, ntiles);
+      kt = kt_at(P, t, nitems);
       pp = make_float4(0.f, 0.f, 0.f, 0.f);
-      mm = make_uint2(0u, 0u);  // rows past the end: empty mask
-      if (t >= ntiles) return;
+      mm = make_uint2(0u, 0u);  // rows outside the work item: empty mask
+      if (t >= nitems) return;
       if (bt < P.nv) ds = P.tile_desc[t * P.nv + bt];
-      if (t * kTile + row < P.n) {
-        pp = P.spts[t * kTile + row];
-        mm = *reinterpret_cast<const uint2*>(P.srec + t * kTile + row);
+      int64_t jr;
+      if (item_row(P, t, ntiles, row, jr)) {
+        pp = P.spts[jr];
+        mm = *reinterpret_cast<const uint2*>(P.srec + jr);
       }
     };
     int kt_nx = 0;
@@ -367,7 +389,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     float4 p_nx;
     fetch(blockIdx.x, kt_nx, ds_nx, p_nx, mw_nx);
     const float wf1 = (float)(S.sv[0].Wf - 1), hf1 = (float)(S.sv[0].Hf - 1);  // uniform maps (tile_path_ok)
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int64_t tile = blockIdx.x; tile < nitems; tile += gridDim.x) {
       const int kt = kt_nx;
       const uint2 ds_cur = ds_nx;
       const float4 p = p_nx;
@@ -382,7 +404,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       // tile box over the valid rows: expansion point and width (this warp's rows, then all four
       // lane groups through shared memory)
       float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-      if (tile * kTile + row < P.n) {
+      int64_t jrow;
+      if (item_row(P, tile, ntiles, row, jrow)) {
         lo[0] = hi[0] = p.x;
         lo[1] = hi[1] = p.y;
         lo[2] = hi[2] = p.z;
@@ -575,28 +598,31 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     float pm_sum = 0.f, pmx = 0.f, pmy = 0.f, pmz = 0.f, featured_n = 0.f, pairs = 0.f;
     const bool outs = P.sims || P.weights;
     const bool p_wide = P.p > 2;
-    int kt_nx = kt_at(P, blockIdx.x, ntiles);
+    int kt_nx = kt_at(P, blockIdx.x, nitems);
     uint4 rec_nx = make_uint4(0u, 0u, 0u, 0u);
     float4 p_nx = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (blockIdx.x * kTile + row < P.n) {
-      rec_nx = *reinterpret_cast<const uint4*>(P.srec + blockIdx.x * kTile + row);
-      p_nx = P.spts[blockIdx.x * kTile + row];
+    int64_t j_nx = 0;
+    bool v_nx = blockIdx.x < nitems && item_row(P, blockIdx.x, ntiles, row, j_nx);
+    if (v_nx) {
+      rec_nx = *reinterpret_cast<const uint4*>(P.srec + j_nx);
+      p_nx = P.spts[j_nx];
     }
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int64_t tile = blockIdx.x; tile < nitems; tile += gridDim.x) {
       const int kt = kt_nx;
       const uint4 rec = rec_nx;
       const float4 pcur = p_nx;
-      kt_nx = kt_at(P, tile + gridDim.x, ntiles);
-      if ((tile + gridDim.x) * kTile + row < P.n) {
-        rec_nx = *reinterpret_cast<const uint4*>(P.srec + (tile + gridDim.x) * kTile + row);
-        p_nx = P.spts[(tile + gridDim.x) * kTile + row];
+      const int64_t jpt = j_nx;
+      const bool valid = v_nx;
+      kt_nx = kt_at(P, tile + gridDim.x, nitems);
+      v_nx = tile + gridDim.x < nitems && item_row(P, tile + gridDim.x, ntiles, row, j_nx);
+      if (v_nx) {
+        rec_nx = *reinterpret_cast<const uint4*>(P.srec + j_nx);
+        p_nx = P.spts[j_nx];
       }
       bool ok;
       ktp_of(kt, ok);
-      const int64_t jpt = tile * kTile + row;
-      const bool valid = jpt < P.n;
-      if (!ok) {
-        if (valid && half == 0) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(pcur.w);
+      if (!ok) {  // kt == -1: re-run as sub-tiles; otherwise the points go to the SIMT kernel
+        if (kt != -1 && valid && half == 0) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(pcur.w);
         continue;
       }
       const int count = (int)rec.z;
@@ -804,7 +830,7 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
   const size_t smem = ws_smem_bytes();
   cudaFuncSetAttribute(k_tile_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_tile_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t ntiles = (P.n + kTile - 1) / kTile;
+  const int64_t ntiles = (P.n + kTile - 1) / kTile;  // (+ sub-tiles, known on the device only)
   int grid = (int)(ntiles < sms ? ntiles : sms);
   if (const char* g = getenv("PF_WS_GRID")) grid = (int)(ntiles < atoi(g) ? ntiles : atoi(g));  // debug knob
   // exp(s / T) with |s| <= 1 (+ bf16 rounding of G) stays below 2^120 unless T < ~0.012
