@@ -493,9 +493,11 @@ int pf_fuse_prepare(const pf_fuse_args_t* a, void* stream) {
   if (tile_path_ok(a)) {
     kpadg = tile::kMaxKpadTC;  // S operand is always one 128-column chunk pair
     unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
-    Gbf = reinterpret_cast<uint16_t*>(ws + tile::tile_layout(a->n, a->nviews, cells, kpadg).gbf);
+    const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg);
+    Gbf = reinterpret_cast<uint16_t*>(ws + L.gbf);
     // bf16 maps: G on the tensor cores (bf16 text), fp32 copy for the SIMT overflow tiles
-    const int rc = tile::run_gproj_tc(a->fmap, cells, a->d, a->text, a->k, kpadg, kpad, Gbf, G, st);
+    const int rc = tile::run_gproj_tc(a->fmap, cells, a->d, a->text, a->k, kpadg, kpad, Gbf, G,
+                                      reinterpret_cast<uint16_t*>(ws + L.textbf), st);
     if (rc >= 0) return rc;
   }
   dim3 grid((unsigned)((cells + TP_CELLS - 1) / TP_CELLS), (unsigned)(kpad / TP_MATS));

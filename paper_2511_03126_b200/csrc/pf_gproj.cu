@@ -2,7 +2,8 @@
 // similarity-by-associativity, see pf_tile.cu): one CTA per 128 feature cells, K = D streamed in
 // 64-channel chunks through a 2-stage cp.async ring, tcgen05.mma (M=128, N=kpadg, K=16) into TMEM,
 // epilogue writes G in bf16 (cells x kpadg, the tile kernel's S operand) and fp32 (cells x kpad,
-// the SIMT overflow path). Text rows are rounded to bf16 on the fly (bf16-feature mode bar 1e-2).
+// the SIMT overflow path). The text rows are rounded to bf16 once (k_text_bf16; bf16-feature mode
+// bar 1e-2) and streamed with cp.async like the map rows; the MMAs are issued warp-uniformly.
 #include <cuda_bf16.h>
 
 #include "pf_common.cuh"
@@ -15,8 +16,16 @@ namespace {
 
 constexpr int kGM = 128;  // cells per CTA
 
-__global__ void __launch_bounds__(128, 1) k_gproj_tc(const uint16_t* __restrict__ fmap, int64_t cells, int d,
-                                                     const float* __restrict__ text, int k, int kpadg,
+__global__ void k_text_bf16(const float* __restrict__ text, int k, int kpadg, int d, uint16_t* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)kpadg * d;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = e / d;
+    out[e] = __bfloat16_as_ushort(__float2bfloat16_rn(n < k ? text[e] : 0.f));
+  }
+}
+
+__global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ fmap, int64_t cells, int d,
+                                                     const uint16_t* __restrict__ textbf, int k, int kpadg,
                                                      int kpad, uint16_t* __restrict__ Gbf,
                                                      float* __restrict__ G32) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -41,22 +50,11 @@ __global__ void __launch_bounds__(128, 1) k_gproj_tc(const uint16_t* __restrict_
       const uint32_t off = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + (((q ^ (r & 7)) & 7) << 4));
       tc::cp_async16(tc::smem_u32(sa + off), fmap + cell * d + ch * 64 + q * 8);
     }
-    // B: material n, channels ch*64 .. +64 rounded to bf16 (K-major SW128)
+    // B: material n, channels ch*64 .. +64 (bf16 text, K-major SW128)
     for (int e = tid; e < kpadg * 8; e += 128) {
       const int n = e >> 3, q = e & 7;
-      uint32_t w[4] = {0u, 0u, 0u, 0u};
-      if (n < k) {
-        const float4 x0 = *reinterpret_cast<const float4*>(text + (int64_t)n * d + ch * 64 + q * 8);
-        const float4 x1 = *reinterpret_cast<const float4*>(text + (int64_t)n * d + ch * 64 + q * 8 + 4);
-        const __nv_bfloat162 p0 = __floats2bfloat162_rn(x0.x, x0.y), p1 = __floats2bfloat162_rn(x0.z, x0.w);
-        const __nv_bfloat162 p2 = __floats2bfloat162_rn(x1.x, x1.y), p3 = __floats2bfloat162_rn(x1.z, x1.w);
-        w[0] = *reinterpret_cast<const uint32_t*>(&p0);
-        w[1] = *reinterpret_cast<const uint32_t*>(&p1);
-        w[2] = *reinterpret_cast<const uint32_t*>(&p2);
-        w[3] = *reinterpret_cast<const uint32_t*>(&p3);
-      }
       const uint32_t off = (uint32_t)((n >> 3) * 1024 + (n & 7) * 128 + (((q ^ (n & 7)) & 7) << 4));
-      *reinterpret_cast<uint4*>(sb + off) = make_uint4(w[0], w[1], w[2], w[3]);
+      tc::cp_async16(tc::smem_u32(sb + off), textbf + (int64_t)n * d + ch * 64 + q * 8);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -80,14 +78,15 @@ __global__ void __launch_bounds__(128, 1) k_gproj_tc(const uint16_t* __restrict_
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    if (tid == 0) {
+    if (warp == 0) {  // warp-uniform issue, elected lane (scripts/umma_rate.py)
       const uint32_t a0 = tc::smem_u32(smem + st * stage_bytes), b0 = a0 + 16384;
+#pragma unroll
       for (int s = 0; s < 4; ++s) {
         const uint64_t ad = tc::smem_desc_sw128(a0 + s * 32, 16, 1024);
         const uint64_t bd = tc::smem_desc_sw128(b0 + s * 32, 16, 1024);
-        tc::mma_bf16(tbase, ad, bd, idesc, (ch | s) ? 1u : 0u);
+        tc::mma_bf16_ss_elect(tbase, ad, bd, idesc, (ch | s) ? 1u : 0u);
       }
-      tc::mma_commit(&mbar);
+      tc::mma_commit_elect(&mbar);
     }
     // stage st^1 was read by the MMAs of chunk ch-1, which completed (waited below last iteration)
     if (ch + 1 < nchunk) load(ch + 1, st ^ 1);
@@ -117,12 +116,14 @@ __global__ void __launch_bounds__(128, 1) k_gproj_tc(const uint16_t* __restrict_
 }  // namespace
 
 int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int k, int kpadg, int kpad,
-                 uint16_t* Gbf, float* G32, cudaStream_t st) {
+                 uint16_t* Gbf, float* G32, uint16_t* textbf, cudaStream_t st) {
   if (d % 64 != 0 || kpadg % 16 != 0 || kpadg > 256) return -1;
+  k_text_bf16<<<grid_for((int64_t)kpadg * d, 256), 256, 0, st>>>(text, k, kpadg, d, textbf);
+  if (int rc = check_launch("text_bf16")) return rc;
   const size_t smem = 2 * (16384 + (size_t)kpadg * 128) + 1024;
   cudaFuncSetAttribute(k_gproj_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const unsigned grid = (unsigned)((cells + kGM - 1) / kGM);
-  k_gproj_tc<<<grid, 128, smem, st>>>(reinterpret_cast<const uint16_t*>(fmap), cells, d, text, k, kpadg, kpad,
+  k_gproj_tc<<<grid, 128, smem, st>>>(reinterpret_cast<const uint16_t*>(fmap), cells, d, textbf, k, kpadg, kpad,
                                       Gbf, G32);
   return check_launch("gproj_tc");
 }

@@ -700,6 +700,7 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg) {
   L.vbound = take(sizeof(float4) * kMaxViewsTC);
   L.ovf = take(sizeof(int32_t) * (size_t)(n + 1));
   L.gbf = take(sizeof(uint16_t) * (size_t)cells * kpadg);
+  L.textbf = take(sizeof(uint16_t) * (size_t)kpadg * 1024);  // text rows in bf16 (D <= 1024)
   L.bytes = off;
   return L;
 }

@@ -94,7 +94,7 @@ struct TileParams {
 struct TileLayout {
   int64_t ntiles;
   int32_t max_sub_tiles;
-  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, gbf, viewf, vbound, bytes;
+  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, gbf, textbf, viewf, vbound, bytes;
 };
 
 TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg);
@@ -104,7 +104,7 @@ int run_unsort(const TileParams& P, cudaStream_t st);
 int run_tile_ws(const TileParams& P, cudaStream_t st);
 int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf, cudaStream_t st);
 int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int k, int kpadg, int kpad,
-                 uint16_t* Gbf, float* G32, cudaStream_t st);
+                 uint16_t* Gbf, float* G32, uint16_t* textbf, cudaStream_t st);
 int ws_kt_max();
 constexpr int kSubRows = 32;  // rows of a sub-tile
 
