@@ -139,6 +139,22 @@ int pf_voxel_accumulate(const int32_t* codes, const float* rho, int64_t n, int32
  * device double[2] = {mass_kg, occupied_voxels}; lo_hi as above (edge recomputed identically). */
 int pf_voxel_mass(const float* grid, int32_t g, const double* lo_hi, double* out, void* stream);
 
+/* integrate.characteristic_length (integrate.py:72-95), device part: for every point of (n,3) f32,
+ * the squared distance to its (k+1)-th nearest point, self included (cKDTree.query(p, k+1)[:, k]),
+ * exact, in fp64; *dk2_sum (device f64) = their sum. dk_sorted (nullable, device f32 (n)) receives
+ * the distances in the library's internal bucket order. Workspace: pf_knn_workspace_bytes(n). */
+uint64_t pf_knn_workspace_bytes(int64_t n);
+int pf_knn_kth_distance(const float* points, int64_t n, int32_t k, double* dk2_sum, float* dk_sorted,
+                        void* workspace, void* stream);
+
+/* integrate_mass partials (integrate.py:124-155) from a probability matrix: weights (n,k) f64
+ * row-major, positions (n,3) f32, normals (n,3) f32 or NULL, mid_theta / theta (k,) f64.
+ * out (k+4) f64 (caller-zeroed): weight_totals[k], sum pm, sum pm * centre (3), with
+ * pm_i = w_i . mid_theta and centre_i = p_i - (w_i . theta / 2) n_i (lam b^2 applied by the host). */
+int pf_integrate_partials(const double* weights, int64_t n, int32_t k, const float* positions,
+                          const float* normals, const double* mid_theta, const double* theta,
+                          double* out, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * The fused path: project -> depth test -> bilinear gather -> cross-view mean -> L2 normalise ->
  * cosine similarity vs K text embeddings -> temperature softmax -> property regression ->

@@ -256,12 +256,16 @@ def voxel_mass(codes, rho, edge):
 
 
 # ---- integrate_mass partials (integrate.py:98-167) ---------------------------------------------------
-def integrate_partials(weights, positions, mid_density, theta):
+def integrate_partials(weights, positions, mid_density, theta, normals=None):
     """The data-parallel part of integrate_mass: weight_totals (integrate.py:133), point mass
-    pm_i = w_i @ (mid * theta) (integrate.py:146, without lam*b^2), sum pm, sum pm * position."""
+    pm_i = w_i @ (mid * theta) (integrate.py:146, without lam*b^2), sum pm, sum pm * centre with
+    centre = position - (w_i @ theta / 2) * normal when normals are given (integrate.py:149-152)."""
     w = np.asarray(weights, dtype=np.float64)
     pm = w @ (np.asarray(mid_density, np.float64) * np.asarray(theta, np.float64))
     pos = np.asarray(positions, dtype=np.float64)
+    if normals is not None:
+        mean_theta = w @ np.asarray(theta, np.float64)
+        pos = pos - (mean_theta[:, None] / 2.0) * np.asarray(normals, np.float64)
     return {
         "weight_totals": w.sum(axis=0),
         "pm_sum": float(pm.sum()),

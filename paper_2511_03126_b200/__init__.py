@@ -9,7 +9,8 @@ Reference-named entry points:
     project_points, default_epsilon, visibility_mask                    (geometry.py:46-103)
     aggregate_geometric_features -> SemanticPointCloud                  (fusion.py:24-93)
     material_similarity, softmax_weights, kernel_regress, regress_with_weights (grounding.py:158-202)
-    adaptive_voxel_side, IntegrationConfig, ObjectEstimate              (integrate.py:22-69)
+    adaptive_voxel_side, characteristic_length, integrate_mass,
+    IntegrationConfig, ObjectEstimate                                   (integrate.py:22-167)
 Fused device path:
     ViewSet, QueryTables, FuseBuffers, fuse_and_query -> FusedResult
 """
@@ -31,7 +32,9 @@ from .fused import FuseBuffers, FusedResult, QueryTables, fuse_and_query, fuse_p
 from .fusion import aggregate_geometric_features
 from .geometry import default_epsilon, project_points, visibility_mask
 from .grounding import kernel_regress, material_similarity, regress_with_weights, softmax_weights
-from .integrate import adaptive_voxel_side, estimate_from_partials, voxel_mass
+from .integrate import (adaptive_voxel_side, characteristic_length, estimate_from_partials, integrate_mass,
+                        voxel_mass)
+from .stream import FusePipeline, HostObject
 from .types import (
     CameraPose,
     IntegrationConfig,
@@ -50,7 +53,8 @@ __all__ = [
     "kernels", "ViewSet", "QueryTables", "FuseBuffers", "FusedResult", "fuse_and_query",
     "aggregate_geometric_features", "default_epsilon", "project_points", "visibility_mask",
     "kernel_regress", "material_similarity", "regress_with_weights", "softmax_weights",
-    "adaptive_voxel_side", "estimate_from_partials", "voxel_mass",
+    "adaptive_voxel_side", "characteristic_length", "integrate_mass", "estimate_from_partials", "voxel_mass",
+    "FusePipeline", "HostObject",
     "CameraPose", "IntegrationConfig", "Intrinsics", "MaterialDictionary", "MaterialEntry",
     "ObjectEstimate", "PropertyField", "SemanticPointCloud", "ViewRecord",
     "PropfieldError", "BundleLoadError", "BundleStructureError", "BundleValidationError",

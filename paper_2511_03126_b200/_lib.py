@@ -114,6 +114,9 @@ SIGNATURES = {
     "pf_fuse_prepare": ([C.POINTER(FuseArgs), _P], C.c_int),
     "pf_fuse_query": ([C.POINTER(FuseArgs), _P], C.c_int),
     "pf_stage_timing": ([_I32], C.c_int),
+    "pf_knn_workspace_bytes": ([_I64], C.c_uint64),
+    "pf_knn_kth_distance": ([_P, _I64, _I32, _P, _P, _P, _P], C.c_int),
+    "pf_integrate_partials": ([_P, _I64, _I32, _P, _P, _P, _P, _P, _P], C.c_int),
     "pf_bench_umma": ([_I32, _I32, _I32, _I32, _P, _P], C.c_int),
     "pf_bench_gather": ([_P, _I32, _I32, _I32, _P, _P], C.c_int),
     "pf_stage_times": ([_P, _I32], C.c_int),

@@ -1,0 +1,267 @@
+// integrate.characteristic_length (integrate.py:72-95) on the device: the distance d_k from every
+// point to its (k+1)-th nearest point, self included (cKDTree.query(p, k+1)[:, k]), and
+// L = sqrt(pi / k * sum d_k^2).
+//
+// Uniform grid of cell c (1.25 x the expected k-NN spacing of a surface sample, from the bbox area),
+// cells hashed into 2^22 buckets; points counting-sorted by bucket (cell id kept per point). A
+// point's search starts with its 3 x 3 x 3 cell block and grows by shells until the (k+1)-th
+// smallest squared distance found is inside the searched block (every unsearched point is then
+// farther), so the result is exact. Distances in fp64 from the f32 coordinates, as the reference
+// computes them on float64-upcast positions.
+#include <cmath>
+
+#include "pf_common.cuh"
+#include "pf_tile.cuh"
+
+namespace pf {
+namespace {
+
+constexpr int kHashLog = 22;
+constexpr uint32_t kHashBins = 1u << kHashLog;
+constexpr int kMaxK = 31;       // k + 1 <= 32 neighbours kept per point
+constexpr int kCellBits = 11;   // cell coordinates < 2048 per axis
+
+__device__ __forceinline__ uint32_t cell_hash(int cx, int cy, int cz) {
+  return ((uint32_t)cx * 73856093u ^ (uint32_t)cy * 19349663u ^ (uint32_t)cz * 83492791u) & (kHashBins - 1);
+}
+
+struct Grid {
+  float lo[3];
+  float c;
+  int dims[3];
+};
+
+__global__ void k_knn_grid(const double* __restrict__ lo_hi, int64_t n, int k, Grid* g) {
+  // expected k-NN spacing of N points on a surface of area A: pi r^2 N / A = k + 1 -> r; A from the bbox
+  const double ex = lo_hi[3] - lo_hi[0], ey = lo_hi[4] - lo_hi[1], ez = lo_hi[5] - lo_hi[2];
+  const double area = fmax(2.0 * (ex * ey + ey * ez + ez * ex), 1e-30);
+  double c = 1.25 * sqrt((double)(k + 1) * area / (3.141592653589793 * (double)n));
+  const double ext = fmax(fmax(ex, ey), ez);
+  c = fmax(c, ext / 2000.0);  // cell ids fit 11 bits per axis
+  if (!(c > 0.0)) c = 1.0;
+  g->c = (float)c;
+  g->lo[0] = (float)lo_hi[0];
+  g->lo[1] = (float)lo_hi[1];
+  g->lo[2] = (float)lo_hi[2];
+  g->dims[0] = (int)(ex / c) + 1;
+  g->dims[1] = (int)(ey / c) + 1;
+  g->dims[2] = (int)(ez / c) + 1;
+}
+
+__device__ __forceinline__ void cell_of(const Grid& g, float x, float y, float z, int& cx, int& cy, int& cz) {
+  const float ic = 1.f / g.c;
+  cx = min(max((int)((x - g.lo[0]) * ic), 0), g.dims[0] - 1);
+  cy = min(max((int)((y - g.lo[1]) * ic), 0), g.dims[1] - 1);
+  cz = min(max((int)((z - g.lo[2]) * ic), 0), g.dims[2] - 1);
+}
+
+__global__ void k_knn_keys(const float* __restrict__ p, int64_t n, const Grid* __restrict__ gp,
+                           uint32_t* __restrict__ keys, uint32_t* __restrict__ hist) {
+  const Grid g = *gp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int cx, cy, cz;
+    cell_of(g, p[3 * i], p[3 * i + 1], p[3 * i + 2], cx, cy, cz);
+    const uint32_t key = cell_hash(cx, cy, cz);
+    keys[i] = key;
+    atomicAdd(hist + key, 1u);
+  }
+}
+
+__global__ void k_knn_scatter(const float* __restrict__ p, int64_t n, const Grid* __restrict__ gp,
+                              const uint32_t* __restrict__ keys, uint32_t* __restrict__ cursor,
+                              float4* __restrict__ kp) {
+  const Grid g = *gp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = p[3 * i], y = p[3 * i + 1], z = p[3 * i + 2];
+    int cx, cy, cz;
+    cell_of(g, x, y, z, cx, cy, cz);
+    const uint32_t id = (uint32_t)cx | ((uint32_t)cy << kCellBits) | ((uint32_t)cz << (2 * kCellBits));
+    const uint32_t pos = atomicAdd(cursor + keys[i], 1u);
+    kp[pos] = make_float4(x, y, z, __uint_as_float(id));
+  }
+}
+
+// one thread per point in bucket order (neighbouring threads query neighbouring cells). KP1 > 0:
+// compile-time list length k + 1 (registers); KP1 == 0: runtime k (local memory)
+template <int KP1>
+__global__ void __launch_bounds__(128) k_knn_query(const float4* __restrict__ kp, int64_t n, const Grid* __restrict__ gp,
+                                                   const uint32_t* __restrict__ ends, int k_rt, double* __restrict__ sum,
+                                                   float* __restrict__ dk_sorted) {
+  constexpr int kCap = KP1 > 0 ? KP1 : kMaxK + 1;
+  const int k = KP1 > 0 ? KP1 - 1 : k_rt;
+  const Grid g = *gp;
+  const double c = (double)g.c;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 q = kp[i];
+    const uint32_t id = __float_as_uint(q.w);
+    const int cx = (int)(id & ((1u << kCellBits) - 1)), cy = (int)((id >> kCellBits) & ((1u << kCellBits) - 1)),
+              cz = (int)(id >> (2 * kCellBits));
+    const double qx = q.x, qy = q.y, qz = q.z;
+    double best[kCap];
+#pragma unroll
+    for (int b = 0; b < kCap; ++b) best[b] = INFINITY;
+    // distance from q to the faces of its own cell (the searched block of shell s reaches s*c beyond)
+    const double fx = fmin(qx - ((double)g.lo[0] + cx * c), (double)g.lo[0] + (cx + 1) * c - qx);
+    const double fy = fmin(qy - ((double)g.lo[1] + cy * c), (double)g.lo[1] + (cy + 1) * c - qy);
+    const double fz = fmin(qz - ((double)g.lo[2] + cz * c), (double)g.lo[2] + (cz + 1) * c - qz);
+    const double face = fmax(fmin(fmin(fx, fy), fz), 0.0);
+    const int maxs = max(max(g.dims[0], g.dims[1]), g.dims[2]);
+    for (int s = 1;; ++s) {
+      for (int dz = -s; dz <= s; ++dz)
+        for (int dy = -s; dy <= s; ++dy)
+          for (int dx = -s; dx <= s; ++dx) {
+            if (max(max(abs(dx), abs(dy)), abs(dz)) != s && s > 1) continue;  // shell only
+            const int x = cx + dx, y = cy + dy, z = cz + dz;
+            if (x < 0 || y < 0 || z < 0 || x >= g.dims[0] || y >= g.dims[1] || z >= g.dims[2]) continue;
+            const uint32_t want = (uint32_t)x | ((uint32_t)y << kCellBits) | ((uint32_t)z << (2 * kCellBits));
+            const uint32_t b = cell_hash(x, y, z);
+            const uint32_t e0 = b ? __ldg(ends + b - 1) : 0u, e1 = __ldg(ends + b);
+            for (uint32_t j = e0; j < e1; ++j) {
+              const float4 r = __ldg(kp + j);
+              if (__float_as_uint(r.w) != want) continue;
+              const double ddx = (double)r.x - qx, ddy = (double)r.y - qy, ddz = (double)r.z - qz;
+              double d2 = fma(ddz, ddz, fma(ddy, ddy, ddx * ddx));
+              if (d2 >= best[k]) continue;
+              // insert into the ascending list best[0..k]
+#pragma unroll
+              for (int t = 0; t < kCap; ++t) {
+                if (KP1 == 0 && t > k) break;
+                const double lo = fmin(best[t], d2);
+                d2 = fmax(best[t], d2);
+                best[t] = lo;
+              }
+            }
+          }
+      // every unsearched point is at least face + (s - 1) * c + c away... block reaches face + s*c
+      const double reach = face + (double)s * c;
+      if (best[k] <= reach * reach || s >= maxs) break;
+    }
+    const double dk = sqrt(best[k]);
+    if (dk_sorted) dk_sorted[i] = (float)dk;
+    acc += best[k];
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) atomicAdd(sum, acc);
+}
+
+}  // namespace
+}  // namespace pf
+
+extern "C" {
+
+uint64_t pf_knn_workspace_bytes(int64_t n) {
+  auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  return al(sizeof(uint32_t) * (uint64_t)n) + al(sizeof(uint32_t) * pf::kHashBins) + al(sizeof(uint32_t) * 1024) +
+         al(sizeof(float4) * (uint64_t)n) + al(sizeof(pf::Grid)) + al(6 * sizeof(double));
+}
+
+int pf_knn_kth_distance(const float* points, int64_t n, int32_t k, double* dk2_sum, float* dk_sorted,
+                        void* workspace, void* stream) {
+  using namespace pf;
+  if (n < 1 || k < 0 || k > kMaxK || k >= n) return set_error(PF_ERR_VALUE, "knn: need 0 <= k < n and k <= %d", kMaxK);
+  if (!workspace || !dk2_sum) return set_error(PF_ERR_VALUE, "knn: workspace and output required");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(ws);
+  ws += al(sizeof(uint32_t) * (uint64_t)n);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws);
+  ws += al(sizeof(uint32_t) * kHashBins);
+  uint32_t* totals = reinterpret_cast<uint32_t*>(ws);
+  ws += al(sizeof(uint32_t) * 1024);
+  float4* kp = reinterpret_cast<float4*>(ws);
+  ws += al(sizeof(float4) * (uint64_t)n);
+  Grid* g = reinterpret_cast<Grid*>(ws);
+  ws += al(sizeof(Grid));
+  double* lo_hi = reinterpret_cast<double*>(ws);
+  if (int rc = pf_bbox(points, n, lo_hi, stream)) return rc;
+  k_knn_grid<<<1, 1, 0, st>>>(lo_hi, n, k, g);
+  if (int rc = check_launch("knn_grid")) return rc;
+  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kHashBins, st);
+  cudaMemsetAsync(dk2_sum, 0, sizeof(double), st);
+  k_knn_keys<<<grid_for(n, 256), 256, 0, st>>>(points, n, g, keys, hist);
+  if (int rc = check_launch("knn_keys")) return rc;
+  if (int rc = tile::run_bucket_scan(hist, totals, kHashBins, st)) return rc;
+  k_knn_scatter<<<grid_for(n, 256), 256, 0, st>>>(points, n, g, keys, hist, kp);
+  if (int rc = check_launch("knn_scatter")) return rc;
+  // after the scatter hist[b] = end of bucket b
+  if (k == 8)  // AREA_KNN (integrate.py:19)
+    k_knn_query<9><<<grid_for(n, 128, 148 * 32), 128, 0, st>>>(kp, n, g, hist, k, dk2_sum, dk_sorted);
+  else
+    k_knn_query<0><<<grid_for(n, 128, 148 * 32), 128, 0, st>>>(kp, n, g, hist, k, dk2_sum, dk_sorted);
+  return check_launch("knn_query");
+}
+
+}  // extern "C"
+
+// ---- integrate_mass partials from a probability matrix (integrate.py:124-155) -------------------------
+namespace pf {
+namespace {
+constexpr int kIntWarps = 8;
+__global__ void __launch_bounds__(32 * kIntWarps) k_integrate_partials(const double* __restrict__ w, int64_t n, int k,
+                                                                         const float* __restrict__ pos,
+                                                                         const float* __restrict__ nrm,
+                                                                         const double* __restrict__ mt,
+                                                                         const double* __restrict__ th,
+                                                                         double* __restrict__ out) {
+  __shared__ double red[kIntWarps][4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double wt[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // weight totals of columns lane + 32 j
+  double pm_s = 0.0, px = 0.0, py = 0.0, pz = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kIntWarps + wid; i < n; i += (int64_t)gridDim.x * kIntWarps) {
+    const double* row = w + i * k;
+    double pm = 0.0, mth = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int kk = lane + 32 * j;
+      if (kk < k) {
+        const double v = row[kk];
+        wt[j] += v;
+        pm = fma(v, mt[kk], pm);
+        mth = fma(v, th[kk], mth);
+      }
+    }
+    pm = warp_sum(pm);
+    mth = warp_sum(mth);
+    double cx = pos[3 * i], cy = pos[3 * i + 1], cz = pos[3 * i + 2];
+    if (nrm) {
+      const double h = mth / 2.0;
+      cx -= h * nrm[3 * i];
+      cy -= h * nrm[3 * i + 1];
+      cz -= h * nrm[3 * i + 2];
+    }
+    pm_s += pm;
+    px += pm * cx;
+    py += pm * cy;
+    pz += pm * cz;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (lane + 32 * j < k && wt[j] != 0.0) atomicAdd(out + lane + 32 * j, wt[j]);
+  if (lane == 0) {
+    red[wid][0] = pm_s;
+    red[wid][1] = px;
+    red[wid][2] = py;
+    red[wid][3] = pz;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double s = 0.0;
+    for (int q = 0; q < kIntWarps; ++q) s += red[q][threadIdx.x];
+    if (s != 0.0) atomicAdd(out + k + threadIdx.x, s);
+  }
+}
+}  // namespace
+}  // namespace pf
+
+extern "C" int pf_integrate_partials(const double* weights, int64_t n, int32_t k, const float* positions,
+                                     const float* normals, const double* mid_theta, const double* theta,
+                                     double* out, void* stream) {
+  using namespace pf;
+  if (n < 0 || k < 1 || k > 256) return set_error(PF_ERR_VALUE, "integrate_partials: need 1 <= k <= 256");
+  if (n == 0) return PF_OK;
+  k_integrate_partials<<<grid_for(n, kIntWarps, 148 * 8), 32 * kIntWarps, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      weights, n, k, positions, normals, mid_theta, theta, out);
+  return check_launch("integrate_partials");
+}

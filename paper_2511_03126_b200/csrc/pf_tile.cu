@@ -710,6 +710,18 @@ int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf
   return check_launch("g_bf16");
 }
 
+// exclusive scan of `nbins` (multiple of 4096, <= 4M) bucket counters in place (k_scan_*)
+int run_bucket_scan(uint32_t* hist, uint32_t* totals, int64_t nbins, cudaStream_t st) {
+  if (nbins % 4096 != 0 || nbins / 4096 > 1024) return set_error(PF_ERR_VALUE, "bucket scan: bad bin count");
+  const int nb = (int)(nbins / 4096);
+  k_scan_blocks<<<nb, 1024, 0, st>>>(hist, totals);
+  if (int rc = check_launch("scan_blocks")) return rc;
+  k_scan_totals<<<1, 1024, 0, st>>>(totals, nb);
+  if (int rc = check_launch("scan_totals")) return rc;
+  k_scan_add<<<(unsigned)(nbins / 256), 256, 0, st>>>(hist, totals);
+  return check_launch("scan_add");
+}
+
 int run_unsort(const TileParams& P, cudaStream_t st) {
   k_unsort<<<grid_for(P.n, 256), 256, 0, st>>>(P.srec, P.inv, P.n, P.nwords, P.p, P.mask_bits, P.counts,
                                               P.codes, P.props);

@@ -106,6 +106,7 @@ int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf
 int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int k, int kpadg, int kpad,
                  uint16_t* Gbf, float* G32, uint16_t* textbf, cudaStream_t st);
 int ws_kt_max();
+int run_bucket_scan(uint32_t* hist, uint32_t* totals, int64_t nbins, cudaStream_t st);
 constexpr int kSubRows = 32;  // rows of a sub-tile
 
 }  // namespace tile
