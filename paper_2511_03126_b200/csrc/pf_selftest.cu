@@ -174,12 +174,30 @@ __global__ void __launch_bounds__(128, 1) k_umma_rate(int n, int ts, int reps, i
     out[blockIdx.x * 2] = (unsigned long long)(t1 - t0);
     out[blockIdx.x * 2 + 1] = (unsigned long long)(t2 - t0);
     done = 1;
-  } else if (stores && warp > 0) {
+  } else if (stores == 1 && warp > 0) {
     uint4* x = reinterpret_cast<uint4*>(sX);
     int i = tid;
     while (!done) {
       x[i & 2047] = make_uint4(i, i, i, i);
       i += 96;
+    }
+  } else if (stores == 2 && warp > 0) {
+    // TMEM load latency under the MMA stream: tcgen05.ld 32x32b.x32 of columns 448.. + wait::ld
+    const uint32_t ta = tbase + 448u + ((uint32_t)(32 * warp) << 16);
+    long long cyc = 0;
+    int cnt = 0;
+    float acc = 0.f;
+    while (!done) {
+      float v[32];
+      const long long a0 = clock64();
+      tc::tmem_ld32(ta, v);
+      cyc += clock64() - a0;
+      ++cnt;
+      acc += v[0];
+    }
+    if (tid == 32) {
+      out[2 * gridDim.x + blockIdx.x * 2] = (unsigned long long)cyc;
+      out[2 * gridDim.x + blockIdx.x * 2 + 1] = (unsigned long long)cnt + (acc == 12345.f ? 1 : 0);
     }
   }
   tc::fence_before_sync();

@@ -51,7 +51,8 @@ constexpr float kAffineR = 12e-3f;     // tiles wider than 2 * kAffineR (m) buil
 constexpr int kTraceCtas = 4, kTraceTiles = 64;
 constexpr int kCG = 2;                 // 64-column B chunks per MMA group (N = 64 * kCG)
 constexpr int kDCols = 64 * kCG;       // TMEM columns of one accumulator slot
-constexpr int kDBufs = 2;              // TMEM accumulator slots (feature groups and the S group rotate)
+constexpr int kDBufs = kCG == 1 ? 5 : 2;  // TMEM accumulator slots (with the two A buffers: 512 columns)
+constexpr int kSGroups = kMaxKpadTC / kDCols;  // similarity groups per tile (1 or 2)
 constexpr int kStages = 8;             // B ring depth (4 chunk groups)
 constexpr int kKtWs = 192;             // taps per tile held in one A buffer / B stage
 constexpr int kStageBytes = kKtWs * 128;
@@ -89,7 +90,7 @@ struct WsShared {
   int32_t vrank[2][kMaxViewsTC];    // builders: view | window base << 8, per rank
   int4 vwin[2][kMaxViewsTC];        // builders: window x0, y0, w, h per rank
   float bbox[2][4][6];              // builders: per lane group box of the tile's points
-  float4 yv[kMaxKpadTC];         // per material: {y0, y1, mid_theta, bias (0 | -inf for padding)}
+  float4 yp[kMaxKpadTC];         // per material pair (k, k+1), at k/2: {y0 y0' y1 y1'} then {mt mt' b b'}
   float4 yv2[kMaxKpadTC];        // per material: {y2, y3, 0, 0} (P > 2)
   float xss[2][kTile];           // accumulator halves: partial |F|^2
   float xm[2][kTile];            //                     partial max (large 1/T only)
@@ -131,6 +132,39 @@ __device__ __forceinline__ bool item_row(const TileParams& P, int64_t t, int64_t
 
 __device__ __forceinline__ uint16_t f2bf16(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+// prefetch loads that must issue where they are written (a plain load may be sunk by the compiler
+// to its first use a whole tile later, putting its DRAM latency on the critical path)
+__device__ __forceinline__ uint4 ld_pref_u4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float4 ld_pref_f4(const void* p) {
+  float4 r;
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+
+// packed fp32 pairs (sm_100 FFMA2 / FADD2): half the FP32 instructions of the epilogue math
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
 }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -191,8 +225,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     float y[4];
 #pragma unroll
     for (int pp = 0; pp < 4; ++pp) y[pp] = (pp < P.p && j < P.k) ? P.values[j * P.p + pp] : 0.f;
-    S.yv[j] = make_float4(y[0], y[1], j < P.k ? P.mid_theta[j] : 0.f, j < P.k ? 0.f : -INFINITY);
     S.yv2[j] = make_float4(y[2], y[3], 0.f, 0.f);
+  }
+  for (int j = tid; j < kMaxKpadTC / 2; j += kWsThreads) {
+    auto val = [&](int kk, int pp) { return (kk < P.k && pp < P.p) ? P.values[kk * P.p + pp] : 0.f; };
+    const int a = 2 * j, b = 2 * j + 1;
+    S.yp[2 * j] = make_float4(val(a, 0), val(b, 0), val(a, 1), val(b, 1));
+    S.yp[2 * j + 1] = make_float4(a < P.k ? P.mid_theta[a] : 0.f, b < P.k ? P.mid_theta[b] : 0.f,
+                                  a < P.k ? 0.f : -INFINITY, b < P.k ? 0.f : -INFINITY);
   }
   for (int j = tid; j < kMaxKpadTC + 8; j += kWsThreads) S.red[j] = 0.0;
   if (tid == 0) {
@@ -202,7 +242,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     }
     for (int b = 0; b < kDBufs; ++b) {
       tc::mbar_init(&S.d_full[b], 1);
-      tc::mbar_init(&S.d_empty[b], kAccThreads / 32);
+      tc::mbar_init(&S.d_empty[b], kAccThreads / 64);  // the 4 warps of the owning parity
     }
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&S.b_full[s], kLoadThreads);  // one cp.async.mbarrier.arrive.noinc per loader thread
@@ -211,7 +251,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   }
   if (warp == kAccWarp0) tc::tmem_alloc(&S.tmem_base, 512);
   static_assert(kDBufs * kDCols + 2 * (kKtWs / 2) <= 512, "TMEM: accumulator slots + 2 A buffers");
-  static_assert(kDCols == kMaxKpadTC, "the S group fills one accumulator slot");
+  static_assert(kSGroups * kDCols == kMaxKpadTC && (kSGroups == 1 || kSGroups == 2), "similarity groups");
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -286,9 +326,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
                      : "memory");
         if constexpr (PROF) {
           wait_cyc[11] += clock64() - tl0;
-          if (warp == 0 && lane == 0 && (++published & 1) == 0) {
-            WS_TRACE(pub_tile, 14 + pub_group);  // (issue time of the group's second chunk)
-            if (++pub_group == nch / 2) { pub_group = 0; ++pub_tile; }
+          if (warp == 0 && lane == 0) {
+            if (pub_group == 0 || pub_group == nch - 1) WS_TRACE(pub_tile, pub_group == 0 ? 14 : 15);
+            if (++pub_group == nch) { pub_group = 0; ++pub_tile; }
           }
         }
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
@@ -335,9 +375,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           // one lane under `if (lane == 0)` measured ~100 cycles per MMA, this reaches the 64-cycle
           // tensor rate of M=128, N=128, K=16 (scripts/umma_rate.py)
           const uint32_t b0 = tc::smem_u32(sB + stage * kStageBytes);
-          for (int s = 0; s < ktp / 16; ++s) {
-            const uint64_t bd = tc::smem_desc_sw128(b0 + s * 2048, kStageBytes, 1024);
-            tc::mma_bf16_ts_elect(dst, tA + (uint32_t)(s * 8), bd, idesc, s > 0 ? 1u : 0u);
+          // descriptors advance by 2048 B (start field +128) and 8 TMEM columns per K=16 step
+          uint64_t bd = tc::smem_desc_sw128(b0, kStageBytes, 1024);
+          uint32_t ta = tA;
+          tc::mma_bf16_ts_elect(dst, ta, bd, idesc, 0u);
+#pragma unroll 4
+          for (int s = 1; s < ktp / 16; ++s) {
+            bd += 128;
+            ta += 8;
+            tc::mma_bf16_ts_elect(dst, ta, bd, idesc, 1u);
           }
 #pragma unroll
           for (int g = 0; g < kCG; ++g) tc::mma_commit_elect(&S.b_empty[stage + g]);
@@ -346,7 +392,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         }
         __syncwarp();
         if constexpr (PROF) issue_cyc += clock64() - ti0;
-        if (lane == 0) WS_TRACE(t_local, 4 + c / kCG);
+        if (lane == 0 && (c == 0 || c == nch / 2 || c + kCG >= nch)) WS_TRACE(t_local, c == 0 ? 4 : (c + kCG >= nch ? 6 : 5));
         ++dcount;
         stage += kCG;
         if (stage == kStages) { stage = 0; phase ^= 1u; }
@@ -380,8 +426,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       if (bt < P.nv) ds = P.tile_desc[t * P.nv + bt];
       int64_t jr;
       if (item_row(P, t, ntiles, row, jr)) {
-        pp = P.spts[jr];
-        mm = *reinterpret_cast<const uint2*>(P.srec + jr);
+        pp = ld_pref_f4(P.spts + jr);
+        const uint4 r4 = ld_pref_u4(P.srec + jr);
+        mm = make_uint2(r4.x, r4.y);
       }
     };
     int kt_nx = 0;
@@ -604,8 +651,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     int64_t j_nx = 0;
     bool v_nx = blockIdx.x < nitems && item_row(P, blockIdx.x, ntiles, row, j_nx);
     if (v_nx) {
-      rec_nx = *reinterpret_cast<const uint4*>(P.srec + j_nx);
-      p_nx = P.spts[j_nx];
+      rec_nx = ld_pref_u4(P.srec + j_nx);
+      p_nx = ld_pref_f4(P.spts + j_nx);
     }
     for (int64_t tile = blockIdx.x; tile < nitems; tile += gridDim.x) {
       const int kt = kt_nx;
@@ -616,8 +663,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       kt_nx = kt_at(P, tile + gridDim.x, nitems);
       v_nx = tile + gridDim.x < nitems && item_row(P, tile + gridDim.x, ntiles, row, j_nx);
       if (v_nx) {
-        rec_nx = *reinterpret_cast<const uint4*>(P.srec + j_nx);
-        p_nx = P.spts[j_nx];
+        rec_nx = ld_pref_u4(P.srec + j_nx);
+        p_nx = ld_pref_f4(P.spts + j_nx);
       }
       bool ok;
       ktp_of(kt, ok);
@@ -629,46 +676,56 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const float invc = count > 0 ? 1.f / (float)count : 0.f;
       const int32_t i = valid ? __float_as_int(pcur.w) : 0;
       float ss0 = 0.f, ss1 = 0.f, ss2 = 0.f, ss3 = 0.f;
-      for (int c = 0; c < nd; c += kCG) {  // kCG chunks: this half drains kDCols / 2 columns
-        const int db = dcount % kDBufs;
-        WS_WAIT(&S.d_full[db], (dcount / kDBufs) & 1u, 6);
-        if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile, 23 + c / kCG);
+      // group g (64 columns) belongs to the warps of parity g & 1: the two warps of a lane group
+      // drain alternate groups, so one's tcgen05.ld latency overlaps the other's arithmetic
+      for (int c = half; c < nd / kCG; c += 2) {  // c: feature group (kCG chunks)
+        const uint32_t gi = dcount + (uint32_t)c;
+        const int db = (int)(gi % kDBufs);
+        WS_WAIT(&S.d_full[db], (gi / kDBufs) & 1u, 6);
+        if (warp == kAccWarp0 && lane == 0 && (c == 0 || c + 2 >= nd / kCG)) WS_TRACE(a_tile, c == 0 ? 23 : 24);
         tc::fence_after_sync();
 #pragma unroll
-        for (int g = 0; g < kCG; ++g) {  // 32 columns at a time (register budget: wacc stays live)
+        for (int g = 0; g < 2 * kCG; ++g) {  // 32 columns at a time (register budget: wacc stays live)
           float v[32];
-          tc::tmem_ld32(tbase + (uint32_t)(db * kDCols + half * (kDCols / 2) + 32 * g) + t_lane, v);
-          if (g == kCG - 1) {
+          tc::tmem_ld32(tbase + (uint32_t)(db * kDCols + 32 * g) + t_lane, v);
+          if (g == 2 * kCG - 1) {
             tc::fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.d_empty[db]);  // data is in registers: release the slot
           }
+          {
+            uint64_t s01 = pk2(ss0, ss1), s23 = pk2(ss2, ss3);
 #pragma unroll
-          for (int q = 0; q < 32; q += 4) {
-            ss0 = fmaf(v[q], v[q], ss0);
-            ss1 = fmaf(v[q + 1], v[q + 1], ss1);
-            ss2 = fmaf(v[q + 2], v[q + 2], ss2);
-            ss3 = fmaf(v[q + 3], v[q + 3], ss3);
+            for (int q = 0; q < 32; q += 4) {
+              const uint64_t a = pk2(v[q], v[q + 1]), b = pk2(v[q + 2], v[q + 3]);
+              s01 = ffma2(a, a, s01);
+              s23 = ffma2(b, b, s23);
+            }
+            up2(s01, ss0, ss1);
+            up2(s23, ss2, ss3);
           }
           if (P.features && valid) {
-            float* dst = P.features + (int64_t)i * P.d + c * 64 + half * (kDCols / 2) + 32 * g;
+            float* dst = P.features + (int64_t)i * P.d + c * kDCols + 32 * g;
 #pragma unroll
             for (int q = 0; q < 32; q += 4)
               *reinterpret_cast<float4*>(dst + q) =
                   make_float4(v[q] * invc, v[q + 1] * invc, v[q + 2] * invc, v[q + 3] * invc);
           }
         }
-        ++dcount;
       }
+      dcount += (uint32_t)(nd / kCG);
       S.xss[half][row] = (ss0 + ss1) + (ss2 + ss3);
       // ---- epilogue on S (this half's materials) ----------------------------------------------------
-      const int sslot = dcount % kDBufs;
-      WS_WAIT(&S.d_full[sslot], (dcount / kDBufs) & 1u, 7);
-      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile, 23 + nd / kCG);
+      // the similarity columns are the tile's last two groups: materials 64 h .. 64 h + 63 in slot h
+      const uint32_t sgi = dcount + (kSGroups == 2 ? (uint32_t)half : 0u);
+      const int sslot = (int)(sgi % kDBufs);
+      WS_WAIT(&S.d_full[sslot], (sgi / kDBufs) & 1u, 7);
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile, 25);
       ++a_tile;
-      const uint32_t tS = tbase + (uint32_t)(sslot * kDCols + k0) + t_lane;
+      const uint32_t tS = tbase + (uint32_t)(sslot * kDCols + (kSGroups == 2 ? 0 : k0)) + t_lane;
       tc::fence_after_sync();
       asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 27);
       const float ss = S.xss[0][row] + S.xss[1][row];
       const bool featured = valid && count > 0;
       const float inv = ss > 0.f ? rsqrtf(ss) : 0.f;
@@ -684,7 +741,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           float v[32];
           tc::tmem_ld32(tS + (uint32_t)c0, v);
 #pragma unroll
-          for (int q = 0; q < 32; ++q) mx = fmaxf(mx, fmaf(v[q], sc, S.yv[k0 + c0 + q].w));
+          for (int q = 0; q < 32; ++q) {
+            const float4 yb = S.yp[2 * ((k0 + c0 + q) >> 1) + 1];
+            mx = fmaxf(mx, fmaf(v[q], sc, (q & 1) ? yb.w : yb.z));
+          }
         }
         S.xm[half][row] = mx;
         asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
@@ -692,28 +752,51 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         if (!(m2 > -INFINITY)) m2 = 0.f;
       }
       float se = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f, pl3 = 0.f, pml = 0.f;
+      {
+        // material pairs (k, k+1): FFMA2 for the exponent, sums and regressions
+        uint64_t sep = 0ull, p0p = 0ull, p1p = 0ull, pmp = 0ull;  // (+0.f, +0.f)
+        const uint64_t scp = pk2(sc, sc);
 #pragma unroll
-      for (int c0 = 0; c0 < kHalfK; c0 += 32) {
-        float v[32];
-        tc::tmem_ld32(tS + (uint32_t)c0, v);
+        for (int c0 = 0; c0 < kHalfK; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(tS + (uint32_t)c0, v);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const float4 y = S.yv[k0 + c0 + q];
-          const float e = ex2(fmaf(v[q], sc, y.w - m2));  // padding columns: bias -inf -> 0
-          se += e;
-          pl0 = fmaf(e, y.x, pl0);
-          pl1 = fmaf(e, y.y, pl1);
-          pml = fmaf(e, y.z, pml);
-        }
-        if (p_wide) {
+          for (int q = 0; q < 32; q += 2) {
+            const int kp = (k0 + c0 + q) >> 1;
+            const float4 ya = S.yp[2 * kp], yb = S.yp[2 * kp + 1];
+            float x0, x1;
+            up2(ffma2(pk2(v[q], v[q + 1]), scp, pk2(yb.z - m2, yb.w - m2)), x0, x1);  // padding: -inf
+            const float e0 = ex2(x0), e1 = ex2(x1);
+            const uint64_t e = pk2(e0, e1);
+            sep = fadd2(sep, e);
+            p0p = ffma2(e, pk2(ya.x, ya.y), p0p);
+            p1p = ffma2(e, pk2(ya.z, ya.w), p1p);
+            pmp = ffma2(e, pk2(yb.x, yb.y), pmp);
+            if (!outs && !p_wide) {  // stash the exponentials in place of S for the weight totals
+              v[q] = e0;
+              v[q + 1] = e1;
+            }
+          }
+          if (!outs && !p_wide) tc::tmem_st32(tS + (uint32_t)c0, v);
+          if (p_wide) {
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const float4 y = S.yv[k0 + c0 + q], y2 = S.yv2[k0 + c0 + q];
-            const float e = ex2(fmaf(v[q], sc, y.w - m2));
-            pl2 = fmaf(e, y2.x, pl2);
-            pl3 = fmaf(e, y2.y, pl3);
+            for (int q = 0; q < 32; ++q) {
+              const float4 yb = S.yp[2 * ((k0 + c0 + q) >> 1) + 1], y2 = S.yv2[k0 + c0 + q];
+              const float e = ex2(fmaf(v[q], sc, ((q & 1) ? yb.w : yb.z) - m2));
+              pl2 = fmaf(e, y2.x, pl2);
+              pl3 = fmaf(e, y2.y, pl3);
+            }
           }
         }
+        float a, b;
+        up2(sep, a, b);
+        se = a + b;
+        up2(p0p, a, b);
+        pl0 = a + b;
+        up2(p1p, a, b);
+        pl1 = a + b;
+        up2(pmp, a, b);
+        pml = a + b;
       }
       S.xsum[half][0][row] = se;
       S.xsum[half][1][row] = pl0;
@@ -722,17 +805,35 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       S.xsum[half][4][row] = pl3;
       S.xsum[half][5][row] = pml;
       asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 28);
       const float se_t = S.xsum[0][0][row] + S.xsum[1][0][row];
       if (featured && isnan(se_t)) atomicOr(P.status, 1);  // NaN similarity (grounding.py:173-174)
       const float rs = featured ? 1.f / se_t : 0.f;
-      // normalised weights of this half -> per-thread weight totals (columns >= K are never read)
+      // normalised weights of this half -> per-thread weight totals (columns >= K are never read):
+      // the exponentials come back from TMEM (stashed by pass 1); with validation outputs / P > 2
+      // S is still in TMEM and they are recomputed
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 29);
+      const bool stashed = !outs && !p_wide;
+      if (stashed) tc::tmem_st_wait();
 #pragma unroll
       for (int c0 = 0; c0 < kHalfK; c0 += 32) {
         float v[32];
         tc::tmem_ld32(tS + (uint32_t)c0, v);
+        const uint64_t scp2 = pk2(sc, sc), mp2 = pk2(-m2, -m2), rsp = pk2(rs, rs);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) wacc[c0 + q] = fmaf(ex2(fmaf(v[q], sc, -m2)), rs, wacc[c0 + q]);
+        for (int q = 0; q < 32; q += 2) {
+          uint64_t e;
+          if (stashed) {
+            e = pk2(v[q], v[q + 1]);
+          } else {
+            float x0, x1;
+            up2(ffma2(pk2(v[q], v[q + 1]), scp2, mp2), x0, x1);
+            e = pk2(ex2(x0), ex2(x1));
+          }
+          up2(ffma2(e, rsp, pk2(wacc[c0 + q], wacc[c0 + q + 1])), wacc[c0 + q], wacc[c0 + q + 1]);
+        }
       }
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 30);
       if (outs) {  // validation outputs (similarities, softmax weights), caller's order
         for (int c0 = 0; c0 < kHalfK; c0 += 32) {
           float v[32];
@@ -747,8 +848,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       }
       tc::fence_before_sync();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.d_empty[sslot]);
-      ++dcount;
+      if (kSGroups == 2) {
+        if (lane == 0) mbar_arrive(&S.d_empty[sslot]);  // similarity group h: read by half h only
+      } else {
+        asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");  // both halves read the group
+        if (lane == 0 && half == 0) mbar_arrive(&S.d_empty[sslot]);
+      }
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 26);
+      dcount += (uint32_t)kSGroups;
       if (valid && half == 0) {
         float prop[4];
 #pragma unroll
