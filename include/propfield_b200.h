@@ -138,6 +138,10 @@ int pf_voxel_accumulate(const int32_t* codes, const float* rho, int64_t n, int32
 /* mass = edge^3 * sum_{count>0} sum/count over the (allreduced) grid. `out` is a caller-zeroed
  * device double[2] = {mass_kg, occupied_voxels}; lo_hi as above (edge recomputed identically). */
 int pf_voxel_mass(const float* grid, int32_t g, const double* lo_hi, double* out, void* stream);
+/* The same mass from the touched-voxel list of pf_fuse_query (one GPU: no dense scan); zeroes the
+ * listed grid entries, leaving the grid clean for the next object. capacity = n (the list holds 2n). */
+int pf_voxel_mass_sparse(float* grid, int32_t g, const int32_t* list, const int32_t* count, int64_t capacity,
+                         const double* lo_hi, double* out, void* stream);
 
 /* integrate.characteristic_length (integrate.py:72-95), device part: for every point of (n,3) f32,
  * the squared distance to its (k+1)-th nearest point, self included (cKDTree.query(p, k+1)[:, k]),
@@ -211,6 +215,10 @@ typedef struct pf_fuse_args {
   float* weights;           /* optional (n,k) f32 (flag WRITE_WEIGHTS)                           */
   /* scratch */
   void* workspace;          /* pf_fuse_workspace_bytes(args) bytes, 256-byte aligned             */
+  /* optional touched-voxel list (2n int32): slots [0,n) per sorted point (voxel code or -1), slots
+   * [n, n + *vox_count) appended by the SIMT kernel                                             */
+  int32_t* vox_list;        /* (2n,) or NULL                                                     */
+  int32_t* vox_count;       /* (1,) device int32, caller-zeroed                                  */
 } pf_fuse_args_t;
 
 uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* args);

@@ -87,6 +87,8 @@ class FuseArgs(C.Structure):
         ("sims", C.c_void_p),
         ("weights", C.c_void_p),
         ("workspace", C.c_void_p),
+        ("vox_list", C.c_void_p),
+        ("vox_count", C.c_void_p),
     ]
 
 
@@ -114,6 +116,7 @@ SIGNATURES = {
     "pf_fuse_prepare": ([C.POINTER(FuseArgs), _P], C.c_int),
     "pf_fuse_query": ([C.POINTER(FuseArgs), _P], C.c_int),
     "pf_stage_timing": ([_I32], C.c_int),
+    "pf_voxel_mass_sparse": ([_P, _I32, _P, _P, _I64, _P, _P, _P], C.c_int),
     "pf_knn_workspace_bytes": ([_I64], C.c_uint64),
     "pf_knn_kth_distance": ([_P, _I64, _I32, _P, _P, _P, _P], C.c_int),
     "pf_integrate_partials": ([_P, _I64, _I32, _P, _P, _P, _P, _P, _P], C.c_int),

@@ -95,6 +95,9 @@ struct FuseParams {
   float* props;
   int32_t* codes;
   float* grid_partials;
+  int32_t* vox_list;   // optional touched-voxel list
+  int32_t* vox_count;
+  int64_t vox_base;    // first list slot of this kernel (n when the tile path owns slots 0..n-1)
   double* partials;
   int32_t* status;
   float* features;
@@ -349,7 +352,9 @@ __global__ void __launch_bounds__(kFuseThreads, 2) k_fuse_simt(FuseParams P) {
 #pragma unroll
         for (int pp = 1; pp < kMaxP; ++pp) rho = P.density_col == pp ? prop[pp] : rho;
         atomicAdd(P.grid_partials + code, rho);
-        atomicAdd(P.grid_partials + cells3 + code, 1.0f);
+        // touched-voxel list: the SIMT points append after the tile path's n slots
+        if (atomicAdd(P.grid_partials + cells3 + code, 1.0f) == 0.0f && P.vox_list)
+          P.vox_list[P.vox_base + atomicAdd(P.vox_count, 1)] = code;
       }
       pm_sum += pm;
       pmx += (double)pm * px;
@@ -528,6 +533,7 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
   prm.inv_temp = (float)(1.0 / a->temperature); prm.eps = a->eps; prm.grid = a->grid;
   prm.lo_hi = a->lo_hi; prm.flags = a->flags; prm.counts = a->counts; prm.mask_bits = a->mask_bits;
   prm.props = a->props; prm.codes = a->codes; prm.grid_partials = a->grid_partials;
+  prm.vox_list = a->vox_list; prm.vox_count = a->vox_count; prm.vox_base = 0;
   prm.partials = a->partials; prm.status = a->status; prm.features = a->features;
   prm.sims = a->sims; prm.weights = a->weights;
 
@@ -550,6 +556,8 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.grid = a->grid; T.cells3 = (int64_t)a->grid * a->grid * a->grid; T.lo_hi = a->lo_hi;
     T.mask_bits = a->mask_bits; T.counts = a->counts; T.codes = a->codes; T.props = a->props;
     T.grid_partials = (a->flags & PF_FUSE_SKIP_VOXELS) ? nullptr : a->grid_partials;
+    T.vox_list = a->vox_list;
+    T.vox_count = a->vox_count;
     T.features = (a->flags & PF_FUSE_WRITE_FEATURES) ? a->features : nullptr;
     T.sims = (a->flags & PF_FUSE_WRITE_SIMS) ? a->sims : nullptr;
     T.weights = (a->flags & PF_FUSE_WRITE_WEIGHTS) ? a->weights : nullptr;
@@ -571,6 +579,7 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     // overflow tiles (more taps than fit in shared memory) run through the SIMT kernel
     prm.list = T.ovf_list;
     prm.list_len = T.ovf_count;
+    prm.vox_base = a->n;
   }
   int rc;
   if (a->fmap_dtype == PF_F32) {

@@ -518,6 +518,7 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     const int32_t code = voxel_code(p.x, p.y, p.z, dlo, edge, P.grid);
     *reinterpret_cast<uint4*>(P.srec + jpt) =
         make_uint4(w0, w1, (uint32_t)(__popc(w0) + __popc(w1)), (uint32_t)code);
+    if (P.vox_list) P.vox_list[jpt] = -1;  // the tile kernel writes the slots of the points it runs
   }
   __syncthreads();
   if (tid < P.nv && s_cls[tid] == kViewMixed && ((s_seen[tid >> 5] >> (tid & 31)) & 1u)) {

@@ -71,6 +71,8 @@ struct TileParams {
   int32_t* codes;
   float* props;
   float* grid_partials;  // nullptr: skip voxels
+  int32_t* vox_list;     // optional touched-voxel list (first point of a voxel appends its code)
+  int32_t* vox_count;
   float* features;       // optional validation outputs, original order
   float* sims;
   float* weights;

@@ -418,10 +418,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     const uint32_t t_lanes = (uint32_t)(32 * bq) << 16;
     uint32_t t_local = 0;
     static_assert(kMaxViewsTC <= kBuildThreads, "one window per builder thread");
-    auto fetch = [&](int64_t t, int& kt, uint2& ds, float4& pp, uint2& mm) {
+    auto fetch = [&](int64_t t, int& kt, uint2& ds, float4& pp, uint2& mm, int32_t& cd) {
       kt = kt_at(P, t, nitems);
       pp = make_float4(0.f, 0.f, 0.f, 0.f);
       mm = make_uint2(0u, 0u);  // rows outside the work item: empty mask
+      cd = -1;
       if (t >= nitems) return;
       if (bt < P.nv) ds = P.tile_desc[t * P.nv + bt];
       int64_t jr;
@@ -429,22 +430,33 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         pp = ld_pref_f4(P.spts + jr);
         const uint4 r4 = ld_pref_u4(P.srec + jr);
         mm = make_uint2(r4.x, r4.y);
+        cd = (int32_t)r4.w;
       }
     };
     int kt_nx = 0;
     uint2 ds_nx = make_uint2(0u, 0u), mw_nx;
     float4 p_nx;
-    fetch(blockIdx.x, kt_nx, ds_nx, p_nx, mw_nx);
+    int32_t cd_nx;
+    fetch(blockIdx.x, kt_nx, ds_nx, p_nx, mw_nx, cd_nx);
     const float wf1 = (float)(S.sv[0].Wf - 1), hf1 = (float)(S.sv[0].Hf - 1);  // uniform maps (tile_path_ok)
     for (int64_t tile = blockIdx.x; tile < nitems; tile += gridDim.x) {
       const int kt = kt_nx;
       const uint2 ds_cur = ds_nx;
       const float4 p = p_nx;
       const uint2 mw = mw_nx;
-      fetch(tile + gridDim.x, kt_nx, ds_nx, p_nx, mw_nx);
+      const int32_t cd = cd_nx;
+      fetch(tile + gridDim.x, kt_nx, ds_nx, p_nx, mw_nx, cd_nx);
       bool ok;
       const int ktp = ktp_of(kt, ok);
       if (!ok) continue;
+      if (bh == 0 && P.vox_list) {
+        // touched-voxel list without returning atomics: slot jpt holds the code when this row starts
+        // a run of equal codes within its warp (sorted neighbours mostly share a voxel), else -1;
+        // pf_voxel_mass_sparse claims each voxel once (atomicExch on its count)
+        const int32_t prev = __shfl_up_sync(0xffffffffu, cd, 1);
+        int64_t jr;
+        if (cd >= 0 && item_row(P, tile, ntiles, row, jr)) P.vox_list[jr] = (lane == 0 || prev != cd) ? cd : -1;
+      }
       const int ab = (int)(t_local & 1u);
       uint2* sdesc = S.desc_a[ab];
       if (bt < P.nv) sdesc[bt] = ds_cur;

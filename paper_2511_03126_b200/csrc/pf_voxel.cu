@@ -105,6 +105,31 @@ __global__ void k_vox_mass(const float* __restrict__ grid, int64_t cells, double
   }
 }
 
+// touched-voxel list: slots [0, n) (code or -1, duplicates allowed) then [n, n + *count) (appended).
+// Each voxel is claimed once (atomicExch on its count), its sum / count accumulated and both
+// entries zeroed: the grid is left clean.
+__global__ void k_vox_mass_sparse(float* __restrict__ grid, int64_t cells, const int32_t* __restrict__ list,
+                                  const int32_t* __restrict__ count, int64_t n, double* __restrict__ out) {
+  const int64_t m = n + min((int64_t)*count, n);
+  double acc = 0.0, occ = 0.0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = __ldg(list + j);
+    if (c < 0) continue;
+    const float cnt = atomicExch(grid + cells + c, 0.0f);
+    if (cnt > 0.0f) {
+      acc += (double)grid[c] / (double)cnt;
+      occ += 1.0;
+      grid[c] = 0.0f;
+    }
+  }
+  acc = warp_sum(acc);
+  occ = warp_sum(occ);
+  if ((threadIdx.x & 31) == 0 && (acc != 0.0 || occ != 0.0)) {
+    atomicAdd(out, acc);
+    atomicAdd(out + 1, occ);
+  }
+}
+
 __global__ void k_vox_scale(const double* __restrict__ lo_hi, int g, double* __restrict__ out) {
   double lo[3];
   const double e = voxel_edge(lo_hi, g, lo);
@@ -119,6 +144,18 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 using namespace pf;
 
 extern "C" {
+
+int pf_voxel_mass_sparse(float* grid, int32_t g, const int32_t* list, const int32_t* count, int64_t capacity,
+                         const double* lo_hi, double* out, void* stream) {
+  if (g < 1) return set_error(PF_ERR_VALUE, "voxel grid side must be >= 1");
+  if (!list || !count) return set_error(PF_ERR_VALUE, "voxel_mass_sparse: list and count required");
+  const int64_t cells = (int64_t)g * g * g;
+  k_vox_mass_sparse<<<grid_for(2 * capacity, 256, 148 * 8), 256, 0, S(stream)>>>(grid, cells, list, count, capacity,
+                                                                                  out);
+  if (int rc = check_launch("voxel_mass_sparse")) return rc;
+  k_vox_scale<<<1, 1, 0, S(stream)>>>(lo_hi, g, out);
+  return check_launch("voxel_mass_scale");
+}
 
 int pf_bbox(const float* points, int64_t n, double* lo_hi, void* stream) {
   if (n <= 0) return set_error(PF_ERR_VALUE, "bbox of an empty point cloud");

@@ -76,6 +76,11 @@ class FuseBuffers:
         self.props = t.empty((n, p), dtype=t.float32, device=dev)
         self.codes = t.empty(n, dtype=t.int32, device=dev)
         self.grid_partials = t.zeros(2 * grid**3, dtype=t.float32, device=dev)
+        # touched-voxel list: on one GPU the mass reduction walks it and re-zeroes those voxels, so
+        # the 2 g^3 grid is neither memset nor scanned per object (dense path after an all-reduce)
+        self.vox_list = t.full((max(1, 2 * n),), -1, dtype=t.int32, device=dev)
+        self.vox_count = t.zeros(1, dtype=t.int32, device=dev)
+        self.grid_clean = True
         self.partials = t.zeros(k + 6, dtype=t.float64, device=dev)
         self.mass = t.zeros(2, dtype=t.float64, device=dev)
         self.status = t.zeros(1, dtype=t.int32, device=dev)
@@ -88,7 +93,10 @@ class FuseBuffers:
         self.workspace = t.empty(max(ws, 256), dtype=t.uint8, device=dev)
 
     def reset(self):
-        self.grid_partials.zero_()
+        if not self.grid_clean:
+            self.grid_partials.zero_()
+            self.grid_clean = True
+        self.vox_count.zero_()
         self.partials.zero_()
         self.mass.zero_()
         self.status.zero_()
@@ -127,6 +135,8 @@ def _make_args(points, n, views, tables, temperature, eps, grid, b, flags):
     a.sims = ptr(b.sims)
     a.weights = ptr(b.weights)
     a.workspace = ptr(getattr(b, "workspace", None))
+    a.vox_list = ptr(getattr(b, "vox_list", None))
+    a.vox_count = ptr(getattr(b, "vox_count", None))
     return a
 
 
@@ -161,13 +171,22 @@ class FusedResult:
         from .dist import allreduce_partials
 
         allreduce_partials(self.buffers.grid_partials, self.buffers.partials, group)
+        self.reduced = True  # the grid now holds other ranks' voxels too: dense finalisation
 
     def finalize(self):
         """Voxel mass from the (reduced) grid: buffers.mass = {mass_kg, occupied_voxels}."""
+        if getattr(self, "finalized", False):  # the sparse pass re-zeroes the grid: run once
+            return self
+        self.finalized = True
         b = self.buffers
         b.mass.zero_()
-        _lib.call("pf_voxel_mass", ptr(b.grid_partials), b.grid, ptr(b.lo_hi), ptr(b.mass),
-                  stream_handle())
+        if getattr(self, "reduced", False):
+            _lib.call("pf_voxel_mass", ptr(b.grid_partials), b.grid, ptr(b.lo_hi), ptr(b.mass), stream_handle())
+            b.grid_clean = False
+        else:
+            _lib.call("pf_voxel_mass_sparse", ptr(b.grid_partials), b.grid, ptr(b.vox_list), ptr(b.vox_count),
+                      int(b.vox_list.numel() // 2), ptr(b.lo_hi), ptr(b.mass), stream_handle())
+            b.grid_clean = True
         return self
 
     def check(self):
