@@ -566,6 +566,7 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.tile_kt = reinterpret_cast<int32_t*>(ws + L.kt);
     T.viewf = reinterpret_cast<tile::ViewF*>(ws + L.viewf);
     T.vbound = reinterpret_cast<float4*>(ws + L.vbound);
+    T.vox = reinterpret_cast<double*>(ws + L.vox);
     T.ovf_list = reinterpret_cast<int32_t*>(ws + L.ovf) + 1;
     T.ovf_count = reinterpret_cast<int32_t*>(ws + L.ovf);
     T.sub_count = reinterpret_cast<int32_t*>(ws + L.sub);

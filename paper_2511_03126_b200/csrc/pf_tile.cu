@@ -264,20 +264,12 @@ __device__ int classify_tile_view(const ViewF& v, const float4& vb, const float*
   if (bw * bh > kScanMax) return kViewExact;
   const float* d = depth + v.depth_off + (int64_t)cy0 * v.W + cx0;
   float dmax = 0.f, dmin = 1e30f;
-  const int npx = bw * bh;
-  for (int k = 0; k < npx; k += 4) {  // four independent loads in flight
-    float s[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int kk = min(k + u, npx - 1), yy = kk / bw;
-      s[u] = __ldg(d + (int64_t)yy * v.W + (kk - yy * bw));
+  for (int y = 0; y < bh; ++y, d += v.W)
+    for (int x = 0; x < bw; x += 2) {  // two independent loads per step
+      const float s0 = __ldg(d + x), s1 = __ldg(d + min(x + 1, bw - 1));
+      dmax = fmaxf(dmax, fmaxf(s0, s1));
+      dmin = fminf(dmin, fminf(s0, s1));
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      dmax = fmaxf(dmax, s[u]);
-      dmin = fminf(dmin, s[u]);
-    }
-  }
   if (zmin - 1e-5f > dmax + eps + 1e-5f) return kViewOff;
   // tap window of every point (taps_f32 on the widened range; fu is monotone in u)
   const float fu0 = __fsub_rn(__fmul_rn(__fadd_rn(ulo, 0.5f), v.ru), 0.5f);
@@ -322,6 +314,41 @@ __global__ void k_view_setup(TileParams P) {
     P.viewf[j] = w;
     P.vbound[j] = view_bound(w, P.views[j], P.lo_hi);
   }
+  if (j == 0) {  // voxel domain once (the fp64 edge division of voxel_edge)
+    double lo[3];
+    const double edge = voxel_edge(P.lo_hi, P.grid, lo);
+    P.vox[0] = lo[0];
+    P.vox[1] = lo[1];
+    P.vox[2] = lo[2];
+    P.vox[3] = edge;
+    float* f = reinterpret_cast<float*>(P.vox + 4);
+    f[0] = (float)lo[0];
+    f[1] = (float)lo[1];
+    f[2] = (float)lo[2];
+    f[3] = edge > 0.0 ? (float)(1.0 / edge) : 0.f;
+  }
+}
+
+// voxel_code (pf_common.cuh, sampling.py:110-123 convention) with an fp32 fast path: q = (p - lo) /
+// edge in fp32 is within g * 4e-7 of the fp64 quotient (|p - lo| exact to 2^-24, one rounded 1/edge
+// and one product); when every axis is > 1e-3 from an integer its floor equals the fp64 one, else
+// the exact fp64 formula decides (~0.6 % of points).
+__device__ __forceinline__ int32_t voxel_code_fast(const float4& p, const double* __restrict__ vox, int g) {
+  const float* f = reinterpret_cast<const float*>(vox + 4);
+  const float inv = f[3];
+  const float q[3] = {(p.x - f[0]) * inv, (p.y - f[1]) * inv, (p.z - f[2]) * inv};
+  bool ok = inv > 0.f;
+  int c[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float fl = floorf(q[a]);
+    const float fr = q[a] - fl;
+    ok = ok && fr > 1e-3f && fr < 1.f - 1e-3f;
+    c[a] = min(max((int)fl, 0), g - 1);
+  }
+  if (ok) return (c[0] * g + c[1]) * g + c[2];
+  const double lo[3] = {vox[0], vox[1], vox[2]};
+  return voxel_code(p.x, p.y, p.z, lo, vox[3], g);
 }
 
 // exact per-point decision for one (point, view) sample; fills the taps when visible
@@ -513,9 +540,7 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     window_reduce(vis, t, wx0, wy0, wx1, wy1, v, lane);
   }
   if (valid) {
-    double dlo[3];
-    const double edge = voxel_edge(P.lo_hi, P.grid, dlo);
-    const int32_t code = voxel_code(p.x, p.y, p.z, dlo, edge, P.grid);
+    const int32_t code = voxel_code_fast(p, P.vox, P.grid);
     *reinterpret_cast<uint4*>(P.srec + jpt) =
         make_uint4(w0, w1, (uint32_t)(__popc(w0) + __popc(w1)), (uint32_t)code);
     if (P.vox_list) P.vox_list[jpt] = -1;  // the tile kernel writes the slots of the points it runs
@@ -699,6 +724,7 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg) {
   L.sub = take(sizeof(int32_t) * ((size_t)L.max_sub_tiles + 1));
   L.viewf = take(sizeof(ViewF) * kMaxViewsTC);
   L.vbound = take(sizeof(float4) * kMaxViewsTC);
+  L.vox = take(sizeof(double) * 8);
   L.ovf = take(sizeof(int32_t) * (size_t)(n + 1));
   L.gbf = take(sizeof(uint16_t) * (size_t)cells * kpadg);
   L.textbf = take(sizeof(uint16_t) * (size_t)kpadg * 1024);  // text rows in bf16 (D <= 1024)

@@ -81,6 +81,7 @@ struct TileParams {
   int32_t* tile_kt;
   ViewF* viewf;   // per-view fp32 camera (k_view_setup)
   float4* vbound; // per-view constant error bounds over the bbox (k_view_setup)
+  double* vox;    // voxel domain (k_view_setup): lo (3), edge (fp64), then lo (3) and 1/edge as f32 bits
   int32_t* ovf_list;
   int32_t* ovf_count;
   // overflow tiles (more taps than one A buffer) are re-run as 4 sub-tiles of 32 rows: work items
@@ -96,7 +97,7 @@ struct TileParams {
 struct TileLayout {
   int64_t ntiles;
   int32_t max_sub_tiles;
-  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, gbf, textbf, viewf, vbound, bytes;
+  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, gbf, textbf, viewf, vbound, vox, bytes;
 };
 
 TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg);
