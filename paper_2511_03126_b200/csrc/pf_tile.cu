@@ -608,51 +608,52 @@ __global__ void k_find_overflow(TileParams P, int64_t ntiles, int kt_max) {
   }
 }
 
-// one block per overflow tile, warp q = sub-tile q (rows 32q .. 32q + 31)
+// blocks stride over the overflow tiles, warp q = sub-tile q (rows 32q .. 32q + 31)
 __global__ void __launch_bounds__(kTile) k_subtile_prep(TileParams P, int64_t ntiles) {
   __shared__ ViewF sv[kMaxViewsTC];
-  const int b = blockIdx.x;
   const int nsub = min(*P.sub_count, P.max_sub_tiles);
-  if (b >= nsub) return;
+  if ((int)blockIdx.x >= nsub) return;
   for (int j = threadIdx.x; j < P.nv; j += kTile) sv[j] = P.viewf[j];
   __syncthreads();
   const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tile = P.sub_tiles[b];
-  const int64_t item = ntiles + 4 * (int64_t)b + q;
-  const int64_t jpt = tile * kTile + kSubRows * q + lane;
-  const bool valid = jpt < P.n;
-  float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-  uint2 mw = make_uint2(0u, 0u);
-  if (valid) {
-    p = P.spts[jpt];
-    mw = *reinterpret_cast<const uint2*>(P.srec + jpt);
-  }
-  uint2* desc = P.tile_desc + item * P.nv;
-  int running = 0;
-  for (int v = 0; v < P.nv; ++v) {  // views in order: exclusive prefix of (even-padded) window sizes
-    const bool vis = (((v < 32 ? mw.x : mw.y) >> (v & 31)) & 1u) != 0u;
-    int x0 = INT_MAX, y0 = INT_MAX, x1 = -1, y1 = -1;
-    if (__any_sync(0xffffffffu, vis)) {
-      if (vis) {
-        const ProjF pr = project_f32(sv[v], p.x, p.y, p.z);
-        const TapF t = taps_f32(sv[v], pr.u, pr.v);
-        x0 = t.x0;
-        y0 = t.y0;
-        x1 = t.x0 + t.dx;
-        y1 = t.y0 + t.dy;
-      }
-      x0 = __reduce_min_sync(0xffffffffu, x0);
-      y0 = __reduce_min_sync(0xffffffffu, y0);
-      x1 = __reduce_max_sync(0xffffffffu, x1);
-      y1 = __reduce_max_sync(0xffffffffu, y1);
+  for (int b = blockIdx.x; b < nsub; b += gridDim.x) {
+    const int64_t tile = P.sub_tiles[b];
+    const int64_t item = ntiles + 4 * (int64_t)b + q;
+    const int64_t jpt = tile * kTile + kSubRows * q + lane;
+    const bool valid = jpt < P.n;
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint2 mw = make_uint2(0u, 0u);
+    if (valid) {
+      p = P.spts[jpt];
+      mw = *reinterpret_cast<const uint2*>(P.srec + jpt);
     }
-    const int w = x1 >= 0 ? x1 - x0 + 1 : 0, h = x1 >= 0 ? y1 - y0 + 1 : 0;
-    if (lane == 0)
-      desc[v] = make_uint2((uint32_t)min(running, 65535) | ((uint32_t)(w ? x0 : 0) << 16) | ((uint32_t)(h ? y0 : 0) << 24),
-                           (uint32_t)w | ((uint32_t)h << 8));
-    running += (w * h + 1) & ~1;
+    uint2* desc = P.tile_desc + item * P.nv;
+    int running = 0;
+    for (int v = 0; v < P.nv; ++v) {  // views in order: exclusive prefix of (even-padded) window sizes
+      const bool vis = (((v < 32 ? mw.x : mw.y) >> (v & 31)) & 1u) != 0u;
+      int x0 = INT_MAX, y0 = INT_MAX, x1 = -1, y1 = -1;
+      if (__any_sync(0xffffffffu, vis)) {
+        if (vis) {
+          const ProjF pr = project_f32(sv[v], p.x, p.y, p.z);
+          const TapF t = taps_f32(sv[v], pr.u, pr.v);
+          x0 = t.x0;
+          y0 = t.y0;
+          x1 = t.x0 + t.dx;
+          y1 = t.y0 + t.dy;
+        }
+        x0 = __reduce_min_sync(0xffffffffu, x0);
+        y0 = __reduce_min_sync(0xffffffffu, y0);
+        x1 = __reduce_max_sync(0xffffffffu, x1);
+        y1 = __reduce_max_sync(0xffffffffu, y1);
+      }
+      const int w = x1 >= 0 ? x1 - x0 + 1 : 0, h = x1 >= 0 ? y1 - y0 + 1 : 0;
+      if (lane == 0)
+        desc[v] = make_uint2((uint32_t)min(running, 65535) | ((uint32_t)(w ? x0 : 0) << 16) | ((uint32_t)(h ? y0 : 0) << 24),
+                             (uint32_t)w | ((uint32_t)h << 8));
+      running += (w * h + 1) & ~1;
+    }
+    if (lane == 0) P.tile_kt[item] = running;
   }
-  if (lane == 0) P.tile_kt[item] = running;
 }
 
 // ---- sorted records -> caller's point order (gather: one 32-byte record read per point) -----------------
@@ -717,7 +718,7 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg) {
   L.inv = take(sizeof(int32_t) * (size_t)n);
   L.spts = take(sizeof(float4) * (size_t)ntiles * kTile);
   L.srec = take(sizeof(SRec) * (size_t)ntiles * kTile);
-  L.max_sub_tiles = (int32_t)(ntiles < 1024 + ntiles / 32 ? ntiles : 1024 + ntiles / 32);
+  L.max_sub_tiles = (int32_t)ntiles;  // every tile may be split (sparse clouds overflow often)
   const int64_t items = ntiles + 4 * (int64_t)L.max_sub_tiles;
   L.desc = take(sizeof(uint2) * (size_t)items * nv);
   L.kt = take(sizeof(int32_t) * (size_t)items);
@@ -793,7 +794,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   cudaMemsetAsync(P.sub_count, 0, sizeof(int32_t), st);
   k_find_overflow<<<grid_for(L.ntiles, 256), 256, 0, st>>>(P, L.ntiles, ws_kt_max());
   if (int rc = check_launch("find_overflow")) return rc;
-  k_subtile_prep<<<(unsigned)L.max_sub_tiles, kTile, 0, st>>>(P, L.ntiles);
+  k_subtile_prep<<<(unsigned)(L.max_sub_tiles < 148 * 16 ? L.max_sub_tiles : 148 * 16), kTile, 0, st>>>(P, L.ntiles);
   if (int rc = check_launch("subtile_prep")) return rc;
   stage_mark(2, st);
   if (debug) {
