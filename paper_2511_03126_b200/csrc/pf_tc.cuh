@@ -205,7 +205,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // debug variant: gives up after ~2 s (a pipeline deadlock) with a message and a trap, so a hang
-// becomes a launch error instead of a stuck GPU
+// becomes a launch error instead of a stuck GPU; no suspend hint, so its wake-up latency (and the
+// PF_WS_TRACE timeline) matches the production wait
 __device__ __forceinline__ void mbar_wait_or_trap(uint64_t* bar, uint32_t parity, int tag) {
   const uint32_t a = smem_u32(bar);
   const long long t0 = clock64();
@@ -213,11 +214,11 @@ __device__ __forceinline__ void mbar_wait_or_trap(uint64_t* bar, uint32_t parity
     uint32_t done;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t"
         "}"
         : "=r"(done)
-        : "r"(a), "r"(parity), "r"(1000000u)
+        : "r"(a), "r"(parity)
         : "memory");
     if (done) return;
     if (clock64() - t0 > 4000000000ll) {

@@ -48,7 +48,7 @@ constexpr int kBuildThreads = 32 * kBuildWarps;
 constexpr int kWsThreads = 768;        // 24 warps = 6 warp groups
 constexpr float kAffineR = 12e-3f;     // tiles wider than 2 * kAffineR (m) build with the exact projection:
                                        // the expansion error is ~fx X / Z^3 r^2 <= ~0.05 px (0.4% of a C5 cell)
-constexpr int kTraceCtas = 4, kTraceTiles = 64;
+constexpr int kTraceCtas = 4, kTraceTiles = 64, kTraceEvents = 64;
 constexpr int kCG = 2;                 // 64-column B chunks per MMA group (N = 64 * kCG)
 constexpr int kDCols = 64 * kCG;       // TMEM columns of one accumulator slot
 constexpr int kDBufs = kCG == 1 ? 5 : 2;  // TMEM accumulator slots (with the two A buffers: 512 columns)
@@ -167,6 +167,22 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   return r;
 }
 
+// warp reduce-scatter of 32 values per lane: afterwards lane l holds the sum over the warp's lanes of
+// value l (recursive halving: at distance o a lane keeps the half of its range selected by lane & o)
+__device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < o; ++j) {
+      const float keep = up ? v[j + o] : v[j];
+      const float send = up ? v[j] : v[j + o];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0];
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -190,14 +206,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   long long issue_cyc = 0;
   const long long t_start = PROF ? clock64() : 0;
   // PROF trace: per-tile role timestamps (cycles since kernel start) of the first kTraceTiles tiles of
-  // the first kTraceCtas CTAs; events: 0 build start, 1 build zeroed, 2 build done, 3 mma A ready,
-  // 4-12 mma group g issued, 13 loader tile start, 14-22 loader group g published, 23-31 acc group g
-  // ready (last = similarity group)
-  uint32_t* trace = (PROF && P.trace && blockIdx.x < kTraceCtas) ? P.trace + blockIdx.x * kTraceTiles * 32 : nullptr;
+  // the first kTraceCtas CTAs (profiles/ws_trace.py); events: 0 build start, 1 build coefficients
+  // ready, 2 build done, 3 mma A ready, 4 + g mma group g committed (g < 10), 14 loader tile start,
+  // 15 + g loader group g issued, 25 + g acc group g ready (lane quarter 0 of the owning parity; the
+  // last group is the similarity group), 35 + g acc F group g released, 45 after the |F|^2 exchange,
+  // 46 pass 1 done, 47 after the sums exchange, 48 pass 2 done, 49 epilogue done (slot released)
+  uint32_t* trace =
+      (PROF && P.trace && blockIdx.x < kTraceCtas) ? P.trace + blockIdx.x * kTraceTiles * kTraceEvents : nullptr;
 #define WS_TRACE(tl, ev)                                                                   \
   do {                                                                                     \
-    if (PROF && trace && (tl) < (uint32_t)kTraceTiles && (ev) < 32)                        \
-      trace[(tl) * 32 + (ev)] = (uint32_t)(clock64() - t_start);                           \
+    if (PROF && trace && (tl) < (uint32_t)kTraceTiles && (ev) < kTraceEvents)              \
+      trace[(tl) * kTraceEvents + (ev)] = (uint32_t)(clock64() - t_start);                 \
   } while (0)
 #define WS_WAIT(bar, par, slot)                    \
   do {                                             \
@@ -294,7 +313,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         }
       }
       asm volatile("bar.sync 3, %0;" ::"n"(kLoadThreads) : "memory");
-      if (tid == 0) WS_TRACE(t_local, 13);
+      if (tid == 0) WS_TRACE(t_local, 14);
       int rc[kRowsPer];
 #pragma unroll
       for (int j = 0; j < kRowsPer; ++j) {
@@ -327,7 +346,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         if constexpr (PROF) {
           wait_cyc[11] += clock64() - tl0;
           if (warp == 0 && lane == 0) {
-            if (pub_group == 0 || pub_group == nch - 1) WS_TRACE(pub_tile, pub_group == 0 ? 14 : 15);
+            if (pub_group % kCG == kCG - 1) WS_TRACE(pub_tile, 15 + pub_group / kCG);
             if (++pub_group == nch) { pub_group = 0; ++pub_tile; }
           }
         }
@@ -392,7 +411,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         }
         __syncwarp();
         if constexpr (PROF) issue_cyc += clock64() - ti0;
-        if (lane == 0 && (c == 0 || c == nch / 2 || c + kCG >= nch)) WS_TRACE(t_local, c == 0 ? 4 : (c + kCG >= nch ? 6 : 5));
+        if (lane == 0) WS_TRACE(t_local, 4 + c / kCG);
         ++dcount;
         stage += kCG;
         if (stage == kStages) { stage = 0; phase ^= 1u; }
@@ -457,6 +476,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         int64_t jr;
         if (cd >= 0 && item_row(P, tile, ntiles, row, jr)) P.vox_list[jr] = (lane == 0 || prev != cd) ? cd : -1;
       }
+      if (bt == 0) WS_TRACE(t_local, 0);
       const int ab = (int)(t_local & 1u);
       uint2* sdesc = S.desc_a[ab];
       if (bt < P.nv) sdesc[bt] = ds_cur;
@@ -650,9 +670,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     const uint32_t t_lane = (uint32_t)(32 * (warp & 3)) << 16;
     const int k0 = half * kHalfK;
     uint32_t dcount = 0, a_tile = 0;
-    float wacc[kHalfK];  // weight totals of this thread's rows (integrate.py:133), all tiles
+    // weight totals (integrate.py:133) of this warp's rows, all tiles: lane l holds materials
+    // k0 + l and k0 + 32 + l (each tile's 32 rows are folded in by a warp reduce-scatter)
+    float wsum[kHalfK / 32];
 #pragma unroll
-    for (int q = 0; q < kHalfK; ++q) wacc[q] = 0.f;
+    for (int q = 0; q < kHalfK / 32; ++q) wsum[q] = 0.f;
     // per-thread integrate partials (<= ~1k tiles per CTA: fp32 accumulation, flushed in fp64)
     float pm_sum = 0.f, pmx = 0.f, pmy = 0.f, pmz = 0.f, featured_n = 0.f, pairs = 0.f;
     const bool outs = P.sims || P.weights;
@@ -684,6 +706,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         if (kt != -1 && valid && half == 0) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(pcur.w);
         continue;
       }
+      if ((warp & 3) == 0 && lane == 0) WS_TRACE(a_tile, 52 + half);
       const int count = (int)rec.z;
       const float invc = count > 0 ? 1.f / (float)count : 0.f;
       const int32_t i = valid ? __float_as_int(pcur.w) : 0;
@@ -693,8 +716,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       for (int c = half; c < nd / kCG; c += 2) {  // c: feature group (kCG chunks)
         const uint32_t gi = dcount + (uint32_t)c;
         const int db = (int)(gi % kDBufs);
+        if ((warp & 3) == 0 && lane == 0 && c < 2) WS_TRACE(a_tile, 50 + c);
         WS_WAIT(&S.d_full[db], (gi / kDBufs) & 1u, 6);
-        if (warp == kAccWarp0 && lane == 0 && (c == 0 || c + 2 >= nd / kCG)) WS_TRACE(a_tile, c == 0 ? 23 : 24);
+        if ((warp & 3) == 0 && lane == 0) WS_TRACE(a_tile, 25 + c);
         tc::fence_after_sync();
 #pragma unroll
         for (int g = 0; g < 2 * kCG; ++g) {  // 32 columns at a time (register budget: wacc stays live)
@@ -704,6 +728,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
             tc::fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.d_empty[db]);  // data is in registers: release the slot
+            if ((warp & 3) == 0 && lane == 0) WS_TRACE(a_tile, 35 + c);
           }
           {
             uint64_t s01 = pk2(ss0, ss1), s23 = pk2(ss2, ss3);
@@ -732,12 +757,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const uint32_t sgi = dcount + (kSGroups == 2 ? (uint32_t)half : 0u);
       const int sslot = (int)(sgi % kDBufs);
       WS_WAIT(&S.d_full[sslot], (sgi / kDBufs) & 1u, 7);
-      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile, 25);
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile, 25 + nd / kCG);
       ++a_tile;
       const uint32_t tS = tbase + (uint32_t)(sslot * kDCols + (kSGroups == 2 ? 0 : k0)) + t_lane;
       tc::fence_after_sync();
       asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
-      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 27);
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 45);
       const float ss = S.xss[0][row] + S.xss[1][row];
       const bool featured = valid && count > 0;
       const float inv = ss > 0.f ? rsqrtf(ss) : 0.f;
@@ -817,14 +842,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       S.xsum[half][4][row] = pl3;
       S.xsum[half][5][row] = pml;
       asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
-      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 28);
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 46);
       const float se_t = S.xsum[0][0][row] + S.xsum[1][0][row];
       if (featured && isnan(se_t)) atomicOr(P.status, 1);  // NaN similarity (grounding.py:173-174)
       const float rs = featured ? 1.f / se_t : 0.f;
-      // normalised weights of this half -> per-thread weight totals (columns >= K are never read):
-      // the exponentials come back from TMEM (stashed by pass 1); with validation outputs / P > 2
-      // S is still in TMEM and they are recomputed
-      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 29);
+      // normalised weights of this half -> the warp's weight totals (columns >= K hold zeros): the
+      // exponentials come back from TMEM (stashed by pass 1); with validation outputs / P > 2 S is
+      // still in TMEM and they are recomputed
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 47);
       const bool stashed = !outs && !p_wide;
       if (stashed) tc::tmem_st_wait();
 #pragma unroll
@@ -842,10 +867,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
             up2(ffma2(pk2(v[q], v[q + 1]), scp2, mp2), x0, x1);
             e = pk2(ex2(x0), ex2(x1));
           }
-          up2(ffma2(e, rsp, pk2(wacc[c0 + q], wacc[c0 + q + 1])), wacc[c0 + q], wacc[c0 + q + 1]);
+          up2(ffma2(e, rsp, 0ull), v[q], v[q + 1]);
         }
+        wsum[c0 / 32] += warp_reduce_scatter32(v, lane);
       }
-      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 30);
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 48);
       if (outs) {  // validation outputs (similarities, softmax weights), caller's order
         for (int c0 = 0; c0 < kHalfK; c0 += 32) {
           float v[32];
@@ -866,7 +892,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");  // both halves read the group
         if (lane == 0 && half == 0) mbar_arrive(&S.d_empty[sslot]);
       }
-      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 26);
+      if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 49);
+      if (warp == kAccWarp0 + 4 && lane == 0) WS_TRACE(a_tile - 1, 54);
       dcount += (uint32_t)kSGroups;
       if (valid && half == 0) {
         float prop[4];
@@ -877,9 +904,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         *(reinterpret_cast<float4*>(P.srec + jpt) + 1) = make_float4(prop[0], prop[1], prop[2], prop[3]);
         if (P.grid_partials) {
           const int32_t code = (int32_t)rec.w;
-          float rho = prop[0];
-#pragma unroll
-          for (int pp = 1; pp < 4; ++pp) rho = P.density_col == pp ? prop[pp] : rho;
+          const int dc = P.density_col;  // selects, not a dynamic index (keeps prop[] in registers)
+          const float rho = dc == 0 ? prop[0] : (dc == 1 ? prop[1] : (dc == 2 ? prop[2] : prop[3]));
           atomicAdd(P.grid_partials + code, rho);
           atomicAdd(P.grid_partials + P.cells3 + code, 1.0f);
         }
@@ -893,9 +919,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     }
     // flush this CTA's partials (integrate.py:133-155) once
 #pragma unroll
-    for (int q = 0; q < kHalfK; ++q) {
-      const float s = warp_sum(wacc[q]);
-      if (lane == 0 && k0 + q < P.k && s != 0.f) atomicAdd(&S.red[k0 + q], (double)s);
+    for (int q = 0; q < kHalfK / 32; ++q) {
+      const int k = k0 + 32 * q + lane;
+      if (k < P.k && wsum[q] != 0.f) atomicAdd(&S.red[k], (double)wsum[q]);
     }
     double r6[6] = {pm_sum, pmx, pmy, pmz, featured_n, pairs};  // fp64 from here on
 #pragma unroll
@@ -965,8 +991,8 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
   static uint32_t* trace = nullptr;
   const char* trace_path = getenv("PF_WS_TRACE");
   if (debug && trace_path) {
-    if (!trace) cudaMalloc(&trace, sizeof(uint32_t) * kTraceCtas * kTraceTiles * 32);
-    cudaMemsetAsync(trace, 0xff, sizeof(uint32_t) * kTraceCtas * kTraceTiles * 32, st);
+    if (!trace) cudaMalloc(&trace, sizeof(uint32_t) * kTraceCtas * kTraceTiles * kTraceEvents);
+    cudaMemsetAsync(trace, 0xff, sizeof(uint32_t) * kTraceCtas * kTraceTiles * kTraceEvents, st);
     Q.trace = trace;
   }
   if (debug) k_tile_ws<true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
@@ -987,7 +1013,7 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
     }
     fprintf(stderr, "\n");
     if (trace_path) {
-      static uint32_t ht[kTraceCtas * kTraceTiles * 32];
+      static uint32_t ht[kTraceCtas * kTraceTiles * kTraceEvents];
       cudaMemcpy(ht, trace, sizeof(ht), cudaMemcpyDeviceToHost);
       if (FILE* f = fopen(trace_path, "wb")) {
         fwrite(ht, sizeof(ht), 1, f);
