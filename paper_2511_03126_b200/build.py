@@ -21,7 +21,7 @@ LIB = OUT_DIR / "libpropfield_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v", f"-I{ROOT / 'include'}"]
+         "-Xptxas", "-v", f"-I{ROOT / 'include'}", *os.environ.get("PF_NVCC_EXTRA", "").split()]
 
 
 def _sources():

@@ -91,7 +91,7 @@ struct WsShared {
   int4 vwin[2][kMaxViewsTC];        // builders: window x0, y0, w, h per rank
   float bbox[2][4][6];              // builders: per lane group box of the tile's points
   float4 yp[kMaxKpadTC];         // per material pair (k, k+1), at k/2: {y0 y0' y1 y1'} then {mt mt' b b'}
-  float4 yv2[kMaxKpadTC];        // per material: {y2, y3, 0, 0} (P > 2)
+  float2 yv2[kMaxKpadTC];        // per material: {y2, y3} (P > 2)
   float xss[2][kTile];           // accumulator halves: partial |F|^2
   float xm[2][kTile];            //                     partial max (large 1/T only)
   float xsum[2][6][kTile];       //                     partial softmax sums
@@ -139,6 +139,11 @@ __device__ __forceinline__ uint16_t f2bf16(float f) {
 __device__ __forceinline__ uint4 ld_pref_u4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ld_pref_u2(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
   return r;
 }
 __device__ __forceinline__ float4 ld_pref_f4(const void* p) {
@@ -244,7 +249,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     float y[4];
 #pragma unroll
     for (int pp = 0; pp < 4; ++pp) y[pp] = (pp < P.p && j < P.k) ? P.values[j * P.p + pp] : 0.f;
-    S.yv2[j] = make_float4(y[2], y[3], 0.f, 0.f);
+    S.yv2[j] = make_float2(y[2], y[3]);
   }
   for (int j = tid; j < kMaxKpadTC / 2; j += kWsThreads) {
     auto val = [&](int kk, int pp) { return (kk < P.k && pp < P.p) ? P.values[kk * P.p + pp] : 0.f; };
@@ -680,24 +685,24 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     const bool outs = P.sims || P.weights;
     const bool p_wide = P.p > 2;
     int kt_nx = kt_at(P, blockIdx.x, nitems);
-    uint4 rec_nx = make_uint4(0u, 0u, 0u, 0u);
+    uint2 rec_nx = make_uint2(0u, 0u);  // record words 2, 3: visible-view count, voxel code
     float4 p_nx = make_float4(0.f, 0.f, 0.f, 0.f);
     int64_t j_nx = 0;
     bool v_nx = blockIdx.x < nitems && item_row(P, blockIdx.x, ntiles, row, j_nx);
     if (v_nx) {
-      rec_nx = ld_pref_u4(P.srec + j_nx);
+      rec_nx = ld_pref_u2(reinterpret_cast<const uint32_t*>(P.srec + j_nx) + 2);
       p_nx = ld_pref_f4(P.spts + j_nx);
     }
     for (int64_t tile = blockIdx.x; tile < nitems; tile += gridDim.x) {
       const int kt = kt_nx;
-      const uint4 rec = rec_nx;
+      const uint2 rec = rec_nx;
       const float4 pcur = p_nx;
       const int64_t jpt = j_nx;
       const bool valid = v_nx;
       kt_nx = kt_at(P, tile + gridDim.x, nitems);
       v_nx = tile + gridDim.x < nitems && item_row(P, tile + gridDim.x, ntiles, row, j_nx);
       if (v_nx) {
-        rec_nx = ld_pref_u4(P.srec + j_nx);
+        rec_nx = ld_pref_u2(reinterpret_cast<const uint32_t*>(P.srec + j_nx) + 2);
         p_nx = ld_pref_f4(P.spts + j_nx);
       }
       bool ok;
@@ -707,7 +712,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         continue;
       }
       if ((warp & 3) == 0 && lane == 0) WS_TRACE(a_tile, 52 + half);
-      const int count = (int)rec.z;
+      const int count = (int)rec.x;
       const float invc = count > 0 ? 1.f / (float)count : 0.f;
       const int32_t i = valid ? __float_as_int(pcur.w) : 0;
       float ss0 = 0.f, ss1 = 0.f, ss2 = 0.f, ss3 = 0.f;
@@ -761,12 +766,28 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       ++a_tile;
       const uint32_t tS = tbase + (uint32_t)(sslot * kDCols + (kSGroups == 2 ? 0 : k0)) + t_lane;
       tc::fence_after_sync();
-      asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
+      // this half's 64 similarity columns -> registers, then the slot goes straight back to the MMA
+      // warp (it moves on to the next tile's feature groups while this epilogue runs)
+      float v[kHalfK];
+      static_assert(kHalfK == 64, "one tcgen05.ld.x64 per half");
+      tc::tmem_ld64(tS, v);
+      tc::fence_before_sync();
+      asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");  // |F|^2 halves + S reads done
+      if (kSGroups == 2) {
+        if (lane == 0) mbar_arrive(&S.d_empty[sslot]);  // similarity group h: read by half h only
+      } else if (lane == 0 && half == 0) {
+        mbar_arrive(&S.d_empty[sslot]);  // both halves have read the group
+      }
       if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 45);
       const float ss = S.xss[0][row] + S.xss[1][row];
       const bool featured = valid && count > 0;
       const float inv = ss > 0.f ? rsqrtf(ss) : 0.f;
       const float sc = inv * P.inv_temp * 1.4426950408889634f;  // log2(e) / (T |F|)
+      if (outs && P.sims && valid) {  // validation output: cosine similarities, caller's order
+#pragma unroll
+        for (int q = 0; q < kHalfK; ++q)
+          if (k0 + q < P.k) P.sims[(int64_t)i * P.k + k0 + q] = featured ? v[q] * inv : 0.f;
+      }
       // |s| <= 1 (cosines), so exp(s / T) cannot overflow for T >= ~0.013 and the row max of the
       // reference's stable softmax (grounding.py:175-177) only changes rounding; below that the
       // max is subtracted as in the reference (host sets need_max).
@@ -774,55 +795,45 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       if (need_max) {
         float mx = -INFINITY;
 #pragma unroll
-        for (int c0 = 0; c0 < kHalfK; c0 += 32) {
-          float v[32];
-          tc::tmem_ld32(tS + (uint32_t)c0, v);
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const float4 yb = S.yp[2 * ((k0 + c0 + q) >> 1) + 1];
-            mx = fmaxf(mx, fmaf(v[q], sc, (q & 1) ? yb.w : yb.z));
-          }
+        for (int q = 0; q < kHalfK; ++q) {
+          const float4 yb = S.yp[2 * ((k0 + q) >> 1) + 1];
+          mx = fmaxf(mx, fmaf(v[q], sc, (q & 1) ? yb.w : yb.z));
         }
         S.xm[half][row] = mx;
         asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
         m2 = fmaxf(S.xm[0][row], S.xm[1][row]);
         if (!(m2 > -INFINITY)) m2 = 0.f;
       }
-      float se = 0.f, pl0 = 0.f, pl1 = 0.f, pl2 = 0.f, pl3 = 0.f, pml = 0.f;
+      // pass 1, material pairs (k, k+1): exponentials (in place of S), their sum and the regressions
+      float se, pl0, pl1, pl2 = 0.f, pl3 = 0.f, pml;
       {
-        // material pairs (k, k+1): FFMA2 for the exponent, sums and regressions
         uint64_t sep = 0ull, p0p = 0ull, p1p = 0ull, pmp = 0ull;  // (+0.f, +0.f)
         const uint64_t scp = pk2(sc, sc);
 #pragma unroll
-        for (int c0 = 0; c0 < kHalfK; c0 += 32) {
-          float v[32];
-          tc::tmem_ld32(tS + (uint32_t)c0, v);
+        for (int q = 0; q < kHalfK; q += 2) {
+          // table reads are not hoisted past this point (8 pairs at a time): holding the whole
+          // table in registers on top of the 64 S values would push loop state into local memory
+          if ((q & 15) == 0) asm volatile("" ::: "memory");
+          const int kp = (k0 + q) >> 1;
+          const float4 ya = S.yp[2 * kp], yb = S.yp[2 * kp + 1];
+          float x0, x1;
+          up2(ffma2(pk2(v[q], v[q + 1]), scp, pk2(yb.z - m2, yb.w - m2)), x0, x1);  // padding: -inf
+          const float e0 = ex2(x0), e1 = ex2(x1);
+          const uint64_t e = pk2(e0, e1);
+          sep = fadd2(sep, e);
+          p0p = ffma2(e, pk2(ya.x, ya.y), p0p);
+          p1p = ffma2(e, pk2(ya.z, ya.w), p1p);
+          pmp = ffma2(e, pk2(yb.x, yb.y), pmp);
+          v[q] = e0;
+          v[q + 1] = e1;
+        }
+        if (p_wide) {  // regressions 2, 3 (P > 2) from the exponentials, outside the hot loop
 #pragma unroll
-          for (int q = 0; q < 32; q += 2) {
-            const int kp = (k0 + c0 + q) >> 1;
-            const float4 ya = S.yp[2 * kp], yb = S.yp[2 * kp + 1];
-            float x0, x1;
-            up2(ffma2(pk2(v[q], v[q + 1]), scp, pk2(yb.z - m2, yb.w - m2)), x0, x1);  // padding: -inf
-            const float e0 = ex2(x0), e1 = ex2(x1);
-            const uint64_t e = pk2(e0, e1);
-            sep = fadd2(sep, e);
-            p0p = ffma2(e, pk2(ya.x, ya.y), p0p);
-            p1p = ffma2(e, pk2(ya.z, ya.w), p1p);
-            pmp = ffma2(e, pk2(yb.x, yb.y), pmp);
-            if (!outs && !p_wide) {  // stash the exponentials in place of S for the weight totals
-              v[q] = e0;
-              v[q + 1] = e1;
-            }
-          }
-          if (!outs && !p_wide) tc::tmem_st32(tS + (uint32_t)c0, v);
-          if (p_wide) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              const float4 yb = S.yp[2 * ((k0 + c0 + q) >> 1) + 1], y2 = S.yv2[k0 + c0 + q];
-              const float e = ex2(fmaf(v[q], sc, ((q & 1) ? yb.w : yb.z) - m2));
-              pl2 = fmaf(e, y2.x, pl2);
-              pl3 = fmaf(e, y2.y, pl3);
-            }
+          for (int q = 0; q < kHalfK; ++q) {
+            if ((q & 7) == 0) asm volatile("" ::: "memory");  // table reads not hoisted (registers)
+            const float2 y2 = S.yv2[k0 + q];
+            pl2 = fmaf(v[q], y2.x, pl2);
+            pl3 = fmaf(v[q], y2.y, pl3);
           }
         }
         float a, b;
@@ -846,52 +857,22 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const float se_t = S.xsum[0][0][row] + S.xsum[1][0][row];
       if (featured && isnan(se_t)) atomicOr(P.status, 1);  // NaN similarity (grounding.py:173-174)
       const float rs = featured ? 1.f / se_t : 0.f;
-      // normalised weights of this half -> the warp's weight totals (columns >= K hold zeros): the
-      // exponentials come back from TMEM (stashed by pass 1); with validation outputs / P > 2 S is
-      // still in TMEM and they are recomputed
       if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 47);
-      const bool stashed = !outs && !p_wide;
-      if (stashed) tc::tmem_st_wait();
+      // pass 2: normalised weights of this half -> the warp's weight totals (materials >= K have
+      // zero exponentials)
+      {
+        const uint64_t rsp = pk2(rs, rs);
 #pragma unroll
-      for (int c0 = 0; c0 < kHalfK; c0 += 32) {
-        float v[32];
-        tc::tmem_ld32(tS + (uint32_t)c0, v);
-        const uint64_t scp2 = pk2(sc, sc), mp2 = pk2(-m2, -m2), rsp = pk2(rs, rs);
-#pragma unroll
-        for (int q = 0; q < 32; q += 2) {
-          uint64_t e;
-          if (stashed) {
-            e = pk2(v[q], v[q + 1]);
-          } else {
-            float x0, x1;
-            up2(ffma2(pk2(v[q], v[q + 1]), scp2, mp2), x0, x1);
-            e = pk2(ex2(x0), ex2(x1));
-          }
-          up2(ffma2(e, rsp, 0ull), v[q], v[q + 1]);
-        }
-        wsum[c0 / 32] += warp_reduce_scatter32(v, lane);
+        for (int q = 0; q < kHalfK; q += 2) up2(ffma2(pk2(v[q], v[q + 1]), rsp, 0ull), v[q], v[q + 1]);
       }
+      if (outs && P.weights && valid) {  // validation output: softmax weights, caller's order
+#pragma unroll
+        for (int q = 0; q < kHalfK; ++q)
+          if (k0 + q < P.k) P.weights[(int64_t)i * P.k + k0 + q] = v[q];
+      }
+#pragma unroll
+      for (int c = 0; c < kHalfK / 32; ++c) wsum[c] += warp_reduce_scatter32(*reinterpret_cast<float(*)[32]>(v + 32 * c), lane);
       if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 48);
-      if (outs) {  // validation outputs (similarities, softmax weights), caller's order
-        for (int c0 = 0; c0 < kHalfK; c0 += 32) {
-          float v[32];
-          tc::tmem_ld32(tS + (uint32_t)c0, v);  // warp-collective: every lane, valid or not
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            if (!valid || k0 + c0 + q >= P.k) continue;
-            if (P.sims) P.sims[(int64_t)i * P.k + k0 + c0 + q] = featured ? v[q] * inv : 0.f;
-            if (P.weights) P.weights[(int64_t)i * P.k + k0 + c0 + q] = ex2(fmaf(v[q], sc, -m2)) * rs;
-          }
-        }
-      }
-      tc::fence_before_sync();
-      __syncwarp();
-      if (kSGroups == 2) {
-        if (lane == 0) mbar_arrive(&S.d_empty[sslot]);  // similarity group h: read by half h only
-      } else {
-        asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");  // both halves read the group
-        if (lane == 0 && half == 0) mbar_arrive(&S.d_empty[sslot]);
-      }
       if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 49);
       if (warp == kAccWarp0 + 4 && lane == 0) WS_TRACE(a_tile - 1, 54);
       dcount += (uint32_t)kSGroups;
@@ -903,7 +884,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         const float4 p = pcur;
         *(reinterpret_cast<float4*>(P.srec + jpt) + 1) = make_float4(prop[0], prop[1], prop[2], prop[3]);
         if (P.grid_partials) {
-          const int32_t code = (int32_t)rec.w;
+          const int32_t code = (int32_t)rec.y;
           const int dc = P.density_col;  // selects, not a dynamic index (keeps prop[] in registers)
           const float rho = dc == 0 ? prop[0] : (dc == 1 ? prop[1] : (dc == 2 ? prop[2] : prop[3]));
           atomicAdd(P.grid_partials + code, rho);
