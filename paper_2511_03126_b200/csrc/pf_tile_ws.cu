@@ -23,6 +23,7 @@
 //               one of two TMEM A buffers with tcgen05.st (warp 16 + j: lane quarter j & 3, views of
 //               rank parity j >> 2) while the current tile's MMAs run.
 // Synchronisation is mbarrier-only (full/empty pairs for A, B stages and TMEM accumulator slots).
+#include <type_traits>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -603,7 +604,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       // windows with sides in {2, 3} (~99.5% of them at C5): the row's weights are separable,
       // vx (over the window's columns) x vy (over its rows); clamping into the window reproduces the
       // reference taps (an exact tap can never leave the window; an expanded one only with ~0 weight)
-      auto small = [&](int v, int base, int ww, int wh, float fu_rel, float fv_rel) {
+      auto small = [&](auto WWc, auto WHc, int v, int base, float fu_rel, float fv_rel) {
+        constexpr int ww = decltype(WWc)::value, wh = decltype(WHc)::value;
         const bool vis = (((v < 32 ? mw.x : mw.y) >> (v & 31)) & 1u) != 0u;
         const float xr = fminf(fmaxf(fu_rel, 0.f), (float)(ww - 1)), yr = fminf(fmaxf(fv_rel, 0.f), (float)(wh - 1));
         const float ixf = fminf(floorf(xr), (float)(ww - 2)), iyf = fminf(floorf(yr), (float)(wh - 2));
@@ -618,12 +620,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           const __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
           return *reinterpret_cast<const uint32_t*>(&b2);
         };
-        if (ww == 2 && wh == 2) {
+        if constexpr (ww == 2 && wh == 2) {
           tc::tmem_st_x2(col0, pk(vy0 * vx0, vy0 * vx1), pk(vy1 * vx0, vy1 * vx1));
-        } else if (ww == 3 && wh == 2) {  // taps r0: 0 1 2, r1: 3 4 5
+        } else if constexpr (ww == 3 && wh == 2) {  // taps r0: 0 1 2, r1: 3 4 5
           tc::tmem_st_x2(col0, pk(vy0 * vx0, vy0 * vx1), pk(vy0 * vx2, vy1 * vx0));
           tc::tmem_st_x1(col0 + 2u, pk(vy1 * vx1, vy1 * vx2));
-        } else if (ww == 2 && wh == 3) {  // taps r0: 0 1, r1: 2 3, r2: 4 5
+        } else if constexpr (ww == 2 && wh == 3) {  // taps r0: 0 1, r1: 2 3, r2: 4 5
           tc::tmem_st_x2(col0, pk(vy0 * vx0, vy0 * vx1), pk(vy1 * vx0, vy1 * vx1));
           tc::tmem_st_x1(col0 + 2u, pk(vy2 * vx0, vy2 * vx1));
         } else {  // 3 x 3: taps 0..8 + one padding tap
@@ -632,27 +634,57 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           tc::tmem_st_x1(col0 + 4u, pk(vy2 * vx2, 0.f));
         }
       };
-      for (int rk = bh; rk < nvp; rk += 2) {
+      // rank rk: view, window base and the row's coordinates relative to the window origin
+      auto coords = [&](int rk, int& v, int& base, float& fu_rel, float& fv_rel) {
         const int vb = S.vrank[ab][rk];
-        const int v = vb & 0xff, base = vb >> 8;
-        const int4 wn = S.vwin[ab][rk];
-        if (wn.z < 2 || wn.z > 3 || wn.w < 2 || wn.w > 3) {
-          unit_general(rk);
-          continue;
-        }
-        float fu_rel, fv_rel;
+        v = vb & 0xff;
+        base = vb >> 8;
         if (!exact) {
           const float4 A0 = S.vcoef[ab][rk][0], A1 = S.vcoef[ab][rk][1];
           fu_rel = fmaf(A0.w, dzp, fmaf(A0.z, dyp, fmaf(A0.y, dxp, A0.x)));
           fv_rel = fmaf(A1.w, dzp, fmaf(A1.z, dyp, fmaf(A1.y, dxp, A1.x)));
         } else {
+          const int4 wn = S.vwin[ab][rk];
           const ProjF pr = project_f32(S.sv[v], p.x, p.y, p.z);
           const TapF tf = taps_f32(S.sv[v], pr.u, pr.v);
           fu_rel = (float)(tf.x0 - wn.x) + tf.wx;
           fv_rel = (float)(tf.y0 - wn.y) + tf.wy;
         }
-        small(v, base, wn.z, wn.w, fu_rel, fv_rel);
+      };
+      // this warp's ranks (bh, bh + 2, ...) grouped by window shape (lane l <-> rank bh + 2 l); two
+      // units of one shape are built together: independent chains the scheduler interleaves
+      int cls = -1;
+      if (lane < ((nvp - bh + 1) >> 1)) {
+        const int4 wn = S.vwin[ab][bh + 2 * lane];
+        cls = (wn.z == 2 && wn.w == 2)   ? 0
+              : (wn.z == 3 && wn.w == 2) ? 1
+              : (wn.z == 2 && wn.w == 3) ? 2
+              : (wn.z == 3 && wn.w == 3) ? 3
+                                         : 4;
       }
+      auto run = [&](uint32_t m, auto WWc, auto WHc) {
+        while (m) {  // warp-uniform
+          int v1, b1, v2, b2;
+          float u1, w1, u2, w2;
+          coords(bh + 2 * (__ffs(m) - 1), v1, b1, u1, w1);
+          m &= m - 1;
+          if (m) {
+            coords(bh + 2 * (__ffs(m) - 1), v2, b2, u2, w2);
+            m &= m - 1;
+            small(WWc, WHc, v1, b1, u1, w1);
+            small(WWc, WHc, v2, b2, u2, w2);
+          } else {
+            small(WWc, WHc, v1, b1, u1, w1);
+          }
+        }
+      };
+      using I2 = std::integral_constant<int, 2>;
+      using I3 = std::integral_constant<int, 3>;
+      run(__ballot_sync(0xffffffffu, cls == 0), I2{}, I2{});
+      run(__ballot_sync(0xffffffffu, cls == 1), I3{}, I2{});
+      run(__ballot_sync(0xffffffffu, cls == 2), I2{}, I3{});
+      run(__ballot_sync(0xffffffffu, cls == 3), I3{}, I3{});
+      for (uint32_t m = __ballot_sync(0xffffffffu, cls == 4); m; m &= m - 1) unit_general(bh + 2 * (__ffs(m) - 1));
       if (bh == 0)  // columns past the last window (K padding to 16) must be zero too
         for (int j = kt >> 1; j < (ktp >> 1); ++j) tc::tmem_st_x1(tAb + (uint32_t)j, 0u);
       const long long tb2 = WS_CLOCK();
