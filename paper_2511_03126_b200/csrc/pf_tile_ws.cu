@@ -195,7 +195,9 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-template <bool PROF>
+// PROF: wait accounting + trace (PF_WS_DEBUG); OUTS: validation outputs (features, similarities,
+// softmax weights) -- a separate instantiation keeps their fully unrolled stores out of the hot code
+template <bool PROF, bool OUTS>
 __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant__ TileParams P, int need_max) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -714,7 +716,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     for (int q = 0; q < kHalfK / 32; ++q) wsum[q] = 0.f;
     // per-thread integrate partials (<= ~1k tiles per CTA: fp32 accumulation, flushed in fp64)
     float pm_sum = 0.f, pmx = 0.f, pmy = 0.f, pmz = 0.f, featured_n = 0.f, pairs = 0.f;
-    const bool outs = P.sims || P.weights;
+    const bool outs = OUTS && (P.sims || P.weights);
     const bool p_wide = P.p > 2;
     int kt_nx = kt_at(P, blockIdx.x, nitems);
     uint2 rec_nx = make_uint2(0u, 0u);  // record words 2, 3: visible-view count, voxel code
@@ -778,7 +780,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
             up2(s01, ss0, ss1);
             up2(s23, ss2, ss3);
           }
-          if (P.features && valid) {
+          if (OUTS && P.features && valid) {
             float* dst = P.features + (int64_t)i * P.d + c * kDCols + 32 * g;
 #pragma unroll
             for (int q = 0; q < 32; q += 4)
@@ -986,8 +988,10 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = ws_smem_bytes();
-  cudaFuncSetAttribute(k_tile_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k_tile_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = (P.n + kTile - 1) / kTile;  // (+ sub-tiles, known on the device only)
   int grid = (int)(ntiles < sms ? ntiles : sms);
   if (const char* g = getenv("PF_WS_GRID")) grid = (int)(ntiles < atoi(g) ? ntiles : atoi(g));  // debug knob
@@ -1008,8 +1012,11 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
     cudaMemsetAsync(trace, 0xff, sizeof(uint32_t) * kTraceCtas * kTraceTiles * kTraceEvents, st);
     Q.trace = trace;
   }
-  if (debug) k_tile_ws<true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
-  else k_tile_ws<false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+  const bool outs = P.sims || P.weights || P.features;
+  if (debug && outs) k_tile_ws<true, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+  else if (debug) k_tile_ws<true, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+  else if (outs) k_tile_ws<false, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+  else k_tile_ws<false, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
   const int rc = check_launch("tile_ws");
   if (debug && rc == PF_OK) {
     static unsigned long long h[16 * 1024];
