@@ -8,7 +8,7 @@ cfg=${1:-c5}
 out=gpurun_out
 mkdir -p $out
 args="--config $cfg --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_[a-z]+" -c 400 --csv \
   --log-file $out/launches_$cfg.csv python bench.py $args > $out/ncu_launch_$cfg.log 2>&1
 for k in k_tile_ws k_tile_prep; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
