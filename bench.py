@@ -199,7 +199,7 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=dev)
     import paper_2511_03126_b200 as pf
     from paper_2511_03126_b200 import _lib, workloads
-    from paper_2511_03126_b200.dist import global_bbox, shard_range
+    from paper_2511_03126_b200.dist import shard_range
 
     wl = workloads.generate(cfg, device_splat=True)
     n_total = cfg.n
@@ -218,31 +218,41 @@ def run_ours(args, cfg):
     pts_host = np.ascontiguousarray(wl.points[lo:hi])
     pts = torch.from_numpy(pts_host).to(dev)
     n = pts.shape[0]
-    bufs = pf.FuseBuffers(n, views, tables, cfg.grid, device=dev)
     stream = torch.cuda.current_stream()
+    if world > 1:
+        # cell-range sharding (dist.cell_sharded_steps): points routed to the rank owning their
+        # voxel, so only a 1 MB histogram and K + 8 doubles are all-reduced (no dense voxel grid)
+        from paper_2511_03126_b200.dist import DeviceShardOps, cell_sharded_steps, run_dist
 
-    def step(ev=None):
-        bufs.reset()
-        if world > 1:
-            _lib.call("pf_bbox", pts.data_ptr(), n, bufs.lo_hi.data_ptr(), stream.cuda_stream)
-            global_bbox(bufs.lo_hi)
-            lohi = bufs.lo_hi
-        else:
-            lohi = None
-        if ev:
-            ev[0].record(stream)
-        pf.fuse_prepare(views, tables, bufs)
-        if ev:
-            ev[1].record(stream)
-        res = pf.fuse_and_query(pts, views, tables, temperature=cfg.temperature, epsilon=cfg.eps,
-                                grid=cfg.grid, lo_hi=lohi, buffers=bufs, reduce=False,
-                                prepared=True, force_simt=args.force_simt, reset=False)
-        if ev:
-            ev[2].record(stream)
-        if world > 1:
-            res.allreduce()
-        res.finalize()
-        return res
+        bufs = None
+        shard_ops = DeviceShardOps(views, tables, temperature=cfg.temperature, epsilon=cfg.eps, grid=cfg.grid)
+        nwords = (nv + 31) // 32
+
+        def step(ev=None):
+            if ev:
+                ev[0].record(stream)
+                ev[1].record(stream)
+            res = run_dist(cell_sharded_steps(pts, rank, world, shard_ops, k=tables.k, p=tables.p, nwords=nwords))
+            if ev:
+                ev[2].record(stream)
+            return res
+    else:
+        bufs = pf.FuseBuffers(n, views, tables, cfg.grid, device=dev)
+
+        def step(ev=None):
+            bufs.reset()
+            if ev:
+                ev[0].record(stream)
+            pf.fuse_prepare(views, tables, bufs)
+            if ev:
+                ev[1].record(stream)
+            res = pf.fuse_and_query(pts, views, tables, temperature=cfg.temperature, epsilon=cfg.eps,
+                                    grid=cfg.grid, buffers=bufs, reduce=False,
+                                    prepared=True, force_simt=args.force_simt, reset=False)
+            if ev:
+                ev[2].record(stream)
+            res.finalize()
+            return res
 
     inputs_bytes = (pts.numel() * 4 + depth_dev.numel() * 4 + fmap_dev.numel() * fmap_dev.element_size())
     flush = inputs_bytes < 2 * L2_BYTES
@@ -307,6 +317,8 @@ def run_ours(args, cfg):
         from paper_2511_03126_b200.stream import FusePipeline, HostObject
 
         del bufs  # the pipeline holds its own two slots
+        if world > 1:
+            del shard_ops
         torch.cuda.empty_cache()
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
         obj = HostObject(
@@ -317,7 +329,8 @@ def run_ours(args, cfg):
             text=pin(wl.text), values=pin(wl.values.astype(np.float32)),
             mid_theta=pin(wl.mid_theta.astype(np.float32)))
         pipe = FusePipeline(n, nv, (cfg.image, cfg.image), cfg.fmap, bf16=cfg.bf16, k=cfg.k, p=tables.p,
-                            grid=cfg.grid, temperature=cfg.temperature, epsilon=cfg.eps, device=dev)
+                            grid=cfg.grid, temperature=cfg.temperature, epsilon=cfg.eps, device=dev,
+                            sharded=world > 1)
         for _ in pipe.run([obj] * max(3, args.warmup)):
             pass
         torch.cuda.synchronize()
@@ -335,7 +348,7 @@ def run_ours(args, cfg):
         e2e = {"value": n_total * nv / (t_e2e * 1e-3), "unit": "samples/s", "ms_per_step": t_e2e,
                "h2d_bytes_per_step": int(pipe.h2d_bytes), "d2h_bytes_per_step": int(pipe.d2h_bytes),
                "api": "paper_2511_03126_b200.stream.FusePipeline (copies of neighbouring objects overlap compute)",
-               "mass_kg_last": masses[-1] if world == 1 else None}
+               "mass_kg_last": masses[-1]}
 
     if rank != 0:
         return
@@ -389,7 +402,8 @@ def run_ours(args, cfg):
         "vs_baseline": None,
         "dtype": "bf16" if tile_path else "f32",
         "data": "synthetic",
-        "config": {**config_desc(cfg), "parallelism": f"point-range x{world}",
+        "config": {**config_desc(cfg), "parallelism": (f"cell-range x{world} (points routed to voxel owners)"
+                                                       if world > 1 else "single GPU"),
                    "l2": ("inputs larger than L2" if not flush else "L2 flushed between steps")},
         "stages_ms": {"fuse_query": t_kern, **{k: v for k, v in stage_avg.items()},
                       "prepare_G": sum(prep_ms) / args.steps,
@@ -398,7 +412,7 @@ def run_ours(args, cfg):
         "gpu_launches": int(launches),
         "clocks": clocks,
         "result": {"mass_kg": mass, "featured": part["featured"], "visible_pairs": vis_pairs,
-                   "visible_fraction": vis_pairs / (n * nv)},
+                   "visible_fraction": vis_pairs / (n_total * nv)},
     }
     if e2e:
         line["e2e"] = e2e

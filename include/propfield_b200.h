@@ -228,6 +228,36 @@ int pf_fuse_prepare(const pf_fuse_args_t* args, void* stream);
 int pf_fuse_query(const pf_fuse_args_t* args, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * Cell-range sharding of one object across ranks (SURVEY §8e "shard by voxel-code ranges after a
+ * pre-sort"; replaces the dense voxel all-reduce of point-range sharding, pipeline.py:304-312 /
+ * integrate.py:133-155 are the per-object reductions it feeds). csrc/pf_shard.cu describes the
+ * protocol; the collectives between the calls belong to the caller (dist.py: NCCL or in-process).
+ * ------------------------------------------------------------------------------------------- */
+
+/* Number of histogram bins (64^3 cells) used by pf_shard_keys / pf_shard_cuts. */
+int32_t pf_shard_bins(void);
+/* keys[i] = Hilbert index of the 64^3 cell enclosing point i's voxel (voxel code of the fused path,
+ * cell_a = code_a * 64 / g); hist[key] += 1 (hist: pf_shard_bins() u32, zeroed by the caller). */
+int pf_shard_keys(const float* points, int64_t n, const double* lo_hi, int32_t g, uint32_t* keys, uint32_t* hist,
+                  void* stream);
+/* cuts (world + 1) u32: rank r owns cells [cuts[r], cuts[r+1]) — balanced split of the GLOBAL
+ * (all-reduced) histogram along the curve. world in [1, 64]. */
+int pf_shard_cuts(const uint32_t* hist, int32_t world, uint32_t* cuts, void* stream);
+/* Group the local points by owner: counts (world) i32, cursor (world) i32 scratch, send (n) float4
+ * {x, y, z, local index bits}, destination blocks contiguous in rank order. */
+int pf_shard_pack(const float* points, int64_t n, const uint32_t* keys, const uint32_t* cuts, int32_t world,
+                  int32_t* counts, int32_t* cursor, void* send, void* stream);
+/* Received float4 points -> (n, 3) f32. */
+int pf_shard_xyz(const void* recv, int64_t n, float* xyz, void* stream);
+/* Per-point results -> int32 rows [props (p, f32 bits) | count | code | mask (nwords)]. */
+int pf_shard_pack_results(int64_t n, int32_t p, int32_t nwords, const float* props, const int32_t* counts,
+                          const int32_t* codes, const int32_t* mask, int32_t* rows, void* stream);
+/* Returned rows (in the order the points were sent) -> caller-order outputs, by the local index each
+ * sent float4 carried. */
+int pf_shard_unpack_results(int64_t n, int32_t p, int32_t nwords, const int32_t* rows, const void* sent,
+                            float* props, int32_t* counts, int32_t* codes, int32_t* mask, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
  * Diagnostics (no reference twin).
  * ------------------------------------------------------------------------------------------- */
 

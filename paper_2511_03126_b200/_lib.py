@@ -120,6 +120,13 @@ SIGNATURES = {
     "pf_knn_workspace_bytes": ([_I64], C.c_uint64),
     "pf_knn_kth_distance": ([_P, _I64, _I32, _P, _P, _P, _P], C.c_int),
     "pf_integrate_partials": ([_P, _I64, _I32, _P, _P, _P, _P, _P, _P], C.c_int),
+    "pf_shard_bins": ([], C.c_int32),
+    "pf_shard_keys": ([_P, _I64, _P, _I32, _P, _P, _P], C.c_int),
+    "pf_shard_cuts": ([_P, _I32, _P, _P], C.c_int),
+    "pf_shard_pack": ([_P, _I64, _P, _P, _I32, _P, _P, _P, _P], C.c_int),
+    "pf_shard_xyz": ([_P, _I64, _P, _P], C.c_int),
+    "pf_shard_pack_results": ([_I64, _I32, _I32, _P, _P, _P, _P, _P, _P], C.c_int),
+    "pf_shard_unpack_results": ([_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P], C.c_int),
     "pf_bench_umma": ([_I32, _I32, _I32, _I32, _P, _P], C.c_int),
     "pf_bench_gather": ([_P, _I32, _I32, _I32, _P, _P], C.c_int),
     "pf_stage_times": ([_P, _I32], C.c_int),

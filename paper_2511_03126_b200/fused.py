@@ -157,6 +157,7 @@ class FusedResult:
     sims = property(lambda self: self.buffers.sims)
     weights = property(lambda self: self.buffers.weights)
     lo_hi = property(lambda self: self.buffers.lo_hi)
+    mass = property(lambda self: self.buffers.mass)  # (2,) f64 {mass_kg, occupied voxels} after finalize()
 
     def visibility(self):
         """Unpack the bitset to (N, V) bool (validation helper)."""

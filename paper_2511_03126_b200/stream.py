@@ -45,7 +45,11 @@ class StreamResult:
 
 class FusePipeline:
     def __init__(self, n: int, nviews: int, image_hw, fmap_shape, *, bf16: bool, k: int, p: int, grid: int,
-                 temperature: float = 0.1, epsilon: float = 0.01, density_col: int = 0, device=None):
+                 temperature: float = 0.1, epsilon: float = 0.01, density_col: int = 0, device=None,
+                 group=None, sharded: bool = False):
+        """sharded=True (torch.distributed initialised): every rank streams ITS points of each
+        object (e.g. its shard_range) and the objects are computed with the cell-range sharded
+        path (dist.cell_sharded_steps over NCCL); `mass` is then the whole object's."""
         dev = require_cuda(device)
         t = torch()
         self.n, self.nviews, self.grid = int(n), int(nviews), int(grid)
@@ -64,7 +68,7 @@ class FusePipeline:
                                          depth, fmap, device=dev)
             tables = QueryTables.build(np.zeros((k, d), np.float32), np.zeros((k, p), np.float32),
                                        np.zeros(k, np.float32), density_col=density_col, device=dev)
-            bufs = FuseBuffers(n, views, tables, grid, device=dev)
+            bufs = None if sharded else FuseBuffers(n, views, tables, grid, device=dev)
             rec_pinned = t.empty(views.records_dev.numel(), dtype=t.uint8).pin_memory()
             self.slots.append({"pts": pts, "depth": depth, "fmap": fmap, "views": views, "tables": tables,
                                "bufs": bufs, "records": rec_pinned})
@@ -79,6 +83,16 @@ class FusePipeline:
         self.host_mass = [t.empty(2, dtype=t.float64).pin_memory() for _ in range(2)]
         self.h2d_bytes = 0
         self.d2h_bytes = n * p * 4 + 16
+        self.sharded, self.group = bool(sharded), group
+        if self.sharded:
+            import torch.distributed as tdist
+
+            from .dist import DeviceShardOps
+
+            self.rank, self.world = tdist.get_rank(group), tdist.get_world_size(group)
+            for sl in self.slots:
+                sl["ops"] = DeviceShardOps(sl["views"], sl["tables"], temperature=self.temperature,
+                                           epsilon=self.epsilon, grid=self.grid)
 
     def _upload(self, slot, obj: HostObject):
         t = torch()
@@ -124,16 +138,26 @@ class FusePipeline:
             with t.cuda.stream(self.comp):
                 self.comp.wait_event(self.ev_h2d[slot])
                 self.comp.wait_event(self.ev_d2h[slot])  # object i-2's outputs are on the host
-                bufs = s["bufs"]
-                bufs.reset()
-                fuse_prepare(s["views"], s["tables"], bufs)
-                fuse_and_query(s["pts"], s["views"], s["tables"], temperature=self.temperature,
-                               epsilon=self.epsilon, grid=self.grid, buffers=bufs, prepared=True, reset=False)
+                if self.sharded:
+                    from .dist import cell_sharded_steps, run_dist
+
+                    v, tb = s["views"], s["tables"]
+                    out = run_dist(cell_sharded_steps(s["pts"], self.rank, self.world, s["ops"], k=tb.k, p=tb.p,
+                                                      nwords=(v.nviews + 31) // 32), self.group)
+                    s["out"] = out  # keeps the result tensors alive until their download
+                    props_dev, mass_dev = out.props, out.mass
+                else:
+                    bufs = s["bufs"]
+                    bufs.reset()
+                    fuse_prepare(s["views"], s["tables"], bufs)
+                    fuse_and_query(s["pts"], s["views"], s["tables"], temperature=self.temperature,
+                                   epsilon=self.epsilon, grid=self.grid, buffers=bufs, prepared=True, reset=False)
+                    props_dev, mass_dev = bufs.props, bufs.mass
                 self.ev_comp[slot].record(self.comp)
             with t.cuda.stream(self.d2h):
                 self.d2h.wait_event(self.ev_comp[slot])
-                self.host_props[slot].copy_(s["bufs"].props, non_blocking=True)
-                self.host_mass[slot].copy_(s["bufs"].mass, non_blocking=True)
+                self.host_props[slot].copy_(props_dev, non_blocking=True)
+                self.host_mass[slot].copy_(mass_dev, non_blocking=True)
                 self.ev_d2h[slot].record(self.d2h)
             pending.append((i, slot))
             if len(pending) == 2:  # yield the older object once its download is done
