@@ -13,9 +13,11 @@ Reference-named entry points:
     IntegrationConfig, ObjectEstimate                                   (integrate.py:22-167)
 Fused device path:
     ViewSet, QueryTables, FuseBuffers, fuse_and_query -> FusedResult
+    fuse_batch -> BatchResult (many objects, config 4), dist.cell_sharded_fuse (one object, W GPUs)
 """
 
 from . import kernels
+from .batch import BatchResult, fuse_batch
 from .device import ViewSet
 from .errors import (
     BundleLoadError,
@@ -54,7 +56,7 @@ __all__ = [
     "aggregate_geometric_features", "default_epsilon", "project_points", "visibility_mask",
     "kernel_regress", "material_similarity", "regress_with_weights", "softmax_weights",
     "adaptive_voxel_side", "characteristic_length", "integrate_mass", "estimate_from_partials", "voxel_mass",
-    "FusePipeline", "HostObject",
+    "FusePipeline", "HostObject", "fuse_batch", "BatchResult",
     "CameraPose", "IntegrationConfig", "Intrinsics", "MaterialDictionary", "MaterialEntry",
     "ObjectEstimate", "PropertyField", "SemanticPointCloud", "ViewRecord",
     "PropfieldError", "BundleLoadError", "BundleStructureError", "BundleValidationError",
