@@ -228,6 +228,27 @@ int pf_fuse_prepare(const pf_fuse_args_t* args, void* stream);
 int pf_fuse_query(const pf_fuse_args_t* args, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * Densification, fp64 like the reference.
+ * ------------------------------------------------------------------------------------------- */
+
+/* Workspace bytes of pf_dino_knn_interpolate for nq queries x ns sources (the (nq, ns) similarity
+ * matrix dominates). */
+uint64_t pf_dino_knn_workspace_bytes(int64_t nq, int64_t ns, int32_t d);
+/* densify.dino_knn_interpolate (densify.py:36-86): out (nq, m) = convex combination of the probs
+ * rows of each query's k most cosine-similar sources (order: similarity desc, index asc; weights
+ * max(sim, 0) renormalised, uniform when all vanish). q (nq, d), s (ns, d), probs (ns, m) f64
+ * row-major. neighbors (nq, k) i32 optional. PF_ERR_VALUE if k outside 1..ns; PF_ERR_MATERIAL
+ * listing the first zero query rows (densify.py:62-64) — that check synchronises the stream. */
+int pf_dino_knn_interpolate(const double* q, int64_t nq, const double* s, int64_t ns, int32_t d,
+                            const double* probs, int32_t m, int32_t k, double* out, int32_t* neighbors,
+                            void* workspace, void* stream);
+/* idx[i] = the point of `points` (np, 3) f64 nearest to queries[i] (fp64 squared distance, lowest
+ * index on ties): the cKDTree k=1 donor query of densify_field's featureless points
+ * (densify.py:142-147). np == 0 -> PF_ERR_MATERIAL. */
+int pf_nearest_index(const double* queries, int64_t nq, const double* points, int64_t np, int64_t* idx,
+                     void* stream);
+
+/* ---------------------------------------------------------------------------------------------
  * Cell-range sharding of one object across ranks (SURVEY §8e "shard by voxel-code ranges after a
  * pre-sort"; replaces the dense voxel all-reduce of point-range sharding, pipeline.py:304-312 /
  * integrate.py:133-155 are the per-object reductions it feeds). csrc/pf_shard.cu describes the

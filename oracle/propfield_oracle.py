@@ -326,3 +326,63 @@ def fuse_and_query(points, views, text, values, temperature, epsilon, grid, dens
     if mid_theta is not None:
         out.update(integrate_partials(weights, p, mid_theta, np.ones_like(mid_theta)))
     return out
+
+
+# ---- densification ---------------------------------------------------------------
+def dino_knn_interpolate(query_features, source_features, source_probs, k):
+    """densify.py:36-86: cosine k-NN in feature space, neighbours by (-sim, index), weights
+    max(sim, 0) renormalised (uniform 1/k when they all vanish), convex combination of the
+    neighbours' probability rows. Zero query rows raise ValueError-compatible MaterialError text."""
+    q = np.atleast_2d(np.asarray(query_features, dtype=np.float64))
+    s = np.atleast_2d(np.asarray(source_features, dtype=np.float64))
+    probs = np.atleast_2d(np.asarray(source_probs, dtype=np.float64))
+    if k < 1 or k > s.shape[0]:
+        raise ValueError(f"k={k} outside 1..{s.shape[0]}")
+    qn = np.linalg.norm(q, axis=1)
+    missing = np.flatnonzero(qn == 0)
+    if missing.size:
+        raise ValueError(f"query features missing for indices {missing[:10].tolist()}")
+    su = s / np.maximum(np.linalg.norm(s, axis=1, keepdims=True), 1e-30)
+    sims = (q / qn[:, None]) @ su.T
+    # full lexicographic order (-sim, index) per row, first k (densify.py:69-76)
+    idx = np.broadcast_to(np.arange(s.shape[0]), sims.shape)
+    order = np.lexsort((idx, -sims), axis=1)[:, :k]
+    nsims = np.take_along_axis(sims, order, axis=1)
+    w = np.maximum(nsims, 0.0)
+    tot = w.sum(axis=1)
+    flat = tot <= 0
+    w[flat] = 1.0
+    tot[flat] = k
+    w /= tot[:, None]
+    return np.einsum("qk,qkm->qm", w, probs[order])
+
+
+def densify_field(positions, features, visible_counts, source_features, source_probs, values_by_prop, k):
+    """densify.py:110-160: featured points interpolate in feature space; featureless ones (count 0
+    or zero feature row) copy their nearest featured neighbour's probabilities (brute-force fp64
+    nearest, lowest index on ties — the cKDTree k=1 query); properties regress the probabilities
+    on each property's [lo, hi] table (one column when lo == hi). Returns a dict."""
+    pos = np.asarray(positions, dtype=np.float64)
+    f = np.asarray(features, dtype=np.float64)
+    n = pos.shape[0]
+    k = min(k, np.asarray(source_features).shape[0])
+    featureless = (np.asarray(visible_counts) == 0) | (np.linalg.norm(f, axis=1) == 0)
+    m = np.asarray(source_probs).shape[1]
+    probs = np.zeros((n, m))
+    featured = np.flatnonzero(~featureless)
+    if featured.size:
+        probs[featured] = dino_knn_interpolate(f[featured], source_features, source_probs, k)
+    orphan = np.flatnonzero(featureless)
+    if orphan.size:
+        if featured.size == 0:
+            raise ValueError("no point in the cloud has a geometric feature")
+        fp = pos[featured]
+        for i in orphan:
+            d2 = ((fp - pos[i]) ** 2).sum(axis=1)
+            probs[i] = probs[featured[int(np.argmin(d2))]]
+    props = {}
+    for name, lo_hi in values_by_prop.items():
+        lo_hi = np.asarray(lo_hi, dtype=np.float64)
+        props[name] = regress_with_weights(probs, lo_hi[:, 0] if np.all(lo_hi[:, 0] == lo_hi[:, 1]) else lo_hi)
+    return {"probabilities": probs, "dominant": probs.argmax(axis=1), "properties": props,
+            "featureless": featureless}

@@ -9,6 +9,7 @@ Reference-named entry points:
     project_points, default_epsilon, visibility_mask                    (geometry.py:46-103)
     aggregate_geometric_features -> SemanticPointCloud                  (fusion.py:24-93)
     material_similarity, softmax_weights, kernel_regress, regress_with_weights (grounding.py:158-202)
+    dino_knn_interpolate, densify_field                                 (densify.py:36-160)
     adaptive_voxel_side, characteristic_length, integrate_mass,
     IntegrationConfig, ObjectEstimate                                   (integrate.py:22-167)
 Fused device path:
@@ -18,6 +19,7 @@ Fused device path:
 
 from . import kernels
 from .batch import BatchResult, fuse_batch
+from .densify import densify_field, dino_knn_interpolate
 from .device import ViewSet
 from .errors import (
     BundleLoadError,
@@ -56,7 +58,7 @@ __all__ = [
     "aggregate_geometric_features", "default_epsilon", "project_points", "visibility_mask",
     "kernel_regress", "material_similarity", "regress_with_weights", "softmax_weights",
     "adaptive_voxel_side", "characteristic_length", "integrate_mass", "estimate_from_partials", "voxel_mass",
-    "FusePipeline", "HostObject", "fuse_batch", "BatchResult",
+    "FusePipeline", "HostObject", "fuse_batch", "BatchResult", "dino_knn_interpolate", "densify_field",
     "CameraPose", "IntegrationConfig", "Intrinsics", "MaterialDictionary", "MaterialEntry",
     "ObjectEstimate", "PropertyField", "SemanticPointCloud", "ViewRecord",
     "PropfieldError", "BundleLoadError", "BundleStructureError", "BundleValidationError",

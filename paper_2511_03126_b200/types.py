@@ -188,6 +188,16 @@ class MaterialDictionary:
     def names(self) -> list:
         return [e.name for e in self.entries]
 
+    @property
+    def property_names(self) -> list:
+        """Every property any entry defines, in first-seen order (grounding.py:77-84)."""
+        names = []
+        for e in self.entries:
+            for p in e.properties:
+                if p not in names:
+                    names.append(p)
+        return names
+
     def property_values(self, prop: str) -> np.ndarray:
         """(K, 2) low/high array; MaterialError if any entry lacks `prop` (grounding.py:67-72)."""
         missing = [e.name for e in self.entries if prop not in e.properties]

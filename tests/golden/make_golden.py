@@ -127,6 +127,34 @@ def pipeline_golden(name, propfield):
     return out
 
 
+def densify_golden():
+    """dino_knn_interpolate on recipes.densify_cases() and densify_field on densify_field_case()."""
+    from propfield.densify import densify_field, dino_knn_interpolate
+    from propfield.fusion import SemanticPointCloud
+    from propfield.grounding import MaterialDictionary, MaterialEntry
+    from propfield.sampling import SourcePointSet
+
+    out = {}
+    for name, q, s, p, k in recipes.densify_cases():
+        out[f"dk_{name}"] = dino_knn_interpolate(q, s, p, k)
+    c = recipes.densify_field_case()
+    n = c["positions"].shape[0]
+    semantic = SemanticPointCloud(positions=c["positions"], features=c["features"], visible_counts=c["counts"],
+                                  visibility=(c["counts"] > 0)[:, None])
+    src = SourcePointSet(indices=c["src_pick"], positions=c["positions"][c["src_pick"]], voxel_size=0.1,
+                         features=c["src_features"], probabilities=c["src_probs"])
+    entries = [MaterialEntry(name=nm, properties={"density": tuple(c["density"][i]), "hardness": tuple(c["hardness"][i])},
+                             thickness_m=0.01) for i, nm in enumerate(["wood", "steel"])]
+    fld = densify_field(semantic, src, MaterialDictionary(entries=entries), k=3)
+    out["df_probabilities"] = fld.probabilities
+    out["df_dominant"] = fld.dominant
+    out["df_density"] = fld.properties["density"]
+    out["df_hardness"] = fld.properties["hardness"]
+    out["df_featureless"] = fld.flags["featureless"]
+    assert n == len(fld)
+    return out
+
+
 def main():
     import propfield  # noqa: F401  (the unmodified reference)
     from propfield import grounding
@@ -134,6 +162,7 @@ def main():
 
     np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernels_golden(numpy_impl))
     np.savez_compressed(os.path.join(HERE, "grounding.npz"), **grounding_golden(grounding))
+    np.savez_compressed(os.path.join(HERE, "densify.npz"), **densify_golden())
     for name in ("mini", "mini_bf16"):
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **pipeline_golden(name, propfield))
     for f in sorted(os.listdir(HERE)):

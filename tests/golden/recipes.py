@@ -47,3 +47,63 @@ def grounding_case(seed=0, s=64, d=32, k=8):
     t /= np.linalg.norm(t, axis=1, keepdims=True)
     y = np.stack([rng.uniform(100, 8000, k), rng.uniform(0, 1, k)], axis=1)
     return f, t, y
+
+
+def densify_cases():
+    """dino_knn_interpolate inputs: the reference's own test_densify.py:29-94 cases draw for draw,
+    plus larger seeded cases (ties from duplicated sources, k == S, negative-similarity rows)."""
+    cases = []
+    rng = np.random.default_rng(0)  # test_k1_copies_nearest_source
+    src_feat = rng.standard_normal((10, 4))
+    src_probs = rng.dirichlet(np.ones(3), size=10)
+    cases.append(("k1_copy", src_feat[4][None, :] * 2.0, src_feat, src_probs, 1))
+    cases.append(("equal_sims", np.array([[1.0, 0.0]]), np.array([[1.0, 0.0], [1.0, 0.0], [0.0, 1.0]]),
+                  np.array([[1.0, 0.0], [0.0, 1.0], [0.5, 0.5]]), 2))
+    for k in (1, 3, 7):  # test_matches_exhaustive_oracle
+        rng = np.random.default_rng(42)
+        src_feat = rng.standard_normal((40, 8))
+        src_probs = rng.dirichlet(np.ones(4), size=40)
+        queries = rng.standard_normal((200, 8))
+        cases.append((f"exhaustive_k{k}", queries, src_feat, src_probs, k))
+    cases.append(("all_negative", np.array([[-1.0, 0.0]]), np.array([[1.0, 0.0], [0.9, 0.1]]),
+                  np.array([[1.0, 0.0], [0.0, 1.0]]), 2))
+    rng = np.random.default_rng(3)  # test_rows_are_convex_combinations
+    cases.append(("convex", rng.standard_normal((100, 6)), rng.standard_normal((30, 6)),
+                  rng.dirichlet(np.ones(5), size=30), 4))
+    rng = np.random.default_rng(4)  # test_exact_feature_match_is_in_neighbor_set
+    src_feat = rng.standard_normal((20, 5))
+    cases.append(("exact_match", src_feat[7][None], src_feat, np.eye(20), 3))
+    # larger: pipeline-like anchors (S=150, k=5, D=64, M=16), duplicated sources (exact ties)
+    rng = np.random.default_rng(11)
+    s = rng.standard_normal((150, 64))
+    s[100:110] = s[0:10]
+    q = rng.standard_normal((3000, 64))
+    q[:50] = s[:50] * rng.uniform(0.5, 2.0, (50, 1))
+    p = rng.dirichlet(np.ones(16), size=150)
+    cases.append(("anchors150_k5", q, s, p, 5))
+    cases.append(("anchors150_kS", q[:200], s, p, 150))
+    return cases
+
+
+def densify_field_case(seed=0, n=1500, n_sources=60, noise=0.05, n_orphans=40):
+    """densify_field inputs in the shape of test_densify.py:97-124 (striped two-part layout) with
+    some featureless points (zero rows, count 0) that take their nearest featured neighbour."""
+    rng = np.random.default_rng(seed)
+    pts = np.zeros((n, 3))
+    pts[:, 0] = rng.uniform(0, 1, size=n)
+    pts[:, 1] = rng.uniform(0, 1, size=n)
+    part = (np.floor(pts[:, 0] / 0.05).astype(int) % 2).astype(np.int64)
+    feats = np.zeros((n, 2))
+    feats[np.arange(n), part] = 1.0
+    feats = feats + noise * rng.standard_normal(feats.shape)
+    counts = np.ones(n, dtype=np.int64)
+    orphans = rng.choice(n, size=n_orphans, replace=False)
+    feats[orphans] = 0.0
+    counts[orphans] = 0
+    featured = np.setdiff1d(np.arange(n), orphans)
+    src_pick = rng.choice(featured, size=n_sources, replace=False)
+    density = np.array([[600.0, 600.0], [7800.0, 7800.0]])
+    hardness = np.array([[0.2, 0.4], [0.8, 0.9]])
+    return dict(positions=pts, features=feats, counts=counts, src_pick=src_pick,
+                src_features=feats[src_pick], src_probs=np.eye(2)[part[src_pick]], density=density,
+                hardness=hardness, part=part)

@@ -168,3 +168,50 @@ class TestGenerator:
         wl = workload("mini")
         d = wl.depth_np()
         assert d.min() >= 0 and (d > 0).mean() > 0.01
+
+
+def boundary_ties(q, s, k):
+    """Rows whose k-th and (k+1)-th similarities are exactly equal: the reference picks among such
+    ties with np.argpartition (introselect, implementation-defined, densify.py:69-70); the oracle and
+    the device take the lower index, matching the reference's own within-set tie-break. These rows
+    are excluded from value parity (the neighbour SET is ambiguous there)."""
+    q = np.atleast_2d(np.asarray(q, np.float64))
+    s = np.atleast_2d(np.asarray(s, np.float64))
+    if k >= s.shape[0]:
+        return np.zeros(q.shape[0], dtype=bool)
+    sims = (q / np.linalg.norm(q, axis=1)[:, None]) @ (s / np.linalg.norm(s, axis=1, keepdims=True)).T
+    srt = -np.sort(-sims, axis=1)
+    return srt[:, k - 1] == srt[:, k]
+
+
+class TestDensifyOracle:
+    """Oracle restatement of densify.py vs the reference's own outputs (tests/golden/densify.npz)."""
+
+    def test_dino_knn_cases(self, golden):
+        import recipes
+
+        g = golden("densify")
+        for name, q, s, p, k in recipes.densify_cases():
+            keep = ~boundary_ties(q, s, k)
+            assert keep.mean() > 0.9
+            np.testing.assert_allclose(O.dino_knn_interpolate(q, s, p, k)[keep], g[f"dk_{name}"][keep], rtol=0,
+                                       atol=1e-12, err_msg=name)
+
+    def test_dino_knn_errors(self):
+        with pytest.raises(ValueError, match=r"\[1\]"):
+            O.dino_knn_interpolate(np.array([[1.0, 0, 0], [0, 0, 0]]), np.eye(3), np.eye(3), 1)
+        with pytest.raises(ValueError):
+            O.dino_knn_interpolate(np.eye(2), np.eye(2), np.eye(2), 3)
+
+    def test_densify_field(self, golden):
+        import recipes
+
+        g = golden("densify")
+        c = recipes.densify_field_case()
+        out = O.densify_field(c["positions"], c["features"], c["counts"], c["src_features"], c["src_probs"],
+                              {"density": c["density"], "hardness": c["hardness"]}, 3)
+        np.testing.assert_allclose(out["probabilities"], g["df_probabilities"], rtol=0, atol=1e-12)
+        np.testing.assert_array_equal(out["dominant"], g["df_dominant"])
+        np.testing.assert_array_equal(out["featureless"], g["df_featureless"])
+        np.testing.assert_allclose(out["properties"]["density"], g["df_density"], rtol=1e-12)
+        np.testing.assert_allclose(out["properties"]["hardness"], g["df_hardness"], rtol=1e-12)
