@@ -39,12 +39,12 @@ namespace tile {
 
 // ---- counting sort by a coarse space-filling-curve key ------------------------------------------------
 
-// 3-D Hilbert index of a cell of the 2^kSortBits grid (Skilling's transpose algorithm): consecutive
+// 3-D Hilbert index of a cell of the 2^bits grid (Skilling's transpose algorithm): consecutive
 // keys are face-adjacent cells, so a run of consecutive sorted points (a tile) stays one compact
 // surface patch far more often than along a Morton (Z) curve, which jumps across the object.
-__device__ __forceinline__ uint32_t hilbert3(uint32_t x, uint32_t y, uint32_t z) {
+__device__ __forceinline__ uint32_t hilbert3(uint32_t x, uint32_t y, uint32_t z, int bits) {
   uint32_t X[3] = {x, y, z};
-  const uint32_t M = 1u << (kSortBits - 1);
+  const uint32_t M = 1u << (bits - 1);
 #pragma unroll
   for (uint32_t Q = M; Q > 1; Q >>= 1) {  // inverse undo
     const uint32_t Pm = Q - 1;
@@ -70,29 +70,30 @@ __device__ __forceinline__ uint32_t hilbert3(uint32_t x, uint32_t y, uint32_t z)
   X[2] ^= t;
   uint32_t key = 0;
 #pragma unroll
-  for (int b = kSortBits - 1; b >= 0; --b)
+  for (int b = bits - 1; b >= 0; --b)
     key = (key << 3) | (((X[0] >> b) & 1u) << 2) | (((X[1] >> b) & 1u) << 1) | ((X[2] >> b) & 1u);
   return key;
 }
 
 __global__ void k_sort_keys(const float* __restrict__ p, int64_t n, const double* __restrict__ lo_hi,
-                            uint32_t* __restrict__ keys, uint32_t* __restrict__ hist) {
+                            uint32_t* __restrict__ keys, uint32_t* __restrict__ hist, int bits) {
+  const int cells = 1 << bits;
   const float lx = (float)lo_hi[0], ly = (float)lo_hi[1], lz = (float)lo_hi[2];
   const float ext = fmaxf(fmaxf((float)(lo_hi[3] - lo_hi[0]), (float)(lo_hi[4] - lo_hi[1])),
                           (float)(lo_hi[5] - lo_hi[2]));
-  const float inv = ext > 0.f ? (float)kSortCells / ext : 0.f;
+  const float inv = ext > 0.f ? (float)cells / ext : 0.f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int cx = min(max((int)((__ldg(p + 3 * i) - lx) * inv), 0), kSortCells - 1);
-    const int cy = min(max((int)((__ldg(p + 3 * i + 1) - ly) * inv), 0), kSortCells - 1);
-    const int cz = min(max((int)((__ldg(p + 3 * i + 2) - lz) * inv), 0), kSortCells - 1);
-    const uint32_t key = hilbert3((uint32_t)cx, (uint32_t)cy, (uint32_t)cz);
+    const int cx = min(max((int)((__ldg(p + 3 * i) - lx) * inv), 0), cells - 1);
+    const int cy = min(max((int)((__ldg(p + 3 * i + 1) - ly) * inv), 0), cells - 1);
+    const int cz = min(max((int)((__ldg(p + 3 * i + 2) - lz) * inv), 0), cells - 1);
+    const uint32_t key = hilbert3((uint32_t)cx, (uint32_t)cy, (uint32_t)cz, bits);
     keys[i] = key;
     atomicAdd(hist + key, 1u);
   }
 }
 
-// exclusive scan of kSortBins counters: per-block scan of 4096 (1024 threads x 4), block totals,
+// exclusive scan of the sort's counters: per-block scan of 4096 (1024 threads x 4), block totals,
 // then add. In place on `hist`.
 __global__ void __launch_bounds__(1024) k_scan_blocks(uint32_t* __restrict__ hist, uint32_t* __restrict__ totals) {
   __shared__ uint32_t warp_sums[32];
@@ -124,17 +125,29 @@ __global__ void __launch_bounds__(1024) k_scan_blocks(uint32_t* __restrict__ his
 }
 
 __global__ void __launch_bounds__(1024) k_scan_totals(uint32_t* __restrict__ totals, int nblocks) {
+  // exclusive scan of <= 4096 block totals, 4 consecutive per thread
   __shared__ uint32_t s[1024];
   const int t = threadIdx.x;
-  s[t] = t < nblocks ? totals[t] : 0u;
+  uint32_t v[4], sum = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v[q] = 4 * t + q < nblocks ? totals[4 * t + q] : 0u;
+    sum += v[q];
+  }
+  s[t] = sum;
   __syncthreads();
   for (int o = 1; o < 1024; o <<= 1) {
-    const uint32_t v = t >= o ? s[t - o] : 0u;
+    const uint32_t x = t >= o ? s[t - o] : 0u;
     __syncthreads();
-    s[t] += v;
+    s[t] += x;
     __syncthreads();
   }
-  if (t < nblocks) totals[t] = s[t] - (t < nblocks ? totals[t] : 0u);
+  uint32_t run = s[t] - sum;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (4 * t + q < nblocks) totals[4 * t + q] = run;
+    run += v[q];
+  }
 }
 
 __global__ void k_scan_add(uint32_t* __restrict__ hist, const uint32_t* __restrict__ totals) {
@@ -234,8 +247,9 @@ struct ViewAff {
 // so the first-order model is within fx r^2 (|X0| + Z0) / (Z0^2 zmin) of the exact value. On top:
 // the fp32 error of u(o) (the view's constant project_f32 bound), 3 fma roundings of a ~|u| value
 // and the gradient's relative error.
-__device__ int classify_tile_view(const ViewF& v, const float4& vb, const float* __restrict__ depth,
-                                  const float* lo, const float* hi, float eps, int4& win, ViewAff& aff) {
+__device__ int classify_tile_view(const ViewF& v, const float4& vb, const pf_view_t& v64,
+                                  const float* __restrict__ depth, const float* lo, const float* hi, float eps,
+                                  int4& win, ViewAff& aff) {
   float zmin = 1e30f, zmax = -1e30f, umin = 1e30f, umax = -1e30f, vmin = 1e30f, vmax = -1e30f;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -288,18 +302,25 @@ __device__ int classify_tile_view(const ViewF& v, const float4& vb, const float*
   const float ox = 0.5f * (lo[0] + hi[0]), oy = 0.5f * (lo[1] + hi[1]), oz = 0.5f * (lo[2] + hi[2]);
   const float hx = 0.5f * (hi[0] - lo[0]), hy = 0.5f * (hi[1] - lo[1]), hz = 0.5f * (hi[2] - lo[2]);
   const float r = sqrtf(hx * hx + hy * hy + hz * hz) * 1.0001f + 1e-7f;
-  const ProjF q = project_f32(v, ox, oy, oz);  // |q.u - u64(o)| <= vb.x (o lies in the object box)
+  const ProjF q = project_f32(v, ox, oy, oz);  // slopes (fp32 is plenty for the gradient)
+  // the model's value at o in fp64 with the reference's camera: |u0 - u64(o)| is only the final
+  // rounding to fp32 (+ ~1e-13), so the view's constant fp32 projection bound drops out
+  const double X0 = cam_row(v64.R, 0, ox, oy, oz, v64.t[0]), Y0 = cam_row(v64.R, 1, ox, oy, oz, v64.t[1]);
+  const double Z0 = cam_row(v64.R, 2, ox, oy, oz, v64.t[2]);
+  const double rz0 = 1.0 / Z0;
+  const float u0 = (float)fma(v64.fx * X0, rz0, v64.cx), v0 = (float)fma(v64.fy * Y0, rz0, v64.cy);
   const float xr = q.X * q.rz, yr = q.Y * q.rz;
   const float su = v.fx * q.rz, sv = v.fy * q.rz;
-  aff.u = make_float4(q.u, su * (v.R[0] - xr * v.R[6]), su * (v.R[1] - xr * v.R[7]), su * (v.R[2] - xr * v.R[8]));
-  aff.v = make_float4(q.v, sv * (v.R[3] - yr * v.R[6]), sv * (v.R[4] - yr * v.R[7]), sv * (v.R[5] - yr * v.R[8]));
-  aff.z = make_float4(q.z, v.R[6], v.R[7], v.R[8]);
-  const float z0 = q.z, rem = r * r / (z0 * z0 * zmin) * 1.05f;
+  aff.u = make_float4(u0, su * (v.R[0] - xr * v.R[6]), su * (v.R[1] - xr * v.R[7]), su * (v.R[2] - xr * v.R[8]));
+  aff.v = make_float4(v0, sv * (v.R[3] - yr * v.R[6]), sv * (v.R[4] - yr * v.R[7]), sv * (v.R[5] - yr * v.R[8]));
+  aff.z = make_float4((float)Z0, v.R[6], v.R[7], v.R[8]);
+  const float z0 = (float)Z0, rem = r * r / (z0 * z0 * zmin) * 1.05f;
   const float gmax_u = fabsf(aff.u.y) + fabsf(aff.u.z) + fabsf(aff.u.w);
   const float gmax_v = fabsf(aff.v.y) + fabsf(aff.v.z) + fabsf(aff.v.w);
-  aff.eu = vb.x + fabsf(v.fx) * (fabsf(q.X) + z0) * rem + 4e-7f * (fabsf(q.u) + gmax_u * r) + 1e-5f * gmax_u * r + 1e-5f;
-  aff.ev = vb.y + fabsf(v.fy) * (fabsf(q.Y) + z0) * rem + 4e-7f * (fabsf(q.v) + gmax_v * r) + 1e-5f * gmax_v * r + 1e-5f;
-  aff.ez = q.e + 4e-7f * (fabsf(z0) + 2.f * r) + 1e-7f;  // z is exactly affine: rounding only
+  // remainder + fp32 rounding of u0 and of the 3-fma evaluation + the fp32 gradient's error
+  aff.eu = fabsf(v.fx) * (fabsf(q.X) + z0) * rem * 1.001f + 4.7e-7f * (fabsf(u0) + gmax_u * r) + 1e-5f * gmax_u * r + 1e-5f;
+  aff.ev = fabsf(v.fy) * (fabsf(q.Y) + z0) * rem * 1.001f + 4.7e-7f * (fabsf(v0) + gmax_v * r) + 1e-5f * gmax_v * r + 1e-5f;
+  aff.ez = 4.7e-7f * (fabsf(z0) + 2.f * r) + 1e-7f;  // z is exactly affine: rounding only
   aff.W = v.W;
   aff.H = v.H;
   aff.depth_off = v.depth_off;
@@ -445,7 +466,7 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     const float4 vb = P.vbound[tid];
     int4 win = make_int4(INT_MAX, INT_MAX, -1, -1);
     ViewAff aff;
-    const int cls = classify_tile_view(v, vb, P.depth, lo, hi, eps_f, win, aff);
+    const int cls = classify_tile_view(v, vb, P.views[tid], P.depth, lo, hi, eps_f, win, aff);
     s_cls[tid] = (unsigned char)cls;
     // FULL: box window now; MIXED: box window once a point is seen visible; EXACT: per-point union
     const bool boxwin = cls == kViewFull;
@@ -713,8 +734,8 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg) {
   };
   L.ntiles = ntiles;
   L.keys = take(sizeof(uint32_t) * (size_t)n);
-  L.hist = take(sizeof(uint32_t) * (size_t)kSortBins);
-  L.totals = take(sizeof(uint32_t) * 1024);
+  L.hist = take(sizeof(uint32_t) * (size_t)(1 << (3 * sort_bits_for(n))));
+  L.totals = take(sizeof(uint32_t) * 4096);
   L.inv = take(sizeof(int32_t) * (size_t)n);
   L.spts = take(sizeof(float4) * (size_t)ntiles * kTile);
   L.srec = take(sizeof(SRec) * (size_t)ntiles * kTile);
@@ -738,9 +759,9 @@ int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf
   return check_launch("g_bf16");
 }
 
-// exclusive scan of `nbins` (multiple of 4096, <= 4M) bucket counters in place (k_scan_*)
+// exclusive scan of `nbins` (multiple of 4096, <= 16M) bucket counters in place (k_scan_*)
 int run_bucket_scan(uint32_t* hist, uint32_t* totals, int64_t nbins, cudaStream_t st) {
-  if (nbins % 4096 != 0 || nbins / 4096 > 1024) return set_error(PF_ERR_VALUE, "bucket scan: bad bin count");
+  if (nbins % 4096 != 0 || nbins / 4096 > 4096) return set_error(PF_ERR_VALUE, "bucket scan: bad bin count");
   const int nb = (int)(nbins / 4096);
   k_scan_blocks<<<nb, 1024, 0, st>>>(hist, totals);
   if (int rc = check_launch("scan_blocks")) return rc;
@@ -764,16 +785,13 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
   uint32_t* totals = reinterpret_cast<uint32_t*>(ws + L.totals);
   stage_mark(0, st);
-  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kSortBins, st);
+  const int bits = sort_bits_for(n);
+  const int64_t nbins = int64_t(1) << (3 * bits);
+  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * nbins, st);
   cudaMemsetAsync(P.ovf_count, 0, sizeof(int32_t), st);
-  k_sort_keys<<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist);
+  k_sort_keys<<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist, bits);
   if (int rc = check_launch("sort_keys")) return rc;
-  k_scan_blocks<<<kSortBins / 4096, 1024, 0, st>>>(hist, totals);
-  if (int rc = check_launch("scan_blocks")) return rc;
-  k_scan_totals<<<1, 1024, 0, st>>>(totals, kSortBins / 4096);
-  if (int rc = check_launch("scan_totals")) return rc;
-  k_scan_add<<<kSortBins / 256, 256, 0, st>>>(hist, totals);
-  if (int rc = check_launch("scan_add")) return rc;
+  if (int rc = run_bucket_scan(hist, totals, nbins, st)) return rc;
   k_sort_scatter<<<grid_for(n, 256), 256, 0, st>>>(points, n, keys, hist, const_cast<int32_t*>(P.inv),
                                                    const_cast<float4*>(P.spts));
   if (int rc = check_launch("sort_scatter")) return rc;

@@ -20,9 +20,9 @@ namespace tile {
 constexpr int kTile = 128;             // points per tile = tcgen05 M
 constexpr int kMaxViewsTC = 64;        // views supported by the tile path (2 bitset words)
 constexpr int kMaxKpadTC = 128;        // padded materials (MMA N of the S chunk pair)
-constexpr int kSortBits = 7;           // Hilbert curve over a 128^3 grid over the bbox
-constexpr int kSortCells = 1 << kSortBits;
-constexpr int kSortBins = 1 << (3 * kSortBits);
+constexpr int kSortBitsMax = 8;        // Hilbert curve over a 2^bits cube grid over the bbox:
+constexpr int kSortBinsMax = 1 << (3 * kSortBitsMax);  // 7 bits (128^3), 8 bits (256^3) from 4M points
+inline int sort_bits_for(int64_t n) { return n >= (int64_t(1) << 22) ? 8 : 7; }
 
 struct ViewF {
   float R[9];

@@ -1,5 +1,5 @@
 """A/B the tile-path stage times of two builds of the library on the same box:
-    python scripts/ab_tile.py <lib_a.so> <lib_b.so> [config]
+    python scripts/ab_tile.py <lib_a.so> <lib_b.so> [more.so ...] [config]
 Each library runs in its own process (reduce=False: no voxel-mass finalisation)."""
 import json
 import os
@@ -46,9 +46,11 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     n, st = _lib.stage_times()
     print(json.dumps({k: v / n for k, v in st.items()}))
 else:
-    cfg = sys.argv[3] if len(sys.argv) > 3 else "c5"
+    libs = [a for a in sys.argv[1:] if a.endswith(".so")]
+    rest = [a for a in sys.argv[1:] if not a.endswith(".so")]
+    cfg = rest[0] if rest else "c5"
     for rep in range(2):
-        for lib in sys.argv[1:3]:
+        for lib in libs:
             out = subprocess.run([sys.executable, __file__, "--child", lib, cfg], capture_output=True, text=True)
             line = [x for x in out.stdout.splitlines() if x.startswith("{")]
             print(os.path.basename(lib), line[-1] if line else out.stderr[-500:], flush=True)
