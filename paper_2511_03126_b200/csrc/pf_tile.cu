@@ -219,7 +219,10 @@ constexpr int kScanMax = 64;  // pixels of depth scanned per (tile, view) at mos
 // Per-(tile, view) affine model of a MIXED view: u, v, z = c0 + g . (p - o) with rigorous bounds
 // eu, ev, ez on |model - numpy's fp64 value| over the tile box (see classify_tile_view).
 struct ViewAff {
-  float4 u, v, z;        // {value at o, gradient}
+  float4 r0, r1, r2;     // camera rotation rows {R_i0, R_i1, R_i2, -}: a, c, b = R . d
+  float4 u, v;           // {value at o, d/da, d/db, d/d(ab)}; the b^2 coefficient is in z.w / q
+  float4 q;              // {u: b^2 coeff, v: b^2 coeff, v: d/dc, v: d/d(cb)}
+  float z0;
   float eu, ev, ez, pad;
   int W, H;
   int64_t depth_off;
@@ -302,25 +305,35 @@ __device__ int classify_tile_view(const ViewF& v, const float4& vb, const pf_vie
   const float ox = 0.5f * (lo[0] + hi[0]), oy = 0.5f * (lo[1] + hi[1]), oz = 0.5f * (lo[2] + hi[2]);
   const float hx = 0.5f * (hi[0] - lo[0]), hy = 0.5f * (hi[1] - lo[1]), hz = 0.5f * (hi[2] - lo[2]);
   const float r = sqrtf(hx * hx + hy * hy + hz * hz) * 1.0001f + 1e-7f;
-  const ProjF q = project_f32(v, ox, oy, oz);  // slopes (fp32 is plenty for the gradient)
   // the model's value at o in fp64 with the reference's camera: |u0 - u64(o)| is only the final
-  // rounding to fp32 (+ ~1e-13), so the view's constant fp32 projection bound drops out
+  // rounding to fp32 (+ ~1e-13), so no fp32 projection bound enters
   const double X0 = cam_row(v64.R, 0, ox, oy, oz, v64.t[0]), Y0 = cam_row(v64.R, 1, ox, oy, oz, v64.t[1]);
   const double Z0 = cam_row(v64.R, 2, ox, oy, oz, v64.t[2]);
   const double rz0 = 1.0 / Z0;
   const float u0 = (float)fma(v64.fx * X0, rz0, v64.cx), v0 = (float)fma(v64.fy * Y0, rz0, v64.cy);
-  const float xr = q.X * q.rz, yr = q.Y * q.rz;
-  const float su = v.fx * q.rz, sv = v.fy * q.rz;
-  aff.u = make_float4(u0, su * (v.R[0] - xr * v.R[6]), su * (v.R[1] - xr * v.R[7]), su * (v.R[2] - xr * v.R[8]));
-  aff.v = make_float4(v0, sv * (v.R[3] - yr * v.R[6]), sv * (v.R[4] - yr * v.R[7]), sv * (v.R[5] - yr * v.R[8]));
-  aff.z = make_float4((float)Z0, v.R[6], v.R[7], v.R[8]);
-  const float z0 = (float)Z0, rem = r * r / (z0 * z0 * zmin) * 1.05f;
-  const float gmax_u = fabsf(aff.u.y) + fabsf(aff.u.z) + fabsf(aff.u.w);
-  const float gmax_v = fabsf(aff.v.y) + fabsf(aff.v.z) + fabsf(aff.v.w);
-  // remainder + fp32 rounding of u0 and of the 3-fma evaluation + the fp32 gradient's error
-  aff.eu = fabsf(v.fx) * (fabsf(q.X) + z0) * rem * 1.001f + 4.7e-7f * (fabsf(u0) + gmax_u * r) + 1e-5f * gmax_u * r + 1e-5f;
-  aff.ev = fabsf(v.fy) * (fabsf(q.Y) + z0) * rem * 1.001f + 4.7e-7f * (fabsf(v0) + gmax_v * r) + 1e-5f * gmax_v * r + 1e-5f;
-  aff.ez = 4.7e-7f * (fabsf(z0) + 2.f * r) + 1e-7f;  // z is exactly affine: rounding only
+  // second-order model in a = R0.d, c = R1.d, b = R2.d (d = p - o):
+  //   X/Z = X0/Z0 + a/Z0 - X0 b/Z0^2 - a b/Z0^2 + X0 b^2/Z0^3 + R3,
+  //   R3 = a b^2/Z0^3 - (X0 + a) b^3 / (Z0^3 Z),  |R3| <= r^3 ((|X0| + r)/(Z0^3 zmin) + 1/Z0^3)
+  const double su = v64.fx * rz0, sv = v64.fy * rz0, xr = X0 * rz0, yr = Y0 * rz0;
+  aff.r0 = make_float4(v.R[0], v.R[1], v.R[2], 0.f);
+  aff.r1 = make_float4(v.R[3], v.R[4], v.R[5], 0.f);
+  aff.r2 = make_float4(v.R[6], v.R[7], v.R[8], 0.f);
+  aff.u = make_float4(u0, (float)su, (float)(-su * xr), (float)(-su * rz0));
+  aff.v = make_float4(v0, (float)sv, (float)(-sv * yr), (float)(-sv * rz0));
+  aff.q = make_float4((float)(su * xr * rz0), (float)(sv * yr * rz0), 0.f, 0.f);
+  aff.z0 = (float)Z0;
+  const double z0 = Z0, rr = (double)r, zl = (double)zmin;
+  const double r3 = rr * rr * rr / (z0 * z0 * z0);
+  const double gu = fabs(su) * (1.0 + fabs(xr)) * rr, gv = fabs(sv) * (1.0 + fabs(yr)) * rr;  // |linear part|
+  const double qu = fabs(su) * rz0 * (1.0 + fabs(xr)) * rr * rr, qv = fabs(sv) * rz0 * (1.0 + fabs(yr)) * rr * rr;
+  // remainder + fp32 rounding of u0 and of the ~6 rounded ops of the evaluation + the fp32 coefficients
+  const double eu = fabs(v64.fx) * r3 * ((fabs(X0) + rr) / zl + 1.0) * 1.05 + 7e-7 * (fabs(u0) + gu + qu) +
+                    1e-5 * (gu + qu) + 1e-5;
+  const double ev = fabs(v64.fy) * r3 * ((fabs(Y0) + rr) / zl + 1.0) * 1.05 + 7e-7 * (fabs(v0) + gv + qv) +
+                    1e-5 * (gv + qv) + 1e-5;
+  aff.eu = (float)eu;
+  aff.ev = (float)ev;
+  aff.ez = 4.7e-7f * (fabsf((float)z0) + 2.f * r) + 1e-7f;  // z = z0 + b is exactly affine: rounding only
   aff.W = v.W;
   aff.H = v.H;
   aff.depth_off = v.depth_off;
@@ -386,22 +399,25 @@ __device__ __forceinline__ bool point_visible(const ViewF& v, const float4& b, c
   return vis;
 }
 
-// MIXED-view decision through the affine model; kAmbiguous sends the sample to point_visible
-__device__ __forceinline__ int affine_visible(const ViewAff& a, const float* __restrict__ depth, float dx,
+// MIXED-view decision through the second-order model; kAmbiguous sends the sample to point_visible
+__device__ __forceinline__ int affine_visible(const ViewAff& m, const float* __restrict__ depth, float dx,
                                               float dy, float dz, float eps_f) {
-  const float u = fmaf(a.u.w, dz, fmaf(a.u.z, dy, fmaf(a.u.y, dx, a.u.x)));
-  const float v = fmaf(a.v.w, dz, fmaf(a.v.z, dy, fmaf(a.v.y, dx, a.v.x)));
+  const float a = fmaf(m.r0.z, dz, fmaf(m.r0.y, dy, m.r0.x * dx));
+  const float c = fmaf(m.r1.z, dz, fmaf(m.r1.y, dy, m.r1.x * dx));
+  const float b = fmaf(m.r2.z, dz, fmaf(m.r2.y, dy, m.r2.x * dx));
+  const float u = fmaf(b, fmaf(m.q.x, b, fmaf(m.u.w, a, m.u.z)), fmaf(m.u.y, a, m.u.x));
+  const float v = fmaf(b, fmaf(m.q.y, b, fmaf(m.v.w, c, m.v.z)), fmaf(m.v.y, c, m.v.x));
   const float du = fabsf(u - floorf(u) - 0.5f), dv = fabsf(v - floorf(v) - 0.5f);
-  if (du <= a.eu || dv <= a.ev) return kAmbiguous;
+  if (du <= m.eu || dv <= m.ev) return kAmbiguous;
   const float ru = rintf(u), rv = rintf(v);
-  if (!(ru >= 0.f && ru < (float)a.W && rv >= 0.f && rv < (float)a.H)) return kInvisible;
-  const float stored = __ldg(depth + a.depth_off + (int64_t)rv * a.W + (int64_t)ru);
+  if (!(ru >= 0.f && ru < (float)m.W && rv >= 0.f && rv < (float)m.H)) return kInvisible;
+  const float stored = __ldg(depth + m.depth_off + (int64_t)rv * m.W + (int64_t)ru);
   if (!(stored > 0.f)) return kInvisible;
-  const float z = fmaf(a.z.w, dz, fmaf(a.z.z, dy, fmaf(a.z.y, dx, a.z.x)));
+  const float z = m.z0 + b;
   const float thr = __fadd_rn(stored, eps_f);
-  const float m = a.ez + 2.4e-7f * fabsf(thr) + 1e-9f;
-  if (z + m < thr) return kNeedDepth;  // visible
-  if (z - m > thr) return kInvisible;
+  const float mz = m.ez + 2.4e-7f * fabsf(thr) + 1e-9f;
+  if (z + mz < thr) return kNeedDepth;  // visible
+  if (z - mz > thr) return kInvisible;
   return kAmbiguous;
 }
 
