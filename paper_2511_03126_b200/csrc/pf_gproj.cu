@@ -1,6 +1,6 @@
 // G = fmap @ text^T on the tensor cores for the bf16 tile path (the per-object table behind the
 // similarity-by-associativity, see pf_tile.cu): one CTA per 128 feature cells, K = D streamed in
-// 64-channel chunks through a 2-stage cp.async ring, tcgen05.mma (M=128, N=kpadg, K=16) into TMEM,
+// 64-channel chunks through a 3-stage cp.async ring, tcgen05.mma (M=128, N=kpadg, K=16) into TMEM,
 // epilogue writes G in bf16 (cells x kpadg, the tile kernel's S operand) and fp32 (cells x kpad,
 // the SIMT overflow path). The text rows are rounded to bf16 once (k_text_bf16; bf16-feature mode
 // bar 1e-2) and streamed with cp.async like the map rows; the MMAs are issued warp-uniformly.
@@ -14,7 +14,10 @@ namespace pf {
 namespace tile {
 namespace {
 
-constexpr int kGM = 128;  // cells per CTA
+constexpr int kGM = 128;     // cells per CTA
+constexpr int kGStages = 3;  // cp.async ring depth (2 CTAs per SM)
+
+__device__ __forceinline__ int lane_of(int tid) { return tid & 31; }
 
 __global__ void k_text_bf16(const float* __restrict__ text, int k, int kpadg, int d, uint16_t* __restrict__ out) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)kpadg * d;
@@ -34,7 +37,7 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
   // stage s: A [128 rows x 64 ch] (16 KB, K-major SW128) then B [kpadg rows x 64 ch] (K-major SW128)
   const int b_bytes = kpadg * 128;
   const int stage_bytes = 16384 + b_bytes;
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t mbar[kGStages];  // MMA completion per ring stage
   __shared__ uint32_t tmem_base_s;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * kGM;
@@ -59,7 +62,7 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  if (tid == 0) tc::mbar_init(&mbar, 1);
+  if (tid < kGStages) tc::mbar_init(&mbar[tid], 1);
   uint32_t ncols = 32;
   while (ncols < (uint32_t)kpadg) ncols <<= 1;
   if (warp == 0) tc::tmem_alloc(&tmem_base_s, ncols);
@@ -69,11 +72,12 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
   const uint32_t tbase = tmem_base_s;
   const uint32_t idesc = tc::idesc_bf16_f32(128, kpadg, false, false);
 
-  load(0, 0);
-  uint32_t phase = 0;
+  // 3-stage ring: chunks ch+1 and ch+2 are in flight while chunk ch's MMAs run
+  for (int c = 0; c < kGStages - 1 && c < nchunk; ++c) load(c, c);
   for (int ch = 0; ch < nchunk; ++ch) {
-    const int st = ch & 1;
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    const int st = ch % kGStages;
+    if (ch + 1 < nchunk) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
     tc::fence_async_shared();
     tc::fence_before_sync();
     __syncthreads();
@@ -86,26 +90,34 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
         const uint64_t bd = tc::smem_desc_sw128(b0 + s * 32, 16, 1024);
         tc::mma_bf16_ss_elect(tbase, ad, bd, idesc, (ch | s) ? 1u : 0u);
       }
-      tc::mma_commit_elect(&mbar);
+      tc::mma_commit_elect(&mbar[st]);
     }
-    // stage st^1 was read by the MMAs of chunk ch-1, which completed (waited below last iteration)
-    if (ch + 1 < nchunk) load(ch + 1, st ^ 1);
-    tc::mbar_wait(&mbar, phase);
-    phase ^= 1u;
+    // chunk ch+2 refills the stage of chunk ch-1 once that chunk's MMAs have completed
+    if (ch + kGStages - 1 < nchunk) {
+      if (ch >= 1) tc::mbar_wait(&mbar[(ch - 1) % kGStages], (uint32_t)(((ch - 1) / kGStages) & 1));
+      load(ch + kGStages - 1, (ch + kGStages - 1) % kGStages);
+    }
   }
+  tc::mbar_wait(&mbar[(nchunk - 1) % kGStages], (uint32_t)(((nchunk - 1) / kGStages) & 1));
   tc::fence_after_sync();
-  const int64_t cell = c0 + tid;
+  // epilogue through shared memory (the ring is free): TMEM row -> smem row, then each warp writes
+  // whole rows of G (coalesced) instead of every thread striding through its own row
+  float* srow = reinterpret_cast<float*>(smem);  // [128][kpadg + 1]
+  const int ld = kpadg + 1;
   for (int cc = 0; cc < kpadg; cc += 32) {
     float v[32];
     tc::tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + cc, v);
-    if (cell < cells) {
 #pragma unroll
-      for (int q = 0; q < 32; q += 2) {
-        const __nv_bfloat162 b = __floats2bfloat162_rn(v[q], v[q + 1]);
-        *reinterpret_cast<__nv_bfloat162*>(Gbf + cell * kpadg + cc + q) = b;
-      }
-      if (G32)
-        for (int q = 0; q < 32 && cc + q < kpad; ++q) G32[cell * kpad + cc + q] = cc + q < k ? v[q] : 0.f;
+    for (int q = 0; q < 32; ++q) srow[tid * ld + cc + q] = v[q];
+  }
+  __syncthreads();
+  for (int r = warp; r < kGM; r += 4) {
+    const int64_t cell = c0 + r;
+    if (cell >= cells) break;
+    for (int c = lane_of(tid); c < kpadg; c += 32) {
+      const float val = srow[r * ld + c];
+      Gbf[cell * kpadg + c] = __bfloat16_as_ushort(__float2bfloat16_rn(val));
+      if (G32 && c < kpad) G32[cell * kpad + c] = c < k ? val : 0.f;
     }
   }
   tc::fence_before_sync();
@@ -120,7 +132,7 @@ int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int 
   if (d % 64 != 0 || kpadg % 16 != 0 || kpadg > 256) return -1;
   k_text_bf16<<<grid_for((int64_t)kpadg * d, 256), 256, 0, st>>>(text, k, kpadg, d, textbf);
   if (int rc = check_launch("text_bf16")) return rc;
-  const size_t smem = 2 * (16384 + (size_t)kpadg * 128) + 1024;
+  const size_t smem = kGStages * (16384 + (size_t)kpadg * 128) + 1024;
   cudaFuncSetAttribute(k_gproj_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const unsigned grid = (unsigned)((cells + kGM - 1) / kGM);
   k_gproj_tc<<<grid, 128, smem, st>>>(reinterpret_cast<const uint16_t*>(fmap), cells, d, textbf, k, kpadg, kpad,
