@@ -477,12 +477,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const int ktp = ktp_of(kt, ok);
       if (!ok) continue;
       if (bh == 0 && P.vox_list) {
-        // touched-voxel list without returning atomics: slot jpt holds the code when this row starts
-        // a run of equal codes within its warp (sorted neighbours mostly share a voxel), else -1;
-        // pf_voxel_mass_sparse claims each voxel once (atomicExch on its count)
-        const int32_t prev = __shfl_up_sync(0xffffffffu, cd, 1);
+        // touched-voxel list without returning atomics: slot jpt holds the code when this row is the
+        // lowest lane of its warp with that code (a warp's sorted points share a few voxels), else
+        // -1; pf_voxel_mass_sparse claims each voxel once (atomicExch on its count)
+        const uint32_t peers = __match_any_sync(0xffffffffu, cd);
+        const bool first = (peers & ((1u << lane) - 1u)) == 0u;
         int64_t jr;
-        if (cd >= 0 && item_row(P, tile, ntiles, row, jr)) P.vox_list[jr] = (lane == 0 || prev != cd) ? cd : -1;
+        if (cd >= 0 && item_row(P, tile, ntiles, row, jr)) P.vox_list[jr] = first ? cd : -1;
       }
       if (bt == 0) WS_TRACE(t_local, 0);
       const int ab = (int)(t_local & 1u);
