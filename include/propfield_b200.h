@@ -35,7 +35,8 @@ enum pf_status {
   PF_ERR_VALUE = 1,     /* bad scalar argument, e.g. temperature <= 0 (grounding.py:170-171) */
   PF_ERR_STRUCTURE = 2, /* inconsistent shapes / unsupported layout (bundle.py:45-55,105-116)   */
   PF_ERR_MATERIAL = 3,  /* NaN similarity / missing property (grounding.py:69-72,173-174)       */
-  PF_ERR_CUDA = 4       /* CUDA runtime failure (no reference twin)                             */
+  PF_ERR_CUDA = 4,      /* CUDA runtime failure (no reference twin)                             */
+  PF_ERR_LOAD = 5       /* missing / unreadable file (BundleLoadError, tensorio.py:44-47)       */
 };
 
 enum pf_dtype { PF_F32 = 0, PF_BF16 = 1, PF_F64 = 2 };
@@ -226,6 +227,22 @@ uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* args);
  * by associativity, see csrc/pf_fused.cu). pf_fuse_query runs it itself unless PF_FUSE_PREPARED. */
 int pf_fuse_prepare(const pf_fuse_args_t* args, void* stream);
 int pf_fuse_query(const pf_fuse_args_t* args, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Capture-bundle ingest, host only: the reference's blob formats into caller-provided
+ * (pinned) host buffers; the caller uploads them (paper_2511_03126_b200/ingest.py).
+ * ------------------------------------------------------------------------------------------- */
+
+/* TB32 blob header (tensorio.read_tensor, tensorio.py:40-64): rank and dims[4] (0 past the rank).
+ * PF_ERR_LOAD if missing, PF_ERR_STRUCTURE with the reference's messages if malformed. */
+int pf_tb32_info(const char* path, int32_t* rank, int64_t* dims);
+/* TB32 payload (little-endian f32, rank-major) into dst (capacity floats). */
+int pf_tb32_read(const char* path, float* dst, int64_t capacity);
+/* binary_little_endian PLY (ply.read_ply, ply.py:80-139): vertex count and whether red/green/blue
+ * exist. */
+int pf_ply_info(const char* path, int64_t* n, int32_t* has_colors);
+/* x, y, z -> positions (n, 3) f32; colors (n, 3) u8 when non-null and present. */
+int pf_ply_read_points(const char* path, float* positions, uint8_t* colors, int64_t capacity);
 
 /* ---------------------------------------------------------------------------------------------
  * Densification, fp64 like the reference.

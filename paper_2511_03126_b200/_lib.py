@@ -15,13 +15,13 @@ import threading
 
 import numpy as np
 
-from .errors import BundleStructureError, CudaError, MaterialError
+from .errors import BundleLoadError, BundleStructureError, CudaError, MaterialError
 
 _LIB_NAME = "libpropfield_b200.so"
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", _LIB_NAME)
 
-PF_OK, PF_ERR_VALUE, PF_ERR_STRUCTURE, PF_ERR_MATERIAL, PF_ERR_CUDA = 0, 1, 2, 3, 4
+PF_OK, PF_ERR_VALUE, PF_ERR_STRUCTURE, PF_ERR_MATERIAL, PF_ERR_CUDA, PF_ERR_LOAD = 0, 1, 2, 3, 4, 5
 PF_F32, PF_BF16, PF_F64 = 0, 1, 2
 
 PF_FUSE_WRITE_FEATURES = 1
@@ -120,6 +120,10 @@ SIGNATURES = {
     "pf_knn_workspace_bytes": ([_I64], C.c_uint64),
     "pf_knn_kth_distance": ([_P, _I64, _I32, _P, _P, _P, _P], C.c_int),
     "pf_integrate_partials": ([_P, _I64, _I32, _P, _P, _P, _P, _P, _P], C.c_int),
+    "pf_tb32_info": ([C.c_char_p, _P, _P], C.c_int),
+    "pf_tb32_read": ([C.c_char_p, _P, _I64], C.c_int),
+    "pf_ply_info": ([C.c_char_p, _P, _P], C.c_int),
+    "pf_ply_read_points": ([C.c_char_p, _P, _P, _I64], C.c_int),
     "pf_dino_knn_workspace_bytes": ([_I64, _I64, _I32], C.c_uint64),
     "pf_dino_knn_interpolate": ([_P, _I64, _P, _I64, _I32, _P, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "pf_nearest_index": ([_P, _I64, _P, _I64, _P, _P], C.c_int),
@@ -174,6 +178,8 @@ def check(status: int) -> None:
         raise BundleStructureError(msg)
     if status == PF_ERR_MATERIAL:
         raise MaterialError(msg)
+    if status == PF_ERR_LOAD:
+        raise BundleLoadError(msg)
     raise CudaError(msg)
 
 

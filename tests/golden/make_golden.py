@@ -155,6 +155,50 @@ def densify_golden():
     return out
 
 
+def bundle_golden(out_dir):
+    """A tiny capture bundle written by the reference's own save_bundle (bundle.py:262-305): 3 views
+    of 48x48 depth / 6x6x32 features, 300 points with colours, materials and reference poses."""
+    import shutil
+
+    from propfield.bundle import CameraPose, CaptureBundle, Intrinsics, PointCloud, ViewRecord, save_bundle
+    from propfield.grounding import MaterialDictionary, MaterialEntry
+
+    rng = np.random.default_rng(21)
+    pts = workloads.sample_ellipsoid(rng, 300, (0.3, 0.25, 0.2)).astype(np.float32)
+    intr = Intrinsics(fx=48.0, fy=48.0, cx=24.0, cy=24.0)
+    views, ref = [], []
+    for j, az in enumerate((0.0, 2.1, 4.2)):
+        eye = np.array([1.5 * np.cos(az), 1.5 * np.sin(az), 0.5])
+        pose = workloads.look_at_pose(np.zeros(3), eye)
+        cam = CameraPose(rotation=pose.rotation, translation=pose.translation)
+        ref.append(cam)
+        depth = workloads.splat_depth(pts.astype(np.float64), pose, intr, 48, 48)
+        feat = rng.standard_normal((6, 6, 32)).astype(np.float32)
+        img = rng.integers(0, 255, (48, 48, 3), dtype=np.uint8)
+        views.append(ViewRecord(image=img, depth=depth, camera=cam, intrinsics=intr, feature_map=feat))
+    cloud = PointCloud(positions=pts, colors=rng.integers(0, 255, (300, 3), dtype=np.uint8))
+    mats = MaterialDictionary(entries=[
+        MaterialEntry(name="wood", properties={"density": (500.0, 700.0), "hardness": (0.3, 0.3)}, thickness_m=0.02),
+        MaterialEntry(name="steel", properties={"density": (7800.0, 7800.0), "hardness": (0.9, 0.95)},
+                      thickness_m=0.002)])
+    bundle = CaptureBundle(views=views, point_cloud=cloud, reference_poses=ref, material_dictionary=mats,
+                           scene_id="tiny", gt_mass_kg=1.25)
+    if os.path.isdir(out_dir):
+        shutil.rmtree(out_dir)
+    save_bundle(bundle, out_dir)
+    # what the reference's load_bundle returns for it (pins the native readers in tests/test_ingest.py)
+    from propfield.bundle import load_bundle
+
+    back = load_bundle(out_dir)
+    np.savez_compressed(out_dir + ".npz", depth=np.stack([v.depth for v in back.views]),
+                        features=np.stack([v.feature_map for v in back.views]),
+                        positions=back.point_cloud.positions, colors=back.point_cloud.colors,
+                        rotations=np.stack([v.camera.rotation for v in back.views]),
+                        translations=np.stack([v.camera.translation for v in back.views]),
+                        intrinsics=np.array([[v.intrinsics.fx, v.intrinsics.fy, v.intrinsics.cx, v.intrinsics.cy]
+                                             for v in back.views]))
+
+
 def main():
     import propfield  # noqa: F401  (the unmodified reference)
     from propfield import grounding
@@ -163,6 +207,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernels_golden(numpy_impl))
     np.savez_compressed(os.path.join(HERE, "grounding.npz"), **grounding_golden(grounding))
     np.savez_compressed(os.path.join(HERE, "densify.npz"), **densify_golden())
+    bundle_golden(os.path.join(HERE, "bundle_tiny"))
     for name in ("mini", "mini_bf16"):
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **pipeline_golden(name, propfield))
     for f in sorted(os.listdir(HERE)):
