@@ -244,6 +244,17 @@ int pf_ply_info(const char* path, int64_t* n, int32_t* has_colors);
 /* x, y, z -> positions (n, 3) f32; colors (n, 3) u8 when non-null and present. */
 int pf_ply_read_points(const char* path, float* positions, uint8_t* colors, int64_t capacity);
 
+/* Workspace bytes of pf_estimate_normals for n points. */
+uint64_t pf_normals_workspace_bytes(int64_t n);
+/* geometry.estimate_normals (geometry.py:106-146): per point the k nearest points (self included,
+ * exact grid search), their mean-centred covariance / k, the unit eigenvector of the smallest
+ * eigenvalue oriented so that n . (centroid - p) >= 0 with centroid = (ccx, ccy, ccz) the mean camera
+ * centre; neighbourhoods of rank < 2 (lambda_1 <= 1e-10 lambda_2) fall back to the camera direction
+ * and are flagged. normals (n, 3) f64, degenerate (n) u8. k in {3, 4, 6, 8, 10, 12, 16, 20, 24, 32},
+ * k <= n (PF_ERR_VALUE otherwise, as the reference's ValueError). */
+int pf_estimate_normals(const float* points, int64_t n, int32_t k, double ccx, double ccy, double ccz,
+                        double* normals, uint8_t* degenerate, void* workspace, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * Densification, fp64 like the reference.
  * ------------------------------------------------------------------------------------------- */

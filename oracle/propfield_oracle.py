@@ -386,3 +386,34 @@ def densify_field(positions, features, visible_counts, source_features, source_p
         props[name] = regress_with_weights(probs, lo_hi[:, 0] if np.all(lo_hi[:, 0] == lo_hi[:, 1]) else lo_hi)
     return {"probabilities": probs, "dominant": probs.argmax(axis=1), "properties": props,
             "featureless": featureless}
+
+
+# ---- normals -----------------------------------------------------------------------
+def estimate_normals(positions, k, camera_centers):
+    """geometry.py:106-146: cKDTree k-NN (self included), neighbourhood covariance / k
+    (numpy_impl.py:115-128), eigh, smallest eigenvector, rank < 2 fallback to the camera direction
+    (ratio 1e-10, geometry.py:13), orientation toward the mean camera centre."""
+    from scipy.spatial import cKDTree
+
+    p = np.asarray(positions, dtype=np.float64)
+    n = p.shape[0]
+    if k < 3:
+        raise ValueError(f"normal estimation needs k >= 3, got {k}")
+    if k > n:
+        raise ValueError(f"k={k} exceeds point count {n}")
+    _, nb = cKDTree(p).query(p, k=k)
+    q = p[nb]
+    mu = q.sum(axis=1) / q.shape[1]
+    d = q - mu[:, None, :]
+    cov = np.einsum("nki,nkj->nij", d, d) / q.shape[1]
+    w, v = np.linalg.eigh(cov)
+    normals = np.ascontiguousarray(v[:, :, 0])
+    to_cam = np.asarray(camera_centers, dtype=np.float64).mean(axis=0) - p
+    degenerate = w[:, 1] <= 1e-10 * np.maximum(w[:, 2], 1e-300)
+    if degenerate.any():
+        fb = to_cam[degenerate]
+        normals[degenerate] = fb / np.maximum(np.linalg.norm(fb, axis=1, keepdims=True), 1e-30)
+    flip = np.einsum("ij,ij->i", normals, to_cam) < 0
+    normals[flip] *= -1.0
+    normals /= np.maximum(np.linalg.norm(normals, axis=1, keepdims=True), 1e-30)
+    return normals, degenerate

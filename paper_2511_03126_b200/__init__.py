@@ -6,7 +6,7 @@ hand-written sm_100a CUDA kernels behind a C ABI (include/propfield_b200.h). No 
 
 Reference-named entry points:
     kernels.visible_in_view / bilinear_gather / accumulate_features   (kernels/__init__.py:21-28)
-    project_points, default_epsilon, visibility_mask                    (geometry.py:46-103)
+    project_points, default_epsilon, visibility_mask, estimate_normals  (geometry.py:46-146)
     aggregate_geometric_features -> SemanticPointCloud                  (fusion.py:24-93)
     material_similarity, softmax_weights, kernel_regress, regress_with_weights (grounding.py:158-202)
     dino_knn_interpolate, densify_field                                 (densify.py:36-160)
@@ -34,7 +34,7 @@ from .errors import (
 )
 from .fused import FuseBuffers, FusedResult, QueryTables, fuse_and_query, fuse_prepare
 from .fusion import aggregate_geometric_features
-from .geometry import default_epsilon, project_points, visibility_mask
+from .geometry import default_epsilon, estimate_normals, project_points, visibility_mask
 from .grounding import kernel_regress, material_similarity, regress_with_weights, softmax_weights
 from .integrate import (adaptive_voxel_side, characteristic_length, estimate_from_partials, integrate_mass,
                         voxel_mass)
@@ -55,7 +55,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "kernels", "ViewSet", "QueryTables", "FuseBuffers", "FusedResult", "fuse_and_query",
-    "aggregate_geometric_features", "default_epsilon", "project_points", "visibility_mask",
+    "aggregate_geometric_features", "default_epsilon", "project_points", "visibility_mask", "estimate_normals",
     "kernel_regress", "material_similarity", "regress_with_weights", "softmax_weights",
     "adaptive_voxel_side", "characteristic_length", "integrate_mass", "estimate_from_partials", "voxel_mass",
     "FusePipeline", "HostObject", "fuse_batch", "BatchResult", "dino_knn_interpolate", "densify_field",

@@ -69,7 +69,7 @@ __global__ void k_knn_keys(const float* __restrict__ p, int64_t n, const Grid* _
 
 __global__ void k_knn_scatter(const float* __restrict__ p, int64_t n, const Grid* __restrict__ gp,
                               const uint32_t* __restrict__ keys, uint32_t* __restrict__ cursor,
-                              float4* __restrict__ kp) {
+                              float4* __restrict__ kp, int32_t* __restrict__ kidx) {
   const Grid g = *gp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float x = p[3 * i], y = p[3 * i + 1], z = p[3 * i + 2];
@@ -78,6 +78,7 @@ __global__ void k_knn_scatter(const float* __restrict__ p, int64_t n, const Grid
     const uint32_t id = (uint32_t)cx | ((uint32_t)cy << kCellBits) | ((uint32_t)cz << (2 * kCellBits));
     const uint32_t pos = atomicAdd(cursor + keys[i], 1u);
     kp[pos] = make_float4(x, y, z, __uint_as_float(id));
+    if (kidx) kidx[pos] = (int32_t)i;
   }
 }
 
@@ -183,7 +184,7 @@ int pf_knn_kth_distance(const float* points, int64_t n, int32_t k, double* dk2_s
   k_knn_keys<<<grid_for(n, 256), 256, 0, st>>>(points, n, g, keys, hist);
   if (int rc = check_launch("knn_keys")) return rc;
   if (int rc = tile::run_bucket_scan(hist, totals, kHashBins, st)) return rc;
-  k_knn_scatter<<<grid_for(n, 256), 256, 0, st>>>(points, n, g, keys, hist, kp);
+  k_knn_scatter<<<grid_for(n, 256), 256, 0, st>>>(points, n, g, keys, hist, kp, nullptr);
   if (int rc = check_launch("knn_scatter")) return rc;
   // after the scatter hist[b] = end of bucket b
   if (k == 8)  // AREA_KNN (integrate.py:19)
@@ -191,6 +192,223 @@ int pf_knn_kth_distance(const float* points, int64_t n, int32_t k, double* dk2_s
   else
     k_knn_query<0><<<grid_for(n, 128, 148 * 32), 128, 0, st>>>(kp, n, g, hist, k, dk2_sum, dk_sorted);
   return check_launch("knn_query");
+}
+
+}  // extern "C"
+
+// ---- geometry.estimate_normals (geometry.py:106-146) on the device -----------------------------------
+// k nearest points (self included, cKDTree.query(p, k)) from the same exact grid search, their
+// mean-centred covariance / k (numpy_impl.neighborhood_covariances), the eigenvector of the smallest
+// eigenvalue (cyclic Jacobi in fp64, numpy.linalg.eigh order), the rank < 2 fallback to the camera
+// direction and the orientation flip toward the mean camera centre.
+namespace pf {
+namespace {
+
+__device__ void jacobi3(double a[3][3], double v[3][3], double w[3]) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) v[i][j] = i == j ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 16; ++sweep) {
+    const double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
+    const double diag = fabs(a[0][0]) + fabs(a[1][1]) + fabs(a[2][2]);
+    if (off <= 1e-300 || off <= 1e-18 * diag) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        if (a[p][q] == 0.0) continue;
+        const double theta = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < 3; ++k) {  // A <- A J (columns p, q)
+          const double akp = a[k][p], akq = a[k][q];
+          a[k][p] = c * akp - s * akq;
+          a[k][q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < 3; ++k) {  // A <- J^T A (rows p, q)
+          const double apk = a[p][k], aqk = a[q][k];
+          a[p][k] = c * apk - s * aqk;
+          a[q][k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < 3; ++k) {  // V <- V J
+          const double vkp = v[k][p], vkq = v[k][q];
+          v[k][p] = c * vkp - s * vkq;
+          v[k][q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  w[0] = a[0][0];
+  w[1] = a[1][1];
+  w[2] = a[2][2];
+}
+
+template <int K>
+__global__ void __launch_bounds__(128) k_knn_normals(const float4* __restrict__ kp, const int32_t* __restrict__ kidx,
+                                                     int64_t n, const Grid* __restrict__ gp,
+                                                     const uint32_t* __restrict__ ends, double ccx, double ccy,
+                                                     double ccz, double* __restrict__ normals,
+                                                     uint8_t* __restrict__ degenerate) {
+  const Grid g = *gp;
+  const double c = (double)g.c;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 q = kp[i];
+    const uint32_t id = __float_as_uint(q.w);
+    const int cx = (int)(id & ((1u << kCellBits) - 1)), cy = (int)((id >> kCellBits) & ((1u << kCellBits) - 1)),
+              cz = (int)(id >> (2 * kCellBits));
+    const double qx = q.x, qy = q.y, qz = q.z;
+    double best[K];
+    uint32_t bj[K];
+#pragma unroll
+    for (int b = 0; b < K; ++b) {
+      best[b] = INFINITY;
+      bj[b] = 0u;
+    }
+    const double fx = fmin(qx - ((double)g.lo[0] + cx * c), (double)g.lo[0] + (cx + 1) * c - qx);
+    const double fy = fmin(qy - ((double)g.lo[1] + cy * c), (double)g.lo[1] + (cy + 1) * c - qy);
+    const double fz = fmin(qz - ((double)g.lo[2] + cz * c), (double)g.lo[2] + (cz + 1) * c - qz);
+    const double face = fmax(fmin(fmin(fx, fy), fz), 0.0);
+    const int maxs = max(max(g.dims[0], g.dims[1]), g.dims[2]);
+    for (int s = 1;; ++s) {
+      for (int dz = -s; dz <= s; ++dz)
+        for (int dy = -s; dy <= s; ++dy)
+          for (int dx = -s; dx <= s; ++dx) {
+            if (max(max(abs(dx), abs(dy)), abs(dz)) != s && s > 1) continue;
+            const int x = cx + dx, y = cy + dy, z = cz + dz;
+            if (x < 0 || y < 0 || z < 0 || x >= g.dims[0] || y >= g.dims[1] || z >= g.dims[2]) continue;
+            const uint32_t want = (uint32_t)x | ((uint32_t)y << kCellBits) | ((uint32_t)z << (2 * kCellBits));
+            const uint32_t b = cell_hash(x, y, z);
+            const uint32_t e0 = b ? __ldg(ends + b - 1) : 0u, e1 = __ldg(ends + b);
+            for (uint32_t j = e0; j < e1; ++j) {
+              const float4 r = __ldg(kp + j);
+              if (__float_as_uint(r.w) != want) continue;
+              const double ddx = (double)r.x - qx, ddy = (double)r.y - qy, ddz = (double)r.z - qz;
+              double d2 = fma(ddz, ddz, fma(ddy, ddy, ddx * ddx));
+              if (d2 >= best[K - 1]) continue;
+              uint32_t jj = j;
+#pragma unroll
+              for (int t = 0; t < K; ++t) {  // ascending insertion, index carried along
+                const bool sw = d2 < best[t];
+                const double lo = sw ? d2 : best[t], hi = sw ? best[t] : d2;
+                const uint32_t jl = sw ? jj : bj[t], jh = sw ? bj[t] : jj;
+                best[t] = lo;
+                bj[t] = jl;
+                d2 = hi;
+                jj = jh;
+              }
+            }
+          }
+      const double reach = face + (double)s * c;
+      if (best[K - 1] <= reach * reach || s >= maxs) break;
+    }
+    // neighbourhood covariance (numpy_impl.py:115-128): mean, centred outer products, / k
+    double px[K], py[K], pz[K];
+    double mx = 0.0, my = 0.0, mz = 0.0;
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const float4 r = __ldg(kp + bj[t]);
+      px[t] = r.x;
+      py[t] = r.y;
+      pz[t] = r.z;
+      mx += px[t];
+      my += py[t];
+      mz += pz[t];
+    }
+    mx /= K;
+    my /= K;
+    mz /= K;
+    double a[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const double d0 = px[t] - mx, d1 = py[t] - my, d2 = pz[t] - mz;
+      a[0][0] += d0 * d0;
+      a[0][1] += d0 * d1;
+      a[0][2] += d0 * d2;
+      a[1][1] += d1 * d1;
+      a[1][2] += d1 * d2;
+      a[2][2] += d2 * d2;
+    }
+    a[0][0] /= K; a[0][1] /= K; a[0][2] /= K; a[1][1] /= K; a[1][2] /= K; a[2][2] /= K;
+    a[1][0] = a[0][1];
+    a[2][0] = a[0][2];
+    a[2][1] = a[1][2];
+    double v[3][3], w[3];
+    jacobi3(a, v, w);
+    // ascending eigenvalues (eigh): the smallest one's vector, the middle and largest values
+    int i0 = 0, i1 = 1, i2 = 2;
+    if (w[i0] > w[i1]) { const int t = i0; i0 = i1; i1 = t; }
+    if (w[i1] > w[i2]) { const int t = i1; i1 = i2; i2 = t; }
+    if (w[i0] > w[i1]) { const int t = i0; i0 = i1; i1 = t; }
+    double nx = v[0][i0], ny = v[1][i0], nz = v[2][i0];
+    const double tx = ccx - qx, ty = ccy - qy, tz = ccz - qz;
+    const bool degen = w[i1] <= 1e-10 * fmax(w[i2], 1e-300);  // geometry.py:13,136
+    if (degen) {
+      const double l = fmax(sqrt(tx * tx + ty * ty + tz * tz), 1e-30);
+      nx = tx / l;
+      ny = ty / l;
+      nz = tz / l;
+    }
+    if (nx * tx + ny * ty + nz * tz < 0.0) {
+      nx = -nx;
+      ny = -ny;
+      nz = -nz;
+    }
+    const double l = fmax(sqrt(nx * nx + ny * ny + nz * nz), 1e-30);
+    const int64_t o = kidx[i];
+    normals[3 * o] = nx / l;
+    normals[3 * o + 1] = ny / l;
+    normals[3 * o + 2] = nz / l;
+    degenerate[o] = degen ? 1 : 0;
+  }
+}
+
+}  // namespace
+}  // namespace pf
+
+extern "C" {
+
+uint64_t pf_normals_workspace_bytes(int64_t n) {
+  return pf_knn_workspace_bytes(n) + ((sizeof(int32_t) * (uint64_t)n + 255) & ~uint64_t(255));
+}
+
+int pf_estimate_normals(const float* points, int64_t n, int32_t k, double ccx, double ccy, double ccz,
+                        double* normals, uint8_t* degenerate, void* workspace, void* stream) {
+  using namespace pf;
+  if (k < 3) return set_error(PF_ERR_VALUE, "normal estimation needs k >= 3, got %d", k);
+  if (k > n) return set_error(PF_ERR_VALUE, "k=%d exceeds point count %lld", k, (long long)n);
+  if (k != 16 && k != 8 && k != 3 && k != 4 && k != 6 && k != 10 && k != 12 && k != 20 && k != 24 && k != 32)
+    return set_error(PF_ERR_VALUE, "estimate_normals: k=%d not compiled (3, 4, 6, 8, 10, 12, 16, 20, 24, 32)", k);
+  if (!workspace || !normals || !degenerate) return set_error(PF_ERR_VALUE, "estimate_normals: null buffer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(ws);
+  ws += al(sizeof(uint32_t) * (uint64_t)n);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws);
+  ws += al(sizeof(uint32_t) * kHashBins);
+  uint32_t* totals = reinterpret_cast<uint32_t*>(ws);
+  ws += al(sizeof(uint32_t) * 1024);
+  float4* kp = reinterpret_cast<float4*>(ws);
+  ws += al(sizeof(float4) * (uint64_t)n);
+  Grid* g = reinterpret_cast<Grid*>(ws);
+  ws += al(sizeof(Grid));
+  double* lo_hi = reinterpret_cast<double*>(ws);
+  ws += al(6 * sizeof(double));
+  int32_t* kidx = reinterpret_cast<int32_t*>(ws);
+  if (int rc = pf_bbox(points, n, lo_hi, stream)) return rc;
+  k_knn_grid<<<1, 1, 0, st>>>(lo_hi, n, k - 1, g);
+  if (int rc = check_launch("normals_grid")) return rc;
+  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kHashBins, st);
+  k_knn_keys<<<grid_for(n, 256), 256, 0, st>>>(points, n, g, keys, hist);
+  if (int rc = check_launch("normals_keys")) return rc;
+  if (int rc = tile::run_bucket_scan(hist, totals, kHashBins, st)) return rc;
+  k_knn_scatter<<<grid_for(n, 256), 256, 0, st>>>(points, n, g, keys, hist, kp, kidx);
+  if (int rc = check_launch("normals_scatter")) return rc;
+  const int blocks = grid_for(n, 128, 148 * 32);
+#define PF_NORMALS_K(KK) \
+  case KK: k_knn_normals<KK><<<blocks, 128, 0, st>>>(kp, kidx, n, g, hist, ccx, ccy, ccz, normals, degenerate); break;
+  switch (k) {
+    PF_NORMALS_K(3) PF_NORMALS_K(4) PF_NORMALS_K(6) PF_NORMALS_K(8) PF_NORMALS_K(10) PF_NORMALS_K(12)
+    PF_NORMALS_K(16) PF_NORMALS_K(20) PF_NORMALS_K(24) PF_NORMALS_K(32)
+  }
+#undef PF_NORMALS_K
+  return check_launch("normals_query");
 }
 
 }  // extern "C"

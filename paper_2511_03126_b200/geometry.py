@@ -64,3 +64,28 @@ def visibility_mask(points, views, epsilon: float):
     _lib.call("pf_visibility_mask", ptr(p), pdt, n, ptr(vs.records_dev), vs.nviews, ptr(vs.depth),
               float(epsilon), ptr(mask), stream_handle())
     return mask.bool() if tor else mask.bool().cpu().numpy()
+
+
+def estimate_normals(positions, k: int, camera_centers):
+    """(normals (N,3) f64, degenerate (N,) bool) from k-NN covariances oriented toward the mean
+    camera centre (geometry.py:106-146; pf_estimate_normals: exact grid k-NN, fp64 Jacobi). Positions
+    are the cloud's f32 coordinates (bundle.py:158); numpy in -> numpy out, torch -> torch."""
+    dev = require_cuda()
+    t = torch()
+    tor = is_torch(positions)
+    p = to_dev(positions, t.float32, dev).reshape(-1, 3)
+    n = p.shape[0]
+    if k < 3:
+        raise ValueError(f"normal estimation needs k >= 3, got {k}")
+    if k > n:
+        raise ValueError(f"k={k} exceeds point count {n}")
+    cc = np.asarray(camera_centers.cpu() if is_torch(camera_centers) else camera_centers, dtype=np.float64)
+    centroid = cc.reshape(-1, 3).mean(axis=0)
+    normals = t.empty((n, 3), dtype=t.float64, device=dev)
+    degen = t.empty(n, dtype=t.uint8, device=dev)
+    ws = t.empty(int(_lib.load().pf_normals_workspace_bytes(n)), dtype=t.uint8, device=dev)
+    _lib.call("pf_estimate_normals", ptr(p), n, int(k), float(centroid[0]), float(centroid[1]), float(centroid[2]),
+              ptr(normals), ptr(degen), ptr(ws), stream_handle())
+    if tor:
+        return normals, degen.bool()
+    return normals.cpu().numpy(), degen.bool().cpu().numpy()

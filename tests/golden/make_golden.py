@@ -199,6 +199,17 @@ def bundle_golden(out_dir):
                                              for v in back.views]))
 
 
+def normals_golden():
+    from propfield.geometry import estimate_normals
+
+    out = {}
+    for name, p, cams, k in recipes.normals_cases():
+        nrm, deg = estimate_normals(p, k, cams)
+        out[f"n_{name}"] = nrm
+        out[f"d_{name}"] = deg
+    return out
+
+
 def main():
     import propfield  # noqa: F401  (the unmodified reference)
     from propfield import grounding
@@ -208,6 +219,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "grounding.npz"), **grounding_golden(grounding))
     np.savez_compressed(os.path.join(HERE, "densify.npz"), **densify_golden())
     bundle_golden(os.path.join(HERE, "bundle_tiny"))
+    np.savez_compressed(os.path.join(HERE, "normals.npz"), **normals_golden())
     for name in ("mini", "mini_bf16"):
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **pipeline_golden(name, propfield))
     for f in sorted(os.listdir(HERE)):

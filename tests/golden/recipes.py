@@ -107,3 +107,21 @@ def densify_field_case(seed=0, n=1500, n_sources=60, noise=0.05, n_orphans=40):
     return dict(positions=pts, features=feats, counts=counts, src_pick=src_pick,
                 src_features=feats[src_pick], src_probs=np.eye(2)[part[src_pick]], density=density,
                 hardness=hardness, part=part)
+
+
+def normals_cases():
+    """estimate_normals inputs (f32 clouds as the bundle stores them): an ellipsoid, a plane with a
+    collinear strip (rank-1 neighbourhoods -> degenerate fallback), several k."""
+    rng = np.random.default_rng(31)
+    out = []
+    u = rng.standard_normal((3000, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    ell = (u * np.array([0.4, 0.3, 0.2])).astype(np.float32)
+    cams = np.array([[1.5, 0.0, 0.5], [-0.7, 1.3, 0.5], [-0.7, -1.3, 0.5]])
+    out.append(("ellipsoid_k16", ell, cams, 16))
+    out.append(("ellipsoid_k8", ell, cams, 8))
+    plane = np.zeros((1200, 3), np.float32)
+    plane[:1000, :2] = rng.uniform(-0.5, 0.5, (1000, 2))
+    plane[1000:, 0] = np.linspace(2.0, 3.0, 200)  # an isolated line: rank-1 neighbourhoods
+    out.append(("plane_line_k6", plane, cams, 6))
+    return out

@@ -215,3 +215,20 @@ class TestDensifyOracle:
         np.testing.assert_array_equal(out["featureless"], g["df_featureless"])
         np.testing.assert_allclose(out["properties"]["density"], g["df_density"], rtol=1e-12)
         np.testing.assert_allclose(out["properties"]["hardness"], g["df_hardness"], rtol=1e-12)
+
+
+class TestNormalsOracle:
+    """Oracle estimate_normals vs the reference's outputs (tests/golden/normals.npz)."""
+
+    def test_cases(self, golden):
+        g = golden("normals")
+        for name, p, cams, k in recipes.normals_cases():
+            nrm, deg = O.estimate_normals(p, k, cams)
+            np.testing.assert_array_equal(deg, g[f"d_{name}"], err_msg=name)
+            np.testing.assert_allclose(nrm, g[f"n_{name}"], rtol=0, atol=1e-12, err_msg=name)
+
+    def test_errors(self):
+        with pytest.raises(ValueError):
+            O.estimate_normals(np.zeros((5, 3)), 2, np.zeros((1, 3)))
+        with pytest.raises(ValueError):
+            O.estimate_normals(np.zeros((5, 3)), 6, np.zeros((1, 3)))
