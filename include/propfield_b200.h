@@ -255,6 +255,13 @@ uint64_t pf_normals_workspace_bytes(int64_t n);
 int pf_estimate_normals(const float* points, int64_t n, int32_t k, double ccx, double ccy, double ccz,
                         double* normals, uint8_t* degenerate, void* workspace, void* stream);
 
+/* view_select.score_views + rank_views (view_select.py:51-124) for s anchors x nviews: (s, nviews)
+ * s_total / s_angle / z and (s, nviews, 2) pixels, f64; ranked (s, k) i32 = the k best visible
+ * views (visibility & z > 0) by (-s_total, view index), -1 padded. visibility (s, nviews) u8. */
+int pf_score_views(const double* positions, const double* normals, int64_t s, const pf_view_t* views,
+                   int32_t nviews, const uint8_t* visibility, double* s_total, double* s_angle, double* z,
+                   double* pixels, int32_t k, int32_t* ranked, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * Densification, fp64 like the reference.
  * ------------------------------------------------------------------------------------------- */

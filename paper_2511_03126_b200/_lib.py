@@ -122,6 +122,7 @@ SIGNATURES = {
     "pf_integrate_partials": ([_P, _I64, _I32, _P, _P, _P, _P, _P, _P], C.c_int),
     "pf_normals_workspace_bytes": ([_I64], C.c_uint64),
     "pf_estimate_normals": ([_P, _I64, _I32, _D, _D, _D, _P, _P, _P, _P], C.c_int),
+    "pf_score_views": ([_P, _P, _I64, _P, _I32, _P, _P, _P, _P, _P, _I32, _P, _P], C.c_int),
     "pf_tb32_info": ([C.c_char_p, _P, _P], C.c_int),
     "pf_tb32_read": ([C.c_char_p, _P, _I64], C.c_int),
     "pf_ply_info": ([C.c_char_p, _P, _P], C.c_int),

@@ -210,6 +210,31 @@ def normals_golden():
     return out
 
 
+def views_golden(propfield):
+    """score_views / rank_views (view_select.py:51-124) on 150 anchors of the `mini` workload."""
+    from propfield import geometry
+    from propfield.sampling import SourcePointSet
+    from propfield.view_select import rank_views, score_views
+
+    wl = workloads.generate("mini")
+    views = ref_views(wl, propfield)
+    pos = wl.points.astype(np.float64)
+    centers = np.stack([v.camera.center for v in views])
+    normals, _ = geometry.estimate_normals(pos, 16, centers)
+    idx = np.random.default_rng(5).choice(len(pos), 150, replace=False)
+    vis = geometry.visibility_mask(pos[idx], views, wl.cfg.eps)
+    vis[:3] = False  # anchors visible nowhere
+    src = SourcePointSet(indices=idx, positions=pos[idx], voxel_size=0.1, normals=normals[idx])
+    st, sa, z, px = score_views(src, views, vis)
+    ranks = rank_views(src, views, vis, 3)
+    ranked = np.full((150, 3), -1, np.int32)
+    for i, r in enumerate(ranks):
+        for q, e in enumerate(r):
+            ranked[i, q] = e.view_index
+    return dict(indices=idx, normals=normals[idx], visibility=vis, s_total=st, s_angle=sa, z=z, pixels=px,
+                ranked=ranked, zero_visible=src.flags["zero_visible"])
+
+
 def main():
     import propfield  # noqa: F401  (the unmodified reference)
     from propfield import grounding
@@ -220,6 +245,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "densify.npz"), **densify_golden())
     bundle_golden(os.path.join(HERE, "bundle_tiny"))
     np.savez_compressed(os.path.join(HERE, "normals.npz"), **normals_golden())
+    np.savez_compressed(os.path.join(HERE, "views.npz"), **views_golden(propfield))
     for name in ("mini", "mini_bf16"):
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **pipeline_golden(name, propfield))
     for f in sorted(os.listdir(HERE)):
