@@ -122,11 +122,27 @@ __global__ void k_vox_mass_sparse(float* __restrict__ grid, int64_t cells, const
       grid[c] = 0.0f;
     }
   }
+  // block reduction first: one pair of fp64 atomics per block (same-address fp64 atomics serialise
+  // in L2; one per warp cost ~0.1 ms at C5)
+  __shared__ double s_acc[32], s_occ[32];
   acc = warp_sum(acc);
   occ = warp_sum(occ);
-  if ((threadIdx.x & 31) == 0 && (acc != 0.0 || occ != 0.0)) {
-    atomicAdd(out, acc);
-    atomicAdd(out + 1, occ);
+  const int wid = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  if ((threadIdx.x & 31) == 0) {
+    s_acc[wid] = acc;
+    s_occ[wid] = occ;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, o = 0.0;
+    for (int q = 0; q < nw; ++q) {
+      a += s_acc[q];
+      o += s_occ[q];
+    }
+    if (a != 0.0 || o != 0.0) {
+      atomicAdd(out, a);
+      atomicAdd(out + 1, o);
+    }
   }
 }
 
