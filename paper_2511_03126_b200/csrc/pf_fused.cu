@@ -448,11 +448,21 @@ static uint64_t g_bytes(const pf_fuse_args_t* a) {
   return (g + 255) & ~uint64_t(255);
 }
 
+// SIMT path over >= this many points: points are visited in Hilbert order (neighbouring warps of a
+// block gather mostly the same taps, so the tap rows are served from L1 instead of L2)
+constexpr int64_t kSimtOrderMin = 65536;
+
+static uint64_t simt_order_bytes(int64_t n) {
+  return ((sizeof(int32_t) * (uint64_t)n + 255) & ~uint64_t(255)) + 256 + tile::point_order_bytes(n);
+}
+
 uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* a) {
   if (!a || !a->views_host || a->d <= 0 || a->k <= 0) return 0;
   uint64_t bytes = g_bytes(a);
   if (tile_path_ok(a))
     bytes += tile::tile_layout(a->n, a->nviews, total_cells(a), tile::kMaxKpadTC).bytes;
+  else if (a->n >= kSimtOrderMin)
+    bytes += simt_order_bytes(a->n);
   return bytes;
 }
 
@@ -581,6 +591,15 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     prm.list = T.ovf_list;
     prm.list_len = T.ovf_count;
     prm.vox_base = a->n;
+  } else if (a->n >= kSimtOrderMin) {
+    unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
+    int32_t* order = reinterpret_cast<int32_t*>(ws);
+    ws += (sizeof(int32_t) * (uint64_t)a->n + 255) & ~uint64_t(255);
+    int32_t* len = reinterpret_cast<int32_t*>(ws);
+    ws += 256;
+    if (int rc = tile::run_point_order(a->points, a->n, a->lo_hi, ws, order, len, st)) return rc;
+    prm.list = order;
+    prm.list_len = len;
   }
   int rc;
   if (a->fmap_dtype == PF_F32) {
@@ -597,7 +616,7 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     else if (d == 1024) rc = launch_fuse<PF_BF16, 8, 4>(prm, smem, st);
     else rc = launch_fuse<PF_BF16, 1, 32>(prm, smem, st);
   }
-  if (prm.list) stage_mark(5, st);
+  if (prm.list && prm.vox_base > 0) stage_mark(5, st);  // tile path: the overflow stage
   return rc;
 }
 

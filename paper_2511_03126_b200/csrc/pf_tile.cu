@@ -770,6 +770,30 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg) {
   return L;
 }
 
+__global__ void k_order_scatter(int64_t n, const uint32_t* __restrict__ keys, uint32_t* __restrict__ cursor,
+                                int32_t* __restrict__ order, int32_t* __restrict__ len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    order[atomicAdd(cursor + keys[i], 1u)] = (int32_t)i;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *len = (int32_t)n;
+}
+
+size_t point_order_bytes(int64_t n) {
+  return align256(sizeof(uint32_t) * (size_t)n) + align256(sizeof(uint32_t) << 21) + align256(sizeof(uint32_t) * 4096);
+}
+
+int run_point_order(const float* points, int64_t n, const double* lo_hi, unsigned char* ws, int32_t* order,
+                    int32_t* len, cudaStream_t st) {
+  uint32_t* keys = reinterpret_cast<uint32_t*>(ws);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws + align256(sizeof(uint32_t) * (size_t)n));
+  uint32_t* totals = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(hist) + align256(sizeof(uint32_t) << 21));
+  cudaMemsetAsync(hist, 0, sizeof(uint32_t) << 21, st);
+  k_sort_keys<<<grid_for(n, 256), 256, 0, st>>>(points, n, lo_hi, keys, hist, 7);
+  if (int rc = check_launch("order_keys")) return rc;
+  if (int rc = run_bucket_scan(hist, totals, int64_t(1) << 21, st)) return rc;
+  k_order_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, keys, hist, order, len);
+  return check_launch("order_scatter");
+}
+
 int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf, cudaStream_t st) {
   k_g_bf16<<<grid_for(cells * kpadg, 256), 256, 0, st>>>(G, cells, kpad, kpadg, Gbf);
   return check_launch("g_bf16");

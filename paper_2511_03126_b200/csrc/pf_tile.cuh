@@ -110,6 +110,11 @@ int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int 
                  uint16_t* Gbf, float* G32, uint16_t* textbf, cudaStream_t st);
 int ws_kt_max();
 int run_bucket_scan(uint32_t* hist, uint32_t* totals, int64_t nbins, cudaStream_t st);
+// Hilbert order of the points for the SIMT path: order[t] = index of the t-th point along the curve
+// (7-bit key over the domain lo_hi), and *len = n (the kernel's list length). ws: point_order_bytes.
+size_t point_order_bytes(int64_t n);
+int run_point_order(const float* points, int64_t n, const double* lo_hi, unsigned char* ws, int32_t* order,
+                    int32_t* len, cudaStream_t st);
 constexpr int kSubRows = 32;  // rows of a sub-tile
 
 }  // namespace tile
