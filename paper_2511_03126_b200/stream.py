@@ -44,6 +44,9 @@ class StreamResult:
 
 
 class FusePipeline:
+    LAG = 2   # objects issued ahead of the one being yielded
+    RING = 4  # host output buffers (> LAG + 1)
+
     def __init__(self, n: int, nviews: int, image_hw, fmap_shape, *, bf16: bool, k: int, p: int, grid: int,
                  temperature: float = 0.1, epsilon: float = 0.01, density_col: int = 0, device=None,
                  group=None, sharded: bool = False):
@@ -79,8 +82,10 @@ class FusePipeline:
         self.ev_h2d = [mk(), mk()]
         self.ev_comp = [mk(), mk()]
         self.ev_d2h = [mk(), mk()]
-        self.host_props = [t.empty((n, p), dtype=t.float32).pin_memory() for _ in range(2)]
-        self.host_mass = [t.empty(2, dtype=t.float64).pin_memory() for _ in range(2)]
+        # host output ring: a result stays valid while the next LAG objects are issued (the host never
+        # blocks on a download before the following uploads and computes are queued)
+        self.host_props = [t.empty((n, p), dtype=t.float32).pin_memory() for _ in range(self.RING)]
+        self.host_mass = [t.empty(2, dtype=t.float64).pin_memory() for _ in range(self.RING)]
         self.h2d_bytes = 0
         self.d2h_bytes = n * p * 4 + 16
         self.sharded, self.group = bool(sharded), group
@@ -128,6 +133,7 @@ class FusePipeline:
         pending = []
         for i, obj in enumerate(objects):
             slot = i & 1
+            hb = i % self.RING
             s = self.slots[slot]
             with t.cuda.stream(self.h2d):
                 if i == 0 and events is not None:
@@ -137,15 +143,16 @@ class FusePipeline:
                 self.ev_h2d[slot].record(self.h2d)
             with t.cuda.stream(self.comp):
                 self.comp.wait_event(self.ev_h2d[slot])
-                self.comp.wait_event(self.ev_d2h[slot])  # object i-2's outputs are on the host
+                self.comp.wait_event(self.ev_d2h[slot])  # object i-2's outputs have been downloaded
                 if self.sharded:
                     from .dist import cell_sharded_steps, run_dist
 
                     v, tb = s["views"], s["tables"]
                     out = run_dist(cell_sharded_steps(s["pts"], self.rank, self.world, s["ops"], k=tb.k, p=tb.p,
                                                       nwords=(v.nviews + 31) // 32), self.group)
-                    s["out"] = out  # keeps the result tensors alive until their download
                     props_dev, mass_dev = out.props, out.mass
+                    props_dev.record_stream(self.d2h)  # freed result tensors stay unreused until downloaded
+                    mass_dev.record_stream(self.d2h)
                 else:
                     bufs = s["bufs"]
                     bufs.reset()
@@ -156,17 +163,19 @@ class FusePipeline:
                 self.ev_comp[slot].record(self.comp)
             with t.cuda.stream(self.d2h):
                 self.d2h.wait_event(self.ev_comp[slot])
-                self.host_props[slot].copy_(props_dev, non_blocking=True)
-                self.host_mass[slot].copy_(mass_dev, non_blocking=True)
+                self.host_props[hb].copy_(props_dev, non_blocking=True)
+                self.host_mass[hb].copy_(mass_dev, non_blocking=True)
                 self.ev_d2h[slot].record(self.d2h)
-            pending.append((i, slot))
-            if len(pending) == 2:  # yield the older object once its download is done
-                j, sl = pending.pop(0)
-                self.ev_d2h[sl].synchronize()
-                yield StreamResult(j, self.host_props[sl], self.host_mass[sl])
+                done = t.cuda.Event()
+                done.record(self.d2h)
+            pending.append((i, hb, done))
+            if len(pending) > self.LAG:  # yield the oldest object once its download is done
+                j, h, ev = pending.pop(0)
+                ev.synchronize()
+                yield StreamResult(j, self.host_props[h], self.host_mass[h])
         if events is not None:
             with t.cuda.stream(self.d2h):
                 events[1].record(self.d2h)
-        for j, sl in pending:
-            self.ev_d2h[sl].synchronize()
-            yield StreamResult(j, self.host_props[sl], self.host_mass[sl])
+        for j, h, ev in pending:
+            ev.synchronize()
+            yield StreamResult(j, self.host_props[h], self.host_mass[h])
