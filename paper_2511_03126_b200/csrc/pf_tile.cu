@@ -225,7 +225,7 @@ struct ViewAff {
   float z0;
   float eu, ev, ez, pad;
   int W, H;
-  int64_t depth_off;
+  const float* dmap;     // this view's depth map
 };
 
 // Decide one view for every point of a tile at once. The points lie in the box [lo, hi] (exact:
@@ -336,7 +336,7 @@ __device__ int classify_tile_view(const ViewF& v, const float4& vb, const pf_vie
   aff.ez = 4.7e-7f * (fabsf((float)z0) + 2.f * r) + 1e-7f;  // z = z0 + b is exactly affine: rounding only
   aff.W = v.W;
   aff.H = v.H;
-  aff.depth_off = v.depth_off;
+  aff.dmap = depth + v.depth_off;
   if (!(aff.eu < 0.25f && aff.ev < 0.25f)) return kViewExact;
   return kViewMixed;
 }
@@ -409,9 +409,10 @@ __device__ __forceinline__ int affine_visible(const ViewAff& m, const float* __r
   const float v = fmaf(b, fmaf(m.q.y, b, fmaf(m.v.w, c, m.v.z)), fmaf(m.v.y, c, m.v.x));
   const float du = fabsf(u - floorf(u) - 0.5f), dv = fabsf(v - floorf(v) - 0.5f);
   if (du <= m.eu || dv <= m.ev) return kAmbiguous;
-  const float ru = rintf(u), rv = rintf(v);
-  if (!(ru >= 0.f && ru < (float)m.W && rv >= 0.f && rv < (float)m.H)) return kInvisible;
-  const float stored = __ldg(depth + m.depth_off + (int64_t)rv * m.W + (int64_t)ru);
+  // rint, then one unsigned compare per axis (finite u, v: the model of finite points)
+  const int iu = (int)rintf(u), iv = (int)rintf(v);
+  if ((unsigned)iu >= (unsigned)m.W || (unsigned)iv >= (unsigned)m.H) return kInvisible;
+  const float stored = __ldg(m.dmap + iv * m.W + iu);  // a view's map has < 2^31 pixels
   if (!(stored > 0.f)) return kInvisible;
   const float z = m.z0 + b;
   const float thr = __fadd_rn(stored, eps_f);
@@ -531,37 +532,30 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
   const int nmixed = s_nmixed, nexact = s_nexact;
   uint32_t w0 = s_full[0], w1 = s_full[1];
   const float dx = p.x - 0.5f * (lo[0] + hi[0]), dy = p.y - 0.5f * (lo[1] + hi[1]), dz = p.z - 0.5f * (lo[2] + hi[2]);
-  uint32_t seen0 = 0u, seen1 = 0u;  // MIXED views this warp saw visible somewhere
+  uint64_t wm = 0ull, seen = 0ull;  // this point's MIXED verdicts; MIXED views this warp saw visible
   for (int l = 0; l < nmixed; ++l) {
     const int v = s_list[l];
-    bool vis = false;
-    if (valid) {
-      int s = affine_visible(saff[v], P.depth, dx, dy, dz, eps_f);
-      if (P.dbg) {
-        atomicAdd(P.dbg + 16 * 1000 + 7, 1ull);
-        if (s == kAmbiguous) atomicAdd(P.dbg + 16 * 1000 + 8, 1ull);
-        if (tid == 0) {  // mean bounds
-          atomicAdd(P.dbg + 16 * 1000 + 9, (unsigned long long)(saff[v].eu * 1e6f));
-          atomicAdd(P.dbg + 16 * 1000 + 10, 1ull);
-        }
-      }
-      if (s == kAmbiguous) {
-        TapF t;
-        vis = point_visible(sv[v], sbound[v], P.views[v], P.depth, p, P.eps, eps_f, t);
-      } else {
-        vis = s == kNeedDepth;
+    const int s = valid ? affine_visible(saff[v], P.depth, dx, dy, dz, eps_f) : kInvisible;
+    if (P.dbg && valid) {
+      atomicAdd(P.dbg + 16 * 1000 + 7, 1ull);
+      if (s == kAmbiguous) atomicAdd(P.dbg + 16 * 1000 + 8, 1ull);
+      if (tid == 0) {  // mean bounds
+        atomicAdd(P.dbg + 16 * 1000 + 9, (unsigned long long)(saff[v].eu * 1e6f));
+        atomicAdd(P.dbg + 16 * 1000 + 10, 1ull);
       }
     }
-    const bool any = __any_sync(0xffffffffu, vis);
-    if (vis) {
-      if (v < 32) w0 |= 1u << v;
-      else w1 |= 1u << (v - 32);
+    bool vis = s == kNeedDepth;
+    if (s == kAmbiguous) {  // rare (0.1 % at C5): the exact test
+      TapF t;
+      vis = point_visible(sv[v], sbound[v], P.views[v], P.depth, p, P.eps, eps_f, t);
     }
-    if (any) {
-      if (v < 32) seen0 |= 1u << v;
-      else seen1 |= 1u << (v - 32);
-    }
+    const uint64_t bit = 1ull << v;
+    wm |= vis ? bit : 0ull;
+    seen |= __any_sync(0xffffffffu, vis) ? bit : 0ull;
   }
+  w0 |= (uint32_t)wm;
+  w1 |= (uint32_t)(wm >> 32);
+  const uint32_t seen0 = (uint32_t)seen, seen1 = (uint32_t)(seen >> 32);
   if (lane == 0 && (seen0 | seen1)) {
     atomicOr(&s_seen[0], seen0);
     atomicOr(&s_seen[1], seen1);
