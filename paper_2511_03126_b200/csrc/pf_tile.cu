@@ -224,6 +224,7 @@ struct ViewAff {
   float4 q;              // {u: b^2 coeff, v: b^2 coeff, v: d/dc, v: d/d(cb)}
   float z0;
   float eu, ev, ez, pad;
+  float hu, hv;          // 0.5 - eu, 0.5 - ev (rounded down)
   int W, H;
   const float* dmap;     // this view's depth map
 };
@@ -337,6 +338,9 @@ __device__ int classify_tile_view(const ViewF& v, const float4& vb, const pf_vie
   aff.W = v.W;
   aff.H = v.H;
   aff.dmap = depth + v.depth_off;
+  aff.hu = __fsub_rd(0.5f, aff.eu);
+  aff.hv = __fsub_rd(0.5f, aff.ev);
+  aff.ez = aff.ez * 1.0001f + 2e-9f;  // + the 1e-9 floor and the margin / difference roundings
   if (!(aff.eu < 0.25f && aff.ev < 0.25f)) return kViewExact;
   return kViewMixed;
 }
@@ -407,18 +411,20 @@ __device__ __forceinline__ int affine_visible(const ViewAff& m, const float* __r
   const float b = fmaf(m.r2.z, dz, fmaf(m.r2.y, dy, m.r2.x * dx));
   const float u = fmaf(b, fmaf(m.q.x, b, fmaf(m.u.w, a, m.u.z)), fmaf(m.u.y, a, m.u.x));
   const float v = fmaf(b, fmaf(m.q.y, b, fmaf(m.v.w, c, m.v.z)), fmaf(m.v.y, c, m.v.x));
-  const float du = fabsf(u - floorf(u) - 0.5f), dv = fabsf(v - floorf(v) - 0.5f);
-  if (du <= m.eu || dv <= m.ev) return kAmbiguous;
-  // rint, then one unsigned compare per axis (finite u, v: the model of finite points)
-  const int iu = (int)rintf(u), iv = (int)rintf(v);
+  // |u - rint(u)| (exact in fp32) >= 0.5 - eu  <=>  u within eu of a pixel boundary (m.pad: 0.5 - eu
+  // and 0.5 - ev rounded down)
+  const float ru = rintf(u), rv = rintf(v);
+  if (fabsf(u - ru) >= m.hu || fabsf(v - rv) >= m.hv) return kAmbiguous;
+  // one unsigned compare per axis (finite u, v: the model of finite points)
+  const int iu = (int)ru, iv = (int)rv;
   if ((unsigned)iu >= (unsigned)m.W || (unsigned)iv >= (unsigned)m.H) return kInvisible;
   const float stored = __ldg(m.dmap + iv * m.W + iu);  // a view's map has < 2^31 pixels
   if (!(stored > 0.f)) return kInvisible;
-  const float z = m.z0 + b;
-  const float thr = __fadd_rn(stored, eps_f);
-  const float mz = m.ez + 2.4e-7f * fabsf(thr) + 1e-9f;
-  if (z + mz < thr) return kNeedDepth;  // visible
-  if (z - mz > thr) return kInvisible;
+  const float thr = __fadd_rn(stored, eps_f);  // > 0
+  const float mz = fmaf(2.4e-7f, thr, m.ez);    // m.ez includes the 1e-9 floor
+  const float dz_ = (m.z0 + b) - thr;
+  if (dz_ < -mz) return kNeedDepth;  // visible (z + mz < thr, up to the margin's own rounding slack)
+  if (dz_ > mz) return kInvisible;
   return kAmbiguous;
 }
 
