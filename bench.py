@@ -55,6 +55,14 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def device_and_backend(local):
+    """cuda:LOCAL_RANK over NCCL. PF_BENCH_DEVICE / PF_BENCH_BACKEND override both for the
+    single-GPU smoke test of the multi-rank code path (gloo: every collective is a host-side step,
+    so ranks sharing one GPU never have kernels waiting on each other); never used for timing."""
+    dev_index = int(os.environ.get("PF_BENCH_DEVICE", local))
+    return dev_index, os.environ.get("PF_BENCH_BACKEND", "nccl")
+
+
 # ---------------------------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
@@ -191,12 +199,16 @@ def run_ours(args, cfg):
     import torch
 
     rank, world, local = env_rank()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev_index, backend = device_and_backend(local)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     import paper_2511_03126_b200 as pf
     from paper_2511_03126_b200 import _lib, workloads
     from paper_2511_03126_b200.dist import shard_range
@@ -270,7 +282,7 @@ def run_ours(args, cfg):
     mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     evs = [[mk() for _ in range(4)] for _ in range(args.steps)]
     starts = [mk() for _ in range(args.steps)]
-    clk = ClockSampler(local)
+    clk = ClockSampler(dev_index)
     clk.start()
     # soak: untimed steps for >= 0.8 s so the clock samples (200 ms period) see the GPU under load
     t_soak = time.time()
@@ -446,12 +458,16 @@ def run_batch(args, cfg):
     import torch
 
     rank, world, local = env_rank()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev_index, backend = device_and_backend(local)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     import paper_2511_03126_b200 as pf
     from paper_2511_03126_b200 import _lib, workloads
     from paper_2511_03126_b200.dist import shard_range
@@ -483,7 +499,7 @@ def run_batch(args, cfg):
         res, ws = pf.fuse_batch(pts, views, tables, workspace=ws, **kw)
     torch.cuda.synchronize()
     mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    clk = ClockSampler(local)
+    clk = ClockSampler(dev_index)
     clk.start()
     t_soak = time.time()
     while time.time() - t_soak < 0.8:
