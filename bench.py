@@ -319,6 +319,16 @@ def run_ours(args, cfg):
         t_step, t_kern = (float(x) for x in tt.cpu())
     mass = res.mass_kg()
     part = res.host_partials()
+    executed_flop = 0.0
+    if bufs is not None:  # tcgen05 FLOPs the tile kernel issued in the last step (diagnostic read-back)
+        import ctypes as C
+
+        from paper_2511_03126_b200.fused import _make_args
+
+        fa = _make_args(pts, n, views, tables, cfg.temperature, cfg.eps, cfg.grid, bufs, 0)
+        ex = C.c_double(0.0)
+        _lib.call("pf_tile_executed_flops", C.byref(fa), C.addressof(ex), stream.cuda_stream)
+        executed_flop = ex.value
 
     # ---- end to end through the public API, host buffers ---------------------------------------
     # paper_2511_03126_b200.stream.FusePipeline: every object's inputs are uploaded from pinned host
@@ -393,6 +403,16 @@ def run_ours(args, cfg):
                     "algorithmic_flop_per_launch": algo_flop,
                     "hbm": {"algorithmic_bytes_per_launch": algo,
                             "achieved_gbs": algo / (t_dom * 1e-3) / 1e9, "peak_gbs": hbm_peak}}
+        # what the tensor cores actually executed (the similarity runs by associativity through the
+        # G table, so fewer FLOPs than the algorithmic count) and ncu's tensor-pipe activity
+        if executed_flop:
+            roofline["executed"] = {"tcgen05_flop_per_launch": executed_flop,
+                                    "tflops": executed_flop / (t_dom * 1e-3) / 1e12,
+                                    "frac": executed_flop / (t_dom * 1e-3) / 1e12 / tc_peak}
+        if os.path.exists(tf):
+            act = json.load(open(tf)).get(cfg.name, {}).get("tensor_pipe_active")
+            if act is not None:
+                roofline["tensor_pipe_active_ncu"] = act
     else:
         ach = algo / (t_kern * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",

@@ -332,6 +332,9 @@ int pf_bench_umma(int32_t n, int32_t ts, int32_t reps, int32_t stores, void* out
  * tile::gather4 (mode 1); writes cycles per SM to out_dev (SMs uint64). */
 int pf_bench_gather(const void* src_bf16, int32_t cells, int32_t stages, int32_t mode, void* out_dev, void* stream);
 int pf_stage_times(float* ms, int32_t n);
+/* tcgen05 FLOPs the last pf_fuse_query on args' workspace issued in the tile kernel: sum over work
+ * items of 2 * 128 * ktp * (D + 128); 0 for the SIMT path. Synchronises the stream. */
+int pf_tile_executed_flops(const pf_fuse_args_t* args, double* flops, void* stream);
 
 /* C (128,n) f32 = A (128,k) bf16 row-major @ B (k,n) bf16 row-major through the tile kernel's
  * tcgen05 operand layouts / descriptors / TMEM read-back. k % 64 == 0 (<= 256), n % 16 == 0.

@@ -20,6 +20,7 @@
 // Featureless points (count 0) get zero probability / property rows (pipeline.py:279-280).
 #include <climits>
 #include <mutex>
+#include <vector>
 
 #include "pf_common.cuh"
 #include "pf_tile.cuh"
@@ -618,6 +619,31 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
   }
   if (prm.list && prm.vox_base > 0) stage_mark(5, st);  // tile path: the overflow stage
   return rc;
+}
+
+/* Diagnostic: tcgen05 FLOPs the last pf_fuse_query on this workspace issued in the tile kernel,
+ * sum over work items (tiles + sub-tiles) of 2 * 128 * ktp * (D + 128) (ktp = taps padded to 16),
+ * read back from the workspace (synchronises the stream). 0 when the SIMT path ran. */
+int pf_tile_executed_flops(const pf_fuse_args_t* a, double* flops, void* stream) {
+  *flops = 0.0;
+  if (!a || !a->workspace || !tile_path_ok(a) || a->n == 0) return PF_OK;
+  const int64_t cells = total_cells(a);
+  const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, tile::kMaxKpadTC);
+  const unsigned char* ws = reinterpret_cast<const unsigned char*>(a->workspace) + g_bytes(a);
+  int32_t nsub = 0;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemcpyAsync(&nsub, ws + L.sub, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("tile_executed_flops");
+  const int64_t items = L.ntiles + (int64_t)tile::kSubPerTile * std::min(nsub, L.max_sub_tiles);
+  std::vector<int32_t> kt((size_t)items);
+  cudaMemcpy(kt.data(), ws + L.kt, sizeof(int32_t) * items, cudaMemcpyDeviceToHost);
+  double f = 0.0;
+  for (int64_t t = 0; t < items; ++t) {
+    const int ktp = (kt[t] + 15) & ~15;
+    if (kt[t] > 0 && ktp <= tile::ws_kt_max()) f += 2.0 * 128.0 * ktp * (double)(a->d + tile::kMaxKpadTC);
+  }
+  *flops = f;
+  return check_launch("tile_executed_flops");
 }
 
 }  // extern "C"

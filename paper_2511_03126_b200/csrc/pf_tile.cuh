@@ -116,6 +116,7 @@ size_t point_order_bytes(int64_t n);
 int run_point_order(const float* points, int64_t n, const double* lo_hi, unsigned char* ws, int32_t* order,
                     int32_t* len, cudaStream_t st);
 constexpr int kSubRows = 32;  // rows of a sub-tile
+constexpr int kSubPerTile = kTile / kSubRows;
 
 }  // namespace tile
 }  // namespace pf

@@ -167,6 +167,43 @@ def test_tile_vs_simt_full_c5(cuda):
     assert mass_a == pytest.approx(b.mass_kg(), rel=TOL_BF16)
 
 
+def test_tile_vs_simt_full_c3(cuda):
+    """Full BASELINE C3 (2M points on 3 intersecting ellipsoids x 32 Fibonacci views, 1024^2 depth,
+    74x74x1024 bf16 maps): tile path == fp64 SIMT path for bitsets / counts / codes, properties and
+    mass at the bf16 bar."""
+    import torch
+
+    from paper_2511_03126_b200 import workloads
+
+    wl = workloads.generate("c3", device_splat=True)
+    nv = wl.cfg.nviews
+    R = np.stack([p.rotation for p in wl.poses])
+    tv = np.stack([p.translation for p in wl.poses])
+    intr = np.tile([wl.intrinsics.fx, wl.intrinsics.fy, wl.intrinsics.cx, wl.intrinsics.cy], (nv, 1))
+    fmap = torch.from_numpy(wl.fmaps.view(np.int16)).cuda().view(torch.bfloat16)
+    views = pf.ViewSet.from_tensors(R, tv, intr, wl.depth.cuda(), fmap)
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta)
+    pts = torch.from_numpy(wl.points).cuda()
+    a = pf.fuse_and_query(pts, views, tables, grid=wl.cfg.grid, check=True)
+    ca, ma, pa, ka, mass_a = (a.counts.clone(), a.mask_bits.clone(), a.props.clone(), a.codes.clone(),
+                              a.mass_kg())
+    b = pf.fuse_and_query(pts, views, tables, grid=wl.cfg.grid, force_simt=True, check=True)
+    assert torch.equal(ca, b.counts)
+    assert torch.equal(ma, b.mask_bits)
+    assert torch.equal(ka, b.codes)
+    feat = b.counts > 0
+    rel = ((pa[:, 0] - b.props[:, 0]).abs() / b.props[:, 0].abs().clamp_min(1e-30))[feat]
+    assert float(rel.max()) <= TOL_BF16
+    assert mass_a == pytest.approx(b.mass_kg(), rel=TOL_BF16)
+
+
+def test_fused_c2_full_vs_oracle(cuda, workload):
+    """Full BASELINE C2 object (200k points x 16 views, 37x37x768 f32, K=32, 128^3) against the CPU
+    oracle at the fp32 bar (the SIMT path in Hilbert order)."""
+    wl = workload("c2")
+    assert_parity(run_gpu(wl), run_oracle(wl), wl)
+
+
 def test_featureless_points(cuda, workload):
     """Points seen by no view: zero probability/property rows, still voxel-occupying (rho=0)."""
     wl = workload("mini")
