@@ -431,8 +431,16 @@ static int kpl_of(int k) { return (k + 31) / 32; }
 
 // The tensor-core tile path (pf_tile.cu) applies to bf16 maps with D a multiple of 128, <= 64
 // views, feature grids <= 255 per side and <= 128 padded materials.
+// f32 maps take the tile path in x3 mode (bf16 hi/lo split operands, three MMAs per k-step)
+static bool tile_x3(const pf_fuse_args_t* a) { return a->fmap_dtype == PF_F32; }
+
+// below this many points the x3 path's fixed costs (sort, prep, operand splits) exceed the SIMT pass
+constexpr int64_t kX3MinPoints = 65536;
+
 static bool tile_path_ok(const pf_fuse_args_t* a) {
-  if (a->fmap_dtype != PF_BF16 || a->d % 128 != 0 || a->nviews > tile::kMaxViewsTC) return false;
+  if ((a->fmap_dtype != PF_BF16 && a->fmap_dtype != PF_F32) || a->d % 128 != 0 || a->nviews > tile::kMaxViewsTC)
+    return false;
+  if (a->fmap_dtype == PF_F32 && a->n < kX3MinPoints) return false;
   if (((a->k + 63) / 64) * 64 > tile::kMaxKpadTC || (a->flags & PF_FUSE_FORCE_SIMT)) return false;
   // uniform, contiguously packed views (the TMA tensor maps address them as one [V*Hf][Wf][D] block)
   const pf_view_t& v0 = a->views_host[0];
@@ -461,7 +469,7 @@ uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* a) {
   if (!a || !a->views_host || a->d <= 0 || a->k <= 0) return 0;
   uint64_t bytes = g_bytes(a);
   if (tile_path_ok(a))
-    bytes += tile::tile_layout(a->n, a->nviews, total_cells(a), tile::kMaxKpadTC).bytes;
+    bytes += tile::tile_layout(a->n, a->nviews, total_cells(a), tile::kMaxKpadTC, a->d, tile_x3(a)).bytes;
   else if (a->n >= kSimtOrderMin)
     bytes += simt_order_bytes(a->n);
   return bytes;
@@ -506,6 +514,20 @@ int pf_fuse_prepare(const pf_fuse_args_t* a, void* stream) {
   float* G = reinterpret_cast<float*>(a->workspace);
   uint16_t* Gbf = nullptr;
   int kpadg = 0;
+  if (tile_path_ok(a) && tile_x3(a)) {
+    // f32 maps: fp32 G (SIMT), then the hi / lo bf16 splits of G and of the maps
+    kpadg = tile::kMaxKpadTC;
+    unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
+    const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg, a->d, true);
+    dim3 grid((unsigned)((cells + TP_CELLS - 1) / TP_CELLS), (unsigned)(kpad / TP_MATS));
+    k_text_proj<PF_F32><<<grid, 256, 0, st>>>(a->fmap, cells, a->d, a->text, a->k, kpad, G);
+    if (int rc = check_launch("text_proj")) return rc;
+    if (int rc = tile::run_split_f32(G, cells, a->k, kpad, kpadg, reinterpret_cast<uint16_t*>(ws + L.gbf),
+                                     reinterpret_cast<uint16_t*>(ws + L.glo), st))
+      return rc;
+    return tile::run_split_f32(reinterpret_cast<const float*>(a->fmap), cells, a->d, a->d, a->d,
+                               reinterpret_cast<uint16_t*>(ws + L.fhi), reinterpret_cast<uint16_t*>(ws + L.flo), st);
+  }
   if (tile_path_ok(a)) {
     kpadg = tile::kMaxKpadTC;  // S operand is always one 128-column chunk pair
     unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
@@ -555,13 +577,19 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     const int64_t cells = total_cells(a);
     const int kpadg = tile::kMaxKpadTC;  // S operand is always one 128-column chunk pair
     unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
-    const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg);
+    const bool x3 = tile_x3(a);
+    const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg, a->d, x3);
     tile::TileParams T{};
     T.spts = reinterpret_cast<const float4*>(ws + L.spts);
     T.inv = reinterpret_cast<const int32_t*>(ws + L.inv);
     T.srec = reinterpret_cast<tile::SRec*>(ws + L.srec);
     T.n = a->n; T.views = a->views; T.nv = a->nviews; T.nwords = (a->nviews + 31) / 32; T.d = d;
-    T.depth = a->depth; T.fmap = a->fmap; T.Gbf = reinterpret_cast<const uint16_t*>(ws + L.gbf);
+    T.depth = a->depth; T.fmap = x3 ? (const void*)(ws + L.fhi) : a->fmap;
+    T.Gbf = reinterpret_cast<const uint16_t*>(ws + L.gbf);
+    T.x3 = x3 ? 1 : 0;
+    T.kt_max = tile::ws_kt_max(x3);
+    T.fmap_lo = x3 ? reinterpret_cast<const uint16_t*>(ws + L.flo) : nullptr;
+    T.Gbf_lo = x3 ? reinterpret_cast<const uint16_t*>(ws + L.glo) : nullptr;
     T.kpadg = kpadg; T.k = a->k; T.p = a->p; T.density_col = a->density_col;
     T.values = a->values; T.mid_theta = a->mid_theta; T.inv_temp = prm.inv_temp; T.eps = a->eps;
     T.grid = a->grid; T.cells3 = (int64_t)a->grid * a->grid * a->grid; T.lo_hi = a->lo_hi;
@@ -628,7 +656,8 @@ int pf_tile_executed_flops(const pf_fuse_args_t* a, double* flops, void* stream)
   *flops = 0.0;
   if (!a || !a->workspace || !tile_path_ok(a) || a->n == 0) return PF_OK;
   const int64_t cells = total_cells(a);
-  const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, tile::kMaxKpadTC);
+  const bool x3 = tile_x3(a);
+  const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, tile::kMaxKpadTC, a->d, x3);
   const unsigned char* ws = reinterpret_cast<const unsigned char*>(a->workspace) + g_bytes(a);
   int32_t nsub = 0;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -640,7 +669,8 @@ int pf_tile_executed_flops(const pf_fuse_args_t* a, double* flops, void* stream)
   double f = 0.0;
   for (int64_t t = 0; t < items; ++t) {
     const int ktp = (kt[t] + 15) & ~15;
-    if (kt[t] > 0 && ktp <= tile::ws_kt_max()) f += 2.0 * 128.0 * ktp * (double)(a->d + tile::kMaxKpadTC);
+    if (kt[t] > 0 && ktp <= tile::ws_kt_max(x3))
+      f += (x3 ? 3.0 : 1.0) * 2.0 * 128.0 * ktp * (double)(a->d + tile::kMaxKpadTC);
   }
   *flops = f;
   return check_launch("tile_executed_flops");

@@ -739,7 +739,7 @@ namespace tile {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg) {
+TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d, bool x3) {
   TileLayout L{};
   const int64_t ntiles = (n + kTile - 1) / kTile;
   size_t off = 0;
@@ -766,6 +766,11 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg) {
   L.ovf = take(sizeof(int32_t) * (size_t)(n + 1));
   L.gbf = take(sizeof(uint16_t) * (size_t)cells * kpadg);
   L.textbf = take(sizeof(uint16_t) * (size_t)kpadg * 1024);  // text rows in bf16 (D <= 1024)
+  if (x3) {  // lo part of G, hi and lo parts of the f32 maps
+    L.glo = take(sizeof(uint16_t) * (size_t)cells * kpadg);
+    L.fhi = take(sizeof(uint16_t) * (size_t)cells * d);
+    L.flo = take(sizeof(uint16_t) * (size_t)cells * d);
+  }
   L.bytes = off;
   return L;
 }
@@ -792,6 +797,26 @@ int run_point_order(const float* points, int64_t n, const double* lo_hi, unsigne
   if (int rc = run_bucket_scan(hist, totals, int64_t(1) << 21, st)) return rc;
   k_order_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, keys, hist, order, len);
   return check_launch("order_scatter");
+}
+
+// hi = bf16_rn(x), lo = bf16_rn(x - hi) (x - hi is exact in fp32); columns >= cols are zero
+__global__ void k_split_f32(const float* __restrict__ src, int64_t rows, int cols, int src_ld, int dst_ld,
+                            uint16_t* __restrict__ hi, uint16_t* __restrict__ lo) {
+  const int64_t total = rows * (int64_t)dst_ld;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / dst_ld;
+    const int c = (int)(e - r * dst_ld);
+    const float x = c < cols ? src[r * src_ld + c] : 0.f;
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    hi[e] = __bfloat16_as_ushort(h);
+    lo[e] = __bfloat16_as_ushort(__float2bfloat16_rn(x - __bfloat162float(h)));
+  }
+}
+
+int run_split_f32(const float* src, int64_t rows, int cols, int src_ld, int dst_ld, uint16_t* hi, uint16_t* lo,
+                  cudaStream_t st) {
+  k_split_f32<<<grid_for(rows * (int64_t)dst_ld, 256), 256, 0, st>>>(src, rows, cols, src_ld, dst_ld, hi, lo);
+  return check_launch("split_f32");
 }
 
 int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf, cudaStream_t st) {
@@ -850,7 +875,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   if (int rc = check_launch("tile_prep")) return rc;
   // overflow tiles -> sub-tile work items (appended after the tiles)
   cudaMemsetAsync(P.sub_count, 0, sizeof(int32_t), st);
-  k_find_overflow<<<grid_for(L.ntiles, 256), 256, 0, st>>>(P, L.ntiles, ws_kt_max());
+  k_find_overflow<<<grid_for(L.ntiles, 256), 256, 0, st>>>(P, L.ntiles, P.kt_max);
   if (int rc = check_launch("find_overflow")) return rc;
   k_subtile_prep<<<(unsigned)(L.max_sub_tiles < 148 * 16 ? L.max_sub_tiles : 148 * 16), kTile, 0, st>>>(P, L.ntiles);
   if (int rc = check_launch("subtile_prep")) return rc;
@@ -868,16 +893,16 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
       std::vector<int32_t> skt(nsi > 0 ? nsi : 1);
       if (nsi) cudaMemcpy(skt.data(), P.tile_kt + L.ntiles, sizeof(int32_t) * nsi, cudaMemcpyDeviceToHost);
       int over2 = 0;
-      for (int k = 0; k < nsi; ++k) over2 += ((skt[k] + 15) & ~15) > ws_kt_max();
+      for (int k = 0; k < nsi; ++k) over2 += ((skt[k] + 15) & ~15) > P.kt_max;
       fprintf(stderr, "[prep debug] overflow tiles %d -> %d sub-tiles, %d of them still over %d taps\n", nsub_tiles,
-              nsi, over2, ws_kt_max());
+              nsi, over2, P.kt_max);
     }
     double ksum = 0;
     int64_t over = 0, kmax = 0;
     for (int32_t k : kt) {
       if (k < 0) { ++over; continue; }
       ksum += k;
-      over += ((k + 15) & ~15) > ws_kt_max();
+      over += ((k + 15) & ~15) > P.kt_max;
       kmax = k > kmax ? k : kmax;
     }
     {  // window shapes

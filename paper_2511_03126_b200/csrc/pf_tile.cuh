@@ -56,8 +56,13 @@ struct TileParams {
   const pf_view_t* views;
   int nv, nwords, d;
   const float* depth;
-  const void* fmap;     // bf16 packed maps
-  const uint16_t* Gbf;  // (cells, kpadg) bf16
+  const void* fmap;     // bf16 packed maps (x3: the bf16 high parts of the f32 maps)
+  const uint16_t* Gbf;  // (cells, kpadg) bf16 (x3: high parts)
+  // x3 (f32 maps): every f32 operand is split hi + lo into bf16 and each MMA k-step issues
+  // hi.hi + hi.lo + lo.hi (fp32-accurate to ~2^-16); kt_max = taps per work item held by one A buffer
+  const uint16_t* fmap_lo;
+  const uint16_t* Gbf_lo;
+  int32_t x3, kt_max;
   int kpadg, k, p, density_col;
   const float* values;
   const float* mid_theta;
@@ -97,10 +102,14 @@ struct TileParams {
 struct TileLayout {
   int64_t ntiles;
   int32_t max_sub_tiles;
-  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, gbf, textbf, viewf, vbound, vox, bytes;
+  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, gbf, textbf, viewf, vbound, vox, glo, fhi, flo,
+      bytes;
 };
 
-TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg);
+TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d = 0, bool x3 = false);
+// x3 operands of f32 maps: hi = bf16(x), lo = bf16(x - hi), for the maps and the G table
+int run_split_f32(const float* src, int64_t rows, int cols, int src_ld, int dst_ld, uint16_t* hi, uint16_t* lo,
+                  cudaStream_t st);
 int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const float* points,
                   int64_t n, cudaStream_t st);
 int run_unsort(const TileParams& P, cudaStream_t st);
@@ -108,7 +117,7 @@ int run_tile_ws(const TileParams& P, cudaStream_t st);
 int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf, cudaStream_t st);
 int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int k, int kpadg, int kpad,
                  uint16_t* Gbf, float* G32, uint16_t* textbf, cudaStream_t st);
-int ws_kt_max();
+int ws_kt_max(bool x3 = false);
 int run_bucket_scan(uint32_t* hist, uint32_t* totals, int64_t nbins, cudaStream_t st);
 // Hilbert order of the points for the SIMT path: order[t] = index of the t-th point along the curve
 // (7-bit key over the domain lo_hi), and *len = n (the kernel's list length). ws: point_order_bytes.

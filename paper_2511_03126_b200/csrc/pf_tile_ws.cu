@@ -57,6 +57,11 @@ constexpr int kSGroups = kMaxKpadTC / kDCols;  // similarity groups per tile (1 
 constexpr int kStages = 8;             // B ring depth (4 chunk groups)
 constexpr int kKtWs = 192;             // taps per tile held in one A buffer / B stage
 constexpr int kStageBytes = kKtWs * 128;
+// x3 (f32 maps): A hi and lo parts per buffer, kKtX3 taps each: 2 x 2 x kKtX3/2 TMEM columns; the
+// B ring holds hi and lo stages of every chunk pair (4 stages per MMA group)
+constexpr int kKtX3 = 128;
+static_assert(kDBufs * kDCols + 2 * kKtX3 <= 512, "TMEM: accumulator slots + 2 x (hi, lo) A buffers");
+static_assert(kStages % 4 == 0, "x3 groups of 4 stages never wrap the ring");
 constexpr int kRowStep = kLoadThreads / 8;                      // rows between one thread's copies
 constexpr int kRowsPer = kKtWs / kRowStep;                      // copies per thread per chunk
 constexpr int kHalfK = kMaxKpadTC / 2;                          // materials per accumulator half
@@ -102,9 +107,9 @@ struct WsShared {
 
 // every role reads the next tile's inputs (tap count, windows, points, records) one tile ahead, so
 // their DRAM latency overlaps the current tile
-__device__ __forceinline__ int ktp_of(int kt, bool& ok) {
+__device__ __forceinline__ int ktp_of(int kt, bool& ok, int kt_max) {
   const int ktp = (kt + 15) & ~15;
-  ok = kt > 0 && ktp <= kKtWs;
+  ok = kt > 0 && ktp <= kt_max;
   return ktp;
 }
 __device__ __forceinline__ int kt_at(const TileParams& P, int64_t tile, int64_t ntiles) {
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       kt_nx = kt_at(P, tile + gridDim.x, nitems);
       if (tid < P.nv && tile + gridDim.x < nitems) ds_nx = P.tile_desc[(tile + gridDim.x) * P.nv + tid];
       bool ok;
-      const int ktp = ktp_of(kt, ok);
+      const int ktp = ktp_of(kt, ok, P.kt_max);
       if (!ok) continue;
       // row -> cell table for this tile
       int32_t* cell = S.cell[t_local & 1];
@@ -328,16 +333,19 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         const int r = r0 + kRowStep * j;
         rc[j] = r < ktp ? cell[r < kt ? r : 0] : -1;
       }
-      for (int c = 0; c < nch; ++c) {
+      const int nstage = P.x3 ? 2 * nch : nch;  // x3: per chunk pair [hi c][hi c+1][lo c][lo c+1]
+      for (int qs = 0; qs < nstage; ++qs) {
+        const int c = P.x3 ? 2 * (qs >> 2) + (qs & 1) : qs;
+        const bool lo = P.x3 && (qs & 2);
         WS_WAIT(&S.b_empty[stage], phase ^ 1u, 0);
         const uint32_t sb = tc::smem_u32(sB + stage * kStageBytes);
         const uint16_t* src;
         int rowlen;
         if (c < nd) {
-          src = reinterpret_cast<const uint16_t*>(P.fmap) + c * 64 + q * 8;
+          src = (lo ? P.fmap_lo : reinterpret_cast<const uint16_t*>(P.fmap)) + c * 64 + q * 8;
           rowlen = P.d;
         } else {
-          src = P.Gbf + (c - nd) * 64 + q * 8;
+          src = (lo ? P.Gbf_lo : P.Gbf) + (c - nd) * 64 + q * 8;
           rowlen = P.kpadg;
         }
         // rows r0 + kRowStep*j: r & 7 is fixed per thread, so the swizzled destination advances by
@@ -355,7 +363,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           wait_cyc[11] += clock64() - tl0;
           if (warp == 0 && lane == 0) {
             if (pub_group % kCG == kCG - 1) WS_TRACE(pub_tile, 15 + pub_group / kCG);
-            if (++pub_group == nch) { pub_group = 0; ++pub_tile; }
+            if (++pub_group == nstage) { pub_group = 0; ++pub_tile; }
           }
         }
         if (++stage == kStages) { stage = 0; phase ^= 1u; }
@@ -379,18 +387,19 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const int kt = kt_nx;
       kt_nx = kt_at(P, tile + gridDim.x, nitems);
       bool ok;
-      const int ktp = ktp_of(kt, ok);
+      const int ktp = ktp_of(kt, ok, P.kt_max);
       if (!ok) continue;
       const int ab = (int)(t_local & 1u);
       WS_WAIT(&S.a_full[ab], (t_local >> 1) & 1u, 1);
       if (lane == 0) WS_TRACE(t_local, 3);
       // the builders wrote A (the tile's bilinear weights) straight into TMEM buffer ab; the MMAs read
       // A from TMEM and B from shared memory; the commit after the last group frees buffer ab
-      const uint32_t tA = tA0 + (uint32_t)(ab * (kKtWs / 2));
+      const uint32_t tA = tA0 + (uint32_t)(ab * (P.x3 ? kKtX3 / 2 : kKtWs / 2));
+      const uint32_t tAlo = tA + (uint32_t)kKtX3;  // x3: lo parts after both hi buffers
+      const int gst = P.x3 ? 2 * kCG : kCG;          // ring stages per MMA group
       tc::fence_after_sync();
       for (int c = 0; c < nch; c += kCG) {
-#pragma unroll
-        for (int g = 0; g < kCG; ++g) WS_WAIT(&S.b_full[stage + g], phase, 2);
+        for (int g = 0; g < gst; ++g) WS_WAIT(&S.b_full[stage + g], phase, 2);
         const int db = dcount % kDBufs;
         if (c < nd) WS_WAIT(&S.d_empty[db], ((dcount / kDBufs) & 1u) ^ 1u, 3);
         else WS_WAIT(&S.d_empty[db], ((dcount / kDBufs) & 1u) ^ 1u, 4);
@@ -405,15 +414,28 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           // descriptors advance by 2048 B (start field +128) and 8 TMEM columns per K=16 step
           uint64_t bd = tc::smem_desc_sw128(b0, kStageBytes, 1024);
           uint32_t ta = tA;
-          tc::mma_bf16_ts_elect(dst, ta, bd, idesc, 0u);
+          if (!P.x3) {
+            tc::mma_bf16_ts_elect(dst, ta, bd, idesc, 0u);
 #pragma unroll 4
-          for (int s = 1; s < ktp / 16; ++s) {
-            bd += 128;
-            ta += 8;
-            tc::mma_bf16_ts_elect(dst, ta, bd, idesc, 1u);
+            for (int s = 1; s < ktp / 16; ++s) {
+              bd += 128;
+              ta += 8;
+              tc::mma_bf16_ts_elect(dst, ta, bd, idesc, 1u);
+            }
+          } else {  // A_hi B_hi + A_hi B_lo + A_lo B_hi (B_lo: the pair's stages + 2)
+            uint64_t bl = tc::smem_desc_sw128(b0 + 2 * kStageBytes, kStageBytes, 1024);
+            uint32_t tl = tAlo;
+            for (int s = 0; s < ktp / 16; ++s) {
+              tc::mma_bf16_ts_elect(dst, ta, bd, idesc, s ? 1u : 0u);
+              tc::mma_bf16_ts_elect(dst, ta, bl, idesc, 1u);
+              tc::mma_bf16_ts_elect(dst, tl, bd, idesc, 1u);
+              bd += 128;
+              bl += 128;
+              ta += 8;
+              tl += 8;
+            }
           }
-#pragma unroll
-          for (int g = 0; g < kCG; ++g) tc::mma_commit_elect(&S.b_empty[stage + g]);
+          for (int g = 0; g < gst; ++g) tc::mma_commit_elect(&S.b_empty[stage + g]);
           tc::mma_commit_elect(&S.d_full[db]);
           if (c + kCG >= nch) tc::mma_commit_elect(&S.a_empty[ab]);
         }
@@ -421,7 +443,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         if constexpr (PROF) issue_cyc += clock64() - ti0;
         if (lane == 0) WS_TRACE(t_local, 4 + c / kCG);
         ++dcount;
-        stage += kCG;
+        stage += gst;
         if (stage == kStages) { stage = 0; phase ^= 1u; }
       }
       ++t_local;
@@ -474,7 +496,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const int32_t cd = cd_nx;
       fetch(tile + gridDim.x, kt_nx, ds_nx, p_nx, mw_nx, cd_nx);
       bool ok;
-      const int ktp = ktp_of(kt, ok);
+      const int ktp = ktp_of(kt, ok, P.kt_max);
       if (!ok) continue;
       if (bh == 0 && P.vox_list) {
         // touched-voxel list without returning atomics: slot jpt holds the code when this row is the
@@ -519,7 +541,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       }
       const float ox = 0.5f * (lo[0] + hi[0]), oy = 0.5f * (lo[1] + hi[1]), oz = 0.5f * (lo[2] + hi[2]);
       const float ex = hi[0] - lo[0], ey = hi[1] - lo[1], ez = hi[2] - lo[2];
-      const bool exact = ex * ex + ey * ey + ez * ez > 4.f * kAffineR * kAffineR;
+      // x3 (fp32 bar): always the exact fp32 projection, as prep's taps
+      const bool exact = P.x3 || ex * ex + ey * ey + ez * ez > 4.f * kAffineR * kAffineR;
       // views with taps in this tile, by rank; coefficients of rank 8 l + bj by lane l of warp bj
       const uint2 dlo = lane < P.nv ? sdesc[lane] : make_uint2(0u, 0u);
       const uint2 dhi = lane + 32 < P.nv ? sdesc[lane + 32] : make_uint2(0u, 0u);
@@ -553,7 +576,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       asm volatile("bar.sync 1, %0;" ::"n"(kBuildThreads) : "memory");  // coefficients visible
       if (bt == 0) WS_TRACE(t_local, 1);
       tc::fence_after_sync();
-      const uint32_t tAb = tA0 + (uint32_t)(ab * (kKtWs / 2)) + t_lanes;
+      const uint32_t tAb = tA0 + (uint32_t)(ab * (P.x3 ? kKtX3 / 2 : kKtWs / 2)) + t_lanes;
+      const bool x3 = P.x3 != 0;  // lo parts at + kKtX3 columns
       const long long tb1 = WS_CLOCK();
       if constexpr (PROF) wait_cyc[14] += tb1 - tb0;
       const float dxp = p.x - ox, dyp = p.y - oy, dzp = p.z - oz;
@@ -600,8 +624,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         };
         const int ncols = (ww * wh + 1) >> 1;
         for (int j = 0; j < ncols; ++j) {  // warp-uniform
-          const __nv_bfloat162 pr = __floats2bfloat162_rn(tapw(2 * j), tapw(2 * j + 1));
+          const float w0 = tapw(2 * j), w1 = tapw(2 * j + 1);
+          const __nv_bfloat162 pr = __floats2bfloat162_rn(w0, w1);
           tc::tmem_st_x1(col0 + (uint32_t)j, *reinterpret_cast<const uint32_t*>(&pr));
+          if (x3) {
+            const __nv_bfloat162 pl = __floats2bfloat162_rn(w0 - __low2float(pr), w1 - __high2float(pr));
+            tc::tmem_st_x1(col0 + (uint32_t)(kKtX3 + j), *reinterpret_cast<const uint32_t*>(&pl));
+          }
         }
       };
       // windows with sides in {2, 3} (~99.5% of them at C5): the row's weights are separable,
@@ -623,19 +652,29 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           const __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
           return *reinterpret_cast<const uint32_t*>(&b2);
         };
-        if constexpr (ww == 2 && wh == 2) {
-          tc::tmem_st_x2(col0, pk(vy0 * vx0, vy0 * vx1), pk(vy1 * vx0, vy1 * vx1));
-        } else if constexpr (ww == 3 && wh == 2) {  // taps r0: 0 1 2, r1: 3 4 5
-          tc::tmem_st_x2(col0, pk(vy0 * vx0, vy0 * vx1), pk(vy0 * vx2, vy1 * vx0));
-          tc::tmem_st_x1(col0 + 2u, pk(vy1 * vx1, vy1 * vx2));
-        } else if constexpr (ww == 2 && wh == 3) {  // taps r0: 0 1, r1: 2 3, r2: 4 5
-          tc::tmem_st_x2(col0, pk(vy0 * vx0, vy0 * vx1), pk(vy1 * vx0, vy1 * vx1));
-          tc::tmem_st_x1(col0 + 2u, pk(vy2 * vx0, vy2 * vx1));
-        } else {  // 3 x 3: taps 0..8 + one padding tap
-          tc::tmem_st_x4(col0, pk(vy0 * vx0, vy0 * vx1), pk(vy0 * vx2, vy1 * vx0), pk(vy1 * vx1, vy1 * vx2),
-                         pk(vy2 * vx0, vy2 * vx1));
-          tc::tmem_st_x1(col0 + 4u, pk(vy2 * vx2, 0.f));
-        }
+        // x3: the bf16 residuals of the same pairs
+        auto pkl = [](float lo, float hi) {
+          const __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
+          const __nv_bfloat162 r2 = __floats2bfloat162_rn(lo - __low2float(b2), hi - __high2float(b2));
+          return *reinterpret_cast<const uint32_t*>(&r2);
+        };
+        auto emit = [&](auto PK, uint32_t c0) {
+          if constexpr (ww == 2 && wh == 2) {
+            tc::tmem_st_x2(c0, PK(vy0 * vx0, vy0 * vx1), PK(vy1 * vx0, vy1 * vx1));
+          } else if constexpr (ww == 3 && wh == 2) {  // taps r0: 0 1 2, r1: 3 4 5
+            tc::tmem_st_x2(c0, PK(vy0 * vx0, vy0 * vx1), PK(vy0 * vx2, vy1 * vx0));
+            tc::tmem_st_x1(c0 + 2u, PK(vy1 * vx1, vy1 * vx2));
+          } else if constexpr (ww == 2 && wh == 3) {  // taps r0: 0 1, r1: 2 3, r2: 4 5
+            tc::tmem_st_x2(c0, PK(vy0 * vx0, vy0 * vx1), PK(vy1 * vx0, vy1 * vx1));
+            tc::tmem_st_x1(c0 + 2u, PK(vy2 * vx0, vy2 * vx1));
+          } else {  // 3 x 3: taps 0..8 + one padding tap
+            tc::tmem_st_x4(c0, PK(vy0 * vx0, vy0 * vx1), PK(vy0 * vx2, vy1 * vx0), PK(vy1 * vx1, vy1 * vx2),
+                           PK(vy2 * vx0, vy2 * vx1));
+            tc::tmem_st_x1(c0 + 4u, PK(vy2 * vx2, 0.f));
+          }
+        };
+        emit(pk, col0);
+        if (x3) emit(pkl, col0 + (uint32_t)kKtX3);
       };
       // rank rk: view, window base and the row's coordinates relative to the window origin
       auto coords = [&](int rk, int& v, int& base, float& fu_rel, float& fv_rel) {
@@ -689,7 +728,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       run(__ballot_sync(0xffffffffu, cls == 3), I3{}, I3{});
       for (uint32_t m = __ballot_sync(0xffffffffu, cls == 4); m; m &= m - 1) unit_general(bh + 2 * (__ffs(m) - 1));
       if (bh == 0)  // columns past the last window (K padding to 16) must be zero too
-        for (int j = kt >> 1; j < (ktp >> 1); ++j) tc::tmem_st_x1(tAb + (uint32_t)j, 0u);
+        for (int j = kt >> 1; j < (ktp >> 1); ++j) {
+          tc::tmem_st_x1(tAb + (uint32_t)j, 0u);
+          if (x3) tc::tmem_st_x1(tAb + (uint32_t)(kKtX3 + j), 0u);
+        }
       const long long tb2 = WS_CLOCK();
       tc::tmem_st_wait();
       if constexpr (PROF) {
@@ -741,7 +783,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         p_nx = ld_pref_f4(P.spts + j_nx);
       }
       bool ok;
-      ktp_of(kt, ok);
+      ktp_of(kt, ok, P.kt_max);
       if (!ok) {  // kt == -1: re-run as sub-tiles; otherwise the points go to the SIMT kernel
         if (kt != -1 && valid && half == 0) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(pcur.w);
         continue;
@@ -978,7 +1020,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
 
 }  // namespace
 
-int ws_kt_max() { return kKtWs; }
+int ws_kt_max(bool x3) { return x3 ? kKtX3 : kKtWs; }
 
 size_t ws_smem_bytes() { return (size_t)kStages * kStageBytes + 1024; }
 

@@ -204,6 +204,29 @@ def test_fused_c2_full_vs_oracle(cuda, workload):
     assert_parity(run_gpu(wl), run_oracle(wl), wl)
 
 
+@pytest.mark.parametrize("name", ["c4", "c2"])
+def test_x3_tile_path_full_object(cuda, workload, name):
+    """f32 maps at full object size take the tensor-core tile path in x3 mode (bf16 hi/lo operand
+    splits, three MMAs per k-step): the fp32 bar against the oracle, and masks / counts / codes
+    identical to the fp64 SIMT path."""
+    import torch
+
+    wl = workload(name)
+    res = run_gpu(wl)
+    assert_parity(res, run_oracle(wl), wl)
+    views = pf.ViewSet.from_views(wl.views())
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta, density_col=0)
+    pts = torch.from_numpy(wl.points).cuda()
+    a = pf.fuse_and_query(pts, views, tables, temperature=wl.cfg.temperature, epsilon=wl.cfg.eps, grid=wl.cfg.grid)
+    ca, ma, pa = a.counts.clone(), a.mask_bits.clone(), a.props.clone()
+    b = pf.fuse_and_query(pts, views, tables, temperature=wl.cfg.temperature, epsilon=wl.cfg.eps, grid=wl.cfg.grid,
+                          force_simt=True)
+    assert torch.equal(ca, b.counts) and torch.equal(ma, b.mask_bits)
+    feat = b.counts > 0
+    rel = ((pa[:, 0] - b.props[:, 0]).abs() / b.props[:, 0].abs().clamp_min(1e-30))[feat]
+    assert float(rel.max()) <= TOL
+
+
 def test_featureless_points(cuda, workload):
     """Points seen by no view: zero probability/property rows, still voxel-occupying (rho=0)."""
     wl = workload("mini")
