@@ -519,14 +519,16 @@ int pf_fuse_prepare(const pf_fuse_args_t* a, void* stream) {
     kpadg = tile::kMaxKpadTC;
     unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
     const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg, a->d, true);
-    dim3 grid((unsigned)((cells + TP_CELLS - 1) / TP_CELLS), (unsigned)(kpad / TP_MATS));
-    k_text_proj<PF_F32><<<grid, 256, 0, st>>>(a->fmap, cells, a->d, a->text, a->k, kpad, G);
-    if (int rc = check_launch("text_proj")) return rc;
-    if (int rc = tile::run_split_f32(G, cells, a->k, kpad, kpadg, reinterpret_cast<uint16_t*>(ws + L.gbf),
-                                     reinterpret_cast<uint16_t*>(ws + L.glo), st))
+    uint16_t* fhi = reinterpret_cast<uint16_t*>(ws + L.fhi);
+    uint16_t* flo = reinterpret_cast<uint16_t*>(ws + L.flo);
+    if (int rc = tile::run_split_f32(reinterpret_cast<const float*>(a->fmap), cells, a->d, a->d, a->d, fhi, flo, st))
       return rc;
-    return tile::run_split_f32(reinterpret_cast<const float*>(a->fmap), cells, a->d, a->d, a->d,
-                               reinterpret_cast<uint16_t*>(ws + L.fhi), reinterpret_cast<uint16_t*>(ws + L.flo), st);
+    // G on the tensor cores from the same splits (hi.hi + hi.lo + lo.hi), fp32 copy for the SIMT
+    // overflow points
+    return tile::run_gproj_tc_x3(fhi, flo, cells, a->d, a->text, a->k, kpadg, kpad,
+                                 reinterpret_cast<uint16_t*>(ws + L.gbf), reinterpret_cast<uint16_t*>(ws + L.glo), G,
+                                 reinterpret_cast<uint16_t*>(ws + L.textbf), reinterpret_cast<uint16_t*>(ws + L.textlo),
+                                 st);
   }
   if (tile_path_ok(a)) {
     kpadg = tile::kMaxKpadTC;  // S operand is always one 128-column chunk pair

@@ -27,16 +27,35 @@ __global__ void k_text_bf16(const float* __restrict__ text, int k, int kpadg, in
   }
 }
 
+// text rows -> bf16 hi and lo (x - hi) parts, rows >= k zero (x3 mode)
+__global__ void k_text_split(const float* __restrict__ text, int k, int kpadg, int d, uint16_t* __restrict__ hi,
+                             uint16_t* __restrict__ lo) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)kpadg * d;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = e / d;
+    const float x = n < k ? text[e] : 0.f;
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    hi[e] = __bfloat16_as_ushort(h);
+    lo[e] = __bfloat16_as_ushort(__float2bfloat16_rn(x - __bfloat162float(h)));
+  }
+}
+
+// X3 (f32 maps): stages hold the hi and lo parts of both operands and each K=16 step issues
+// hi.hi + hi.lo + lo.hi; the epilogue also writes the lo part of G (Gbf_lo)
+template <bool X3>
 __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ fmap, int64_t cells, int d,
                                                      const uint16_t* __restrict__ textbf, int k, int kpadg,
                                                      int kpad, uint16_t* __restrict__ Gbf,
-                                                     float* __restrict__ G32) {
+                                                     float* __restrict__ G32, const uint16_t* __restrict__ fmap_lo,
+                                                     const uint16_t* __restrict__ text_lo,
+                                                     uint16_t* __restrict__ Gbf_lo) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // stage s: A [128 rows x 64 ch] (16 KB, K-major SW128) then B [kpadg rows x 64 ch] (K-major SW128)
   const int b_bytes = kpadg * 128;
-  const int stage_bytes = 16384 + b_bytes;
+  const int part_bytes = 16384 + b_bytes;  // [A | B] of one precision part
+  const int stage_bytes = X3 ? 2 * part_bytes : part_bytes;
   __shared__ uint64_t mbar[kGStages];  // MMA completion per ring stage
   __shared__ uint32_t tmem_base_s;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -44,20 +63,25 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
   const int nchunk = d / 64;
 
   auto load = [&](int ch, int st) {
-    unsigned char* sa = smem + st * stage_bytes;
-    unsigned char* sb = sa + 16384;
-    // A: row r, 16-byte piece q (8 channels): K-major SW128, one 64-channel atom column
-    for (int e = tid; e < kGM * 8; e += 128) {
-      const int r = e >> 3, q = e & 7;
-      const int64_t cell = c0 + r < cells ? c0 + r : cells - 1;
-      const uint32_t off = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + (((q ^ (r & 7)) & 7) << 4));
-      tc::cp_async16(tc::smem_u32(sa + off), fmap + cell * d + ch * 64 + q * 8);
-    }
-    // B: material n, channels ch*64 .. +64 (bf16 text, K-major SW128)
-    for (int e = tid; e < kpadg * 8; e += 128) {
-      const int n = e >> 3, q = e & 7;
-      const uint32_t off = (uint32_t)((n >> 3) * 1024 + (n & 7) * 128 + (((q ^ (n & 7)) & 7) << 4));
-      tc::cp_async16(tc::smem_u32(sb + off), textbf + (int64_t)n * d + ch * 64 + q * 8);
+#pragma unroll
+    for (int part = 0; part < (X3 ? 2 : 1); ++part) {
+      unsigned char* sa = smem + st * stage_bytes + part * part_bytes;
+      unsigned char* sb = sa + 16384;
+      const uint16_t* fa = part ? fmap_lo : fmap;
+      const uint16_t* fb = part ? text_lo : textbf;
+      // A: row r, 16-byte piece q (8 channels): K-major SW128, one 64-channel atom column
+      for (int e = tid; e < kGM * 8; e += 128) {
+        const int r = e >> 3, q = e & 7;
+        const int64_t cell = c0 + r < cells ? c0 + r : cells - 1;
+        const uint32_t off = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + (((q ^ (r & 7)) & 7) << 4));
+        tc::cp_async16(tc::smem_u32(sa + off), fa + cell * d + ch * 64 + q * 8);
+      }
+      // B: material n, channels ch*64 .. +64 (bf16 text, K-major SW128)
+      for (int e = tid; e < kpadg * 8; e += 128) {
+        const int n = e >> 3, q = e & 7;
+        const uint32_t off = (uint32_t)((n >> 3) * 1024 + (n & 7) * 128 + (((q ^ (n & 7)) & 7) << 4));
+        tc::cp_async16(tc::smem_u32(sb + off), fb + (int64_t)n * d + ch * 64 + q * 8);
+      }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -89,6 +113,12 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
         const uint64_t ad = tc::smem_desc_sw128(a0 + s * 32, 16, 1024);
         const uint64_t bd = tc::smem_desc_sw128(b0 + s * 32, 16, 1024);
         tc::mma_bf16_ss_elect(tbase, ad, bd, idesc, (ch | s) ? 1u : 0u);
+        if constexpr (X3) {
+          const uint64_t adl = tc::smem_desc_sw128(a0 + part_bytes + s * 32, 16, 1024);
+          const uint64_t bdl = tc::smem_desc_sw128(b0 + part_bytes + s * 32, 16, 1024);
+          tc::mma_bf16_ss_elect(tbase, ad, bdl, idesc, 1u);
+          tc::mma_bf16_ss_elect(tbase, adl, bd, idesc, 1u);
+        }
       }
       tc::mma_commit_elect(&mbar[st]);
     }
@@ -116,7 +146,9 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
     if (cell >= cells) break;
     for (int c = lane_of(tid); c < kpadg; c += 32) {
       const float val = srow[r * ld + c];
-      Gbf[cell * kpadg + c] = __bfloat16_as_ushort(__float2bfloat16_rn(val));
+      const __nv_bfloat16 h = __float2bfloat16_rn(val);
+      Gbf[cell * kpadg + c] = __bfloat16_as_ushort(h);
+      if constexpr (X3) Gbf_lo[cell * kpadg + c] = __bfloat16_as_ushort(__float2bfloat16_rn(val - __bfloat162float(h)));
       if (G32 && c < kpad) G32[cell * kpad + c] = c < k ? val : 0.f;
     }
   }
@@ -133,11 +165,24 @@ int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int 
   k_text_bf16<<<grid_for((int64_t)kpadg * d, 256), 256, 0, st>>>(text, k, kpadg, d, textbf);
   if (int rc = check_launch("text_bf16")) return rc;
   const size_t smem = kGStages * (16384 + (size_t)kpadg * 128) + 1024;
-  cudaFuncSetAttribute(k_gproj_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_gproj_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const unsigned grid = (unsigned)((cells + kGM - 1) / kGM);
-  k_gproj_tc<<<grid, 128, smem, st>>>(reinterpret_cast<const uint16_t*>(fmap), cells, d, textbf, k, kpadg, kpad,
-                                      Gbf, G32);
+  k_gproj_tc<false><<<grid, 128, smem, st>>>(reinterpret_cast<const uint16_t*>(fmap), cells, d, textbf, k, kpadg,
+                                             kpad, Gbf, G32, nullptr, nullptr, nullptr);
   return check_launch("gproj_tc");
+}
+
+int run_gproj_tc_x3(const uint16_t* fhi, const uint16_t* flo, int64_t cells, int d, const float* text, int k,
+                    int kpadg, int kpad, uint16_t* Gbf, uint16_t* Gbf_lo, float* G32, uint16_t* text_hi,
+                    uint16_t* text_lo, cudaStream_t st) {
+  if (d % 64 != 0 || kpadg % 16 != 0 || kpadg > 256) return set_error(PF_ERR_VALUE, "gproj_x3: bad shapes");
+  k_text_split<<<grid_for((int64_t)kpadg * d, 256), 256, 0, st>>>(text, k, kpadg, d, text_hi, text_lo);
+  if (int rc = check_launch("text_split")) return rc;
+  const size_t smem = kGStages * 2 * (16384 + (size_t)kpadg * 128) + 1024;
+  cudaFuncSetAttribute(k_gproj_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned grid = (unsigned)((cells + kGM - 1) / kGM);
+  k_gproj_tc<true><<<grid, 128, smem, st>>>(fhi, cells, d, text_hi, k, kpadg, kpad, Gbf, G32, flo, text_lo, Gbf_lo);
+  return check_launch("gproj_tc_x3");
 }
 
 }  // namespace tile

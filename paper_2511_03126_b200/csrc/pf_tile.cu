@@ -770,6 +770,7 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d, bool 
     L.glo = take(sizeof(uint16_t) * (size_t)cells * kpadg);
     L.fhi = take(sizeof(uint16_t) * (size_t)cells * d);
     L.flo = take(sizeof(uint16_t) * (size_t)cells * d);
+    L.textlo = take(sizeof(uint16_t) * (size_t)kpadg * 1024);
   }
   L.bytes = off;
   return L;

@@ -102,7 +102,7 @@ struct TileParams {
 struct TileLayout {
   int64_t ntiles;
   int32_t max_sub_tiles;
-  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, gbf, textbf, viewf, vbound, vox, glo, fhi, flo,
+  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, gbf, textbf, viewf, vbound, vox, glo, fhi, flo, textlo,
       bytes;
 };
 
@@ -118,6 +118,9 @@ int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf
 int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int k, int kpadg, int kpad,
                  uint16_t* Gbf, float* G32, uint16_t* textbf, cudaStream_t st);
 int ws_kt_max(bool x3 = false);
+int run_gproj_tc_x3(const uint16_t* fhi, const uint16_t* flo, int64_t cells, int d, const float* text, int k,
+                    int kpadg, int kpad, uint16_t* Gbf, uint16_t* Gbf_lo, float* G32, uint16_t* text_hi,
+                    uint16_t* text_lo, cudaStream_t st);
 int run_bucket_scan(uint32_t* hist, uint32_t* totals, int64_t nbins, cudaStream_t st);
 // Hilbert order of the points for the SIMT path: order[t] = index of the t-th point along the curve
 // (7-bit key over the domain lo_hi), and *len = n (the kernel's list length). ws: point_order_bytes.
