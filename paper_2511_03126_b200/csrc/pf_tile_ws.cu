@@ -202,7 +202,7 @@ __device__ __forceinline__ float ex2(float x) {
 
 // PROF: wait accounting + trace (PF_WS_DEBUG); OUTS: validation outputs (features, similarities,
 // softmax weights) -- a separate instantiation keeps their fully unrolled stores out of the hot code
-template <bool PROF, bool OUTS>
+template <bool PROF, bool OUTS, bool X3>
 __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant__ TileParams P, int need_max) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       kt_nx = kt_at(P, tile + gridDim.x, nitems);
       if (tid < P.nv && tile + gridDim.x < nitems) ds_nx = P.tile_desc[(tile + gridDim.x) * P.nv + tid];
       bool ok;
-      const int ktp = ktp_of(kt, ok, P.kt_max);
+      const int ktp = ktp_of(kt, ok, X3 ? kKtX3 : kKtWs);
       if (!ok) continue;
       // row -> cell table for this tile
       int32_t* cell = S.cell[t_local & 1];
@@ -333,10 +333,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         const int r = r0 + kRowStep * j;
         rc[j] = r < ktp ? cell[r < kt ? r : 0] : -1;
       }
-      const int nstage = P.x3 ? 2 * nch : nch;  // x3: per chunk pair [hi c][hi c+1][lo c][lo c+1]
+      const int nstage = X3 ? 2 * nch : nch;  // x3: per chunk pair [hi c][hi c+1][lo c][lo c+1]
       for (int qs = 0; qs < nstage; ++qs) {
-        const int c = P.x3 ? 2 * (qs >> 2) + (qs & 1) : qs;
-        const bool lo = P.x3 && (qs & 2);
+        const int c = X3 ? 2 * (qs >> 2) + (qs & 1) : qs;
+        const bool lo = X3 && (qs & 2);
         WS_WAIT(&S.b_empty[stage], phase ^ 1u, 0);
         const uint32_t sb = tc::smem_u32(sB + stage * kStageBytes);
         const uint16_t* src;
@@ -387,18 +387,19 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const int kt = kt_nx;
       kt_nx = kt_at(P, tile + gridDim.x, nitems);
       bool ok;
-      const int ktp = ktp_of(kt, ok, P.kt_max);
+      const int ktp = ktp_of(kt, ok, X3 ? kKtX3 : kKtWs);
       if (!ok) continue;
       const int ab = (int)(t_local & 1u);
       WS_WAIT(&S.a_full[ab], (t_local >> 1) & 1u, 1);
       if (lane == 0) WS_TRACE(t_local, 3);
       // the builders wrote A (the tile's bilinear weights) straight into TMEM buffer ab; the MMAs read
       // A from TMEM and B from shared memory; the commit after the last group frees buffer ab
-      const uint32_t tA = tA0 + (uint32_t)(ab * (P.x3 ? kKtX3 / 2 : kKtWs / 2));
+      const uint32_t tA = tA0 + (uint32_t)(ab * (X3 ? kKtX3 / 2 : kKtWs / 2));
       const uint32_t tAlo = tA + (uint32_t)kKtX3;  // x3: lo parts after both hi buffers
-      const int gst = P.x3 ? 2 * kCG : kCG;          // ring stages per MMA group
+      constexpr int gst = X3 ? 2 * kCG : kCG;      // ring stages per MMA group
       tc::fence_after_sync();
       for (int c = 0; c < nch; c += kCG) {
+#pragma unroll
         for (int g = 0; g < gst; ++g) WS_WAIT(&S.b_full[stage + g], phase, 2);
         const int db = dcount % kDBufs;
         if (c < nd) WS_WAIT(&S.d_empty[db], ((dcount / kDBufs) & 1u) ^ 1u, 3);
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           // descriptors advance by 2048 B (start field +128) and 8 TMEM columns per K=16 step
           uint64_t bd = tc::smem_desc_sw128(b0, kStageBytes, 1024);
           uint32_t ta = tA;
-          if (!P.x3) {
+          if constexpr (!X3) {
             tc::mma_bf16_ts_elect(dst, ta, bd, idesc, 0u);
 #pragma unroll 4
             for (int s = 1; s < ktp / 16; ++s) {
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
               tl += 8;
             }
           }
+#pragma unroll
           for (int g = 0; g < gst; ++g) tc::mma_commit_elect(&S.b_empty[stage + g]);
           tc::mma_commit_elect(&S.d_full[db]);
           if (c + kCG >= nch) tc::mma_commit_elect(&S.a_empty[ab]);
@@ -496,7 +498,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const int32_t cd = cd_nx;
       fetch(tile + gridDim.x, kt_nx, ds_nx, p_nx, mw_nx, cd_nx);
       bool ok;
-      const int ktp = ktp_of(kt, ok, P.kt_max);
+      const int ktp = ktp_of(kt, ok, X3 ? kKtX3 : kKtWs);
       if (!ok) continue;
       if (bh == 0 && P.vox_list) {
         // touched-voxel list without returning atomics: slot jpt holds the code when this row is the
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const float ox = 0.5f * (lo[0] + hi[0]), oy = 0.5f * (lo[1] + hi[1]), oz = 0.5f * (lo[2] + hi[2]);
       const float ex = hi[0] - lo[0], ey = hi[1] - lo[1], ez = hi[2] - lo[2];
       // x3 (fp32 bar): always the exact fp32 projection, as prep's taps
-      const bool exact = P.x3 || ex * ex + ey * ey + ez * ez > 4.f * kAffineR * kAffineR;
+      const bool exact = X3 || ex * ex + ey * ey + ez * ez > 4.f * kAffineR * kAffineR;
       // views with taps in this tile, by rank; coefficients of rank 8 l + bj by lane l of warp bj
       const uint2 dlo = lane < P.nv ? sdesc[lane] : make_uint2(0u, 0u);
       const uint2 dhi = lane + 32 < P.nv ? sdesc[lane + 32] : make_uint2(0u, 0u);
@@ -576,8 +578,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       asm volatile("bar.sync 1, %0;" ::"n"(kBuildThreads) : "memory");  // coefficients visible
       if (bt == 0) WS_TRACE(t_local, 1);
       tc::fence_after_sync();
-      const uint32_t tAb = tA0 + (uint32_t)(ab * (P.x3 ? kKtX3 / 2 : kKtWs / 2)) + t_lanes;
-      const bool x3 = P.x3 != 0;  // lo parts at + kKtX3 columns
+      const uint32_t tAb = tA0 + (uint32_t)(ab * (X3 ? kKtX3 / 2 : kKtWs / 2)) + t_lanes;
+      constexpr bool x3 = X3;  // lo parts at + kKtX3 columns
       const long long tb1 = WS_CLOCK();
       if constexpr (PROF) wait_cyc[14] += tb1 - tb0;
       const float dxp = p.x - ox, dyp = p.y - oy, dzp = p.z - oz;
@@ -627,7 +629,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           const float w0 = tapw(2 * j), w1 = tapw(2 * j + 1);
           const __nv_bfloat162 pr = __floats2bfloat162_rn(w0, w1);
           tc::tmem_st_x1(col0 + (uint32_t)j, *reinterpret_cast<const uint32_t*>(&pr));
-          if (x3) {
+          if constexpr (x3) {
             const __nv_bfloat162 pl = __floats2bfloat162_rn(w0 - __low2float(pr), w1 - __high2float(pr));
             tc::tmem_st_x1(col0 + (uint32_t)(kKtX3 + j), *reinterpret_cast<const uint32_t*>(&pl));
           }
@@ -674,7 +676,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
           }
         };
         emit(pk, col0);
-        if (x3) emit(pkl, col0 + (uint32_t)kKtX3);
+        if constexpr (x3) emit(pkl, col0 + (uint32_t)kKtX3);
       };
       // rank rk: view, window base and the row's coordinates relative to the window origin
       auto coords = [&](int rk, int& v, int& base, float& fu_rel, float& fv_rel) {
@@ -730,7 +732,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       if (bh == 0)  // columns past the last window (K padding to 16) must be zero too
         for (int j = kt >> 1; j < (ktp >> 1); ++j) {
           tc::tmem_st_x1(tAb + (uint32_t)j, 0u);
-          if (x3) tc::tmem_st_x1(tAb + (uint32_t)(kKtX3 + j), 0u);
+          if constexpr (x3) tc::tmem_st_x1(tAb + (uint32_t)(kKtX3 + j), 0u);
         }
       const long long tb2 = WS_CLOCK();
       tc::tmem_st_wait();
@@ -783,7 +785,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         p_nx = ld_pref_f4(P.spts + j_nx);
       }
       bool ok;
-      ktp_of(kt, ok, P.kt_max);
+      ktp_of(kt, ok, X3 ? kKtX3 : kKtWs);
       if (!ok) {  // kt == -1: re-run as sub-tiles; otherwise the points go to the SIMT kernel
         if (kt != -1 && valid && half == 0) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(pcur.w);
         continue;
@@ -1031,10 +1033,14 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = ws_smem_bytes();
-  cudaFuncSetAttribute(k_tile_ws<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k_tile_ws<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k_tile_ws<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k_tile_ws<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_tile_ws<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = (P.n + kTile - 1) / kTile;  // (+ sub-tiles, known on the device only)
   int grid = (int)(ntiles < sms ? ntiles : sms);
   if (const char* g = getenv("PF_WS_GRID")) grid = (int)(ntiles < atoi(g) ? ntiles : atoi(g));  // debug knob
@@ -1056,10 +1062,17 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
     Q.trace = trace;
   }
   const bool outs = P.sims || P.weights || P.features;
-  if (debug && outs) k_tile_ws<true, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
-  else if (debug) k_tile_ws<true, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
-  else if (outs) k_tile_ws<false, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
-  else k_tile_ws<false, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+  if (P.x3) {  // f32 maps: the hi / lo split instantiation (the bf16 code is untouched by it)
+    if (debug && outs) k_tile_ws<true, true, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+    else if (debug) k_tile_ws<true, false, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+    else if (outs) k_tile_ws<false, true, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+    else k_tile_ws<false, false, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+  } else {
+    if (debug && outs) k_tile_ws<true, true, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+    else if (debug) k_tile_ws<true, false, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+    else if (outs) k_tile_ws<false, true, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+    else k_tile_ws<false, false, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+  }
   const int rc = check_launch("tile_ws");
   if (debug && rc == PF_OK) {
     static unsigned long long h[16 * 1024];
