@@ -142,7 +142,7 @@ __device__ __forceinline__ int chan(int j, int e, int lane) {
 }
 
 template <int DT, int VEC, int NCHUNK>
-__global__ void __launch_bounds__(kFuseThreads, 2) k_fuse_simt(FuseParams P) {
+__global__ void __launch_bounds__(kFuseThreads, 3) k_fuse_simt(FuseParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   pf_view_t* s_views = reinterpret_cast<pf_view_t*>(smem);
   float* s_vals = reinterpret_cast<float*>(s_views + P.nv);       // [kpad][kMaxP]
