@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
   const int tid = threadIdx.x, warp = tid >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * kGM;
   const int nchunk = d / 64;
+  const int nk = (k + 15) & ~15;  // MMA N: the materials rounded up to 16 (columns >= nk of G are 0)
 
   auto load = [&](int ch, int st) {
 #pragma unroll
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
         tc::cp_async16(tc::smem_u32(sa + off), fa + cell * d + ch * 64 + q * 8);
       }
       // B: material n, channels ch*64 .. +64 (bf16 text, K-major SW128)
-      for (int e = tid; e < kpadg * 8; e += 128) {
+      for (int e = tid; e < nk * 8; e += 128) {
         const int n = e >> 3, q = e & 7;
         const uint32_t off = (uint32_t)((n >> 3) * 1024 + (n & 7) * 128 + (((q ^ (n & 7)) & 7) << 4));
         tc::cp_async16(tc::smem_u32(sb + off), fb + (int64_t)n * d + ch * 64 + q * 8);
@@ -88,13 +89,13 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
 
   if (tid < kGStages) tc::mbar_init(&mbar[tid], 1);
   uint32_t ncols = 32;
-  while (ncols < (uint32_t)kpadg) ncols <<= 1;
+  while (ncols < (uint32_t)nk) ncols <<= 1;
   if (warp == 0) tc::tmem_alloc(&tmem_base_s, ncols);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = tmem_base_s;
-  const uint32_t idesc = tc::idesc_bf16_f32(128, kpadg, false, false);
+  const uint32_t idesc = tc::idesc_bf16_f32(128, nk, false, false);
 
   // 3-stage ring: chunks ch+1 and ch+2 are in flight while chunk ch's MMAs run
   for (int c = 0; c < kGStages - 1 && c < nchunk; ++c) load(c, c);
@@ -136,9 +137,14 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
   const int ld = kpadg + 1;
   for (int cc = 0; cc < kpadg; cc += 32) {
     float v[32];
-    tc::tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + cc, v);
+    if (cc < nk) {
+      tc::tmem_ld32(tbase + ((uint32_t)(warp * 32) << 16) + cc, v);
+    } else {
 #pragma unroll
-    for (int q = 0; q < 32; ++q) srow[tid * ld + cc + q] = v[q];
+      for (int q = 0; q < 32; ++q) v[q] = 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < 32; ++q) srow[tid * ld + cc + q] = cc + q < nk ? v[q] : 0.f;
   }
   __syncthreads();
   for (int r = warp; r < kGM; r += 4) {
