@@ -75,9 +75,10 @@ __device__ __forceinline__ uint32_t hilbert3(uint32_t x, uint32_t y, uint32_t z,
   return key;
 }
 
+template <int BITS>  // compile-time grid order: the Hilbert loops fully unrolled
 __global__ void k_sort_keys(const float* __restrict__ p, int64_t n, const double* __restrict__ lo_hi,
-                            uint32_t* __restrict__ keys, uint32_t* __restrict__ hist, int bits) {
-  const int cells = 1 << bits;
+                            uint32_t* __restrict__ keys, uint32_t* __restrict__ hist) {
+  constexpr int cells = 1 << BITS;
   const float lx = (float)lo_hi[0], ly = (float)lo_hi[1], lz = (float)lo_hi[2];
   const float ext = fmaxf(fmaxf((float)(lo_hi[3] - lo_hi[0]), (float)(lo_hi[4] - lo_hi[1])),
                           (float)(lo_hi[5] - lo_hi[2]));
@@ -87,7 +88,7 @@ __global__ void k_sort_keys(const float* __restrict__ p, int64_t n, const double
     const int cx = min(max((int)((__ldg(p + 3 * i) - lx) * inv), 0), cells - 1);
     const int cy = min(max((int)((__ldg(p + 3 * i + 1) - ly) * inv), 0), cells - 1);
     const int cz = min(max((int)((__ldg(p + 3 * i + 2) - lz) * inv), 0), cells - 1);
-    const uint32_t key = hilbert3((uint32_t)cx, (uint32_t)cy, (uint32_t)cz, bits);
+    const uint32_t key = hilbert3((uint32_t)cx, (uint32_t)cy, (uint32_t)cz, BITS);
     keys[i] = key;
     atomicAdd(hist + key, 1u);
   }
@@ -793,7 +794,7 @@ int run_point_order(const float* points, int64_t n, const double* lo_hi, unsigne
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + align256(sizeof(uint32_t) * (size_t)n));
   uint32_t* totals = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(hist) + align256(sizeof(uint32_t) << 21));
   cudaMemsetAsync(hist, 0, sizeof(uint32_t) << 21, st);
-  k_sort_keys<<<grid_for(n, 256), 256, 0, st>>>(points, n, lo_hi, keys, hist, 7);
+  k_sort_keys<7><<<grid_for(n, 256), 256, 0, st>>>(points, n, lo_hi, keys, hist);
   if (int rc = check_launch("order_keys")) return rc;
   if (int rc = run_bucket_scan(hist, totals, int64_t(1) << 21, st)) return rc;
   k_order_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, keys, hist, order, len);
@@ -855,7 +856,8 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   const int64_t nbins = int64_t(1) << (3 * bits);
   cudaMemsetAsync(hist, 0, sizeof(uint32_t) * nbins, st);
   cudaMemsetAsync(P.ovf_count, 0, sizeof(int32_t), st);
-  k_sort_keys<<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist, bits);
+  if (bits == 8) k_sort_keys<8><<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist);
+  else k_sort_keys<7><<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist);
   if (int rc = check_launch("sort_keys")) return rc;
   if (int rc = run_bucket_scan(hist, totals, nbins, st)) return rc;
   k_sort_scatter<<<grid_for(n, 256), 256, 0, st>>>(points, n, keys, hist, const_cast<int32_t*>(P.inv),
