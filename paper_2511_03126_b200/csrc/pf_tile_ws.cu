@@ -805,9 +805,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         if ((warp & 3) == 0 && lane == 0) WS_TRACE(a_tile, 25 + c);
         tc::fence_after_sync();
 #pragma unroll
-        for (int g = 0; g < 2 * kCG; ++g) {  // 32 columns at a time (register budget: wacc stays live)
-          float v[32];
-          tc::tmem_ld32(tbase + (uint32_t)(db * kDCols + 32 * g) + t_lane, v);
+        for (int g2 = 0; g2 < kCG; ++g2) {  // 64 columns per wait (two x32 loads in flight)
+          float v64[64];
+          tc::tmem_ld64(tbase + (uint32_t)(db * kDCols + 64 * g2) + t_lane, v64);
+#pragma unroll
+          for (int gh = 0; gh < 2; ++gh) {
+          const int g = 2 * g2 + gh;
+          float* v = v64 + 32 * gh;
           if (g == 2 * kCG - 1) {
             tc::fence_before_sync();
             __syncwarp();
@@ -831,6 +835,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
             for (int q = 0; q < 32; q += 4)
               *reinterpret_cast<float4*>(dst + q) =
                   make_float4(v[q] * invc, v[q + 1] * invc, v[q + 2] * invc, v[q + 3] * invc);
+          }
           }
         }
       }
