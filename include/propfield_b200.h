@@ -282,6 +282,11 @@ int pf_dino_knn_interpolate(const double* q, int64_t nq, const double* s, int64_
  * (densify.py:142-147). np == 0 -> PF_ERR_MATERIAL. */
 int pf_nearest_index(const double* queries, int64_t nq, const double* points, int64_t np, int64_t* idx,
                      void* stream);
+/* The same result through a uniform grid over `points` (exact shell search, O(n) instead of
+ * O(nq * np)); workspace pf_nearest_workspace_bytes(np). */
+uint64_t pf_nearest_workspace_bytes(int64_t np);
+int pf_nearest_index_grid(const double* queries, int64_t nq, const double* points, int64_t np, int64_t* idx,
+                          void* workspace, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
  * Cell-range sharding of one object across ranks (SURVEY §8e "shard by voxel-code ranges after a

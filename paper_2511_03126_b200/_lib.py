@@ -130,6 +130,8 @@ SIGNATURES = {
     "pf_dino_knn_workspace_bytes": ([_I64, _I64, _I32], C.c_uint64),
     "pf_dino_knn_interpolate": ([_P, _I64, _P, _I64, _I32, _P, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "pf_nearest_index": ([_P, _I64, _P, _I64, _P, _P], C.c_int),
+    "pf_nearest_workspace_bytes": ([_I64], C.c_uint64),
+    "pf_nearest_index_grid": ([_P, _I64, _P, _I64, _P, _P, _P], C.c_int),
     "pf_shard_bins": ([], C.c_int32),
     "pf_shard_keys": ([_P, _I64, _P, _I32, _P, _P, _P], C.c_int),
     "pf_shard_cuts": ([_P, _I32, _P, _P], C.c_int),

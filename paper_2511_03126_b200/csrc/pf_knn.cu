@@ -413,6 +413,164 @@ int pf_estimate_normals(const float* points, int64_t n, int32_t k, double ccx, d
 
 }  // extern "C"
 
+// ---- nearest point of another set (densify_field's donor query, densify.py:142-147) --------------------
+// Grid over the donor points (the k-NN grid above with k = 1), each query searches shells around its
+// cell until its best fp64 squared distance is inside the searched block; lowest donor index on ties
+// (as a brute-force scan would give).
+namespace pf {
+namespace {
+
+__device__ __forceinline__ unsigned long long dflip(double d) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dunflip(unsigned long long u) {
+  u = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
+  return __longlong_as_double((long long)u);
+}
+
+__global__ void k_bbox64(const double* __restrict__ p, int64_t n, unsigned long long* __restrict__ mm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int a = 0; a < 3; ++a) {
+      const unsigned long long f = dflip(p[3 * i + a]);
+      atomicMin(mm + a, f);
+      atomicMax(mm + 3 + a, f);
+    }
+}
+
+__global__ void k_bbox64_final(const unsigned long long* __restrict__ mm, double* __restrict__ lo_hi) {
+  if (threadIdx.x < 6) lo_hi[threadIdx.x] = dunflip(mm[threadIdx.x]);
+}
+
+__global__ void k_f64_to_f32(const double* __restrict__ p, int64_t n3, float* __restrict__ q) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n3; i += (int64_t)gridDim.x * blockDim.x)
+    q[i] = (float)p[i];
+}
+
+__global__ void __launch_bounds__(128) k_cross_nearest(const double* __restrict__ qp, int64_t nq,
+                                                       const double* __restrict__ pp, int64_t np,
+                                                       const float4* __restrict__ kp,
+                                                       const int32_t* __restrict__ kidx, const Grid* __restrict__ gp,
+                                                       const uint32_t* __restrict__ ends, int64_t* __restrict__ out) {
+  const Grid g = *gp;
+  const double c = (double)g.c;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
+    const double qx = qp[3 * i], qy = qp[3 * i + 1], qz = qp[3 * i + 2];
+    double bd = INFINITY;
+    int64_t bi = INT64_MAX;
+    const double gx1 = (double)g.lo[0] + g.dims[0] * c, gy1 = (double)g.lo[1] + g.dims[1] * c,
+                 gz1 = (double)g.lo[2] + g.dims[2] * c;
+    if (!(qx >= g.lo[0] && qx < gx1 && qy >= g.lo[1] && qy < gy1 && qz >= g.lo[2] && qz < gz1)) {
+      // outside the donors' grid (rare): the shell bound does not apply, scan every donor
+      for (int64_t o = 0; o < np; ++o) {
+        const double ex = __dsub_rn(qx, pp[3 * o]), ey = __dsub_rn(qy, pp[3 * o + 1]), ez = __dsub_rn(qz, pp[3 * o + 2]);
+        const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
+        if (d2 < bd) {  // ascending o: the first minimum is the lowest index
+          bd = d2;
+          bi = o;
+        }
+      }
+      out[i] = bi;
+      continue;
+    }
+    int cx, cy, cz;
+    cell_of(g, (float)qx, (float)qy, (float)qz, cx, cy, cz);
+    const int maxs = max(max(g.dims[0], g.dims[1]), g.dims[2]);
+    for (int s = 0;; ++s) {
+      // shell s (cells at Chebyshev distance s), clipped to the grid: O(s^2) cells per shell
+      const int z0 = max(cz - s, 0), z1 = min(cz + s, g.dims[2] - 1);
+      const int y0 = max(cy - s, 0), y1 = min(cy + s, g.dims[1] - 1);
+      for (int z = z0; z <= z1; ++z)
+        for (int y = y0; y <= y1; ++y) {
+          const bool face = abs(z - cz) == s || abs(y - cy) == s;
+          const int xs = face ? 1 : 2 * s;  // interior rows of the cube: only x = cx -+ s
+          for (int x = cx - s; x <= cx + s; x += (s == 0 ? 1 : xs)) {
+            if (x < 0 || x >= g.dims[0]) continue;
+            const uint32_t want = (uint32_t)x | ((uint32_t)y << kCellBits) | ((uint32_t)z << (2 * kCellBits));
+            const uint32_t b = cell_hash(x, y, z);
+            const uint32_t e0 = b ? __ldg(ends + b - 1) : 0u, e1 = __ldg(ends + b);
+            for (uint32_t j = e0; j < e1; ++j) {
+              if (__float_as_uint(__ldg(&kp[j].w)) != want) continue;
+              const int64_t o = __ldg(kidx + j);
+              const double ex = __dsub_rn(qx, pp[3 * o]), ey = __dsub_rn(qy, pp[3 * o + 1]),
+                           ez = __dsub_rn(qz, pp[3 * o + 2]);
+              const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
+              if (d2 < bd || (d2 == bd && o < bi)) {
+                bd = d2;
+                bi = o;
+              }
+            }
+          }
+        }
+      // every donor outside the searched block [c - s, c + s] is at least `reach` away from q
+      const double bx0 = (double)g.lo[0] + (cx - s) * c, bx1 = (double)g.lo[0] + (cx + s + 1) * c;
+      const double by0 = (double)g.lo[1] + (cy - s) * c, by1 = (double)g.lo[1] + (cy + s + 1) * c;
+      const double bz0 = (double)g.lo[2] + (cz - s) * c, bz1 = (double)g.lo[2] + (cz + s + 1) * c;
+      const double reach = fmax(fmin(fmin(fmin(qx - bx0, bx1 - qx), fmin(qy - by0, by1 - qy)),
+                                     fmin(qz - bz0, bz1 - qz)), 0.0) * (1.0 - 1e-9);
+      if ((bi != INT64_MAX && bd < reach * reach) || s >= maxs) break;
+    }
+    out[i] = bi;
+  }
+}
+
+}  // namespace
+}  // namespace pf
+
+extern "C" {
+
+uint64_t pf_nearest_workspace_bytes(int64_t np) {
+  auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  return pf_knn_workspace_bytes(np) + al(sizeof(int32_t) * (uint64_t)np) + al(sizeof(float) * 3 * (uint64_t)np) +
+         al(8 * sizeof(unsigned long long));
+}
+
+int pf_nearest_index_grid(const double* queries, int64_t nq, const double* points, int64_t np, int64_t* idx,
+                          void* workspace, void* stream) {
+  using namespace pf;
+  if (nq < 0 || np < 0) return set_error(PF_ERR_VALUE, "nearest_index: negative size");
+  if (nq == 0) return PF_OK;
+  if (np == 0) return set_error(PF_ERR_MATERIAL, "no point in the cloud has a geometric feature");
+  if (!workspace) return set_error(PF_ERR_VALUE, "nearest_index: workspace missing");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  auto al = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(ws);
+  ws += al(sizeof(uint32_t) * (uint64_t)np);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws);
+  ws += al(sizeof(uint32_t) * kHashBins);
+  uint32_t* totals = reinterpret_cast<uint32_t*>(ws);
+  ws += al(sizeof(uint32_t) * 1024);
+  float4* kp = reinterpret_cast<float4*>(ws);
+  ws += al(sizeof(float4) * (uint64_t)np);
+  Grid* g = reinterpret_cast<Grid*>(ws);
+  ws += al(sizeof(Grid));
+  double* lo_hi = reinterpret_cast<double*>(ws);
+  ws += al(6 * sizeof(double));
+  int32_t* kidx = reinterpret_cast<int32_t*>(ws);
+  ws += al(sizeof(int32_t) * (uint64_t)np);
+  float* p32 = reinterpret_cast<float*>(ws);
+  ws += al(sizeof(float) * 3 * (uint64_t)np);
+  unsigned long long* mm = reinterpret_cast<unsigned long long*>(ws);
+  cudaMemsetAsync(mm, 0xff, 3 * sizeof(unsigned long long), st);
+  cudaMemsetAsync(mm + 3, 0, 3 * sizeof(unsigned long long), st);
+  k_bbox64<<<grid_for(np, 256), 256, 0, st>>>(points, np, mm);
+  k_bbox64_final<<<1, 32, 0, st>>>(mm, lo_hi);
+  k_f64_to_f32<<<grid_for(3 * np, 256), 256, 0, st>>>(points, 3 * np, p32);
+  if (int rc = check_launch("nearest_bbox")) return rc;
+  k_knn_grid<<<1, 1, 0, st>>>(lo_hi, np, 1, g);
+  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kHashBins, st);
+  k_knn_keys<<<grid_for(np, 256), 256, 0, st>>>(p32, np, g, keys, hist);
+  if (int rc = check_launch("nearest_keys")) return rc;
+  if (int rc = tile::run_bucket_scan(hist, totals, kHashBins, st)) return rc;
+  k_knn_scatter<<<grid_for(np, 256), 256, 0, st>>>(p32, np, g, keys, hist, kp, kidx);
+  if (int rc = check_launch("nearest_scatter")) return rc;
+  k_cross_nearest<<<grid_for(nq, 128, 148 * 32), 128, 0, st>>>(queries, nq, points, np, kp, kidx, g, hist, idx);
+  return check_launch("nearest_query");
+}
+
+}  // extern "C"
+
 // ---- integrate_mass partials from a probability matrix (integrate.py:124-155) -------------------------
 namespace pf {
 namespace {

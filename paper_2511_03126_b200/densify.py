@@ -64,14 +64,25 @@ def dino_knn_interpolate(query_features, source_features, source_probs, k: int):
     return out if tor else out.cpu().numpy()
 
 
-def nearest_index(queries, points):
-    """Index of the nearest point (fp64, lowest index on ties) for every query (cKDTree k=1)."""
+BRUTE_FORCE_MAX = 1 << 24  # query x point pairs below which the brute-force kernel is used
+
+
+def nearest_index(queries, points, grid: bool | None = None):
+    """Index of the nearest point (fp64, lowest index on ties) for every query (cKDTree k=1):
+    brute force for small sets, the exact grid search otherwise."""
     dev = require_cuda()
     t = torch()
     qq = to_dev(queries, t.float64, dev).reshape(-1, 3)
     pp = to_dev(points, t.float64, dev).reshape(-1, 3)
     idx = t.empty(qq.shape[0], dtype=t.int64, device=dev)
-    _lib.call("pf_nearest_index", ptr(qq), qq.shape[0], ptr(pp), pp.shape[0], ptr(idx), stream_handle())
+    nq, np_ = qq.shape[0], pp.shape[0]
+    if grid is None:
+        grid = nq * np_ > BRUTE_FORCE_MAX
+    if grid and np_ > 0:
+        ws = t.empty(int(_lib.load().pf_nearest_workspace_bytes(np_)), dtype=t.uint8, device=dev)
+        _lib.call("pf_nearest_index_grid", ptr(qq), nq, ptr(pp), np_, ptr(idx), ptr(ws), stream_handle())
+    else:
+        _lib.call("pf_nearest_index", ptr(qq), nq, ptr(pp), np_, ptr(idx), stream_handle())
     return idx
 
 

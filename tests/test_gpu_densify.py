@@ -119,3 +119,22 @@ def test_dino_knn_pipeline_scale(cuda):
     keep = ~boundary_ties(q[rows], s, 5)
     np.testing.assert_allclose(out[rows][keep], O.dino_knn_interpolate(q[rows], s, p, 5)[keep], rtol=0, atol=1e-12)
     np.testing.assert_allclose(out.sum(axis=1), 1.0, atol=1e-9)
+
+
+def test_nearest_grid_equals_brute_force(cuda):
+    """pf_nearest_index_grid == the brute-force scan (lowest index on exact ties), including duplicated
+    donors, queries outside the donors' bbox and a surface-like donor set of 300k points."""
+    from paper_2511_03126_b200.densify import nearest_index
+
+    rng = np.random.default_rng(12)
+    u = rng.standard_normal((300_000, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    donors = (u * [0.4, 0.3, 0.2]).astype(np.float32).astype(np.float64)
+    donors[1000:1100] = donors[0:100]  # exact ties: the lower index must win
+    q = np.concatenate([donors[rng.choice(300_000, 2000)] + rng.normal(0, 1e-3, (2000, 3)),
+                        rng.uniform(-1.0, 1.0, (200, 3)),  # many outside the bbox
+                        donors[1000:1100]])
+    g = nearest_index(q, donors, grid=True).cpu().numpy()
+    b = nearest_index(q, donors, grid=False).cpu().numpy()
+    np.testing.assert_array_equal(g, b)
+    assert (g[-100:] == np.arange(100)).all()
