@@ -839,7 +839,7 @@ int run_bucket_scan(uint32_t* hist, uint32_t* totals, int64_t nbins, cudaStream_
 }
 
 int run_unsort(const TileParams& P, cudaStream_t st) {
-  k_unsort<<<grid_for(P.n, 256), 256, 0, st>>>(P.srec, P.inv, P.n, P.nwords, P.p, P.mask_bits, P.counts,
+  k_unsort<<<grid_for(P.n, 256, 1 << 30), 256, 0, st>>>(P.srec, P.inv, P.n, P.nwords, P.p, P.mask_bits, P.counts,
                                               P.codes, P.props);
   const int rc = check_launch("unsort");
   stage_mark(4, st);
@@ -856,11 +856,11 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   const int64_t nbins = int64_t(1) << (3 * bits);
   cudaMemsetAsync(hist, 0, sizeof(uint32_t) * nbins, st);
   cudaMemsetAsync(P.ovf_count, 0, sizeof(int32_t), st);
-  if (bits == 8) k_sort_keys<8><<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist);
+  if (bits == 8) k_sort_keys<8><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(points, n, P.lo_hi, keys, hist);
   else k_sort_keys<7><<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist);
   if (int rc = check_launch("sort_keys")) return rc;
   if (int rc = run_bucket_scan(hist, totals, nbins, st)) return rc;
-  k_sort_scatter<<<grid_for(n, 256), 256, 0, st>>>(points, n, keys, hist, const_cast<int32_t*>(P.inv),
+  k_sort_scatter<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(points, n, keys, hist, const_cast<int32_t*>(P.inv),
                                                    const_cast<float4*>(P.spts));
   if (int rc = check_launch("sort_scatter")) return rc;
   stage_mark(1, st);
