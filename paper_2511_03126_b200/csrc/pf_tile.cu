@@ -252,7 +252,15 @@ struct ViewAff {
 // so the first-order model is within fx r^2 (|X0| + Z0) / (Z0^2 zmin) of the exact value. On top:
 // the fp32 error of u(o) (the view's constant project_f32 bound), 3 fma roundings of a ~|u| value
 // and the gradient's relative error.
-__device__ int classify_tile_view(const ViewF& v, const float4& vb, const pf_view_t& v64,
+// 1 / z for z > 1e-3 without the fp64 division subroutine: fp32 seed + two Newton steps (a few
+// fp64 ulps; the model's bounds allow ~1e-13)
+__device__ __forceinline__ double rcp_f64(double z) {
+  double r = (double)__frcp_rn((float)z);
+  r = fma(r, fma(-z, r, 1.0), r);
+  return fma(r, fma(-z, r, 1.0), r);
+}
+
+__device__ __forceinline__ int classify_tile_view(const ViewF& v, const float4& vb, const pf_view_t& v64,
                                   const float* __restrict__ depth, const float* lo, const float* hi, float eps,
                                   int4& win, ViewAff& aff) {
   float zmin = 1e30f, zmax = -1e30f, umin = 1e30f, umax = -1e30f, vmin = 1e30f, vmax = -1e30f;
@@ -311,7 +319,7 @@ __device__ int classify_tile_view(const ViewF& v, const float4& vb, const pf_vie
   // rounding to fp32 (+ ~1e-13), so no fp32 projection bound enters
   const double X0 = cam_row(v64.R, 0, ox, oy, oz, v64.t[0]), Y0 = cam_row(v64.R, 1, ox, oy, oz, v64.t[1]);
   const double Z0 = cam_row(v64.R, 2, ox, oy, oz, v64.t[2]);
-  const double rz0 = 1.0 / Z0;
+  const double rz0 = rcp_f64(Z0);
   const float u0 = (float)fma(v64.fx * X0, rz0, v64.cx), v0 = (float)fma(v64.fy * Y0, rz0, v64.cy);
   // second-order model in a = R0.d, c = R1.d, b = R2.d (d = p - o):
   //   X/Z = X0/Z0 + a/Z0 - X0 b/Z0^2 - a b/Z0^2 + X0 b^2/Z0^3 + R3,
@@ -325,13 +333,14 @@ __device__ int classify_tile_view(const ViewF& v, const float4& vb, const pf_vie
   aff.q = make_float4((float)(su * xr * rz0), (float)(sv * yr * rz0), 0.f, 0.f);
   aff.z0 = (float)Z0;
   const double z0 = Z0, rr = (double)r, zl = (double)zmin;
-  const double r3 = rr * rr * rr / (z0 * z0 * z0);
+  const double r3 = rr * rr * rr * (rz0 * rz0 * rz0);  // bounds below carry a 1.05 factor
+  const double rzl = rcp_f64(zl);
   const double gu = fabs(su) * (1.0 + fabs(xr)) * rr, gv = fabs(sv) * (1.0 + fabs(yr)) * rr;  // |linear part|
   const double qu = fabs(su) * rz0 * (1.0 + fabs(xr)) * rr * rr, qv = fabs(sv) * rz0 * (1.0 + fabs(yr)) * rr * rr;
   // remainder + fp32 rounding of u0 and of the ~6 rounded ops of the evaluation + the fp32 coefficients
-  const double eu = fabs(v64.fx) * r3 * ((fabs(X0) + rr) / zl + 1.0) * 1.05 + 7e-7 * (fabs(u0) + gu + qu) +
+  const double eu = fabs(v64.fx) * r3 * ((fabs(X0) + rr) * rzl + 1.0) * 1.05 + 7e-7 * (fabs(u0) + gu + qu) +
                     1e-5 * (gu + qu) + 1e-5;
-  const double ev = fabs(v64.fy) * r3 * ((fabs(Y0) + rr) / zl + 1.0) * 1.05 + 7e-7 * (fabs(v0) + gv + qv) +
+  const double ev = fabs(v64.fy) * r3 * ((fabs(Y0) + rr) * rzl + 1.0) * 1.05 + 7e-7 * (fabs(v0) + gv + qv) +
                     1e-5 * (gv + qv) + 1e-5;
   aff.eu = (float)eu;
   aff.ev = (float)ev;
