@@ -172,6 +172,8 @@ int pf_integrate_partials(const double* weights, int64_t n, int32_t k, const flo
 #define PF_FUSE_SKIP_VOXELS 8u     /* do not touch the voxel grid (codes still written)    */
 #define PF_FUSE_FORCE_SIMT 16u     /* use the SIMT gather even where the tensor path applies */
 #define PF_FUSE_PREPARED 32u       /* workspace already holds pf_fuse_prepare's tables: skip it */
+#define PF_FUSE_FEATURE_KERNEL 64u /* bf16 maps: the feature-product tile kernel (k_tile_ws) instead
+                                      of the Gram kernel (always taken with PF_FUSE_WRITE_FEATURES) */
 
 /* Number of doubles in the `partials` output of pf_fuse_query. Layout:
  * [0,k)          weight_totals_k = sum_i w_ik                       (integrate.py:133)
@@ -210,7 +212,8 @@ typedef struct pf_fuse_args {
   int32_t* codes;           /* (n,) voxel code                                                   */
   float* grid_partials;     /* (2*g^3) f32 [sum rho | count], caller-zeroed unless SKIP_VOXELS   */
   double* partials;         /* (PF_PARTIALS_LEN(k)) caller-zeroed, accumulated                   */
-  int32_t* status;          /* (1,) device int32, caller-zeroed; bit0 = NaN similarity seen      */
+  int32_t* status;          /* (1,) device int32, caller-zeroed; bit0 = NaN similarity seen,     *
+                             * bit1 = non-finite softmax sum (inf inputs)                        */
   float* features;          /* optional (n,d) f32 mean features (flag WRITE_FEATURES)            */
   float* sims;              /* optional (n,k) f32 (flag WRITE_SIMS)                              */
   float* weights;           /* optional (n,k) f32 (flag WRITE_WEIGHTS)                           */

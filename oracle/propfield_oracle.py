@@ -27,6 +27,15 @@ except ImportError:  # pragma: no cover
         return wrap if not (a and callable(a[0])) else a[0]
 
 
+class PropfieldError(Exception):
+    """errors.py:4-5 (restated so the oracle raises the reference's classes without importing the
+    product package)."""
+
+
+class MaterialError(PropfieldError):
+    """errors.py:24-25: softmax_weights raises it on NaN similarities (grounding.py:173-174)."""
+
+
 # ---- geometry -----------------------------------------------------------------------------------
 def project_points(points, rotation, translation, fx, fy, cx, cy):
     """geometry.py:46-59: cam = p @ R.T + t; u = fx X / z + cx; v = fy Y / z + cy."""
@@ -211,7 +220,7 @@ def softmax_weights(similarities, temperature):
         raise ValueError(f"temperature must be positive, got {temperature}")
     sims = np.atleast_2d(np.asarray(similarities, dtype=np.float64))
     if np.isnan(sims).any():
-        raise ValueError("NaN similarity passed to kernel regression")
+        raise MaterialError("NaN similarity passed to kernel regression")
     scaled = sims / temperature
     scaled -= scaled.max(axis=1, keepdims=True)
     w = np.exp(scaled)

@@ -20,7 +20,7 @@ Fused device path:
 from . import kernels
 from .batch import BatchResult, fuse_batch
 from .densify import densify_field, dino_knn_interpolate
-from .device import ViewSet
+from .device import ViewSet, cached_view_set, clear_view_cache
 from .errors import (
     BundleLoadError,
     BundleStructureError,
@@ -54,7 +54,7 @@ from .types import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "kernels", "ViewSet", "QueryTables", "FuseBuffers", "FusedResult", "fuse_and_query",
+    "kernels", "ViewSet", "cached_view_set", "clear_view_cache", "QueryTables", "FuseBuffers", "FusedResult", "fuse_and_query",
     "aggregate_geometric_features", "default_epsilon", "project_points", "visibility_mask", "estimate_normals",
     "kernel_regress", "material_similarity", "regress_with_weights", "softmax_weights",
     "adaptive_voxel_side", "characteristic_length", "integrate_mass", "estimate_from_partials", "voxel_mass",

@@ -30,6 +30,7 @@ PF_FUSE_WRITE_WEIGHTS = 4
 PF_FUSE_SKIP_VOXELS = 8
 PF_FUSE_FORCE_SIMT = 16
 PF_FUSE_PREPARED = 32
+PF_FUSE_FEATURE_KERNEL = 64
 
 # pf_view_t (160 bytes)
 VIEW_DTYPE = np.dtype(

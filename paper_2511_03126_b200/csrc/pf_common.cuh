@@ -2,7 +2,8 @@
 //
 // The fp64 projection helpers reproduce the reference's numpy arithmetic bit for bit:
 // `cam = p @ R.T + t` (geometry.py:54) is an OpenBLAS dgemm whose per-element result is
-// fma(p2,R[.,2], fma(p1,R[.,1], p0*R[.,0])) + t (checked against numpy in oracle/README.md), and
+// fma(p2,R[.,2], fma(p1,R[.,1], p0*R[.,0])) + t (pinned by tests/test_oracle.py::
+// TestProjectionOperationOrder against this image's numpy), and
 // `u = fx * X / z + cx` (geometry.py:57-58) is three separately rounded ops. Explicit __fma_rn /
 // __dmul_rn / __ddiv_rn / __dadd_rn intrinsics stop nvcc from contracting or reordering them.
 #pragma once

@@ -303,7 +303,11 @@ __global__ void __launch_bounds__(kFuseThreads, 3) k_fuse_simt(FuseParams P) {
         w[q] = e;
         se += e;
       }
-      const float rs = 1.f / warp_sum(se);
+      const float se_t = warp_sum(se);
+      // a non-finite sum without a NaN similarity means infinite inputs: flag it (bit 1) rather than
+      // return NaN properties silently
+      if (lane == 0 && !(se_t <= 3.4e38f)) atomicOr(P.status, 2);
+      const float rs = 1.f / se_t;
       float pl[kMaxP] = {0.f, 0.f, 0.f, 0.f};
       float pml = 0.f;
 #pragma unroll
@@ -452,6 +456,18 @@ static bool tile_path_ok(const pf_fuse_args_t* a) {
   return true;
 }
 
+// bf16 maps take the Gram-formulation kernel (pf_gram.cu, 512-point tiles) unless mean features are
+// requested (validation output only the feature-product kernel k_tile_ws produces); PF_GRAM=0 forces
+// k_tile_ws (A/B measurements)
+static bool tile_gram(const pf_fuse_args_t* a) {
+  static const bool off = [] {
+    const char* e = getenv("PF_GRAM");
+    return e && e[0] == '0';
+  }();
+  return !off && a->fmap_dtype == PF_BF16 && !(a->flags & (PF_FUSE_WRITE_FEATURES | PF_FUSE_FEATURE_KERNEL));
+}
+static int tile_rows(const pf_fuse_args_t* a) { return tile_gram(a) ? tile::kGramTile : tile::kTile; }
+
 static uint64_t g_bytes(const pf_fuse_args_t* a) {
   const uint64_t g = (uint64_t)total_cells(a) * (uint64_t)(32 * kpl_of(a->k)) * sizeof(float);
   return (g + 255) & ~uint64_t(255);
@@ -468,8 +484,13 @@ static uint64_t simt_order_bytes(int64_t n) {
 uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* a) {
   if (!a || !a->views_host || a->d <= 0 || a->k <= 0) return 0;
   uint64_t bytes = g_bytes(a);
-  if (tile_path_ok(a))
-    bytes += tile::tile_layout(a->n, a->nviews, total_cells(a), tile::kMaxKpadTC, a->d, tile_x3(a)).bytes;
+  if (tile_path_ok(a)) {
+    // sized for either tile kernel: a buffer set may be reused with and without feature outputs
+    const uint64_t b128 = tile::tile_layout(a->n, a->nviews, total_cells(a), tile::kMaxKpadTC, a->d, tile_x3(a)).bytes;
+    const uint64_t b512 = tile_x3(a) ? 0 : tile::tile_layout(a->n, a->nviews, total_cells(a), tile::kMaxKpadTC, a->d,
+                                                             false, tile::kGramTile).bytes;
+    bytes += b128 > b512 ? b128 : b512;
+  }
   else if (a->n >= kSimtOrderMin)
     bytes += simt_order_bytes(a->n);
   return bytes;
@@ -525,6 +546,7 @@ int pf_fuse_prepare(const pf_fuse_args_t* a, void* stream) {
       return rc;
     // G on the tensor cores from the same splits (hi.hi + hi.lo + lo.hi), fp32 copy for the SIMT
     // overflow points
+    if (int rc = tile::run_text_bound(a->text, a->k, a->d, reinterpret_cast<float*>(ws + L.tbound), st)) return rc;
     return tile::run_gproj_tc_x3(fhi, flo, cells, a->d, a->text, a->k, kpadg, kpad,
                                  reinterpret_cast<uint16_t*>(ws + L.gbf), reinterpret_cast<uint16_t*>(ws + L.glo), G,
                                  reinterpret_cast<uint16_t*>(ws + L.textbf), reinterpret_cast<uint16_t*>(ws + L.textlo),
@@ -535,6 +557,7 @@ int pf_fuse_prepare(const pf_fuse_args_t* a, void* stream) {
     unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
     const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg);
     Gbf = reinterpret_cast<uint16_t*>(ws + L.gbf);
+    if (int rc = tile::run_text_bound(a->text, a->k, a->d, reinterpret_cast<float*>(ws + L.tbound), st)) return rc;
     // bf16 maps: G on the tensor cores (bf16 text), fp32 copy for the SIMT overflow tiles
     const int rc = tile::run_gproj_tc(a->fmap, cells, a->d, a->text, a->k, kpadg, kpad, Gbf, G,
                                       reinterpret_cast<uint16_t*>(ws + L.textbf), st);
@@ -580,8 +603,11 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     const int kpadg = tile::kMaxKpadTC;  // S operand is always one 128-column chunk pair
     unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace) + g_bytes(a);
     const bool x3 = tile_x3(a);
-    const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg, a->d, x3);
+    const int tr = tile_rows(a);
+    const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg, a->d, x3, tr);
     tile::TileParams T{};
+    T.tr = tr;
+    T.sub1_rows = tr == tile::kGramTile ? 128 : tile::kSubRows;
     T.spts = reinterpret_cast<const float4*>(ws + L.spts);
     T.inv = reinterpret_cast<const int32_t*>(ws + L.inv);
     T.srec = reinterpret_cast<tile::SRec*>(ws + L.srec);
@@ -589,7 +615,7 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.depth = a->depth; T.fmap = x3 ? (const void*)(ws + L.fhi) : a->fmap;
     T.Gbf = reinterpret_cast<const uint16_t*>(ws + L.gbf);
     T.x3 = x3 ? 1 : 0;
-    T.kt_max = tile::ws_kt_max(x3);
+    T.kt_max = tr == tile::kGramTile ? tile::kGramKt : tile::ws_kt_max(x3);
     T.fmap_lo = x3 ? reinterpret_cast<const uint16_t*>(ws + L.flo) : nullptr;
     T.Gbf_lo = x3 ? reinterpret_cast<const uint16_t*>(ws + L.glo) : nullptr;
     T.kpadg = kpadg; T.k = a->k; T.p = a->p; T.density_col = a->density_col;
@@ -613,7 +639,14 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.sub_count = reinterpret_cast<int32_t*>(ws + L.sub);
     T.sub_tiles = T.sub_count + 1;
     T.max_sub_tiles = L.max_sub_tiles;
+    T.sub2_count = reinterpret_cast<int32_t*>(ws + L.sub2);
+    T.sub2_items = T.sub2_count + 1;
+    T.max_sub2 = L.max_sub2;
+    T.ibox = tr == tile::kGramTile ? reinterpret_cast<float4*>(ws + L.ibox) : nullptr;
+    T.work_count = tr == tile::kGramTile ? reinterpret_cast<int32_t*>(ws + L.work) : nullptr;
+    T.work = tr == tile::kGramTile ? reinterpret_cast<int4*>(ws + L.work) + 1 : nullptr;
     T.partials = a->partials;
+    T.tbound = reinterpret_cast<const float*>(ws + L.tbound);
     if (int rc = tile::run_tile_path(T, L, ws, a->points, a->n, st)) return rc;
     // sorted records -> caller's order; then the overflow points (tiles with more taps than fit in
     // shared memory) run through the SIMT kernel, which writes their outputs directly
@@ -651,28 +684,44 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
   return rc;
 }
 
-/* Diagnostic: tcgen05 FLOPs the last pf_fuse_query on this workspace issued in the tile kernel,
- * sum over work items (tiles + sub-tiles) of 2 * 128 * ktp * (D + 128) (ktp = taps padded to 16),
- * read back from the workspace (synchronises the stream). 0 when the SIMT path ran. */
+/* Diagnostic: tcgen05 FLOPs the last pf_fuse_query on this workspace issued in the tile kernel, read
+ * back from the workspace (synchronises the stream); 0 when the SIMT path ran. Per work item with
+ * ktp = taps padded to 16: k_tile_ws 2 * 128 * ktp * (D + 128) (x3: three products); the Gram
+ * kernel 2 * 128 * ktp * D (block 0) [+ 2 * 128 * (ktp - 128) * D (block 1)] + per 128-row block
+ * 2 * 128 * ktp * (128 + ktp). */
 int pf_tile_executed_flops(const pf_fuse_args_t* a, double* flops, void* stream) {
   *flops = 0.0;
   if (!a || !a->workspace || !tile_path_ok(a) || a->n == 0) return PF_OK;
   const int64_t cells = total_cells(a);
   const bool x3 = tile_x3(a);
-  const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, tile::kMaxKpadTC, a->d, x3);
+  const int tr = tile_rows(a);
+  const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, tile::kMaxKpadTC, a->d, x3, tr);
   const unsigned char* ws = reinterpret_cast<const unsigned char*>(a->workspace) + g_bytes(a);
-  int32_t nsub = 0;
+  int32_t cnt[2] = {0, 0};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaMemcpyAsync(&nsub, ws + L.sub, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&cnt[0], ws + L.sub, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  if (L.max_sub2 > 0) cudaMemcpyAsync(&cnt[1], ws + L.sub2, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("tile_executed_flops");
-  const int64_t items = L.ntiles + (int64_t)tile::kSubPerTile * std::min(nsub, L.max_sub_tiles);
+  const int64_t n1 = std::min(cnt[0], L.max_sub_tiles), n2 = std::min(cnt[1], L.max_sub2);
+  const int64_t items = L.ntiles + 4 * (int64_t)L.max_sub_tiles + 4 * n2;
   std::vector<int32_t> kt((size_t)items);
   cudaMemcpy(kt.data(), ws + L.kt, sizeof(int32_t) * items, cudaMemcpyDeviceToHost);
+  const bool gram = tr == tile::kGramTile;
+  const int ktmax = gram ? tile::kGramKt : tile::ws_kt_max(x3);
   double f = 0.0;
   for (int64_t t = 0; t < items; ++t) {
+    if (t >= L.ntiles + 4 * n1 && t < L.ntiles + 4 * (int64_t)L.max_sub_tiles) continue;  // unused slots
     const int ktp = (kt[t] + 15) & ~15;
-    if (kt[t] > 0 && ktp <= tile::ws_kt_max(x3))
+    if (!(kt[t] > 0 && ktp <= ktmax)) continue;
+    if (!gram) {
       f += (x3 ? 3.0 : 1.0) * 2.0 * 128.0 * ktp * (double)(a->d + tile::kMaxKpadTC);
+      continue;
+    }
+    const int rows = t < L.ntiles ? tr : (t < L.ntiles + 4 * (int64_t)L.max_sub_tiles ? 128 : 32);
+    int64_t nb = (rows + 127) / 128;
+    if (t == L.ntiles - 1) nb = std::min(nb, ((a->n - t * (int64_t)tr) + 127) / 128);  // the last tile ends early
+    f += 2.0 * 128.0 * ktp * a->d + (ktp > 128 ? 2.0 * 128.0 * (ktp - 128) * a->d : 0.0);
+    f += (double)nb * 2.0 * 128.0 * ktp * (double)(tile::kMaxKpadTC + ktp);
   }
   *flops = f;
   return check_launch("tile_executed_flops");

@@ -27,6 +27,30 @@ __global__ void k_text_bf16(const float* __restrict__ text, int k, int kpadg, in
   }
 }
 
+// softmax exponent bound of the tile epilogue: out[0] = max_k |t_k| (fp32, the rows exactly as the
+// caller passed them: QueryTables does not normalise, grounding.py:86-93 does it upstream). NaN rows
+// give NaN (the epilogue then takes the per-row max path and flags the NaN similarities).
+__global__ void k_text_bound(const float* __restrict__ text, int k, int d, float* __restrict__ out) {
+  __shared__ float wmax[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float m = 0.f;
+  for (int r = warp; r < k; r += blockDim.x >> 5) {
+    float ss = 0.f;
+    for (int c = lane; c < d; c += 32) ss = fmaf(text[(int64_t)r * d + c], text[(int64_t)r * d + c], ss);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float nr = sqrtf(ss);
+    m = (nr > m || nr != nr) ? nr : m;  // NaN sticks
+  }
+  if (lane == 0) wmax[warp] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float r = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = (wmax[w] > r || wmax[w] != wmax[w]) ? wmax[w] : r;
+    out[0] = r;
+  }
+}
+
 // text rows -> bf16 hi and lo (x - hi) parts, rows >= k zero (x3 mode)
 __global__ void k_text_split(const float* __restrict__ text, int k, int kpadg, int d, uint16_t* __restrict__ hi,
                              uint16_t* __restrict__ lo) {
@@ -164,6 +188,11 @@ __global__ void __launch_bounds__(128) k_gproj_tc(const uint16_t* __restrict__ f
 }
 
 }  // namespace
+
+int run_text_bound(const float* text, int k, int d, float* out, cudaStream_t st) {
+  k_text_bound<<<1, 1024, 0, st>>>(text, k, d, out);
+  return check_launch("text_bound");
+}
 
 int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int k, int kpadg, int kpad,
                  uint16_t* Gbf, float* G32, uint16_t* textbf, cudaStream_t st) {

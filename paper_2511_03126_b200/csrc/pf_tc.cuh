@@ -246,6 +246,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// back-off variant for roles that wait long and are not latency-critical: after a failed probe the
+// warp sleeps ~ns nanoseconds instead of re-issuing the probe (spinning warps take issue slots from
+// the busy roles of the same SM sub-partition)
+template <int NS>
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (true) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t"
+        "}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(NS);
+  }
+}
+
 // debug variant: gives up after ~2 s (a pipeline deadlock) with a message and a trap, so a hang
 // becomes a launch error instead of a stuck GPU; no suspend hint, so its wake-up latency (and the
 // PF_WS_TRACE timeline) matches the production wait

@@ -455,7 +455,9 @@ __device__ __forceinline__ void window_reduce(bool vis, const TapF& t, int* wx0,
   }
 }
 
-__global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
+// TR = rows per tile (128: k_tile_ws; kGramTile: the Gram kernel), one thread per point
+template <int TR>
+__global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParams P) {
   __shared__ ViewF sv[kMaxViewsTC];
   __shared__ ViewAff saff[kMaxViewsTC];
   __shared__ float4 sbound[kMaxViewsTC];
@@ -464,10 +466,10 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
   __shared__ unsigned char s_list[kMaxViewsTC];  // MIXED views, then EXACT views
   __shared__ uint32_t s_full[2], s_seen[2];
   __shared__ int s_nmixed, s_nexact;
-  __shared__ float sbb[kTile / 32][6];
+  __shared__ float sbb[TR / 32][6];
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t tile = blockIdx.x;
-  const int64_t jpt = tile * kTile + tid;
+  const int64_t jpt = tile * TR + tid;
   const bool valid = jpt < P.n;
   const float4 p = valid ? P.spts[jpt] : make_float4(0.f, 0.f, 0.f, 0.f);
   {
@@ -487,11 +489,27 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
   }
   if (tid < 2) s_seen[tid] = 0u;
   __syncthreads();
+  if (TR > kTile && P.ibox && tid < TR / kTile) {  // Gram path: box of each 128-row block
+    float bl[6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      bl[a] = sbb[4 * tid][a];
+#pragma unroll
+      for (int w = 1; w < 4; ++w) bl[a] = a < 3 ? fminf(bl[a], sbb[4 * tid + w][a]) : fmaxf(bl[a], sbb[4 * tid + w][a]);
+    }
+    P.ibox[2 * (tile * (TR / kTile) + tid)] = make_float4(bl[0], bl[1], bl[2], 0.f);
+    P.ibox[2 * (tile * (TR / kTile) + tid) + 1] = make_float4(bl[3], bl[4], bl[5], 0.f);
+  }
   float lo[3], hi[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    lo[a] = fminf(fminf(sbb[0][a], sbb[1][a]), fminf(sbb[2][a], sbb[3][a]));
-    hi[a] = fmaxf(fmaxf(sbb[0][a + 3], sbb[1][a + 3]), fmaxf(sbb[2][a + 3], sbb[3][a + 3]));
+    lo[a] = sbb[0][a];
+    hi[a] = sbb[0][a + 3];
+#pragma unroll
+    for (int w = 1; w < TR / 32; ++w) {
+      lo[a] = fminf(lo[a], sbb[w][a]);
+      hi[a] = fmaxf(hi[a], sbb[w][a + 3]);
+    }
   }
   const float eps_f = (float)P.eps;
   if (tid < P.nv) {
@@ -586,11 +604,18 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
     }
     window_reduce(vis, t, wx0, wy0, wx1, wy1, v, lane);
   }
-  if (valid) {
-    const int32_t code = voxel_code_fast(p, P.vox, P.grid);
+  const int32_t code = valid ? voxel_code_fast(p, P.vox, P.grid) : -1;
+  if (valid)
     *reinterpret_cast<uint4*>(P.srec + jpt) =
         make_uint4(w0, w1, (uint32_t)(__popc(w0) + __popc(w1)), (uint32_t)code);
-    if (P.vox_list) P.vox_list[jpt] = -1;  // the tile kernel writes the slots of the points it runs
+  if (P.vox_list) {
+    // touched-voxel list without returning atomics: slot jpt holds the code when this point is the
+    // lowest lane of its warp with that code (a warp's sorted points share a few voxels), else -1;
+    // pf_voxel_mass_sparse claims each voxel once (atomicExch on its count), so a voxel the SIMT
+    // overflow kernel lists again is harmless
+    const uint32_t peers = __match_any_sync(0xffffffffu, code);
+    const bool first = (peers & ((1u << lane) - 1u)) == 0u;
+    if (valid) P.vox_list[jpt] = first ? code : -1;
   }
   __syncthreads();
   if (tid < P.nv && s_cls[tid] == kViewMixed && ((s_seen[tid >> 5] >> (tid & 31)) & 1u)) {
@@ -639,10 +664,12 @@ __global__ void __launch_bounds__(kTile, 8) k_tile_prep(TileParams P) {
   }
 }
 
-// ---- overflow tiles -> sub-tiles ----------------------------------------------------------------------
-// A tile whose windows need more taps than one A buffer holds (it straddles a jump of the Hilbert
-// order: two distant surface patches) is re-run as four sub-tiles of 32 consecutive sorted points,
-// each with the exact union of its visible points' taps; the original tile is marked -1 (skipped).
+// ---- overflow tiles -> smaller work items -------------------------------------------------------------
+// A tile whose windows need more taps than one work item holds (it straddles a jump of the Hilbert
+// order, or is a sparse patch) is re-run as 4 level-1 items of sub1_rows consecutive sorted points
+// (k_tile_ws: 32 rows; Gram path: 128 rows), each with the exact union of its visible points' taps;
+// the Gram path splits overflowing level-1 items once more into 4 level-2 items of 32 rows. A split
+// parent is marked -1 (skipped); an item that still overflows goes to the SIMT kernel.
 __global__ void k_find_overflow(TileParams P, int64_t ntiles, int kt_max) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
     const int kt = P.tile_kt[t];
@@ -655,18 +682,49 @@ __global__ void k_find_overflow(TileParams P, int64_t ntiles, int kt_max) {
   }
 }
 
-// blocks stride over the overflow tiles, warp q = sub-tile q (rows 32q .. 32q + 31)
-__global__ void __launch_bounds__(kTile) k_subtile_prep(TileParams P, int64_t ntiles) {
+// level-1 items that overflow -> level-2 parents (Gram path)
+__global__ void k_find_overflow2(TileParams P, int64_t ntiles, int kt_max) {
+  const int64_t n1 = 4 * (int64_t)min(*P.sub_count, P.max_sub_tiles);
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n1; u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = ntiles + u;
+    const int kt = P.tile_kt[t];
+    if (((kt + 15) & ~15) <= kt_max) continue;
+    const int b = atomicAdd(P.sub2_count, 1);
+    if (b < P.max_sub2) {
+      P.sub2_items[b] = (int32_t)t;
+      P.tile_kt[t] = -1;
+    }
+  }
+}
+
+// first sorted row of a level-1 item
+__device__ __forceinline__ int64_t level1_row0(const TileParams& P, int64_t ntiles, int64_t item) {
+  const int64_t u = item - ntiles;
+  return (int64_t)P.sub_tiles[u >> 2] * P.tr + (u & 3) * P.sub1_rows;
+}
+
+// Children of R rows (4 per parent) with exact windows. R = 32: a block is one parent, warp q its
+// child q; R = 128: a block is one child. level 1: parents are tiles; level 2: level-1 items.
+template <int R>
+__global__ void __launch_bounds__(128) k_item_prep(TileParams P, int64_t ntiles, int level) {
+  constexpr int kChildren = 128 / R;  // children per block
   __shared__ ViewF sv[kMaxViewsTC];
-  const int nsub = min(*P.sub_count, P.max_sub_tiles);
-  if ((int)blockIdx.x >= nsub) return;
-  for (int j = threadIdx.x; j < P.nv; j += kTile) sv[j] = P.viewf[j];
+  __shared__ int sx0[kMaxViewsTC], sy0[kMaxViewsTC], sx1[kMaxViewsTC], sy1[kMaxViewsTC];
+  __shared__ float sbox[4][6];
+  const int nparents = level == 1 ? min(*P.sub_count, P.max_sub_tiles) : min(*P.sub2_count, P.max_sub2);
+  const int64_t first = level == 1 ? ntiles : ntiles + 4 * (int64_t)P.max_sub_tiles;
+  const int nblocks = nparents * (4 / kChildren);
+  if ((int)blockIdx.x >= nblocks) return;
+  for (int j = threadIdx.x; j < P.nv; j += 128) sv[j] = P.viewf[j];
   __syncthreads();
-  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int b = blockIdx.x; b < nsub; b += gridDim.x) {
-    const int64_t tile = P.sub_tiles[b];
-    const int64_t item = ntiles + 4 * (int64_t)b + q;
-    const int64_t jpt = tile * kTile + kSubRows * q + lane;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+    const int b = blk / (4 / kChildren);
+    const int c = R == 32 ? warp : blk % 4;          // child of parent b
+    const int r = R == 32 ? lane : (int)threadIdx.x;  // row within the child
+    const int64_t item = first + 4 * (int64_t)b + c;
+    const int64_t prow = level == 1 ? (int64_t)P.sub_tiles[b] * P.tr : level1_row0(P, ntiles, P.sub2_items[b]);
+    const int64_t jpt = prow + (int64_t)c * R + r;
     const bool valid = jpt < P.n;
     float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
     uint2 mw = make_uint2(0u, 0u);
@@ -675,8 +733,43 @@ __global__ void __launch_bounds__(kTile) k_subtile_prep(TileParams P, int64_t nt
       mw = *reinterpret_cast<const uint2*>(P.srec + jpt);
     }
     uint2* desc = P.tile_desc + item * P.nv;
+    if (P.ibox) {  // Gram path: the child's box (one 128-row block)
+      float b6[6] = {valid ? p.x : INFINITY, valid ? p.y : INFINITY, valid ? p.z : INFINITY,
+                     valid ? p.x : -INFINITY, valid ? p.y : -INFINITY, valid ? p.z : -INFINITY};
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          b6[a] = fminf(b6[a], __shfl_xor_sync(0xffffffffu, b6[a], o));
+          b6[a + 3] = fmaxf(b6[a + 3], __shfl_xor_sync(0xffffffffu, b6[a + 3], o));
+        }
+      if (R > 32) {
+        if (lane == 0)
+#pragma unroll
+          for (int a = 0; a < 6; ++a) sbox[warp][a] = b6[a];
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+          b6[a] = a < 3 ? fminf(fminf(sbox[0][a], sbox[1][a]), fminf(sbox[2][a], sbox[3][a]))
+                        : fmaxf(fmaxf(sbox[0][a], sbox[1][a]), fmaxf(sbox[2][a], sbox[3][a]));
+      }
+      if (r == 0) {
+        const int64_t bi = 4 * ntiles + (item - ntiles);
+        P.ibox[2 * bi] = make_float4(b6[0], b6[1], b6[2], 0.f);
+        P.ibox[2 * bi + 1] = make_float4(b6[3], b6[4], b6[5], 0.f);
+      }
+    }
+    if (R > 32) {
+      for (int v = threadIdx.x; v < P.nv; v += 128) {
+        sx0[v] = INT_MAX;
+        sy0[v] = INT_MAX;
+        sx1[v] = -1;
+        sy1[v] = -1;
+      }
+      __syncthreads();
+    }
     int running = 0;
-    for (int v = 0; v < P.nv; ++v) {  // views in order: exclusive prefix of (even-padded) window sizes
+    for (int v = 0; v < P.nv; ++v) {
       const bool vis = (((v < 32 ? mw.x : mw.y) >> (v & 31)) & 1u) != 0u;
       int x0 = INT_MAX, y0 = INT_MAX, x1 = -1, y1 = -1;
       if (__any_sync(0xffffffffu, vis)) {
@@ -692,14 +785,37 @@ __global__ void __launch_bounds__(kTile) k_subtile_prep(TileParams P, int64_t nt
         y0 = __reduce_min_sync(0xffffffffu, y0);
         x1 = __reduce_max_sync(0xffffffffu, x1);
         y1 = __reduce_max_sync(0xffffffffu, y1);
+        if (R > 32 && lane == 0) {
+          atomicMin(sx0 + v, x0);
+          atomicMin(sy0 + v, y0);
+          atomicMax(sx1 + v, x1);
+          atomicMax(sy1 + v, y1);
+        }
       }
-      const int w = x1 >= 0 ? x1 - x0 + 1 : 0, h = x1 >= 0 ? y1 - y0 + 1 : 0;
-      if (lane == 0)
-        desc[v] = make_uint2((uint32_t)min(running, 65535) | ((uint32_t)(w ? x0 : 0) << 16) | ((uint32_t)(h ? y0 : 0) << 24),
-                             (uint32_t)w | ((uint32_t)h << 8));
-      running += (w * h + 1) & ~1;
+      if (R == 32) {  // views in order: exclusive prefix of (even-padded) window sizes
+        const int w = x1 >= 0 ? x1 - x0 + 1 : 0, h = x1 >= 0 ? y1 - y0 + 1 : 0;
+        if (lane == 0)
+          desc[v] = make_uint2((uint32_t)min(running, 65535) | ((uint32_t)(w ? x0 : 0) << 16) | ((uint32_t)(h ? y0 : 0) << 24),
+                               (uint32_t)w | ((uint32_t)h << 8));
+        running += (w * h + 1) & ~1;
+      }
     }
-    if (lane == 0) P.tile_kt[item] = running;
+    if (R > 32) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int v = 0; v < P.nv; ++v) {
+          const int x0 = sx0[v], y0 = sy0[v], x1 = sx1[v], y1 = sy1[v];
+          const int w = x1 >= 0 ? x1 - x0 + 1 : 0, h = x1 >= 0 ? y1 - y0 + 1 : 0;
+          desc[v] = make_uint2((uint32_t)min(running, 65535) | ((uint32_t)(w ? x0 : 0) << 16) | ((uint32_t)(h ? y0 : 0) << 24),
+                               (uint32_t)w | ((uint32_t)h << 8));
+          running += (w * h + 1) & ~1;
+        }
+        P.tile_kt[item] = running;
+      }
+      __syncthreads();
+    } else if (lane == 0) {
+      P.tile_kt[item] = running;
+    }
   }
 }
 
@@ -749,39 +865,48 @@ namespace tile {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d, bool x3) {
+TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d, bool x3, int tr) {
   TileLayout L{};
-  const int64_t ntiles = (n + kTile - 1) / kTile;
+  const int64_t ntiles = (n + tr - 1) / tr;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
     off += align256(bytes);
     return o;
   };
-  L.ntiles = ntiles;
-  L.keys = take(sizeof(uint32_t) * (size_t)n);
-  L.hist = take(sizeof(uint32_t) * (size_t)(1 << (3 * sort_bits_for(n))));
-  L.totals = take(sizeof(uint32_t) * 4096);
-  L.inv = take(sizeof(int32_t) * (size_t)n);
-  L.spts = take(sizeof(float4) * (size_t)ntiles * kTile);
-  L.srec = take(sizeof(SRec) * (size_t)ntiles * kTile);
-  L.max_sub_tiles = (int32_t)ntiles;  // every tile may be split (sparse clouds overflow often)
-  const int64_t items = ntiles + 4 * (int64_t)L.max_sub_tiles;
-  L.desc = take(sizeof(uint2) * (size_t)items * nv);
-  L.kt = take(sizeof(int32_t) * (size_t)items);
-  L.sub = take(sizeof(int32_t) * ((size_t)L.max_sub_tiles + 1));
-  L.viewf = take(sizeof(ViewF) * kMaxViewsTC);
-  L.vbound = take(sizeof(float4) * kMaxViewsTC);
-  L.vox = take(sizeof(double) * 8);
-  L.ovf = take(sizeof(int32_t) * (size_t)(n + 1));
+  // per-object tables first: their offsets do not depend on the point count or the tile size, so
+  // pf_fuse_prepare's tables stay valid for either kernel (tile sizes 128 / 512)
   L.gbf = take(sizeof(uint16_t) * (size_t)cells * kpadg);
   L.textbf = take(sizeof(uint16_t) * (size_t)kpadg * 1024);  // text rows in bf16 (D <= 1024)
+  L.tbound = take(sizeof(float) * 4);
   if (x3) {  // lo part of G, hi and lo parts of the f32 maps
     L.glo = take(sizeof(uint16_t) * (size_t)cells * kpadg);
     L.fhi = take(sizeof(uint16_t) * (size_t)cells * d);
     L.flo = take(sizeof(uint16_t) * (size_t)cells * d);
     L.textlo = take(sizeof(uint16_t) * (size_t)kpadg * 1024);
   }
+  L.viewf = take(sizeof(ViewF) * kMaxViewsTC);
+  L.vbound = take(sizeof(float4) * kMaxViewsTC);
+  L.vox = take(sizeof(double) * 8);
+  L.ntiles = ntiles;
+  L.keys = take(sizeof(uint32_t) * (size_t)n);
+  L.hist = take(sizeof(uint32_t) * (size_t)(1 << (3 * sort_bits_for(n))));
+  L.totals = take(sizeof(uint32_t) * 4096);
+  L.inv = take(sizeof(int32_t) * (size_t)n);
+  L.spts = take(sizeof(float4) * (size_t)ntiles * tr);
+  L.srec = take(sizeof(SRec) * (size_t)ntiles * tr);
+  L.max_sub_tiles = (int32_t)ntiles;  // every tile may be split (sparse clouds overflow often)
+  // Gram path: up to ntiles level-1 items may split again (each into 4 level-2 items)
+  L.max_sub2 = tr == kTile ? 0 : (int32_t)(4 * ntiles);  // sparse clouds: most level-1 items may split
+  const int64_t items = ntiles + 4 * (int64_t)L.max_sub_tiles + 4 * (int64_t)L.max_sub2;
+  L.desc = take(sizeof(uint2) * (size_t)items * nv);
+  L.kt = take(sizeof(int32_t) * (size_t)items);
+  L.sub = take(sizeof(int32_t) * ((size_t)L.max_sub_tiles + 1));
+  L.sub2 = take(sizeof(int32_t) * ((size_t)L.max_sub2 + 1));
+  L.ibox = tr == kTile ? 0 : take(2 * sizeof(float4) * (size_t)(4 * ntiles + 4 * (int64_t)L.max_sub_tiles +
+                                                                 4 * (int64_t)L.max_sub2));
+  L.ovf = take(sizeof(int32_t) * (size_t)(n + 1));
+  L.work = tr == kTile ? 0 : take(sizeof(int4) * (size_t)(items + 1));  // [count | pad] then entries
   L.bytes = off;
   return L;
 }
@@ -883,14 +1008,24 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   }
   k_view_setup<<<1, kMaxViewsTC, 0, st>>>(Q);
   if (int rc = check_launch("view_setup")) return rc;
-  k_tile_prep<<<(unsigned)L.ntiles, kTile, 0, st>>>(Q);
+  if (P.tr == kGramTile) k_tile_prep<kGramTile><<<(unsigned)L.ntiles, kGramTile, 0, st>>>(Q);
+  else k_tile_prep<kTile><<<(unsigned)L.ntiles, kTile, 0, st>>>(Q);
   if (int rc = check_launch("tile_prep")) return rc;
-  // overflow tiles -> sub-tile work items (appended after the tiles)
+  // overflow tiles -> smaller work items (appended after the tiles)
   cudaMemsetAsync(P.sub_count, 0, sizeof(int32_t), st);
   k_find_overflow<<<grid_for(L.ntiles, 256), 256, 0, st>>>(P, L.ntiles, P.kt_max);
   if (int rc = check_launch("find_overflow")) return rc;
-  k_subtile_prep<<<(unsigned)(L.max_sub_tiles < 148 * 16 ? L.max_sub_tiles : 148 * 16), kTile, 0, st>>>(P, L.ntiles);
-  if (int rc = check_launch("subtile_prep")) return rc;
+  const unsigned pgrid = (unsigned)(L.max_sub_tiles < 148 * 16 ? L.max_sub_tiles : 148 * 16);
+  if (P.sub1_rows == 32) k_item_prep<32><<<pgrid, 128, 0, st>>>(P, L.ntiles, 1);
+  else k_item_prep<128><<<4 * pgrid, 128, 0, st>>>(P, L.ntiles, 1);
+  if (int rc = check_launch("item_prep")) return rc;
+  if (P.max_sub2 > 0) {
+    cudaMemsetAsync(P.sub2_count, 0, sizeof(int32_t), st);
+    k_find_overflow2<<<grid_for(4 * (int64_t)L.max_sub_tiles, 256), 256, 0, st>>>(P, L.ntiles, P.kt_max);
+    if (int rc = check_launch("find_overflow2")) return rc;
+    k_item_prep<32><<<(unsigned)(L.max_sub2 < 148 * 16 ? L.max_sub2 : 148 * 16), 128, 0, st>>>(P, L.ntiles, 2);
+    if (int rc = check_launch("item_prep2")) return rc;
+  }
   stage_mark(2, st);
   if (debug) {
     unsigned long long h[11];
@@ -948,7 +1083,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
     fprintf(stderr, "[prep debug] MIXED samples ambiguous under the affine model: %.2f%%, mean eu %.4f px\n",
             100.0 * h[8] / (double)(h[7] ? h[7] : 1), 1e-6 * h[9] / (double)(h[10] ? h[10] : 1));
   }
-  const int rc = run_tile_ws(P, st);
+  const int rc = P.tr == kGramTile ? run_tile_gram(P, st) : run_tile_ws(P, st);
   stage_mark(3, st);
   return rc;
 }

@@ -94,19 +94,36 @@ struct TileParams {
   int32_t* sub_tiles;
   int32_t* sub_count;
   int32_t max_sub_tiles;
+  // Gram path (pf_gram.cu): level-0 tiles of `tr` rows (512); overflow tiles split into 4 level-1
+  // items of `sub1_rows` (128) rows, overflowing level-1 items into 4 level-2 items of 32 rows:
+  // work items ntiles + 4 max_sub_tiles + 4 c + q (c < min(*sub2_count, max_sub2)) cover rows 32q..
+  // of level-1 item sub2_items[c]. The tcgen05 tile kernel k_tile_ws uses tr = 128, sub1_rows = 32.
+  int32_t tr, sub1_rows;
+  int32_t* sub2_items;
+  int32_t* sub2_count;
+  int32_t max_sub2;
   unsigned long long* dbg;  // optional counters (PF_WS_DEBUG)
+  int32_t ablate;           // Gram kernel timing experiments only (PF_GRAM_ABLATE bits; results invalid)
   uint32_t* trace;          // optional per-tile role timestamps (PF_WS_DEBUG + PF_WS_TRACE=<file>)
   double* partials;
+  // Gram path: bounding box (lo.xyz, hi.xyz as two float4) of every 128-row block of a work item,
+  // written by the prep kernels: level-0 tile t block b at 4 t + b, split item i at 4 ntiles + i - ntiles
+  float4* ibox;
+  // Gram path: compact list of the work items that run in the tile kernel ({item, first row,
+  // rows | taps << 16, 0}, k_collect_work) and its length
+  int4* work;
+  int32_t* work_count;
+  const float* tbound;  // max_k |t_k| (run_text_bound, per object): bounds the softmax exponents
 };
 
 struct TileLayout {
   int64_t ntiles;
-  int32_t max_sub_tiles;
-  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, gbf, textbf, viewf, vbound, vox, glo, fhi, flo, textlo,
+  int32_t max_sub_tiles, max_sub2;
+  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, sub2, ibox, work, gbf, textbf, viewf, vbound, vox, tbound, glo, fhi, flo, textlo,
       bytes;
 };
 
-TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d = 0, bool x3 = false);
+TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d = 0, bool x3 = false, int tr = 128);
 // x3 operands of f32 maps: hi = bf16(x), lo = bf16(x - hi), for the maps and the G table
 int run_split_f32(const float* src, int64_t rows, int cols, int src_ld, int dst_ld, uint16_t* hi, uint16_t* lo,
                   cudaStream_t st);
@@ -114,10 +131,15 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
                   int64_t n, cudaStream_t st);
 int run_unsort(const TileParams& P, cudaStream_t st);
 int run_tile_ws(const TileParams& P, cudaStream_t st);
+// Gram formulation (pf_gram.cu): bf16 maps, no mean-feature output
+int run_tile_gram(const TileParams& P, cudaStream_t st);
+constexpr int kGramTile = 512;   // rows of a level-0 tile of the Gram path
+constexpr int kGramKt = 192;     // taps per work item held by the Gram kernel
 int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf, cudaStream_t st);
 int run_gproj_tc(const void* fmap, int64_t cells, int d, const float* text, int k, int kpadg, int kpad,
                  uint16_t* Gbf, float* G32, uint16_t* textbf, cudaStream_t st);
 int ws_kt_max(bool x3 = false);
+int run_text_bound(const float* text, int k, int d, float* out, cudaStream_t st);
 int run_gproj_tc_x3(const uint16_t* fhi, const uint16_t* flo, int64_t cells, int d, const float* text, int k,
                     int kpadg, int kpad, uint16_t* Gbf, uint16_t* Gbf_lo, float* G32, uint16_t* text_hi,
                     uint16_t* text_lo, cudaStream_t st);

@@ -203,7 +203,7 @@ __device__ __forceinline__ float ex2(float x) {
 // PROF: wait accounting + trace (PF_WS_DEBUG); OUTS: validation outputs (features, similarities,
 // softmax weights) -- a separate instantiation keeps their fully unrolled stores out of the hot code
 template <bool PROF, bool OUTS, bool X3>
-__global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant__ TileParams P, int need_max) {
+__global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant__ TileParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -259,12 +259,20 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     for (int pp = 0; pp < 4; ++pp) y[pp] = (pp < P.p && j < P.k) ? P.values[j * P.p + pp] : 0.f;
     S.yv2[j] = make_float2(y[2], y[3]);
   }
+  // softmax shift. The reference subtracts each row's max (grounding.py:175-177); |s_k| <= |t_k| bounds
+  // every exponent s_k / T by c = max_k |t_k| / T (in log2 units here), so subtracting the constant c
+  // instead keeps the exponents in [-2c, 0]: no overflow, and the row's largest term cannot underflow
+  // while 2c <= 120. Beyond that (tiny T or long text rows) the row max is subtracted per point.
+  // The 1.05 margin covers the bf16 rounding of the text / G operands.
+  const float cbound = 1.05f * __ldg(P.tbound) * P.inv_temp * 1.4426950408889634f;
+  const int need_max = (2.f * cbound <= 120.f) ? 0 : 1;  // NaN / inf bound: per-row max
+  const float shift = need_max ? 0.f : -cbound;
   for (int j = tid; j < kMaxKpadTC / 2; j += kWsThreads) {
     auto val = [&](int kk, int pp) { return (kk < P.k && pp < P.p) ? P.values[kk * P.p + pp] : 0.f; };
     const int a = 2 * j, b = 2 * j + 1;
     S.yp[2 * j] = make_float4(val(a, 0), val(b, 0), val(a, 1), val(b, 1));
     S.yp[2 * j + 1] = make_float4(a < P.k ? P.mid_theta[a] : 0.f, b < P.k ? P.mid_theta[b] : 0.f,
-                                  a < P.k ? 0.f : -INFINITY, b < P.k ? 0.f : -INFINITY);
+                                  a < P.k ? shift : -INFINITY, b < P.k ? shift : -INFINITY);
   }
   for (int j = tid; j < kMaxKpadTC + 8; j += kWsThreads) S.red[j] = 0.0;
   if (tid == 0) {
@@ -872,9 +880,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         for (int q = 0; q < kHalfK; ++q)
           if (k0 + q < P.k) P.sims[(int64_t)i * P.k + k0 + q] = featured ? v[q] * inv : 0.f;
       }
-      // |s| <= 1 (cosines), so exp(s / T) cannot overflow for T >= ~0.013 and the row max of the
-      // reference's stable softmax (grounding.py:175-177) only changes rounding; below that the
-      // max is subtracted as in the reference (host sets need_max).
+      // exponents are shifted by the constant -c of the setup (yp .z/.w), or by the row max when
+      // need_max (grounding.py:175-177); both leave the softmax unchanged up to rounding
       float m2 = 0.f;
       if (need_max) {
         float mx = -INFINITY;
@@ -939,7 +946,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
       if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 46);
       const float se_t = S.xsum[0][0][row] + S.xsum[1][0][row];
-      if (featured && isnan(se_t)) atomicOr(P.status, 1);  // NaN similarity (grounding.py:173-174)
+      // NaN similarity (grounding.py:173-174) -> MaterialError; a non-finite sum otherwise (inf
+      // inputs) is flagged too rather than returning NaN properties silently
+      if (featured && !(se_t <= 3.4e38f)) atomicOr(P.status, isnan(se_t) ? 1 : 2);
       const float rs = featured ? 1.f / se_t : 0.f;
       if (warp == kAccWarp0 && lane == 0) WS_TRACE(a_tile - 1, 47);
       // pass 2: normalised weights of this half -> the warp's weight totals (materials >= K have
@@ -1049,8 +1058,6 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
   const int64_t ntiles = (P.n + kTile - 1) / kTile;  // (+ sub-tiles, known on the device only)
   int grid = (int)(ntiles < sms ? ntiles : sms);
   if (const char* g = getenv("PF_WS_GRID")) grid = (int)(ntiles < atoi(g) ? ntiles : atoi(g));  // debug knob
-  // exp(s / T) with |s| <= 1 (+ bf16 rounding of G) stays below 2^120 unless T < ~0.012
-  const int need_max = (double)P.inv_temp * 1.4426950408889634 * 1.05 > 120.0 ? 1 : 0;
   static unsigned long long* dbg = nullptr;
   TileParams Q = P;
   const bool debug = getenv("PF_WS_DEBUG") != nullptr;
@@ -1068,15 +1075,15 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
   }
   const bool outs = P.sims || P.weights || P.features;
   if (P.x3) {  // f32 maps: the hi / lo split instantiation (the bf16 code is untouched by it)
-    if (debug && outs) k_tile_ws<true, true, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
-    else if (debug) k_tile_ws<true, false, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
-    else if (outs) k_tile_ws<false, true, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
-    else k_tile_ws<false, false, true><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+    if (debug && outs) k_tile_ws<true, true, true><<<grid, kWsThreads, smem, st>>>(Q);
+    else if (debug) k_tile_ws<true, false, true><<<grid, kWsThreads, smem, st>>>(Q);
+    else if (outs) k_tile_ws<false, true, true><<<grid, kWsThreads, smem, st>>>(Q);
+    else k_tile_ws<false, false, true><<<grid, kWsThreads, smem, st>>>(Q);
   } else {
-    if (debug && outs) k_tile_ws<true, true, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
-    else if (debug) k_tile_ws<true, false, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
-    else if (outs) k_tile_ws<false, true, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
-    else k_tile_ws<false, false, false><<<grid, kWsThreads, smem, st>>>(Q, need_max);
+    if (debug && outs) k_tile_ws<true, true, false><<<grid, kWsThreads, smem, st>>>(Q);
+    else if (debug) k_tile_ws<true, false, false><<<grid, kWsThreads, smem, st>>>(Q);
+    else if (outs) k_tile_ws<false, true, false><<<grid, kWsThreads, smem, st>>>(Q);
+    else k_tile_ws<false, false, false><<<grid, kWsThreads, smem, st>>>(Q);
   }
   const int rc = check_launch("tile_ws");
   if (debug && rc == PF_OK) {

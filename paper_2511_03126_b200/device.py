@@ -97,8 +97,10 @@ class ViewSet:
         return self.records[j : j + 1]
 
     @classmethod
-    def from_views(cls, views, device=None, fmap_kind: str | None = None) -> "ViewSet":
-        """Pack reference-style view records (bundle.py:93-139 attribute names)."""
+    def from_views(cls, views, device=None, fmap_kind: str | None = None, with_fmap: bool = True) -> "ViewSet":
+        """Pack reference-style view records (bundle.py:93-139 attribute names). with_fmap=False
+        uploads records + depth only (the records still carry the maps' offsets and sizes, read from
+        their shapes); `attach_fmaps` adds the maps later."""
         dev = require_cuda(device)
         t = torch()
         views = list(views)
@@ -128,14 +130,26 @@ class ViewSet:
             rec[j]["depth_offset"], rec[j]["fmap_offset"] = doff, foff
             rec[j]["H"], rec[j]["W"], rec[j]["Hf"], rec[j]["Wf"] = h, w, hf, wf
             depth_parts.append(t.from_numpy(np.ascontiguousarray(dm)).reshape(-1))
-            vk = getattr(v, "feature_dtype", None) or feature_dtype_of(v.feature_map)
-            fm = fmap_to_dev(v.feature_map, vk if vk in ("f32", "bf16") else "f32", dev)
-            fmap_parts.append(fm.to(t.bfloat16 if kind == "bf16" else t.float32).reshape(-1))
             doff += h * w
             foff += hf * wf * d
         depth = t.cat(depth_parts).to(dev)
-        fmap = t.cat(fmap_parts).contiguous()
-        return cls(rec, depth, fmap, kind, d, dev)
+        vs = cls(rec, depth, None, kind, d, dev)
+        if with_fmap:
+            vs.attach_fmaps(views)
+        return vs
+
+    def attach_fmaps(self, views) -> "ViewSet":
+        """Upload the views' feature maps into the packed channel-last block (no-op if present)."""
+        if self.fmap is not None:
+            return self
+        t = torch()
+        parts = []
+        for v in views:
+            vk = getattr(v, "feature_dtype", None) or feature_dtype_of(v.feature_map)
+            fm = fmap_to_dev(v.feature_map, vk if vk in ("f32", "bf16") else "f32", self.device)
+            parts.append(fm.to(t.bfloat16 if self.fmap_kind == "bf16" else t.float32).reshape(-1))
+        self.fmap = t.cat(parts).contiguous()
+        return self
 
     @classmethod
     def from_tensors(cls, R, tvec, intr, depth, fmap, device=None) -> "ViewSet":
@@ -164,3 +178,49 @@ class ViewSet:
             d,
             dev,
         )
+
+
+# ---- per-object view cache of the drop-in op API ------------------------------------------------
+# The reference's pipeline calls visibility_mask and then aggregate_geometric_features on the same
+# view list (pipeline.py:225-232). Both take reference-style views, so without a cache each call
+# re-packs and re-uploads every depth map and feature map. The cache keys on the identity of the
+# view objects and of their depth / feature arrays and keeps strong references to them (an id cannot
+# be recycled while its entry lives), so rebinding `view.depth` or `view.feature_map` is a miss.
+# In-place writes into a cached array are NOT detected: call clear_view_cache() after mutating one.
+_VIEW_CACHE: "dict" = {}
+_VIEW_CACHE_ORDER: list = []
+VIEW_CACHE_SIZE = 2  # objects (a C5 object's views are 243 MB of HBM)
+
+
+def _view_key(views, device) -> tuple:
+    return (str(device),) + tuple((id(v), id(v.depth), id(v.feature_map)) for v in views)
+
+
+def clear_view_cache() -> None:
+    _VIEW_CACHE.clear()
+    _VIEW_CACHE_ORDER.clear()
+
+
+def cached_view_set(views, with_fmap: bool = True, device=None) -> ViewSet:
+    """ViewSet of a reference-style view list, packed and uploaded once per list (see above);
+    visibility-only callers ask for with_fmap=False and never upload the feature maps."""
+    if isinstance(views, ViewSet):
+        return views
+    dev = require_cuda(device)
+    views = list(views)
+    key = _view_key(views, dev)
+    hit = _VIEW_CACHE.get(key)
+    if hit is None:
+        vs = ViewSet.from_views(views, dev, with_fmap=with_fmap)
+        # strong refs: the views and their arrays outlive the entry, so the ids stay theirs
+        _VIEW_CACHE[key] = (vs, views, [(v.depth, v.feature_map) for v in views])
+        _VIEW_CACHE_ORDER.append(key)
+        while len(_VIEW_CACHE_ORDER) > VIEW_CACHE_SIZE:
+            _VIEW_CACHE.pop(_VIEW_CACHE_ORDER.pop(0), None)
+    else:
+        vs = hit[0]
+        _VIEW_CACHE_ORDER.remove(key)
+        _VIEW_CACHE_ORDER.append(key)
+    if with_fmap:
+        vs.attach_fmaps(views)
+    return vs

@@ -191,8 +191,11 @@ class FusedResult:
         return self
 
     def check(self):
-        if int(self.buffers.status.item()) & 1:
+        st = int(self.buffers.status.item())
+        if st & 1:
             raise MaterialError("NaN similarity passed to kernel regression")
+        if st & 2:
+            raise MaterialError("non-finite softmax sum (infinite feature or text values)")
         return self
 
     def mass_kg(self) -> float:
@@ -215,12 +218,14 @@ def fuse_and_query(points, views: ViewSet, tables: QueryTables, *, temperature: 
                    write_features: bool = False, write_sims: bool = False,
                    write_weights: bool = False, reduce: bool = True, check: bool = False,
                    force_simt: bool = False, prepared: bool = False,
-                   reset: bool = True) -> FusedResult:
+                   reset: bool = True, feature_kernel: bool = False) -> FusedResult:
     """Run the whole path on `points` (N,3) f32 device tensor (numpy is uploaded).
 
     lo_hi: voxel domain (6,) f64 device tensor; None = this call's bbox (pf_bbox). Multi-GPU
     callers pass the all-reduced global bbox so every rank indexes the same grid.
     reduce=False skips the voxel-mass finalisation (call allreduce() then finalize()).
+    bf16 maps run the Gram-formulation tile kernel; write_features (a validation output only the
+    feature-product kernel produces) or feature_kernel=True select k_tile_ws instead.
     """
     if temperature <= 0:
         raise ValueError(f"temperature must be positive, got {temperature}")
@@ -256,9 +261,14 @@ def fuse_and_query(points, views: ViewSet, tables: QueryTables, *, temperature: 
         flags |= _lib.PF_FUSE_FORCE_SIMT
     if prepared:
         flags |= _lib.PF_FUSE_PREPARED
+    if feature_kernel:
+        flags |= _lib.PF_FUSE_FEATURE_KERNEL
     args = _make_args(pts, n, views, tables, temperature, epsilon, grid, buffers, flags)
     _lib.call("pf_fuse_query", args, st)
     res = FusedResult(buffers, views.nviews, tables.k)
+    # the grid now holds this call's voxels until finalize() re-zeroes the touched ones (sparse) or
+    # marks it for a full reset (dense): an un-finalised grid must be zeroed by the next reset()
+    buffers.grid_clean = False
     if reduce:
         res.finalize()
     if check:

@@ -11,7 +11,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .device import ViewSet, is_torch, ptr, require_cuda, stream_handle, to_dev, torch
+from .device import cached_view_set, is_torch, ptr, require_cuda, stream_handle, to_dev, torch
 from .errors import BundleStructureError
 from .types import SemanticPointCloud
 
@@ -20,7 +20,7 @@ def aggregate_geometric_features(positions, views, visibility) -> SemanticPointC
     dev = require_cuda()
     t = torch()
     tor = is_torch(positions)
-    vs = views if isinstance(views, ViewSet) else ViewSet.from_views(views)
+    vs = cached_view_set(views)  # uploaded once per view list (device.cached_view_set)
     if tor and positions.dtype == t.float32:
         p, pdt = positions.to(dev).contiguous(), _lib.PF_F32
     else:

@@ -10,13 +10,13 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .device import ViewSet, is_torch, ptr, require_cuda, stream_handle, to_dev, torch
+from .device import ViewSet, cached_view_set, is_torch, ptr, require_cuda, stream_handle, to_dev, torch
 
 DEFAULT_EPSILON_FRACTION = 0.01  # geometry.py:12
 
 
-def _views_of(views) -> ViewSet:
-    return views if isinstance(views, ViewSet) else ViewSet.from_views(views)
+def _views_of(views, with_fmap: bool = True) -> ViewSet:
+    return cached_view_set(views, with_fmap=with_fmap)
 
 
 def project_points(points, camera, intrinsics):
@@ -53,7 +53,7 @@ def visibility_mask(points, views, epsilon: float):
     dev = require_cuda()
     t = torch()
     tor = is_torch(points)
-    vs = _views_of(views)
+    vs = _views_of(views, with_fmap=False)  # the depth test never reads the feature maps
     if tor and points.dtype == t.float32:
         p, pdt = points.to(dev).contiguous(), _lib.PF_F32
     else:

@@ -8,7 +8,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .device import ViewSet, ptr, require_cuda, stream_handle, to_dev, torch
+from .device import ViewSet, cached_view_set, ptr, require_cuda, stream_handle, to_dev, torch
 
 
 @dataclass
@@ -29,7 +29,7 @@ def _run(source, views, visibility, k):
         raise ValueError("source set has no normals; run normal estimation first")
     dev = require_cuda()
     t = torch()
-    vs = views if isinstance(views, ViewSet) else ViewSet.from_views(views)
+    vs = cached_view_set(views, with_fmap=False)  # cameras only
     pos = to_dev(source.positions, t.float64, dev).reshape(-1, 3)
     nrm = to_dev(source.normals, t.float64, dev).reshape(-1, 3)
     s, nv = pos.shape[0], vs.nviews

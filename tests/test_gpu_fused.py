@@ -24,7 +24,9 @@ def tol_for(wl, force_simt=False):
     return TOL_BF16 if (wl.cfg.bf16 and wl.cfg.d % 128 == 0 and not force_simt) else TOL
 
 
-def run_gpu(wl, points=None, **kw):
+def run_gpu(wl, points=None, features=True, **kw):
+    """features=True also writes the mean features, which bf16 maps compute with the feature-product
+    tile kernel (k_tile_ws); features=False runs the production Gram kernel (pf_gram.cu)."""
     import torch
 
     views = pf.ViewSet.from_views(wl.views())
@@ -32,7 +34,7 @@ def run_gpu(wl, points=None, **kw):
     pts = wl.points if points is None else points
     res = pf.fuse_and_query(torch.from_numpy(np.ascontiguousarray(pts)).cuda(), views, tables,
                             temperature=wl.cfg.temperature, epsilon=wl.cfg.eps, grid=wl.cfg.grid,
-                            write_features=True, write_sims=True, write_weights=True, check=True, **kw)
+                            write_features=features, write_sims=True, write_weights=True, check=True, **kw)
     torch.cuda.synchronize()
     return res
 
@@ -68,14 +70,14 @@ def assert_parity(res, ref, wl, pts=None, tol=TOL):
     else:
         assert np.array_equal(res.counts.cpu().numpy(), ref["counts"])
     assert np.array_equal(res.codes.cpu().numpy(), ref["codes"])
-    # features: per-point relative L2
-    f = res.features.cpu().numpy().astype(np.float64)
-    rf = ref["features"]
-    rn = np.linalg.norm(rf, axis=1)
     featured = ref["counts"] > 0
-    rel = np.linalg.norm(f - rf, axis=1)[featured] / rn[featured]
-    assert rel.max() <= tol, rel.max()
-    assert np.all(f[~featured] == 0)
+    if res.features is not None:  # features: per-point relative L2
+        f = res.features.cpu().numpy().astype(np.float64)
+        rf = ref["features"]
+        rn = np.linalg.norm(rf, axis=1)
+        rel = np.linalg.norm(f - rf, axis=1)[featured] / rn[featured]
+        assert rel.max() <= tol, rel.max()
+        assert np.all(f[~featured] == 0)
     s = res.sims.cpu().numpy().astype(np.float64)
     scale = np.maximum(1e-2, np.abs(ref["sims"]).max(axis=1))
     assert (np.abs(s - ref["sims"]).max(axis=1) <= tol * scale).all()
@@ -100,9 +102,9 @@ def test_fused_vs_reference_goldens(cuda, golden, workload, name):
     """Against the reference's own outputs (golden fixtures), not just the oracle."""
     g = golden(name)
     wl = workload(name)
-    for force in (False, True):
+    for force, feats in ((False, True), (False, False), (True, True)):
         tol = tol_for(wl, force)
-        res = run_gpu(wl, force_simt=force)
+        res = run_gpu(wl, force_simt=force, features=feats)
         vis = np.unpackbits(g["visibility"], axis=1)[:, : wl.cfg.nviews].astype(bool)
         assert np.array_equal(res.visibility().cpu().numpy(), vis)
         assert np.array_equal(res.counts.cpu().numpy(), g["counts"])
@@ -112,10 +114,11 @@ def test_fused_vs_reference_goldens(cuda, golden, workload, name):
         np.testing.assert_allclose(res.props.cpu().numpy(), g["props"], rtol=tol, atol=1e-6)
 
 
+@pytest.mark.parametrize("features", [True, False])
 @pytest.mark.parametrize("name", ["mini", "mini_bf16", "mini_fib40", "pr1"])
-def test_fused_vs_oracle(cuda, workload, name):
+def test_fused_vs_oracle(cuda, workload, name, features):
     wl = workload(name)
-    assert_parity(run_gpu(wl), run_oracle(wl), wl, tol=tol_for(wl))
+    assert_parity(run_gpu(wl, features=features), run_oracle(wl), wl, tol=tol_for(wl))
 
 
 def test_bf16_simt_path_meets_fp32_bar(cuda, workload):
@@ -123,12 +126,14 @@ def test_bf16_simt_path_meets_fp32_bar(cuda, workload):
     assert_parity(run_gpu(wl, force_simt=True), run_oracle(wl), wl, tol=TOL)
 
 
+@pytest.mark.parametrize("features", [True, False])
 @pytest.mark.parametrize("name", ["c5", "c3"])
-def test_tile_path_large_config_shapes(cuda, workload, name):
+def test_tile_path_large_config_shapes(cuda, workload, name, features):
     """Tensor-core tile path on the real C5 / C3 view + map + material shapes (subset of points
-    so the oracle finishes in seconds): masks / counts / codes exact, the rest at the bf16 bar."""
+    so the oracle finishes in seconds): masks / counts / codes exact, the rest at the bf16 bar.
+    features=False: the Gram kernel; True: the feature-product kernel."""
     wl = workload(name, n=24_000)
-    assert_parity(run_gpu(wl), run_oracle(wl), wl, tol=TOL_BF16)
+    assert_parity(run_gpu(wl, features=features), run_oracle(wl), wl, tol=TOL_BF16)
 
 
 def test_fused_c2_shapes_subset(cuda, workload):

@@ -58,8 +58,10 @@ class TestGroundingGoldens:
     def test_softmax_rejects(self):
         with pytest.raises(ValueError):
             O.softmax_weights(np.array([[0.1]]), 0.0)
-        with pytest.raises(ValueError):
+        # grounding.py:173-174 raises MaterialError (not a ValueError) on NaN similarities
+        with pytest.raises(O.MaterialError) as ei:
             O.softmax_weights(np.array([[np.nan, 0.0]]), 0.1)
+        assert not isinstance(ei.value, ValueError)
 
 
 @pytest.mark.parametrize("name", ["mini", "mini_bf16"])
@@ -141,6 +143,23 @@ class TestAgainstLiveReference:
         a_ref = fusion.aggregate_geometric_features(p, rviews, vis_ref)
         a, c = O.aggregate_geometric_features(p, wl.views(), vis)
         assert np.array_equal(a, a_ref.features) and np.array_equal(c, a_ref.visible_counts)
+
+    def test_softmax_error_classes(self):
+        """The oracle raises the reference's exception classes (grounding.py:170-174)."""
+        import sys
+
+        sys.path.insert(0, "/root/reference/pkg/src")
+        from propfield import errors, grounding
+
+        bad = np.array([[np.nan, 0.0]])
+        with pytest.raises(errors.MaterialError):
+            grounding.softmax_weights(bad, 0.1)
+        with pytest.raises(O.MaterialError):
+            O.softmax_weights(bad, 0.1)
+        assert O.MaterialError.__name__ == errors.MaterialError.__name__
+        assert not issubclass(errors.MaterialError, ValueError)
+        with pytest.raises(ValueError):
+            grounding.softmax_weights(np.array([[0.1]]), 0.0)
 
 
 class TestGenerator:
@@ -232,3 +251,33 @@ class TestNormalsOracle:
             O.estimate_normals(np.zeros((5, 3)), 2, np.zeros((1, 3)))
         with pytest.raises(ValueError):
             O.estimate_normals(np.zeros((5, 3)), 6, np.zeros((1, 3)))
+
+
+class TestProjectionOperationOrder:
+    """pf_common.cuh:cam_row reproduces `cam = p @ R.T + t` (geometry.py:54) as the fma chain
+    fma(p2, R[r,2], fma(p1, R[r,1], p0 * R[r,0])) + t. That is the order of this image's numpy BLAS
+    (OpenBLAS dgemm small-matrix kernel); the fp64 visibility masks are bit-exact only because the
+    device uses the same order. This test pins it: exact fma via Fraction (correctly rounded) and
+    numpy's own matmul must agree bit for bit on points and rotations of the workloads' kind."""
+
+    @staticmethod
+    def _fma(a, b, c):
+        from fractions import Fraction
+
+        return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+    def test_numpy_matmul_is_the_fma_chain(self):
+        rng = np.random.default_rng(11)
+        wl = workloads.generate("mini_fib40")
+        pts = np.concatenate([wl.points[:300].astype(np.float64), rng.uniform(-0.5, 0.5, (200, 3))])
+        for pose in wl.poses[:8]:
+            R = np.asarray(pose.rotation, np.float64)
+            t = np.asarray(pose.translation, np.float64)
+            cam = pts @ R.T + t  # the reference's expression (geometry.py:54)
+            for i in range(pts.shape[0]):
+                p0, p1, p2 = (float(x) for x in pts[i])
+                for r in range(3):
+                    acc = p0 * float(R[r, 0])
+                    acc = self._fma(p1, float(R[r, 1]), acc)
+                    acc = self._fma(p2, float(R[r, 2]), acc)
+                    assert acc + float(t[r]) == cam[i, r], (i, r)
