@@ -642,7 +642,6 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.sub2_count = reinterpret_cast<int32_t*>(ws + L.sub2);
     T.sub2_items = T.sub2_count + 1;
     T.max_sub2 = L.max_sub2;
-    T.ibox = tr == tile::kGramTile ? reinterpret_cast<float4*>(ws + L.ibox) : nullptr;
     T.work_count = tr == tile::kGramTile ? reinterpret_cast<int32_t*>(ws + L.work) : nullptr;
     T.work = tr == tile::kGramTile ? reinterpret_cast<int4*>(ws + L.work) + 1 : nullptr;
     T.partials = a->partials;
@@ -697,31 +696,32 @@ int pf_tile_executed_flops(const pf_fuse_args_t* a, double* flops, void* stream)
   const int tr = tile_rows(a);
   const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, tile::kMaxKpadTC, a->d, x3, tr);
   const unsigned char* ws = reinterpret_cast<const unsigned char*>(a->workspace) + g_bytes(a);
-  int32_t cnt[2] = {0, 0};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaMemcpyAsync(&cnt[0], ws + L.sub, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-  if (L.max_sub2 > 0) cudaMemcpyAsync(&cnt[1], ws + L.sub2, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  double f = 0.0;
+  if (tr == tile::kGramTile) {  // the work list the Gram kernel walked
+    int32_t nw = 0;
+    cudaMemcpyAsync(&nw, ws + L.work, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("tile_executed_flops");
+    std::vector<int4> w((size_t)std::max(nw, 1));
+    if (nw) cudaMemcpy(w.data(), ws + L.work + sizeof(int4), sizeof(int4) * nw, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < nw; ++i) {
+      const int rows = w[i].z & 0xffff, kt = w[i].z >> 16, ktp = (kt + 15) & ~15, nb = (rows + 127) / 128;
+      f += 2.0 * 128.0 * ktp * a->d + (ktp > 128 ? 2.0 * 128.0 * (ktp - 128) * a->d : 0.0);
+      f += (double)nb * 2.0 * 128.0 * ktp * (double)(tile::kMaxKpadTC + ktp);
+    }
+    *flops = f;
+    return check_launch("tile_executed_flops");
+  }
+  int32_t nsub = 0;
+  cudaMemcpyAsync(&nsub, ws + L.sub, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("tile_executed_flops");
-  const int64_t n1 = std::min(cnt[0], L.max_sub_tiles), n2 = std::min(cnt[1], L.max_sub2);
-  const int64_t items = L.ntiles + 4 * (int64_t)L.max_sub_tiles + 4 * n2;
+  const int64_t items = L.ntiles + 4 * (int64_t)std::min(nsub, L.max_sub_tiles);
   std::vector<int32_t> kt((size_t)items);
   cudaMemcpy(kt.data(), ws + L.kt, sizeof(int32_t) * items, cudaMemcpyDeviceToHost);
-  const bool gram = tr == tile::kGramTile;
-  const int ktmax = gram ? tile::kGramKt : tile::ws_kt_max(x3);
-  double f = 0.0;
   for (int64_t t = 0; t < items; ++t) {
-    if (t >= L.ntiles + 4 * n1 && t < L.ntiles + 4 * (int64_t)L.max_sub_tiles) continue;  // unused slots
     const int ktp = (kt[t] + 15) & ~15;
-    if (!(kt[t] > 0 && ktp <= ktmax)) continue;
-    if (!gram) {
+    if (kt[t] > 0 && ktp <= tile::ws_kt_max(x3))
       f += (x3 ? 3.0 : 1.0) * 2.0 * 128.0 * ktp * (double)(a->d + tile::kMaxKpadTC);
-      continue;
-    }
-    const int rows = t < L.ntiles ? tr : (t < L.ntiles + 4 * (int64_t)L.max_sub_tiles ? 128 : 32);
-    int64_t nb = (rows + 127) / 128;
-    if (t == L.ntiles - 1) nb = std::min(nb, ((a->n - t * (int64_t)tr) + 127) / 128);  // the last tile ends early
-    f += 2.0 * 128.0 * ktp * a->d + (ktp > 128 ? 2.0 * 128.0 * (ktp - 128) * a->d : 0.0);
-    f += (double)nb * 2.0 * 128.0 * ktp * (double)(tile::kMaxKpadTC + ktp);
   }
   *flops = f;
   return check_launch("tile_executed_flops");

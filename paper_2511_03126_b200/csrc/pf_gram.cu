@@ -198,33 +198,6 @@ __device__ __forceinline__ uint32_t mt_off(int n, int j, int q) {
   return (uint32_t)(j * kChunkBytes + (n >> 3) * 1024 + (n & 7) * 128 + (((q ^ n) & 7) << 4));
 }
 
-// dense work index -> item (tiles, level-1 items, level-2 items) and its rows
-struct ItemG {
-  int64_t item, row0;
-  int nrows;
-};
-__device__ __forceinline__ ItemG item_of(const TileParams& P, int64_t w, int64_t ntiles, int n1) {
-  ItemG g;
-  if (w < ntiles) {
-    g.item = w;
-    g.row0 = w * P.tr;
-    g.nrows = P.tr;
-  } else if (w < ntiles + 4 * (int64_t)n1) {
-    const int64_t u = w - ntiles;
-    g.item = w;
-    g.row0 = (int64_t)P.sub_tiles[u >> 2] * P.tr + (u & 3) * P.sub1_rows;
-    g.nrows = P.sub1_rows;
-  } else {
-    const int64_t u = w - ntiles - 4 * (int64_t)n1;
-    g.item = ntiles + 4 * (int64_t)P.max_sub_tiles + u;
-    const int64_t pu = (int64_t)P.sub2_items[u >> 2] - ntiles;
-    g.row0 = (int64_t)P.sub_tiles[pu >> 2] * P.tr + (pu & 3) * P.sub1_rows + (u & 3) * 32;
-    g.nrows = 32;
-  }
-  const int64_t left = P.n - g.row0;  // the last tile (and its splits) may end early
-  if (left < g.nrows) g.nrows = left > 0 ? (int)left : 0;
-  return g;
-}
 __device__ __forceinline__ int ktp_ok(int kt, bool& ok) {
   const int ktp = (kt + 15) & ~15;
   ok = kt > 0 && ktp <= kKt;
@@ -923,29 +896,52 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
 }
 
 // Work items -> the compact list the tile kernel walks (items that fit the tap budget) and the
-// SIMT kernel's point list (rows of items with no visible taps or more than kKt that were not split
-// further); one warp per item
+// SIMT kernel's point list (rows of items with no visible taps, or more than kKt taps and not split
+// further). One warp per 512-row tile (and its 128-row tiles when it overflows) or per 32-row item.
 __global__ void k_collect_work(TileParams P) {
-  const int64_t ntiles = (P.n + P.tr - 1) / P.tr;
-  const int n1 = min(*P.sub_count, P.max_sub_tiles);
-  const int n2 = P.max_sub2 > 0 ? min(*P.sub2_count, P.max_sub2) : 0;
-  const int64_t nwork = ntiles + 4 * (int64_t)n1 + 4 * (int64_t)n2;
+  const int64_t nt = (P.n + P.tr - 1) / P.tr;
+  const int n2 = min(*P.sub2_count, P.max_sub2);
+  const int64_t first2 = nt + 4 * (int64_t)P.max_sub_tiles;
   const int lane = threadIdx.x & 31;
-  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nwork;
+  auto push = [&](int64_t item, int64_t row0, int rows, int kt) {
+    if (lane == 0) P.work[atomicAdd(P.work_count, 1)] = make_int4((int)item, (int)row0, rows | (kt << 16), 0);
+  };
+  auto overflow = [&](int64_t row0, int rows) {
+    for (int r = lane; r < rows; r += 32) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(P.spts[row0 + r].w);
+  };
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nt + 4 * (int64_t)n2;
        w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const ItemG g = item_of(P, w, ntiles, n1);
-    const int kt = P.tile_kt[g.item];
     bool ok;
-    ktp_ok(kt, ok);
-    if (kt == -1 || g.nrows <= 0) continue;  // split into smaller items / past the last point
-    if (ok) {
-      if (lane == 0)
-        P.work[atomicAdd(P.work_count, 1)] = make_int4((int)g.item, (int)g.row0, g.nrows | (kt << 16), 0);
-      continue;
-    }
-    for (int r = lane; r < g.nrows; r += 32) {
-      const int64_t jr = g.row0 + r;
-      if (jr < P.n) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(P.spts[jr].w);
+    if (w < nt) {
+      const int kt = P.tile_kt[w];
+      const int rows = (int)min((int64_t)P.tr, P.n - w * P.tr);
+      ktp_ok(kt, ok);
+      if (ok) {
+        push(w, w * P.tr, rows, kt);
+      } else if (kt <= 0) {
+        overflow(w * P.tr, rows);  // nothing visible: featureless points
+      } else {
+        for (int q = 0; q < P.tr / kTile; ++q) {  // the 128-row tiles (level-1 items)
+          const int64_t r0 = w * P.tr + q * kTile;
+          if (r0 >= P.n) break;
+          const int k = P.tile_kt[nt + w * (P.tr / kTile) + q];
+          const int r = (int)min((int64_t)kTile, P.n - r0);
+          if (k == -1) continue;  // split into 32-row items
+          ktp_ok(k, ok);
+          if (ok) push(nt + w * (P.tr / kTile) + q, r0, r, k);
+          else overflow(r0, r);
+        }
+      }
+    } else {
+      const int64_t u = w - nt;
+      const int64_t item = first2 + u;
+      const int64_t r0 = ((int64_t)P.sub2_items[u >> 2] - nt) * kTile + 32 * (u & 3);
+      if (r0 >= P.n) continue;
+      const int r = (int)min((int64_t)32, P.n - r0);
+      const int k = P.tile_kt[item];
+      ktp_ok(k, ok);
+      if (ok) push(item, r0, r, k);
+      else overflow(r0, r);
     }
   }
 }
@@ -967,8 +963,7 @@ int run_tile_gram(const TileParams& P, cudaStream_t st) {
   if (const char* g = getenv("PF_WS_GRID")) grid = atoi(g) > 0 ? atoi(g) : grid;  // debug knob
   if (grid < 1) grid = 1;
   cudaMemsetAsync(P.work_count, 0, sizeof(int32_t), st);
-  k_collect_work<<<grid_for(32 * (ntiles + 4 * (int64_t)P.max_sub_tiles + 4 * (int64_t)P.max_sub2), 256, 148 * 8),
-                   256, 0, st>>>(P);
+  k_collect_work<<<grid_for(32 * (ntiles + 4 * (int64_t)P.max_sub2), 256, 148 * 8), 256, 0, st>>>(P);
   if (int rc = check_launch("collect_work")) return rc;
   const bool debug = getenv("PF_WS_DEBUG") != nullptr;
   static unsigned long long* dbg = nullptr;

@@ -489,17 +489,6 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
   }
   if (tid < 2) s_seen[tid] = 0u;
   __syncthreads();
-  if (TR > kTile && P.ibox && tid < TR / kTile) {  // Gram path: box of each 128-row block
-    float bl[6];
-#pragma unroll
-    for (int a = 0; a < 6; ++a) {
-      bl[a] = sbb[4 * tid][a];
-#pragma unroll
-      for (int w = 1; w < 4; ++w) bl[a] = a < 3 ? fminf(bl[a], sbb[4 * tid + w][a]) : fmaxf(bl[a], sbb[4 * tid + w][a]);
-    }
-    P.ibox[2 * (tile * (TR / kTile) + tid)] = make_float4(bl[0], bl[1], bl[2], 0.f);
-    P.ibox[2 * (tile * (TR / kTile) + tid) + 1] = make_float4(bl[3], bl[4], bl[5], 0.f);
-  }
   float lo[3], hi[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -682,17 +671,71 @@ __global__ void k_find_overflow(TileParams P, int64_t ntiles, int kt_max) {
   }
 }
 
-// level-1 items that overflow -> level-2 parents (Gram path)
-__global__ void k_find_overflow2(TileParams P, int64_t ntiles, int kt_max) {
-  const int64_t n1 = 4 * (int64_t)min(*P.sub_count, P.max_sub_tiles);
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n1; u += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = ntiles + u;
-    const int kt = P.tile_kt[t];
-    if (((kt + 15) & ~15) <= kt_max) continue;
+// Gram path: windows of a 512-row tile = per view, the hull of its four 128-row tiles' windows (the
+// 128-row prep's FULL / MIXED box windows or EXACT unions all bound the visible points' taps), padded
+// to even sizes and laid out by an exclusive prefix over the views. One warp per tile.
+__global__ void k_merge512(TileParams P, int64_t nt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nt128 = (P.n + kTile - 1) / kTile;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < nt;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int w[2], h[2], x0[2], y0[2], sz[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int v = lane + 32 * r;
+      int ax0 = INT_MAX, ay0 = INT_MAX, ax1 = -1, ay1 = -1;
+      if (v < P.nv)
+        for (int q = 0; q < 4; ++q) {
+          const int64_t t128 = 4 * t + q;
+          if (t128 >= nt128) break;
+          const uint2 d = P.tile_desc[(nt + t128) * P.nv + v];
+          const int ww = d.y & 0xff, hh = (d.y >> 8) & 0xff;
+          if (!ww) continue;
+          const int dx = (d.x >> 16) & 0xff, dy = d.x >> 24;
+          ax0 = min(ax0, dx);
+          ay0 = min(ay0, dy);
+          ax1 = max(ax1, dx + ww - 1);
+          ay1 = max(ay1, dy + hh - 1);
+        }
+      w[r] = ax1 >= 0 ? ax1 - ax0 + 1 : 0;
+      h[r] = ax1 >= 0 ? ay1 - ay0 + 1 : 0;
+      x0[r] = w[r] ? ax0 : 0;
+      y0[r] = w[r] ? ay0 : 0;
+      sz[r] = (w[r] * h[r] + 1) & ~1;
+    }
+    int incl0 = sz[0], incl1 = sz[1];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t0 = __shfl_up_sync(0xffffffffu, incl0, o), t1 = __shfl_up_sync(0xffffffffu, incl1, o);
+      if (lane >= o) {
+        incl0 += t0;
+        incl1 += t1;
+      }
+    }
+    const int tot0 = __shfl_sync(0xffffffffu, incl0, 31);
+    const int base0 = incl0 - sz[0], base1 = tot0 + incl1 - sz[1];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int v = lane + 32 * r;
+      const int base = r ? base1 : base0;
+      if (v < P.nv)
+        P.tile_desc[t * P.nv + v] = make_uint2((uint32_t)min(base, 65535) | ((uint32_t)x0[r] << 16) | ((uint32_t)y0[r] << 24),
+                                               (uint32_t)w[r] | ((uint32_t)h[r] << 8));
+    }
+    if (lane == 31) P.tile_kt[t] = tot0 + incl1;
+  }
+}
+
+// Gram path: 128-row tiles of overflowing 512-row tiles that overflow too -> level-2 parents
+__global__ void k_find_overflow128(TileParams P, int64_t nt, int kt_max) {
+  const int64_t nt128 = (P.n + kTile - 1) / kTile;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt128; t += (int64_t)gridDim.x * blockDim.x) {
+    const int k512 = P.tile_kt[t >> 2], k128 = P.tile_kt[nt + t];
+    if (((k512 + 15) & ~15) <= kt_max || ((k128 + 15) & ~15) <= kt_max) continue;
     const int b = atomicAdd(P.sub2_count, 1);
     if (b < P.max_sub2) {
-      P.sub2_items[b] = (int32_t)t;
-      P.tile_kt[t] = -1;
+      P.sub2_items[b] = (int32_t)(nt + t);
+      P.tile_kt[nt + t] = -1;
     }
   }
 }
@@ -710,7 +753,6 @@ __global__ void __launch_bounds__(128) k_item_prep(TileParams P, int64_t ntiles,
   constexpr int kChildren = 128 / R;  // children per block
   __shared__ ViewF sv[kMaxViewsTC];
   __shared__ int sx0[kMaxViewsTC], sy0[kMaxViewsTC], sx1[kMaxViewsTC], sy1[kMaxViewsTC];
-  __shared__ float sbox[4][6];
   const int nparents = level == 1 ? min(*P.sub_count, P.max_sub_tiles) : min(*P.sub2_count, P.max_sub2);
   const int64_t first = level == 1 ? ntiles : ntiles + 4 * (int64_t)P.max_sub_tiles;
   const int nblocks = nparents * (4 / kChildren);
@@ -723,7 +765,9 @@ __global__ void __launch_bounds__(128) k_item_prep(TileParams P, int64_t ntiles,
     const int c = R == 32 ? warp : blk % 4;          // child of parent b
     const int r = R == 32 ? lane : (int)threadIdx.x;  // row within the child
     const int64_t item = first + 4 * (int64_t)b + c;
-    const int64_t prow = level == 1 ? (int64_t)P.sub_tiles[b] * P.tr : level1_row0(P, ntiles, P.sub2_items[b]);
+    const int64_t prow = level == 1               ? (int64_t)P.sub_tiles[b] * P.tr
+                         : P.tr == kGramTile ? ((int64_t)P.sub2_items[b] - ntiles) * kTile  // a 128-row tile
+                                             : level1_row0(P, ntiles, P.sub2_items[b]);
     const int64_t jpt = prow + (int64_t)c * R + r;
     const bool valid = jpt < P.n;
     float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -733,32 +777,6 @@ __global__ void __launch_bounds__(128) k_item_prep(TileParams P, int64_t ntiles,
       mw = *reinterpret_cast<const uint2*>(P.srec + jpt);
     }
     uint2* desc = P.tile_desc + item * P.nv;
-    if (P.ibox) {  // Gram path: the child's box (one 128-row block)
-      float b6[6] = {valid ? p.x : INFINITY, valid ? p.y : INFINITY, valid ? p.z : INFINITY,
-                     valid ? p.x : -INFINITY, valid ? p.y : -INFINITY, valid ? p.z : -INFINITY};
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          b6[a] = fminf(b6[a], __shfl_xor_sync(0xffffffffu, b6[a], o));
-          b6[a + 3] = fmaxf(b6[a + 3], __shfl_xor_sync(0xffffffffu, b6[a + 3], o));
-        }
-      if (R > 32) {
-        if (lane == 0)
-#pragma unroll
-          for (int a = 0; a < 6; ++a) sbox[warp][a] = b6[a];
-        __syncthreads();
-#pragma unroll
-        for (int a = 0; a < 6; ++a)
-          b6[a] = a < 3 ? fminf(fminf(sbox[0][a], sbox[1][a]), fminf(sbox[2][a], sbox[3][a]))
-                        : fmaxf(fmaxf(sbox[0][a], sbox[1][a]), fmaxf(sbox[2][a], sbox[3][a]));
-      }
-      if (r == 0) {
-        const int64_t bi = 4 * ntiles + (item - ntiles);
-        P.ibox[2 * bi] = make_float4(b6[0], b6[1], b6[2], 0.f);
-        P.ibox[2 * bi + 1] = make_float4(b6[3], b6[4], b6[5], 0.f);
-      }
-    }
     if (R > 32) {
       for (int v = threadIdx.x; v < P.nv; v += 128) {
         sx0[v] = INT_MAX;
@@ -903,8 +921,6 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d, bool 
   L.kt = take(sizeof(int32_t) * (size_t)items);
   L.sub = take(sizeof(int32_t) * ((size_t)L.max_sub_tiles + 1));
   L.sub2 = take(sizeof(int32_t) * ((size_t)L.max_sub2 + 1));
-  L.ibox = tr == kTile ? 0 : take(2 * sizeof(float4) * (size_t)(4 * ntiles + 4 * (int64_t)L.max_sub_tiles +
-                                                                 4 * (int64_t)L.max_sub2));
   L.ovf = take(sizeof(int32_t) * (size_t)(n + 1));
   L.work = tr == kTile ? 0 : take(sizeof(int4) * (size_t)(items + 1));  // [count | pad] then entries
   L.bytes = off;
@@ -1008,8 +1024,30 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   }
   k_view_setup<<<1, kMaxViewsTC, 0, st>>>(Q);
   if (int rc = check_launch("view_setup")) return rc;
-  if (P.tr == kGramTile) k_tile_prep<kGramTile><<<(unsigned)L.ntiles, kGramTile, 0, st>>>(Q);
-  else k_tile_prep<kTile><<<(unsigned)L.ntiles, kTile, 0, st>>>(Q);
+  if (P.tr == kGramTile) {
+    // Gram path: per-point visibility and windows from the 128-row prep (its tiles are the level-1
+    // items, ids ntiles + t128), the 512-row tiles' windows merged from theirs, the 128-row tiles
+    // that still overflow split into 32-row items
+    const int64_t nt128 = (n + kTile - 1) / kTile;
+    TileParams Q128 = Q;
+    Q128.tr = kTile;
+    Q128.tile_desc = P.tile_desc + L.ntiles * P.nv;
+    Q128.tile_kt = P.tile_kt + L.ntiles;
+    k_tile_prep<kTile><<<(unsigned)nt128, kTile, 0, st>>>(Q128);
+    if (int rc = check_launch("tile_prep")) return rc;
+    k_merge512<<<grid_for(32 * L.ntiles, 256), 256, 0, st>>>(P, L.ntiles);
+    if (int rc = check_launch("merge512")) return rc;
+    cudaMemsetAsync(P.sub2_count, 0, sizeof(int32_t), st);
+    k_find_overflow128<<<grid_for(nt128, 256), 256, 0, st>>>(P, L.ntiles, P.kt_max);
+    if (int rc = check_launch("find_overflow128")) return rc;
+    k_item_prep<32><<<(unsigned)(L.max_sub2 < 148 * 16 ? L.max_sub2 : 148 * 16), 128, 0, st>>>(P, L.ntiles, 2);
+    if (int rc = check_launch("item_prep2")) return rc;
+    stage_mark(2, st);
+    const int rc = run_tile_gram(P, st);
+    stage_mark(3, st);
+    return rc;
+  }
+  k_tile_prep<kTile><<<(unsigned)L.ntiles, kTile, 0, st>>>(Q);
   if (int rc = check_launch("tile_prep")) return rc;
   // overflow tiles -> smaller work items (appended after the tiles)
   cudaMemsetAsync(P.sub_count, 0, sizeof(int32_t), st);
@@ -1019,13 +1057,6 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
   if (P.sub1_rows == 32) k_item_prep<32><<<pgrid, 128, 0, st>>>(P, L.ntiles, 1);
   else k_item_prep<128><<<4 * pgrid, 128, 0, st>>>(P, L.ntiles, 1);
   if (int rc = check_launch("item_prep")) return rc;
-  if (P.max_sub2 > 0) {
-    cudaMemsetAsync(P.sub2_count, 0, sizeof(int32_t), st);
-    k_find_overflow2<<<grid_for(4 * (int64_t)L.max_sub_tiles, 256), 256, 0, st>>>(P, L.ntiles, P.kt_max);
-    if (int rc = check_launch("find_overflow2")) return rc;
-    k_item_prep<32><<<(unsigned)(L.max_sub2 < 148 * 16 ? L.max_sub2 : 148 * 16), 128, 0, st>>>(P, L.ntiles, 2);
-    if (int rc = check_launch("item_prep2")) return rc;
-  }
   stage_mark(2, st);
   if (debug) {
     unsigned long long h[11];
@@ -1083,7 +1114,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
     fprintf(stderr, "[prep debug] MIXED samples ambiguous under the affine model: %.2f%%, mean eu %.4f px\n",
             100.0 * h[8] / (double)(h[7] ? h[7] : 1), 1e-6 * h[9] / (double)(h[10] ? h[10] : 1));
   }
-  const int rc = P.tr == kGramTile ? run_tile_gram(P, st) : run_tile_ws(P, st);
+  const int rc = run_tile_ws(P, st);
   stage_mark(3, st);
   return rc;
 }

@@ -94,10 +94,11 @@ struct TileParams {
   int32_t* sub_tiles;
   int32_t* sub_count;
   int32_t max_sub_tiles;
-  // Gram path (pf_gram.cu): level-0 tiles of `tr` rows (512); overflow tiles split into 4 level-1
-  // items of `sub1_rows` (128) rows, overflowing level-1 items into 4 level-2 items of 32 rows:
-  // work items ntiles + 4 max_sub_tiles + 4 c + q (c < min(*sub2_count, max_sub2)) cover rows 32q..
-  // of level-1 item sub2_items[c]. The tcgen05 tile kernel k_tile_ws uses tr = 128, sub1_rows = 32.
+  // Gram path (pf_gram.cu): work items are the 512-row tiles (ids < ntiles), the 128-row tiles
+  // (ids ntiles + t128: the level-1 items of overflowing tiles) and 32-row splits of overflowing
+  // 128-row tiles (ids ntiles + 4 max_sub_tiles + 4 c + q, c < min(*sub2_count, max_sub2), rows 32 q
+  // .. of the 128-row tile with item id sub2_items[c]). k_tile_ws uses tr = 128, sub1_rows = 32
+  // (level-1 items ntiles + 4 b + q: rows 32 q .. of tile sub_tiles[b]).
   int32_t tr, sub1_rows;
   int32_t* sub2_items;
   int32_t* sub2_count;
@@ -106,9 +107,6 @@ struct TileParams {
   int32_t ablate;           // Gram kernel timing experiments only (PF_GRAM_ABLATE bits; results invalid)
   uint32_t* trace;          // optional per-tile role timestamps (PF_WS_DEBUG + PF_WS_TRACE=<file>)
   double* partials;
-  // Gram path: bounding box (lo.xyz, hi.xyz as two float4) of every 128-row block of a work item,
-  // written by the prep kernels: level-0 tile t block b at 4 t + b, split item i at 4 ntiles + i - ntiles
-  float4* ibox;
   // Gram path: compact list of the work items that run in the tile kernel ({item, first row,
   // rows | taps << 16, 0}, k_collect_work) and its length
   int4* work;
@@ -119,7 +117,7 @@ struct TileParams {
 struct TileLayout {
   int64_t ntiles;
   int32_t max_sub_tiles, max_sub2;
-  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, sub2, ibox, work, gbf, textbf, viewf, vbound, vox, tbound, glo, fhi, flo, textlo,
+  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, sub2, work, gbf, textbf, viewf, vbound, vox, tbound, glo, fhi, flo, textlo,
       bytes;
 };
 
