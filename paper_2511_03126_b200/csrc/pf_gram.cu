@@ -43,11 +43,17 @@ namespace pf {
 namespace tile {
 namespace {
 
-constexpr int kLoadWarps = 3;       // warps 0-2: tap-row loaders
+#ifndef PF_GRAM_BUILD_GROUPS
+#define PF_GRAM_BUILD_GROUPS 2  // 8 builder warps, 7 loader warps (measured: 3 groups + 3 loaders is slower)
+#endif
+// warps 0-2 (and 4 .. kBuildWarp0-1): tap-row loaders; warp 3: MMA issuer; kBuildWarp0 ..15: W builders
+// (kBuildGroups per TMEM lane quarter); warps 16-23: accumulators
+constexpr int kBuildGroups = PF_GRAM_BUILD_GROUPS;
+constexpr int kBuildWarps = 4 * kBuildGroups;
+constexpr int kBuildWarp0 = 16 - kBuildWarps;
+constexpr int kLoadWarps = kBuildWarp0 - 1;
 constexpr int kLoadThreads = 32 * kLoadWarps;
-constexpr int kMmaWarp = 3;         // warp 3: MMA issuer
-constexpr int kBuildWarp0 = 4;      // warps 4-15: W builders (three per TMEM lane quarter)
-constexpr int kBuildWarps = 12;
+constexpr int kMmaWarp = 3;
 constexpr int kBuildThreads = 32 * kBuildWarps;
 constexpr int kAccWarp0 = 16;       // warps 16-23: accumulators (two per lane quarter)
 constexpr int kAccThreads = 256;
@@ -59,12 +65,12 @@ constexpr int kStages = 4;          // ring depth (even: the two G chunks of an 
 constexpr int kChunkBytes = kKt * 128;   // one 64-tap K chunk of M~ (kKt rows x 128 B)
 constexpr int kMtBytes = 3 * kChunkBytes;
 constexpr int kRowStep = kLoadThreads / 8;
-constexpr int kRowsPer = kKt / kRowStep;
+constexpr int kRowsPer = (kKt + kRowStep - 1) / kRowStep;
 constexpr int kHalfK = kMaxKpadTC / 2;
 constexpr int kRegProducer = 48, kRegAcc = 144;
 constexpr uint32_t kColS = 0, kColY = 128, kColG0 = 0, kColG1 = 192, kColW = 320, kWCols = kKt / 2;
 static_assert(kColY + kKt <= kColW && kColW + 2 * kWCols <= 512, "TMEM budget");
-static_assert(kRowsPer * kRowStep == kKt, "loader rows");
+static_assert(kRowsPer * kRowStep >= kKt, "loader rows");
 static_assert(4 * 128 * kRegProducer + 2 * 128 * kRegAcc <= kThreads * 80, "register pool");
 static_assert(kBuildWarp0 % 4 == 0 && kAccWarp0 % 4 == 0, "TMEM lane quarter = warp % 4");
 static_assert(kStages % 2 == 0, "G chunk pairs never wrap the ring");
@@ -83,6 +89,15 @@ static_assert(kStages % 2 == 0, "G chunk pairs never wrap the ring");
 // PROF instantiation (PF_WS_DEBUG=1): cycles spent in each wait site, per CTA (printed by the host):
 // 0 load:b_empty 1 mma:r_empty(gram) 2 mma:b_full(gram) 3 mma:b_full(G) 4 mma:a_full 5 mma:r_empty(blk)
 // 6 build:a_empty 7 acc:r_full(gram) 8 acc:r_full(blk); 9 build busy, 10 acc busy, 11 total
+// all other waits back off with a short sleep (PF_GRAM_WAIT_NS; 0 = spin): a spinning warp takes issue
+// slots from the builders and accumulators on its SM sub-partition
+#ifndef PF_GRAM_WAIT_NS
+#define PF_GRAM_WAIT_NS 32
+#endif
+#if PF_GRAM_WAIT_NS > 0 && !defined(PF_GRAM_TRAP)
+#undef GWAIT
+#define GWAIT(bar, par) tc::mbar_wait_sleep<PF_GRAM_WAIT_NS>(bar, par)
+#endif
 #define GWAITP(bar, par, slot)                 \
   do {                                          \
     if constexpr (PROF) {                       \
@@ -117,8 +132,8 @@ struct GramShared {
   int32_t cell[2][kKt];
   ViewF sv[kMaxViewsTC];
   float4 vpk[kMaxViewsTC][5];
-  int4 wlist[kBuildWarps][kMaxViewsTC / 3 + 1];      // builders: per-warp view list (per item)
-  float4 wcoef[kBuildWarps][2 * (kMaxViewsTC / 3 + 1)];  // builders: per-warp expansion coefficients (per block)
+  int4 wlist[kBuildWarps][kMaxViewsTC / kBuildGroups + 1];      // builders: per-warp view list (per item)
+  float4 wcoef[kBuildWarps][2 * (kMaxViewsTC / kBuildGroups + 1)];  // builders: per-warp expansion coefficients
   float4 yp[kMaxKpadTC];
   float2 yv2[kMaxKpadTC];
   float xss[2][kTile];
@@ -292,10 +307,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
   const uint32_t tbase = S.tmem_base;
   const int i0 = blockIdx.x, istep = gridDim.x;
 
-  if (warp < kLoadWarps) {
+  if (warp < kMmaWarp || (warp > kMmaWarp && warp < kBuildWarp0)) {
     // ================= loaders: tap rows (D / 64 chunks), then G rows (2 chunks) =================
     reg_dealloc<kRegProducer>();
-    const int q = tid & 7, r0 = tid >> 3;
+    const int lt = warp < kMmaWarp ? tid : tid - 32;  // loader thread index
+    const int q = lt & 7, r0 = lt >> 3;
     int stage = 0;
     uint32_t phase = 0, il = 0;
     for (int i = i0; i < nwork; i += istep) {
@@ -303,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
       const int kt = e_kt(e), ktp = (kt + 15) & ~15;
       int32_t* cell = S.cell[il & 1];
       asm volatile("bar.sync 3, %0;" ::"n"(kLoadThreads) : "memory");
-      for (int v = tid; v < P.nv; v += kLoadThreads) {
+      for (int v = lt; v < P.nv; v += kLoadThreads) {
         const uint2 ds = P.tile_desc[(int64_t)e.x * P.nv + v];
         const int base = ds.x & 0xffff, x0 = (ds.x >> 16) & 0xff, y0 = ds.x >> 24;
         const int ww = ds.y & 0xff, hh = (ds.y >> 8) & 0xff;
@@ -451,19 +467,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
         p_nx = ld_pref_f4(P.spts + e.y + row);
         mw_nx = ld_pref_u2(P.srec + e.y + row);
       }
-      int nmine;
-      {  // this warp's views (rank = bh mod 3), in rank order
+      int nmine, n22, ncls[5];
+      {  // this warp's views (rank = bh mod 3): the 2 x 2 windows first (built in pairs), then the rest
         const int c0 = shape_cls(d0), c1 = shape_cls(d1);
         const uint32_t m0 = __ballot_sync(0xffffffffu, c0 >= 0), m1 = __ballot_sync(0xffffffffu, c1 >= 0);
-        const bool mine0 = c0 >= 0 && (int)(__popc(m0 & below) % 3) == bh;
-        const bool mine1 = c1 >= 0 && (int)((__popc(m0) + __popc(m1 & below)) % 3) == bh;
-        const uint32_t b0 = __ballot_sync(0xffffffffu, mine0), b1 = __ballot_sync(0xffffffffu, mine1);
+        const bool mine0 = c0 >= 0 && (int)(__popc(m0 & below) % kBuildGroups) == bh;
+        const bool mine1 = c1 >= 0 && (int)((__popc(m0) + __popc(m1 & below)) % kBuildGroups) == bh;
+        // order: 2 x 2, 3 x 2, 2 x 3, 3 x 3, other (classes 0..4); n_c views per class
+        int pos0 = 0, pos1 = 0, tot = 0;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          const uint32_t a0 = __ballot_sync(0xffffffffu, mine0 && c0 == c), a1 = __ballot_sync(0xffffffffu, mine1 && c1 == c);
+          if (c0 == c) pos0 = tot + __popc(a0 & below);
+          if (c1 == c) pos1 = tot + __popc(a0) + __popc(a1 & below);
+          ncls[c] = __popc(a0) + __popc(a1);
+          tot += ncls[c];
+        }
+        n22 = ncls[0];
+        nmine = tot;
         auto put = [&](int k, int v, uint2 d, int c) {
           wl[k] = make_int4(v, (int)(d.x & 0xffff) | (c << 16), (int)((d.x >> 16) & 0xffff) | (int)((d.y & 0xffff) << 16), 0);
         };
-        if (mine0) put(__popc(b0 & below), lane, d0, c0);
-        if (mine1) put(__popc(b0) + __popc(b1 & below), lane + 32, d1, c1);
-        nmine = __popc(b0) + __popc(b1);
+        if (mine0) put(pos0, lane, d0, c0);
+        if (mine1) put(pos1, lane + 32, d1, c1);
         __syncwarp();
       }
       PT(12);
@@ -520,7 +546,92 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
         // timing experiment (PF_GRAM_ABLATE & 4): weights computed but not stored to TMEM
         const bool nost = (P.ablate & 4) != 0;
         const int nunits = (P.ablate & 1) ? 0 : nmine;
-        for (int k = 0; k < nunits; ++k) {  // warp-uniform: one view (32 rows) per iteration
+        int k0 = 0;
+        if (!exact && nunits) {
+          // 2 x 2 windows, two views per step (independent chains): fu_rel, fv_rel in [0, 1] after the
+          // clamp; weights (1-x)(1-y), x(1-y), (1-x)y, xy (numpy_impl.py:50-57) as two bf16 pairs
+          auto w22 = [&](int k, uint32_t& lo, uint32_t& hi, uint32_t& col) {
+            const int2 wk = *reinterpret_cast<const int2*>(&wl[k]);
+            const float4 A0 = wc[2 * k], A1 = wc[2 * k + 1];
+            const float wx = __saturatef(fmaf(A0.w, dzp, fmaf(A0.z, dyp, fmaf(A0.y, dxp, A0.x))));
+            const float wy = __saturatef(fmaf(A1.w, dzp, fmaf(A1.z, dyp, fmaf(A1.y, dxp, A1.x))));
+            const int v = wk.x;
+            const float gg = (((v < 32 ? mw.x : mw.y) >> (v & 31)) & 1u) ? 1.f : 0.f;
+            const float ux = 1.f - wx, uy = gg - gg * wy, vy = gg * wy;
+            lo = pack_bf16(uy * ux, uy * wx);
+            hi = pack_bf16(vy * ux, vy * wx);
+            col = tAb + (uint32_t)((wk.y & 0xffff) >> 1);
+          };
+          for (; k0 + 1 < n22; k0 += 2) {
+            uint32_t l1, h1, c1, l2, h2, c2;
+            w22(k0, l1, h1, c1);
+            w22(k0 + 1, l2, h2, c2);
+            if (nost) {
+              asm volatile("" ::"r"(l1), "r"(h1), "r"(l2), "r"(h2));
+            } else {
+              tc::tmem_st_x2(c1, l1, h1);
+              tc::tmem_st_x2(c2, l2, h2);
+            }
+          }
+          if (k0 < n22) {
+            uint32_t l1, h1, c1;
+            w22(k0, l1, h1, c1);
+            if (nost) asm volatile("" ::"r"(l1), "r"(h1)); else tc::tmem_st_x2(c1, l1, h1);
+            ++k0;
+          }
+          // 3 x 2 and 2 x 3 windows in pairs: separable weights over the 3-tap side (vx0, vx1, vx2) and
+          // the 2-tap side; three bf16 pairs each (taps in row-major window order)
+          auto w3 = [&](int k, bool wide, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& col) {
+            const int2 wk = *reinterpret_cast<const int2*>(&wl[k]);
+            const float4 A0 = wc[2 * k], A1 = wc[2 * k + 1];
+            const float fu = fmaf(A0.w, dzp, fmaf(A0.z, dyp, fmaf(A0.y, dxp, A0.x)));
+            const float fv = fmaf(A1.w, dzp, fmaf(A1.z, dyp, fmaf(A1.y, dxp, A1.x)));
+            const int v = wk.x;
+            const float gg = (((v < 32 ? mw.x : mw.y) >> (v & 31)) & 1u) ? 1.f : 0.f;
+            // the 3-tap side: t in [0, 2], cell i = min(floor(t), 1), weight t - i
+            const float t3 = fminf(fmaxf(wide ? fu : fv, 0.f), 2.f), t2 = __saturatef(wide ? fv : fu);
+            const float i3 = fminf(floorf(t3), 1.f), f3 = t3 - i3;
+            const bool lo3 = i3 == 0.f;
+            const float s0 = lo3 ? 1.f - f3 : 0.f, s1 = lo3 ? f3 : 1.f - f3, s2 = lo3 ? 0.f : f3;
+            const float q0 = gg - gg * t2, q1 = gg * t2;  // the 2-tap side
+            if (wide) {  // 3 x 2: r0 = (s0 s1 s2) q0, r1 = (s0 s1 s2) q1
+              a = pack_bf16(q0 * s0, q0 * s1);
+              b = pack_bf16(q0 * s2, q1 * s0);
+              c = pack_bf16(q1 * s1, q1 * s2);
+            } else {  // 2 x 3: rows s0, s1, s2 of (q0 q1) (q: the x side here)
+              a = pack_bf16(s0 * q0, s0 * q1);
+              b = pack_bf16(s1 * q0, s1 * q1);
+              c = pack_bf16(s2 * q0, s2 * q1);
+            }
+            col = tAb + (uint32_t)((wk.y & 0xffff) >> 1);
+          };
+          auto st3 = [&](uint32_t col, uint32_t a, uint32_t b, uint32_t c) {
+            if (nost) {
+              asm volatile("" ::"r"(a), "r"(b), "r"(c));
+            } else {
+              tc::tmem_st_x2(col, a, b);
+              tc::tmem_st_x1(col + 2u, c);
+            }
+          };
+          for (int cl = 1; cl <= 2; ++cl) {
+            const int kend = k0 + ncls[cl];
+            const bool wide = cl == 1;
+            for (; k0 + 1 < kend; k0 += 2) {
+              uint32_t a1, b1, c1, col1, a2, b2, c2, col2;
+              w3(k0, wide, a1, b1, c1, col1);
+              w3(k0 + 1, wide, a2, b2, c2, col2);
+              st3(col1, a1, b1, c1);
+              st3(col2, a2, b2, c2);
+            }
+            if (k0 < kend) {
+              uint32_t a1, b1, c1, col1;
+              w3(k0, wide, a1, b1, c1, col1);
+              st3(col1, a1, b1, c1);
+              ++k0;
+            }
+          }
+        }
+        for (int k = k0; k < nunits; ++k) {  // warp-uniform: one view (32 rows) per iteration
           const int4 wk = wl[k];
           const int v = wk.x, base = wk.y & 0xffff, cls = wk.y >> 16;
           float fu_rel, fv_rel;
