@@ -47,7 +47,8 @@ def test_load_bundle_device_matches_reference(cuda, golden):
     r = pf.fuse_and_query(torch.from_numpy(g["positions"]).cuda(), ref_views, tables, grid=16)
     assert torch.equal(a.counts, r.counts) and torch.equal(a.mask_bits, r.mask_bits)
     assert torch.equal(a.props, r.props)
-    assert a.mass_kg() == r.mass_kg()
+    # voxel sums are fp32 atomics: the accumulation order (and so the last bits) varies run to run
+    assert a.mass_kg() == pytest.approx(r.mass_kg(), rel=1e-6)
     b2 = ingest.load_bundle_device(BUNDLE, view_limit=2, fmap_kind="bf16")
     assert b2.views.nviews == 2 and b2.views.fmap.dtype == torch.bfloat16 and len(b2.reference_poses) == 2
 
