@@ -32,6 +32,19 @@ def _deps():
     return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + sorted((ROOT / "include").glob("*.h"))
 
 
+def source_hash() -> str:
+    """16 hex digits identifying the native sources and compile flags (stable across rebuilds, unlike
+    the .so bytes): profiles/ncu_traffic.json entries are tied to the build they were measured on."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for p in _deps():
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    h.update(" ".join(ARCH + FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
 def up_to_date() -> bool:
     if not LIB.exists():
         return False

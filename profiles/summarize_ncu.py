@@ -65,8 +65,43 @@ def report(path):
                 print(f"  {k:70s} {r[j]} {units[j]}")
 
 
+def traffic(path, config, kernel):
+    """Record the DRAM bytes and tensor-pipe activity of `kernel` (one launch captured with
+    --set full) for `config` in profiles/ncu_traffic.json, stamped with the native source hash the
+    capture was built from (bench.py uses an entry only when the hash matches its own build)."""
+    import json
+    import os
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2511_03126_b200.build import source_hash
+
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True,
+                         check=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, units = rows[0], rows[1]
+    r = next(r for r in rows[2:] if re.search(kernel, r[h.index("Kernel Name")]))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1.0, "usecond": 1e3,
+             "msecond": 1e6, "second": 1e9, "ns": 1.0, "us": 1e3, "ms": 1e6, "s": 1e9, "%": 1.0, "": 1.0}
+
+    def val(k):  # bytes / nanoseconds / percent
+        j = h.index(k)
+        return float(r[j].replace(",", "")) * scale.get(units[j], 1.0)
+
+    rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
+    fn = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ncu_traffic.json")
+    db = json.load(open(fn)) if os.path.exists(fn) else {}
+    db[config] = {"kernel": kernel, "dram_bytes_per_launch": int(rd + wr), "read": int(rd), "write": int(wr),
+                  "duration_ms": val("gpu__time_duration.sum") / 1e6,
+                  "tensor_pipe_active": val("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active") / 100.0,
+                  "source_hash": source_hash(), "source": f"ncu --set full --clock-control none, {os.path.basename(path)}"}
+    json.dump(db, open(fn, "w"), indent=1)
+    print(json.dumps(db[config]))
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
     else:
         report(sys.argv[2])
