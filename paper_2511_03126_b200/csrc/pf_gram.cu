@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
       const int gs = stage;  // G chunk pair (adjacent stages, same phase)
       GWAITP(&S.b_full[gs], phase, 3);
       GWAITP(&S.b_full[gs + 1], phase, 3);
-      const uint32_t idY = tc::idesc_bf16_f32(128, ktp, false, false);
+      // Y over N = ktp rounded up to 32 columns: M~ rows ktp.. are zero (the drain writes them), so the
+      // accumulators read whole 32-column chunks without a bound check
+      const uint32_t idY = tc::idesc_bf16_f32(128, (ktp + 31) & ~31, false, false);
       for (int b = 0; b < nb; ++b) {
         const int ab = (int)(wuse & 1u);
         GWAITP(&S.a_full[ab], (wuse >> 1) & 1u, 4);
@@ -717,8 +719,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
             }
           }
         }
-        if (bh == 0)  // K padding columns (kt .. ktp) must be zero
-          for (int j = kt >> 1; j < (ktp >> 1); ++j) tc::tmem_st_x1(tAb + (uint32_t)j, 0u);
+        if (bh == 0)  // K padding columns (kt .. ktp) and the |F|^2 chunk tail (.. ktp rounded to 32) are zero
+          for (int j = kt >> 1; j < (((ktp + 31) & ~31) >> 1); ++j) tc::tmem_st_x1(tAb + (uint32_t)j, 0u);
         PT(15);
         tc::tmem_st_wait();
         tc::fence_before_sync();
@@ -782,6 +784,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
             }
           }
         }
+        {  // zero rows ktp .. ktp rounded to 32 (Y's N padding): <= 16 rows x the K chunks below ktp
+          const int t = row + 128 * half, n = ktp + (t & 15), j = t >> 4;
+          if (j < 3 && 64 * j < ktp && n < ((ktp + 31) & ~31))
+#pragma unroll
+            for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(sM + mt_off(n, j, q)) = make_uint4(0u, 0u, 0u, 0u);
+        }
         if (two && half == 1) {  // block 1: rows 128 + row, columns 128..
           float v[64];
           tc::tmem_ld64(tbase + kColG1 + t_lane, v);
@@ -823,20 +831,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
         // |F|^2 = sum_t W[row, t] Y[row, t]: this half takes 32-column chunks c = half, half + 2, ...
         float ss = 0.f;
         const uint32_t tW = tbase + kColW + (uint32_t)ab * kWCols + t_lane;
-        for (int c = half; 32 * c < ktp; c += 2) {
-          float y[32];
-          tc::tmem_ld32(tbase + kColY + 32u * c + t_lane, y);
-          uint32_t wr[16];
-          tmem_ld16u(tW + 16u * c, wr);
-          const int lim = ktp - 32 * c;  // 16 or >= 32 valid columns
+        {
+          uint64_t ss2 = 0ull;
+          for (int c = half; 32 * c < ktp; c += 2) {  // whole chunks: columns ktp.. are zero
+            float y[32];
+            tc::tmem_ld32(tbase + kColY + 32u * c + t_lane, y);
+            uint32_t wr[16];
+            tmem_ld16u(tW + 16u * c, wr);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            if (2 * q < lim) {
-              const __nv_bfloat162 w2 = *reinterpret_cast<const __nv_bfloat162*>(&wr[q]);
-              ss = fmaf(__low2float(w2), y[2 * q], ss);
-              ss = fmaf(__high2float(w2), y[2 * q + 1], ss);
-            }
+            for (int q = 0; q < 16; ++q)  // bf16 pair -> two floats (exact: bf16 is the top half)
+              ss2 = ffma2(pk2(__uint_as_float(wr[q] << 16), __uint_as_float(wr[q] & 0xffff0000u)),
+                          pk2(y[2 * q], y[2 * q + 1]), ss2);
           }
+          float s_a, s_b;
+          up2(ss2, s_a, s_b);
+          ss = s_a + s_b;
         }
         PT(18);
         float v[kHalfK];
