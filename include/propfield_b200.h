@@ -321,6 +321,35 @@ int pf_shard_pack_results(int64_t n, int32_t p, int32_t nwords, const float* pro
 int pf_shard_unpack_results(int64_t n, int32_t p, int32_t nwords, const int32_t* rows, const void* sent,
                             float* props, int32_t* counts, int32_t* codes, int32_t* mask, void* stream);
 
+/* Fixed-capacity exchange (no host synchronisation; graph-capturable with NCCL collectives): the
+ * send buffer is world blocks of (capacity + 1) float4, row 0 of block o = {count (int bits),
+ * flags (int bits), 0, 0} and rows 1.. the points for owner o ({x, y, z, local index bits});
+ * unused rows are NaN points, which the fused path treats as padding slots (invisible, voxel code
+ * -1, no voxel or partial contribution). An owner receiving more than `capacity` points from this
+ * rank sets flags bit 0 (the surplus is dropped: the caller re-runs with a larger capacity or the
+ * count-exchanging pf_shard_pack). cursor: world i32 scratch; flags: one device i32. After an
+ * equal-split all-to-all of the blocks: */
+int pf_shard_pack_padded(const float* points, int64_t n, const uint32_t* keys, const uint32_t* cuts, int32_t world,
+                         int32_t capacity, int32_t* cursor, void* send, int32_t* flags, void* stream);
+/* received blocks -> (world * capacity, 3) f32 in slot order (padding rows NaN), the input of a
+ * fixed-size pf_fuse_query; */
+int pf_shard_unpad(const void* recv, int32_t world, int32_t capacity, float* xyz, void* stream);
+/* and, after the reverse equal-split all-to-all of pf_shard_pack_results rows (world * capacity
+ * rows, slot order), the rows of the points this rank sent (row 0 counts of `sent`) -> caller order. */
+int pf_shard_unpack_results_padded(int32_t world, int32_t capacity, int32_t p, int32_t nwords, const int32_t* rows,
+                                   const void* sent, float* props, int32_t* counts, int32_t* codes, int32_t* mask,
+                                   void* stream);
+
+/* The per-object reductions over NCCL for C/C++ hosts (integrate.py:133-155 partials +
+ * the voxel grid of point-range sharding): in-place sum of grid_partials (n_grid f32, may be 0) and
+ * partials (n_partials f64) over `comm` (an ncclComm_t) on `stream`. NCCL is resolved at run time
+ * (dlopen libnccl.so.2, preferring the copy already loaded in the process). */
+int pf_allreduce_partials(float* grid_partials, int64_t n_grid, double* partials, int64_t n_partials, void* comm,
+                          void* stream);
+/* A one-rank NCCL communicator (loopback tests of pf_allreduce_partials); destroy with the call below. */
+int pf_nccl_comm_init_single(void** comm);
+int pf_nccl_comm_destroy(void* comm);
+
 /* ---------------------------------------------------------------------------------------------
  * Diagnostics (no reference twin).
  * ------------------------------------------------------------------------------------------- */
@@ -340,8 +369,10 @@ int pf_bench_umma(int32_t n, int32_t ts, int32_t reps, int32_t stores, void* out
  * tile::gather4 (mode 1); writes cycles per SM to out_dev (SMs uint64). */
 int pf_bench_gather(const void* src_bf16, int32_t cells, int32_t stages, int32_t mode, void* out_dev, void* stream);
 int pf_stage_times(float* ms, int32_t n);
-/* tcgen05 FLOPs the last pf_fuse_query on args' workspace issued in the tile kernel: sum over work
- * items of 2 * 128 * ktp * (D + 128); 0 for the SIMT path. Synchronises the stream. */
+/* tcgen05 FLOPs the last pf_fuse_query on args' workspace issued in the tile kernel (ktp = a work
+ * item's taps padded to 16): feature-product kernel 2 * 128 * ktp * (D + 128) per item; Gram kernel
+ * 2 * 128 * ktp * D (+ the taps-128.. block) per item + 2 * 128 * ktp * (128 + ktp) per 128-row
+ * block; 0 for the SIMT path. Synchronises the stream. */
 int pf_tile_executed_flops(const pf_fuse_args_t* args, double* flops, void* stream);
 
 /* C (128,n) f32 = A (128,k) bf16 row-major @ B (k,n) bf16 row-major through the tile kernel's

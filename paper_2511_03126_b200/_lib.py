@@ -140,6 +140,12 @@ SIGNATURES = {
     "pf_shard_xyz": ([_P, _I64, _P, _P], C.c_int),
     "pf_shard_pack_results": ([_I64, _I32, _I32, _P, _P, _P, _P, _P, _P], C.c_int),
     "pf_shard_unpack_results": ([_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "pf_shard_pack_padded": ([_P, _I64, _P, _P, _I32, _I32, _P, _P, _P, _P], C.c_int),
+    "pf_shard_unpad": ([_P, _I32, _I32, _P, _P], C.c_int),
+    "pf_shard_unpack_results_padded": ([_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+    "pf_allreduce_partials": ([_P, _I64, _P, _I64, _P, _P], C.c_int),
+    "pf_nccl_comm_init_single": ([C.POINTER(C.c_void_p)], C.c_int),
+    "pf_nccl_comm_destroy": ([_P], C.c_int),
     "pf_bench_umma": ([_I32, _I32, _I32, _I32, _P, _P], C.c_int),
     "pf_bench_gather": ([_P, _I32, _I32, _I32, _P, _P], C.c_int),
     "pf_stage_times": ([_P, _I32], C.c_int),

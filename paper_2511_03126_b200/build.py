@@ -74,7 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         for s, log in zip(srcs, logs):
             print(f"== {s.name}\n{log}", file=sys.stderr)
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

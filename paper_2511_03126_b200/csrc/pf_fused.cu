@@ -350,9 +350,11 @@ __global__ void __launch_bounds__(kFuseThreads, 3) k_fuse_simt(FuseParams P) {
     }
     if (lane == 0) {
       P.counts[i] = count;
-      const int32_t code = voxel_code(px, py, pz, lo, edge, P.grid);
+      // a NaN point is a padding slot of the fixed-capacity sharded exchange (pf_shard_pack_padded):
+      // it projects nowhere (count 0, zero outputs), has voxel code -1 and no voxel contribution
+      const int32_t code = isnan(px) ? -1 : voxel_code(px, py, pz, lo, edge, P.grid);
       P.codes[i] = code;
-      if (do_vox) {
+      if (do_vox && code >= 0) {
         float rho = prop[0];
 #pragma unroll
         for (int pp = 1; pp < kMaxP; ++pp) rho = P.density_col == pp ? prop[pp] : rho;
@@ -361,12 +363,14 @@ __global__ void __launch_bounds__(kFuseThreads, 3) k_fuse_simt(FuseParams P) {
         if (atomicAdd(P.grid_partials + cells3 + code, 1.0f) == 0.0f && P.vox_list)
           P.vox_list[P.vox_base + atomicAdd(P.vox_count, 1)] = code;
       }
-      pm_sum += pm;
-      pmx += (double)pm * px;
-      pmy += (double)pm * py;
-      pmz += (double)pm * pz;
-      featured += count > 0 ? 1.0 : 0.0;
-      pairs += count;
+      if (code >= 0) {  // padding slots (NaN coordinates) stay out of the integrate partials
+        pm_sum += pm;
+        pmx += (double)pm * px;
+        pmy += (double)pm * py;
+        pmz += (double)pm * pz;
+        featured += count > 0 ? 1.0 : 0.0;
+        pairs += count;
+      }
     }
   }
   // ---- block + grid reduction of the integrate_mass partials ---------------------------------------

@@ -221,6 +221,94 @@ __global__ void k_shard_unpack_results(int64_t n, int p, int nwords, const int32
   }
 }
 
+// ---- fixed-capacity exchange (no host synchronisation) ---------------------------------------------
+// send / recv blocks: W x (C + 1) float4; row 0 of block o = {count (int bits), flags, 0, 0}, rows
+// 1.. the points for owner o. Unused rows are NaN points: the fused path treats a NaN point as a
+// padding slot (invisible, voxel code -1, no voxel / partial contribution), so the receiver runs a
+// fixed W*C-point pass whose size the host knows without reading the counts back.
+__global__ void __launch_bounds__(256) k_shard_route_padded(const float* __restrict__ p, int64_t n,
+                                                            const uint32_t* __restrict__ keys,
+                                                            const uint32_t* __restrict__ cuts, int world, int cap,
+                                                            int32_t* __restrict__ cursor, float4* __restrict__ send,
+                                                            int32_t* __restrict__ flags) {
+  __shared__ uint32_t s_cut[kMaxWorld + 1];
+  __shared__ int32_t s_cnt[kMaxWorld], s_base[kMaxWorld];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int q = tid; q <= world; q += blockDim.x) s_cut[q] = cuts[q];
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + tid;
+    const bool valid = i < n;
+    if (tid < world) s_cnt[tid] = 0;
+    __syncthreads();
+    const int r = valid ? owner_of(keys[i], s_cut, world) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, r);
+    const int leader = __ffs(peers) - 1;
+    int off = 0;
+    if (valid && lane == leader) off = atomicAdd(&s_cnt[r], __popc(peers));
+    off = __shfl_sync(0xffffffffu, off, leader) + __popc(peers & ((1u << lane) - 1u));
+    __syncthreads();
+    if (tid < world) {
+      const int32_t c = s_cnt[tid];
+      s_base[tid] = c ? atomicAdd(cursor + tid, c) : 0;
+    }
+    __syncthreads();
+    if (valid) {
+      const int slot = s_base[r] + off;
+      if (slot < cap)
+        send[(int64_t)r * (cap + 1) + 1 + slot] = make_float4(__ldg(p + 3 * i), __ldg(p + 3 * i + 1),
+                                                              __ldg(p + 3 * i + 2), __int_as_float((int32_t)i));
+      else
+        atomicOr(flags, 1);  // more points for one owner than the capacity: dropped, flagged
+    }
+    __syncthreads();
+  }
+}
+
+// per-block header (count, flags) and NaN padding of the unused rows
+__global__ void k_shard_pad_finish(float4* __restrict__ send, const int32_t* __restrict__ cursor, int world,
+                                   int cap, const int32_t* __restrict__ flags) {
+  const float nan = __int_as_float(0x7fc00000);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)world * (cap + 1);
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(e / (cap + 1)), row = (int)(e % (cap + 1));
+    const int cnt = min(cursor[o], cap);
+    if (row == 0) send[e] = make_float4(__int_as_float(cnt), __int_as_float(*flags), 0.f, 0.f);
+    else if (row - 1 >= cnt) send[e] = make_float4(nan, nan, nan, __int_as_float(-1));
+  }
+}
+
+// received blocks -> (W*C, 3) points in slot order (NaN rows stay NaN: padding)
+__global__ void k_shard_unpad(const float4* __restrict__ recv, int world, int cap, float* __restrict__ xyz) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)world * cap;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(e / cap), c = (int)(e % cap);
+    const float4 q = recv[(int64_t)s * (cap + 1) + 1 + c];
+    xyz[3 * e] = q.x;
+    xyz[3 * e + 1] = q.y;
+    xyz[3 * e + 2] = q.z;
+  }
+}
+
+// the owner's result rows come back in slot order: row (o, c) belongs to the local point whose
+// index the sent float4 (o, c) carried, for c < the block's count
+__global__ void k_shard_unpack_results_padded(int world, int cap, int p, int nwords, const int32_t* __restrict__ rows,
+                                              const float4* __restrict__ sent, float* __restrict__ props,
+                                              int32_t* __restrict__ counts, int32_t* __restrict__ codes,
+                                              int32_t* __restrict__ mask) {
+  const int w = p + 2 + nwords;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)world * cap;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(e / cap), c = (int)(e % cap);
+    if (c >= __float_as_int(sent[(int64_t)o * (cap + 1)].x)) continue;
+    const int64_t i = __float_as_int(sent[(int64_t)o * (cap + 1) + 1 + c].w);
+    const int32_t* r = rows + e * w;
+    for (int q = 0; q < p; ++q) props[i * p + q] = __int_as_float(r[q]);
+    counts[i] = r[p];
+    codes[i] = r[p + 1];
+    for (int q = 0; q < nwords; ++q) mask[i * nwords + q] = r[p + 2 + q];
+  }
+}
+
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 }  // namespace
@@ -292,6 +380,44 @@ int pf_shard_unpack_results(int64_t n, int32_t p, int32_t nwords, const int32_t*
                                                                   reinterpret_cast<const float4*>(sent), props,
                                                                   counts, codes, mask);
   return check_launch("shard_unpack_results");
+}
+
+int pf_shard_pack_padded(const float* points, int64_t n, const uint32_t* keys, const uint32_t* cuts, int32_t world,
+                         int32_t capacity, int32_t* cursor, void* send, int32_t* flags, void* stream) {
+  if (world < 1 || world > kMaxWorld) return set_error(PF_ERR_VALUE, "world size must be in [1, 64]");
+  if (n < 0 || n > INT32_MAX) return set_error(PF_ERR_VALUE, "point count must be in [0, 2^31)");
+  if (capacity < 1) return set_error(PF_ERR_VALUE, "capacity must be >= 1");
+  if (!cursor || !cuts || !send || !flags) return set_error(PF_ERR_VALUE, "shard_pack_padded: null buffer");
+  cudaMemsetAsync(cursor, 0, sizeof(int32_t) * world, S(stream));
+  cudaMemsetAsync(flags, 0, sizeof(int32_t), S(stream));
+  if (n > 0) {
+    if (!points || !keys) return set_error(PF_ERR_VALUE, "shard_pack_padded: null buffer");
+    k_shard_route_padded<<<grid_for(n, 256), 256, 0, S(stream)>>>(points, n, keys, cuts, world, capacity, cursor,
+                                                                 reinterpret_cast<float4*>(send), flags);
+    if (int rc = check_launch("shard_route_padded")) return rc;
+  }
+  k_shard_pad_finish<<<grid_for((int64_t)world * (capacity + 1), 256), 256, 0, S(stream)>>>(
+      reinterpret_cast<float4*>(send), cursor, world, capacity, flags);
+  return check_launch("shard_pad_finish");
+}
+
+int pf_shard_unpad(const void* recv, int32_t world, int32_t capacity, float* xyz, void* stream) {
+  if (world < 1 || world > kMaxWorld || capacity < 1) return set_error(PF_ERR_VALUE, "shard_unpad: bad shape");
+  if (!recv || !xyz) return set_error(PF_ERR_VALUE, "shard_unpad: null buffer");
+  k_shard_unpad<<<grid_for((int64_t)world * capacity, 256), 256, 0, S(stream)>>>(reinterpret_cast<const float4*>(recv),
+                                                                                world, capacity, xyz);
+  return check_launch("shard_unpad");
+}
+
+int pf_shard_unpack_results_padded(int32_t world, int32_t capacity, int32_t p, int32_t nwords, const int32_t* rows,
+                                   const void* sent, float* props, int32_t* counts, int32_t* codes, int32_t* mask,
+                                   void* stream) {
+  if (world < 1 || world > kMaxWorld || capacity < 1) return set_error(PF_ERR_VALUE, "unpack_results_padded: bad shape");
+  if (!rows || !sent || !props || !counts || !codes || !mask)
+    return set_error(PF_ERR_VALUE, "shard_unpack_results_padded: null buffer");
+  k_shard_unpack_results_padded<<<grid_for((int64_t)world * capacity, 256), 256, 0, S(stream)>>>(
+      world, capacity, p, nwords, rows, reinterpret_cast<const float4*>(sent), props, counts, codes, mask);
+  return check_launch("shard_unpack_results_padded");
 }
 
 }  // extern "C"

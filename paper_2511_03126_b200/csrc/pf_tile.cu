@@ -554,11 +554,12 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
   __syncthreads();
   const int nmixed = s_nmixed, nexact = s_nexact;
   uint32_t w0 = s_full[0], w1 = s_full[1];
+  const bool live = valid && !isnan(p.x);  // NaN point: a padding slot (pf_shard_pack_padded)
   const float dx = p.x - 0.5f * (lo[0] + hi[0]), dy = p.y - 0.5f * (lo[1] + hi[1]), dz = p.z - 0.5f * (lo[2] + hi[2]);
   uint64_t wm = 0ull, seen = 0ull;  // this point's MIXED verdicts; MIXED views this warp saw visible
   for (int l = 0; l < nmixed; ++l) {
     const int v = s_list[l];
-    const int s = valid ? affine_visible(saff[v], P.depth, dx, dy, dz, eps_f) : kInvisible;
+    const int s = live ? affine_visible(saff[v], P.depth, dx, dy, dz, eps_f) : kInvisible;
     if (P.dbg && valid) {
       atomicAdd(P.dbg + 16 * 1000 + 7, 1ull);
       if (s == kAmbiguous) atomicAdd(P.dbg + 16 * 1000 + 8, 1ull);
@@ -586,14 +587,17 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
   for (int l = nmixed; l < nmixed + nexact; ++l) {
     const int v = s_list[l];
     TapF t;
-    const bool vis = valid && point_visible(sv[v], sbound[v], P.views[v], P.depth, p, P.eps, eps_f, t);
+    const bool vis = live && point_visible(sv[v], sbound[v], P.views[v], P.depth, p, P.eps, eps_f, t);
     if (vis) {
       if (v < 32) w0 |= 1u << v;
       else w1 |= 1u << (v - 32);
     }
     window_reduce(vis, t, wx0, wy0, wx1, wy1, v, lane);
   }
-  const int32_t code = valid ? voxel_code_fast(p, P.vox, P.grid) : -1;
+  // NaN point = padding slot (pf_shard_pack_padded): no view, voxel code -1 (the tile box above
+  // already ignores it: fminf / fmaxf drop NaN)
+  if (!live) w0 = w1 = 0u;
+  const int32_t code = live ? voxel_code_fast(p, P.vox, P.grid) : -1;
   if (valid)
     *reinterpret_cast<uint4*>(P.srec + jpt) =
         make_uint4(w0, w1, (uint32_t)(__popc(w0) + __popc(w1)), (uint32_t)code);

@@ -976,17 +976,18 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         const float pm = (S.xsum[0][5][row] + S.xsum[1][5][row]) * rs;
         const float4 p = pcur;
         *(reinterpret_cast<float4*>(P.srec + jpt) + 1) = make_float4(prop[0], prop[1], prop[2], prop[3]);
-        if (P.grid_partials) {
+        if (P.grid_partials && (int32_t)rec.y >= 0) {  // code -1: a padding slot
           const int32_t code = (int32_t)rec.y;
           const int dc = P.density_col;  // selects, not a dynamic index (keeps prop[] in registers)
           const float rho = dc == 0 ? prop[0] : (dc == 1 ? prop[1] : (dc == 2 ? prop[2] : prop[3]));
           atomicAdd(P.grid_partials + code, rho);
           atomicAdd(P.grid_partials + P.cells3 + code, 1.0f);
         }
-        pm_sum += pm;
-        pmx = fmaf(pm, p.x, pmx);
-        pmy = fmaf(pm, p.y, pmy);
-        pmz = fmaf(pm, p.z, pmz);
+        const bool live = (int32_t)rec.y >= 0;  // a padding slot (NaN point): no partial contribution
+        pm_sum += live ? pm : 0.f;
+        pmx = fmaf(live ? pm : 0.f, live ? p.x : 0.f, pmx);
+        pmy = fmaf(live ? pm : 0.f, live ? p.y : 0.f, pmy);
+        pmz = fmaf(live ? pm : 0.f, live ? p.z : 0.f, pmz);
         featured_n += featured ? 1.f : 0.f;
         pairs += (float)count;
       }

@@ -132,8 +132,9 @@ class DeviceShardOps:
         n = recv.shape[0]
         xyz = t.empty((n, 3), dtype=t.float32, device=recv.device)
         _lib.call("pf_shard_xyz", recv.data_ptr(), n, xyz.data_ptr(), self._st())
-        if self._bufs is None or self._bufs.n != n:
-            self._bufs = FuseBuffers(n, self.views, self.tables, self.grid, device=recv.device)
+        if self._bufs is None or self._bufs.capacity < n:  # capacity: a new point count reuses them
+            cap = n if self._bufs is None else max(n, int(self._bufs.capacity * 1.25))
+            self._bufs = FuseBuffers(max(cap, 1), self.views, self.tables, self.grid, device=recv.device)
         res = fuse_and_query(xyz, self.views, self.tables, temperature=self.temperature, epsilon=self.epsilon,
                              grid=self.grid, lo_hi=lo_hi, buffers=self._bufs, reduce=True)
         return res
@@ -143,12 +144,61 @@ class DeviceShardOps:
         from .device import torch
 
         t = torch()
-        b = res.buffers
-        n, p, nwords = b.n, b.props.shape[1], b.mask_bits.shape[1]
-        rows = t.empty((n, p + 2 + nwords), dtype=t.int32, device=b.props.device)
-        _lib.call("pf_shard_pack_results", n, p, nwords, b.props.data_ptr(), b.counts.data_ptr(),
-                  b.codes.data_ptr(), b.mask_bits.data_ptr(), rows.data_ptr(), self._st())
+        props = res.props
+        n, p, nwords = props.shape[0], props.shape[1], res.mask_bits.shape[1]
+        rows = t.empty((n, p + 2 + nwords), dtype=t.int32, device=props.device)
+        _lib.call("pf_shard_pack_results", n, p, nwords, props.data_ptr(), res.counts.data_ptr(),
+                  res.codes.data_ptr(), res.mask_bits.data_ptr(), rows.data_ptr(), self._st())
         return rows
+
+    # ---- fixed-capacity exchange (no host synchronisation) ----------------------------------------
+    def pack_padded(self, points, keys, cuts, world, capacity):
+        """(world, capacity + 1, 4) f32 blocks: row 0 = {count, flags} bits, then the owner's points,
+        NaN padding (pf_shard_pack_padded)."""
+        from . import _lib
+        from .device import torch
+
+        t = torch()
+        n = points.shape[0]
+        send = t.empty((world, capacity + 1, 4), dtype=t.float32, device=points.device)
+        cursor = t.empty(world, dtype=t.int32, device=points.device)
+        flags = t.empty(1, dtype=t.int32, device=points.device)
+        _lib.call("pf_shard_pack_padded", points.data_ptr(), n, keys.data_ptr(), cuts.data_ptr(), world, capacity,
+                  cursor.data_ptr(), send.data_ptr(), flags.data_ptr(), self._st())
+        return send, flags
+
+    def unpad(self, recv, world, capacity):
+        from . import _lib
+        from .device import torch
+
+        t = torch()
+        xyz = t.empty((world * capacity, 3), dtype=t.float32, device=recv.device)
+        _lib.call("pf_shard_unpad", recv.data_ptr(), world, capacity, xyz.data_ptr(), self._st())
+        return xyz
+
+    def fuse_points(self, xyz, lo_hi):
+        """The fused path on (m, 3) points (NaN rows: padding slots)."""
+        from .fused import FuseBuffers, fuse_and_query
+
+        n = xyz.shape[0]
+        if self._bufs is None or self._bufs.capacity < n:
+            self._bufs = FuseBuffers(max(n, 1), self.views, self.tables, self.grid, device=xyz.device)
+        return fuse_and_query(xyz, self.views, self.tables, temperature=self.temperature, epsilon=self.epsilon,
+                              grid=self.grid, lo_hi=lo_hi, buffers=self._bufs, reduce=True)
+
+    def unpack_results_padded(self, rows, sent, n, p, nwords, world, capacity):
+        from . import _lib
+        from .device import torch
+
+        t = torch()
+        dev = rows.device
+        out = {"props": t.zeros((n, p), dtype=t.float32, device=dev), "counts": t.zeros(n, dtype=t.int32, device=dev),
+               "codes": t.full((n,), -1, dtype=t.int32, device=dev),
+               "mask_bits": t.zeros((n, nwords), dtype=t.int32, device=dev)}
+        _lib.call("pf_shard_unpack_results_padded", world, capacity, p, nwords, rows.data_ptr(), sent.data_ptr(),
+                  out["props"].data_ptr(), out["counts"].data_ptr(), out["codes"].data_ptr(),
+                  out["mask_bits"].data_ptr(), self._st())
+        return out
 
     def unpack_results(self, rows, sent, n, p, nwords):
         from . import _lib
@@ -169,11 +219,17 @@ class ShardedResult:
     """Outputs of one cell-sharded pass on one rank: this rank's input points in caller order, the
     global (all-reduced) partials and voxel mass."""
 
-    def __init__(self, out, partials, mass, lo_hi, k, received):
+    def __init__(self, out, partials, mass, lo_hi, k, received, overflow=None):
         self.props, self.counts, self.codes, self.mask_bits = (out["props"], out["counts"], out["codes"],
                                                                out["mask_bits"])
         self.partials, self.mass, self.lo_hi, self.k = partials, mass, lo_hi, k
-        self.received = received  # points this rank computed (owned cells)
+        self.received = received  # points this rank computed (owned cells); a device count when padded
+        self._overflow = overflow  # padded exchange: device scalar, > 0 if any rank dropped points
+
+    def overflowed(self) -> bool:
+        """Fixed-capacity exchange only: did some owner get more points than the capacity from some
+        rank (results then incomplete: re-run with a larger capacity)? Reads one device value."""
+        return bool(self._overflow is not None and float(self._overflow.item()) > 0.0)
 
     def mass_kg(self) -> float:
         return float(self.mass[0].item())
@@ -224,6 +280,54 @@ def cell_sharded_steps(points, rank: int, world: int, ops, *, k: int, p: int, nw
     yield ("alltoallv", back, rows, send_splits, recv_splits)
     out = ops.unpack_results(back, send, n, p, nwords)
     return ShardedResult(out, red[: k + 6], red[k + 6 :], lo_hi, k, sum(recv_splits))
+
+
+def padded_capacity(n_local: int, world: int, slack: float = 1.25) -> int:
+    """Rows per peer block of the fixed-capacity exchange: this rank's share for one owner with
+    slack (the global cuts balance owners; a rank's points spread over them unless its input
+    range is spatially sorted — then the exchange flags an overflow and the caller re-runs)."""
+    return max(64, int(slack * n_local / max(1, world)) + 64)
+
+
+def cell_sharded_steps_padded(points, rank: int, world: int, ops, *, k: int, p: int, nwords: int,
+                              capacity: int, lo_hi=None):
+    """The cell-range protocol with a fixed-capacity exchange: every collective has host-known
+    sizes and nothing is read back to the host, so the whole step can be captured in a CUDA graph.
+    `capacity` rows per peer block (padded_capacity); `lo_hi` (6,) f64 device tensor = a fixed voxel
+    domain shared by all ranks (drops the bbox all-reduce), None = the union of the ranks' bboxes.
+    Every rank runs the fused pass on world * capacity points (NaN padding slots are inert)."""
+    import torch as t
+
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} / world {world}")
+    n = int(points.shape[0])
+    # 1. shared voxel domain (skipped for a fixed domain)
+    if lo_hi is None:
+        lo_hi = ops.bbox(points)
+        lo_hi[3:].neg_()
+        yield ("allreduce", lo_hi, "min")
+        lo_hi[3:].neg_()
+    # 2. cell keys + global histogram -> identical cuts on every rank
+    keys, hist = ops.keys(points, lo_hi)
+    yield ("allreduce", hist, "sum")
+    cuts = ops.cuts(hist, world)
+    # 3. points to their owners: equal-split all-to-all of fixed blocks, counts in-band
+    send, flags = ops.pack_padded(points, keys, cuts, world, capacity)
+    recv = t.empty_like(send)
+    yield ("alltoall", recv, send)
+    xyz = ops.unpad(recv, world, capacity)
+    # 4. fused pass on world * capacity slots; partials + owned-voxel mass + the overflow flag in one
+    #    reduction (the flag as a double: any rank's dropped points make the sum > 0)
+    res = ops.fuse_points(xyz, lo_hi)
+    red = t.cat([res.partials.reshape(-1), res.mass.reshape(-1), flags.to(t.float64)]).to(t.float64)
+    yield ("allreduce", red, "sum")
+    # 5. result rows back in slot order, equal splits
+    rows = ops.pack_results(res).reshape(world, capacity, -1)
+    back = t.empty_like(rows)
+    yield ("alltoall", back, rows)
+    out = ops.unpack_results_padded(back.reshape(world * capacity, -1), send, n, p, nwords, world, capacity)
+    received = res.counts.shape[0]  # slots (device-side count of real points: (codes >= 0).sum())
+    return ShardedResult(out, red[: k + 6], red[k + 6 : k + 8], lo_hi, k, received, overflow=red[k + 8])
 
 
 def run_dist(gen, group=None):

@@ -61,8 +61,10 @@ class QueryTables:
 
 
 class FuseBuffers:
-    """Preallocated outputs + workspace for repeated calls on same-shaped inputs (no allocation in
-    the hot loop, CUDA-graph capturable)."""
+    """Preallocated outputs + workspace for repeated calls (no allocation in the hot loop, CUDA-graph
+    capturable). `n` is a CAPACITY: any call with at most n points reuses them (outputs are the
+    leading rows); the voxel grid is allocated once and never reallocated or re-zeroed for a new
+    point count."""
 
     def __init__(self, n, views: ViewSet, tables: QueryTables, grid: int, *, features=False,
                  sims=False, weights=False, device=None):
@@ -70,6 +72,7 @@ class FuseBuffers:
         dev = views.device if device is None else device
         k, p, nv = tables.k, tables.p, views.nviews
         self.n, self.grid = int(n), int(grid)
+        self.capacity = self.n
         nwords = (nv + 31) // 32
         self.counts = t.empty(n, dtype=t.int32, device=dev)
         self.mask_bits = t.empty((n, nwords), dtype=t.int32, device=dev)
@@ -147,15 +150,19 @@ class FusedResult:
     buffers: FuseBuffers
     nviews: int
     k: int
+    n: int = -1  # points of this call (<= buffers.capacity); -1: the whole capacity
 
-    counts = property(lambda self: self.buffers.counts)
-    mask_bits = property(lambda self: self.buffers.mask_bits)
-    props = property(lambda self: self.buffers.props)
-    codes = property(lambda self: self.buffers.codes)
+    def _rows(self, x):
+        return x if (x is None or self.n < 0 or self.n == x.shape[0]) else x[: self.n]
+
+    counts = property(lambda self: self._rows(self.buffers.counts))
+    mask_bits = property(lambda self: self._rows(self.buffers.mask_bits))
+    props = property(lambda self: self._rows(self.buffers.props))
+    codes = property(lambda self: self._rows(self.buffers.codes))
     partials = property(lambda self: self.buffers.partials)
-    features = property(lambda self: self.buffers.features)
-    sims = property(lambda self: self.buffers.sims)
-    weights = property(lambda self: self.buffers.weights)
+    features = property(lambda self: self._rows(self.buffers.features))
+    sims = property(lambda self: self._rows(self.buffers.sims))
+    weights = property(lambda self: self._rows(self.buffers.weights))
     lo_hi = property(lambda self: self.buffers.lo_hi)
     mass = property(lambda self: self.buffers.mass)  # (2,) f64 {mass_kg, occupied voxels} after finalize()
 
@@ -240,8 +247,9 @@ def fuse_and_query(points, views: ViewSet, tables: QueryTables, *, temperature: 
                               weights=write_weights, device=dev)
     elif reset:
         buffers.reset()
-    if buffers.n != n or buffers.grid != grid:
-        raise BundleStructureError("buffers were sized for a different point count / grid")
+    if n > buffers.capacity or buffers.grid != grid:
+        raise BundleStructureError(f"buffers hold {buffers.capacity} points on a {buffers.grid}^3 grid; "
+                                   f"this call has {n} points on {grid}^3")
     st = stream_handle()
     if lo_hi is None:
         if n == 0:
@@ -265,7 +273,7 @@ def fuse_and_query(points, views: ViewSet, tables: QueryTables, *, temperature: 
         flags |= _lib.PF_FUSE_FEATURE_KERNEL
     args = _make_args(pts, n, views, tables, temperature, epsilon, grid, buffers, flags)
     _lib.call("pf_fuse_query", args, st)
-    res = FusedResult(buffers, views.nviews, tables.k)
+    res = FusedResult(buffers, views.nviews, tables.k, n)
     # the grid now holds this call's voxels until finalize() re-zeroes the touched ones (sparse) or
     # marks it for a full reset (dense): an un-finalised grid must be zeroed by the next reset()
     buffers.grid_clean = False

@@ -134,6 +134,63 @@ class CpuShardOps:
         return {k: torch.from_numpy(v) for k, v in out.items()}
 
 
+class CpuPaddedOps(CpuShardOps):
+    """numpy restatement of the fixed-capacity exchange (pf_shard_pack_padded / unpad /
+    unpack_results_padded): blocks of capacity + 1 rows, row 0 = {count, flags} bits, NaN padding."""
+
+    def pack_padded(self, points, keys, cuts, world, capacity):
+        owner = np.searchsorted(cuts.numpy()[1:world], keys.numpy(), side="right")
+        p = points.numpy()
+        send = np.full((world, capacity + 1, 4), np.nan, dtype=np.float32)
+        send[:, :, 3] = np.array(-1, np.int32).view(np.float32)
+        flags = 0
+        for o in range(world):
+            idx = np.nonzero(owner == o)[0]
+            if idx.size > capacity:
+                flags, idx = 1, idx[:capacity]
+            send[o, 1 : 1 + idx.size, :3] = p[idx]
+            send[o, 1 : 1 + idx.size, 3] = idx.astype(np.int32).view(np.float32)
+            send[o, 0, :] = 0.0
+            send[o, 0, 0] = np.array(idx.size, np.int32).view(np.float32)
+        for o in range(world):
+            send[o, 0, 1] = np.array(flags, np.int32).view(np.float32)
+        return torch.from_numpy(send), torch.tensor([flags], dtype=torch.int32)
+
+    def unpad(self, recv, world, capacity):
+        return recv[:, 1:, :3].reshape(world * capacity, 3).contiguous()
+
+    def fuse_points(self, xyz, lo_hi):
+        x = xyz.numpy()
+        real = ~np.isnan(x[:, 0])
+        d = super().fuse(torch.from_numpy(np.concatenate([x[real], np.zeros((int(real.sum()), 1), np.float32)], 1)),
+                         lo_hi)
+        m = x.shape[0]
+        out = {"props": np.zeros((m, d["props"].shape[1]), np.float32), "counts": np.zeros(m, np.int32),
+               "codes": np.full(m, -1, np.int32), "mask": np.zeros((m, d["mask"].shape[1]), np.int32)}
+        for key in out:
+            out[key][real] = d[key]
+        out.update(partials=d["partials"], mass=d["mass"], voxels=d["voxels"])
+        self.real_slots = int(real.sum())
+        return _Res(out)
+
+    def pack_results(self, res):
+        return CpuShardOps.pack_results(self, res.d)
+
+    def unpack_results_padded(self, rows, sent, n, p, nwords, world, capacity):
+        r = rows.numpy().reshape(world, capacity, -1)
+        s = sent.numpy()
+        out = {"props": np.zeros((n, p), np.float32), "counts": np.zeros(n, np.int32),
+               "codes": np.full(n, -1, np.int32), "mask_bits": np.zeros((n, nwords), np.int32)}
+        for o in range(world):
+            cnt = int(s[o, 0, 0:1].view(np.int32)[0])
+            idx = s[o, 1 : 1 + cnt, 3].view(np.int32)
+            out["props"][idx] = r[o, :cnt, :p].view(np.float32)
+            out["counts"][idx] = r[o, :cnt, p]
+            out["codes"][idx] = r[o, :cnt, p + 1]
+            out["mask_bits"][idx] = r[o, :cnt, p + 2 :]
+        return {k: torch.from_numpy(v) for k, v in out.items()}
+
+
 class _Res:
     """Adapter: CpuShardOps.fuse returns a dict; the protocol reads .partials / .mass."""
 
@@ -159,6 +216,17 @@ def _steps(wl, rank, world):
     return gen, ops
 
 
+def _steps_padded(wl, rank, world, capacity, fixed_domain):
+    lo, hi = pdist.shard_range(wl.cfg.n, rank, world)
+    pts = torch.from_numpy(np.ascontiguousarray(wl.points[lo:hi]))
+    ops = CpuPaddedOps(wl)
+    p64 = wl.points.astype(np.float64)
+    lo_hi = torch.from_numpy(np.concatenate([p64.min(0), p64.max(0)])) if fixed_domain else None
+    gen = pdist.cell_sharded_steps_padded(pts, rank, world, ops, k=wl.text.shape[0], p=wl.values.shape[1],
+                                          nwords=(wl.cfg.nviews + 31) // 32, capacity=capacity, lo_hi=lo_hi)
+    return gen, ops
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -176,6 +244,19 @@ def _worker(rank, world, port, q):
         res = pdist.run_dist(gen)
         q.put((rank, res.props.numpy(), res.counts.numpy(), res.codes.numpy(), res.mask_bits.numpy(),
                res.partials.numpy(), res.mass.numpy(), res.received, ops.last_voxels))
+    finally:
+        dist.destroy_process_group()
+
+
+def _worker_padded(rank, world, port, q, capacity, fixed_domain):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wl = workloads.generate("mini")
+        gen, ops = _steps_padded(wl, rank, world, capacity, fixed_domain)
+        res = pdist.run_dist(gen)
+        q.put((rank, res.props.numpy(), res.counts.numpy(), res.codes.numpy(), res.mask_bits.numpy(),
+               res.partials.numpy(), res.mass.numpy(), ops.real_slots, ops.last_voxels, res.overflowed()))
     finally:
         dist.destroy_process_group()
 
@@ -264,3 +345,50 @@ def test_cuts_balanced_and_edge_cases():
     c = cuts_ref(one, 4)  # all points in one cell: exactly one rank owns it
     prefix = np.concatenate([[0], np.cumsum(one)])
     assert sorted((prefix[c[1:]] - prefix[c[:-1]]).tolist()) == [0, 0, 0, 5]
+
+
+def _spawn(target, world, extra=()):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q, *extra)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort(key=lambda r: r[0])
+    return res
+
+
+@pytest.mark.parametrize("world,fixed", [(2, False), (3, True)])
+def test_padded_exchange_gloo_matches_single_process(world, fixed):
+    """Fixed-capacity exchange (no host synchronisation, counts in-band, NaN padding slots), with the
+    union-of-bboxes or a fixed voxel domain: identical results to the single-process oracle."""
+    wl = workloads.generate("mini")
+    cap = pdist.padded_capacity(wl.cfg.n // world, world)
+    res = _spawn(_worker_padded, world, (cap, fixed))
+    assert not any(r[9] for r in res)
+    _check(wl, [r[:9] for r in res], world)
+
+
+def test_padded_exchange_overflow_is_flagged():
+    """A capacity below one owner's share: every rank sees the overflow flag (reduced in-band)."""
+    wl = workloads.generate("mini")
+    world = 2
+    steps = [_steps_padded(wl, r, world, 16, False) for r in range(world)]
+    results = pdist.run_loopback([g for g, _ in steps])
+    assert all(r.overflowed() for r in results)
+
+
+@pytest.mark.parametrize("world", [1, 4])
+def test_padded_exchange_loopback_matches_single_process(world):
+    wl = workloads.generate("mini")
+    cap = pdist.padded_capacity(wl.cfg.n // world, world)
+    steps = [_steps_padded(wl, r, world, cap, True) for r in range(world)]
+    results = pdist.run_loopback([g for g, _ in steps])
+    per_rank = [(r, x.props.numpy(), x.counts.numpy(), x.codes.numpy(), x.mask_bits.numpy(), x.partials.numpy(),
+                 x.mass.numpy(), ops.real_slots, ops.last_voxels) for r, (x, (_, ops)) in enumerate(zip(results, steps))]
+    assert not any(x.overflowed() for x in results)
+    _check(wl, per_rank, world)
