@@ -68,6 +68,9 @@ CONFIGS = {
                         bf16=True, k=40, grid=32, seed=3),
     "mini_fib40": Config("mini_fib40", n=1500, fib=40, radius=1.5, image=96, fmap=(12, 12, 128),
                          k=8, grid=16, seed=5),
+    # config 4's code path (object-wise batch) at test size: 6 mini objects
+    "mini_batch": Config("mini_batch", n=2000, rings=((8, 20.0),), image=128, fmap=(16, 16, 64), k=8, grid=32,
+                         objects=6),
     "pr1": Config("pr1", n=20_000, rings=((8, 20.0),), image=256, fmap=(32, 32, 512), k=16, grid=64),
     "c2": Config("c2", n=200_000, rings=((8, 10.0), (8, 40.0)), image=512, fmap=(37, 37, 768),
                  k=32, grid=128),
