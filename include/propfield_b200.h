@@ -172,6 +172,9 @@ int pf_integrate_partials(const double* weights, int64_t n, int32_t k, const flo
 #define PF_FUSE_SKIP_VOXELS 8u     /* do not touch the voxel grid (codes still written)    */
 #define PF_FUSE_FORCE_SIMT 16u     /* use the SIMT gather even where the tensor path applies */
 #define PF_FUSE_PREPARED 32u       /* workspace already holds pf_fuse_prepare's tables: skip it */
+#define PF_FUSE_DETERMINISTIC 128u /* tile path: stable radix sort of the points (run-to-run identical
+                                      tiles and results; the default counting sort orders the points of
+                                      one sort cell differently per run, a ~1e-6 effect on properties) */
 #define PF_FUSE_FEATURE_KERNEL 64u /* bf16 maps: the feature-product tile kernel (k_tile_ws) instead
                                       of the Gram kernel (always taken with PF_FUSE_WRITE_FEATURES) */
 

@@ -31,6 +31,7 @@ PF_FUSE_SKIP_VOXELS = 8
 PF_FUSE_FORCE_SIMT = 16
 PF_FUSE_PREPARED = 32
 PF_FUSE_FEATURE_KERNEL = 64
+PF_FUSE_DETERMINISTIC = 128
 
 # pf_view_t (160 bytes)
 VIEW_DTYPE = np.dtype(

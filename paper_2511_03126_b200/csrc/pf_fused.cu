@@ -611,6 +611,7 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     const tile::TileLayout L = tile::tile_layout(a->n, a->nviews, cells, kpadg, a->d, x3, tr);
     tile::TileParams T{};
     T.tr = tr;
+    T.deterministic = (a->flags & PF_FUSE_DETERMINISTIC) ? 1 : 0;
     T.sub1_rows = tr == tile::kGramTile ? 128 : tile::kSubRows;
     T.spts = reinterpret_cast<const float4*>(ws + L.spts);
     T.inv = reinterpret_cast<const int32_t*>(ws + L.inv);

@@ -14,8 +14,9 @@
 // integrate.py:133-155).
 //
 // Kernels (this file; the tensor-core tile kernel is pf_tile_ws.cu):
-//   k_sort_keys / k_scan_* / k_sort_scatter — counting sort of the points by a 21-bit Hilbert key of
-//       a 128^3 grid over the bbox (spatial coherence of tiles; no library sort);
+//   k_sort_keys + CUB DeviceRadixSort::SortPairs + k_sort_gather — stable sort of the points by a
+//       21-bit (24-bit from 4M points) Hilbert key of a 128^3 (256^3) grid over the bbox (spatially
+//       coherent tiles; the stable sort makes them deterministic);
 //   k_tile_prep — per tile: each view is first classified for the box of every 32 points (OFF:
 //       occluded or off-image for every point; FULL: visible for every point; MIXED), rigorously,
 //       from the box corners and the stored depths under the box's pixel footprint. Only MIXED views get the
@@ -32,6 +33,8 @@
 #include "pf_common.cuh"
 #include "pf_tc.cuh"
 #include "pf_tile.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
 #include "pf_tile_dev.cuh"
 
 namespace pf {
@@ -77,7 +80,7 @@ __device__ __forceinline__ uint32_t hilbert3(uint32_t x, uint32_t y, uint32_t z,
 
 template <int BITS>  // compile-time grid order: the Hilbert loops fully unrolled
 __global__ void k_sort_keys(const float* __restrict__ p, int64_t n, const double* __restrict__ lo_hi,
-                            uint32_t* __restrict__ keys, uint32_t* __restrict__ hist) {
+                            uint32_t* __restrict__ keys, uint32_t* __restrict__ hist, uint32_t* __restrict__ iota) {
   constexpr int cells = 1 << BITS;
   const float lx = (float)lo_hi[0], ly = (float)lo_hi[1], lz = (float)lo_hi[2];
   const float ext = fmaxf(fmaxf((float)(lo_hi[3] - lo_hi[0]), (float)(lo_hi[4] - lo_hi[1])),
@@ -90,7 +93,32 @@ __global__ void k_sort_keys(const float* __restrict__ p, int64_t n, const double
     const int cz = min(max((int)((__ldg(p + 3 * i + 2) - lz) * inv), 0), cells - 1);
     const uint32_t key = hilbert3((uint32_t)cx, (uint32_t)cy, (uint32_t)cz, BITS);
     keys[i] = key;
-    atomicAdd(hist + key, 1u);
+    if (hist) atomicAdd(hist + key, 1u);
+    if (iota) iota[i] = (uint32_t)i;
+  }
+}
+
+__global__ void k_sort_scatter(const float* __restrict__ p, int64_t n, const uint32_t* __restrict__ keys,
+                               uint32_t* __restrict__ cursor, int32_t* __restrict__ inv,
+                               float4* __restrict__ spts) {
+  // one scattered 16-byte write per point (the sorted point carries its original index in .w);
+  // the inverse permutation is written coalesced
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t pos = atomicAdd(cursor + keys[i], 1u);
+    inv[i] = (int32_t)pos;
+    spts[pos] = make_float4(__ldg(p + 3 * i), __ldg(p + 3 * i + 1), __ldg(p + 3 * i + 2),
+                            __int_as_float((int32_t)i));
+  }
+}
+
+// sorted (key, index) pairs -> sorted points carrying their original index, inverse permutation
+__global__ void k_sort_gather(const float* __restrict__ p, int64_t n, const uint32_t* __restrict__ idx,
+                              int32_t* __restrict__ inv, float4* __restrict__ spts) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx[j];
+    spts[j] = make_float4(__ldg(p + 3 * i), __ldg(p + 3 * i + 1), __ldg(p + 3 * i + 2), __int_as_float((int32_t)i));
+    inv[i] = (int32_t)j;
   }
 }
 
@@ -154,20 +182,6 @@ __global__ void __launch_bounds__(1024) k_scan_totals(uint32_t* __restrict__ tot
 __global__ void k_scan_add(uint32_t* __restrict__ hist, const uint32_t* __restrict__ totals) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   hist[i] += totals[i / 4096];
-}
-
-__global__ void k_sort_scatter(const float* __restrict__ p, int64_t n, const uint32_t* __restrict__ keys,
-                               uint32_t* __restrict__ cursor, int32_t* __restrict__ inv,
-                               float4* __restrict__ spts) {
-  // one scattered 16-byte write per point (the sorted point carries its original index in .w);
-  // the inverse permutation is written coalesced
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t pos = atomicAdd(cursor + keys[i], 1u);
-    inv[i] = (int32_t)pos;
-    spts[pos] = make_float4(__ldg(p + 3 * i), __ldg(p + 3 * i + 1), __ldg(p + 3 * i + 2),
-                            __int_as_float((int32_t)i));
-  }
 }
 
 // Per-view constant error bounds over the object's bbox (all points lie inside it): the camera
@@ -887,6 +901,15 @@ namespace tile {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// CUB radix-sort scratch for n (key, index) pairs (a host-side size query, no device work)
+static size_t radix_sort_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)(n > 0 ? n : 1), 0,
+                                  3 * sort_bits_for(n));
+  return bytes;
+}
+
 TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d, bool x3, int tr) {
   TileLayout L{};
   const int64_t ntiles = (n + tr - 1) / tr;
@@ -911,9 +934,16 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d, bool 
   L.vbound = take(sizeof(float4) * kMaxViewsTC);
   L.vox = take(sizeof(double) * 8);
   L.ntiles = ntiles;
+  // Hilbert keys: counting sort (histogram + scan + atomic scatter; the order of the points of one
+  // key varies from run to run) or, with PF_FUSE_DETERMINISTIC, a stable LSD radix sort of (key,
+  // index) pairs (CUB): deterministic tiles, ~0.7 ms slower at C5
   L.keys = take(sizeof(uint32_t) * (size_t)n);
   L.hist = take(sizeof(uint32_t) * (size_t)(1 << (3 * sort_bits_for(n))));
   L.totals = take(sizeof(uint32_t) * 4096);
+  L.keys_out = take(sizeof(uint32_t) * (size_t)n);
+  L.idx = take(sizeof(uint32_t) * (size_t)n);
+  L.idx_out = take(sizeof(uint32_t) * (size_t)n);
+  L.sort_tmp = take(radix_sort_temp_bytes(n));
   L.inv = take(sizeof(int32_t) * (size_t)n);
   L.spts = take(sizeof(float4) * (size_t)ntiles * tr);
   L.srec = take(sizeof(SRec) * (size_t)ntiles * tr);
@@ -948,7 +978,7 @@ int run_point_order(const float* points, int64_t n, const double* lo_hi, unsigne
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + align256(sizeof(uint32_t) * (size_t)n));
   uint32_t* totals = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(hist) + align256(sizeof(uint32_t) << 21));
   cudaMemsetAsync(hist, 0, sizeof(uint32_t) << 21, st);
-  k_sort_keys<7><<<grid_for(n, 256), 256, 0, st>>>(points, n, lo_hi, keys, hist);
+  k_sort_keys<7><<<grid_for(n, 256), 256, 0, st>>>(points, n, lo_hi, keys, hist, nullptr);
   if (int rc = check_launch("order_keys")) return rc;
   if (int rc = run_bucket_scan(hist, totals, int64_t(1) << 21, st)) return rc;
   k_order_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, keys, hist, order, len);
@@ -1003,20 +1033,36 @@ int run_unsort(const TileParams& P, cudaStream_t st) {
 int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const float* points,
                   int64_t n, cudaStream_t st) {
   uint32_t* keys = reinterpret_cast<uint32_t*>(ws + L.keys);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
-  uint32_t* totals = reinterpret_cast<uint32_t*>(ws + L.totals);
   stage_mark(0, st);
   const int bits = sort_bits_for(n);
-  const int64_t nbins = int64_t(1) << (3 * bits);
-  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * nbins, st);
   cudaMemsetAsync(P.ovf_count, 0, sizeof(int32_t), st);
-  if (bits == 8) k_sort_keys<8><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(points, n, P.lo_hi, keys, hist);
-  else k_sort_keys<7><<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist);
-  if (int rc = check_launch("sort_keys")) return rc;
-  if (int rc = run_bucket_scan(hist, totals, nbins, st)) return rc;
-  k_sort_scatter<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(points, n, keys, hist, const_cast<int32_t*>(P.inv),
-                                                   const_cast<float4*>(P.spts));
-  if (int rc = check_launch("sort_scatter")) return rc;
+  if (P.deterministic) {
+    uint32_t* keys_out = reinterpret_cast<uint32_t*>(ws + L.keys_out);
+    uint32_t* idx = reinterpret_cast<uint32_t*>(ws + L.idx);
+    uint32_t* idx_out = reinterpret_cast<uint32_t*>(ws + L.idx_out);
+    if (bits == 8) k_sort_keys<8><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(points, n, P.lo_hi, keys, nullptr, idx);
+    else k_sort_keys<7><<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, nullptr, idx);
+    if (int rc = check_launch("sort_keys")) return rc;
+    size_t tmp_bytes = radix_sort_temp_bytes(n);
+    if (cub::DeviceRadixSort::SortPairs(ws + L.sort_tmp, tmp_bytes, keys, keys_out, idx, idx_out, (int)n, 0,
+                                        3 * bits, st) != cudaSuccess)
+      return check_launch("radix_sort");
+    k_sort_gather<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(points, n, idx_out, const_cast<int32_t*>(P.inv),
+                                                            const_cast<float4*>(P.spts));
+    if (int rc = check_launch("sort_gather")) return rc;
+  } else {
+    uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
+    uint32_t* totals = reinterpret_cast<uint32_t*>(ws + L.totals);
+    const int64_t nbins = int64_t(1) << (3 * bits);
+    cudaMemsetAsync(hist, 0, sizeof(uint32_t) * nbins, st);
+    if (bits == 8) k_sort_keys<8><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(points, n, P.lo_hi, keys, hist, nullptr);
+    else k_sort_keys<7><<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist, nullptr);
+    if (int rc = check_launch("sort_keys")) return rc;
+    if (int rc = run_bucket_scan(hist, totals, nbins, st)) return rc;
+    k_sort_scatter<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(points, n, keys, hist, const_cast<int32_t*>(P.inv),
+                                                             const_cast<float4*>(P.spts));
+    if (int rc = check_launch("sort_scatter")) return rc;
+  }
   stage_mark(1, st);
   static unsigned long long* pdbg = nullptr;
   const bool debug = getenv("PF_WS_DEBUG") != nullptr;

@@ -105,6 +105,7 @@ struct TileParams {
   int32_t max_sub2;
   unsigned long long* dbg;  // optional counters (PF_WS_DEBUG)
   int32_t ablate;           // Gram kernel timing experiments only (PF_GRAM_ABLATE bits; results invalid)
+  int32_t deterministic;    // PF_FUSE_DETERMINISTIC: stable radix sort (run-to-run identical tiles)
   uint32_t* trace;          // optional per-tile role timestamps (PF_WS_DEBUG + PF_WS_TRACE=<file>)
   double* partials;
   // Gram path: compact list of the work items that run in the tile kernel ({item, first row,
@@ -117,7 +118,7 @@ struct TileParams {
 struct TileLayout {
   int64_t ntiles;
   int32_t max_sub_tiles, max_sub2;
-  size_t keys, hist, totals, inv, spts, srec, desc, kt, ovf, sub, sub2, work, gbf, textbf, viewf, vbound, vox, tbound, glo, fhi, flo, textlo,
+  size_t keys, hist, totals, keys_out, idx, idx_out, sort_tmp, inv, spts, srec, desc, kt, ovf, sub, sub2, work, gbf, textbf, viewf, vbound, vox, tbound, glo, fhi, flo, textlo,
       bytes;
 };
 

@@ -225,7 +225,7 @@ def fuse_and_query(points, views: ViewSet, tables: QueryTables, *, temperature: 
                    write_features: bool = False, write_sims: bool = False,
                    write_weights: bool = False, reduce: bool = True, check: bool = False,
                    force_simt: bool = False, prepared: bool = False,
-                   reset: bool = True, feature_kernel: bool = False) -> FusedResult:
+                   reset: bool = True, feature_kernel: bool = False, deterministic: bool = False) -> FusedResult:
     """Run the whole path on `points` (N,3) f32 device tensor (numpy is uploaded).
 
     lo_hi: voxel domain (6,) f64 device tensor; None = this call's bbox (pf_bbox). Multi-GPU
@@ -233,6 +233,7 @@ def fuse_and_query(points, views: ViewSet, tables: QueryTables, *, temperature: 
     reduce=False skips the voxel-mass finalisation (call allreduce() then finalize()).
     bf16 maps run the Gram-formulation tile kernel; write_features (a validation output only the
     feature-product kernel produces) or feature_kernel=True select k_tile_ws instead.
+    deterministic=True: run-to-run identical results (stable sort of the points; slower).
     """
     if temperature <= 0:
         raise ValueError(f"temperature must be positive, got {temperature}")
@@ -271,6 +272,8 @@ def fuse_and_query(points, views: ViewSet, tables: QueryTables, *, temperature: 
         flags |= _lib.PF_FUSE_PREPARED
     if feature_kernel:
         flags |= _lib.PF_FUSE_FEATURE_KERNEL
+    if deterministic:
+        flags |= _lib.PF_FUSE_DETERMINISTIC
     args = _make_args(pts, n, views, tables, temperature, epsilon, grid, buffers, flags)
     _lib.call("pf_fuse_query", args, st)
     res = FusedResult(buffers, views.nviews, tables.k, n)
