@@ -649,6 +649,13 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.max_sub2 = L.max_sub2;
     T.work_count = tr == tile::kGramTile ? reinterpret_cast<int32_t*>(ws + L.work) : nullptr;
     T.work = tr == tile::kGramTile ? reinterpret_cast<int4*>(ws + L.work) + 1 : nullptr;
+    // split items to the feature-product kernel (PF_GRAM_SPLIT=0: all items in the Gram kernel)
+    static const bool split = [] {
+      const char* e = getenv("PF_GRAM_SPLIT");
+      return !(e && e[0] == '0');
+    }();
+    T.wcount = tr == tile::kGramTile && split ? reinterpret_cast<int32_t*>(ws + L.wlist) : nullptr;
+    T.wlist = tr == tile::kGramTile && split ? reinterpret_cast<int4*>(ws + L.wlist) + 1 : nullptr;
     T.partials = a->partials;
     T.tbound = reinterpret_cast<const float*>(ws + L.tbound);
     if (int rc = tile::run_tile_path(T, L, ws, a->points, a->n, st)) return rc;

@@ -1025,7 +1025,12 @@ __global__ void k_collect_work(TileParams P) {
   const int64_t first2 = nt + 4 * (int64_t)P.max_sub_tiles;
   const int lane = threadIdx.x & 31;
   auto push = [&](int64_t item, int64_t row0, int rows, int kt) {
-    if (lane == 0) P.work[atomicAdd(P.work_count, 1)] = make_int4((int)item, (int)row0, rows | (kt << 16), 0);
+    if (lane != 0) return;
+    const int4 e = make_int4((int)item, (int)row0, rows | (kt << 16), 0);
+    // split items (128 / 32 rows) run in the feature-product kernel: per 128 rows the Gram product
+    // (kt^2 D) costs more than the feature product (128 kt D) once kt exceeds ~128
+    if (P.wlist && rows < P.tr) P.wlist[atomicAdd(P.wcount, 1)] = e;
+    else P.work[atomicAdd(P.work_count, 1)] = e;
   };
   auto overflow = [&](int64_t row0, int rows) {
     for (int r = lane; r < rows; r += 32) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(P.spts[row0 + r].w);
@@ -1084,6 +1089,7 @@ int run_tile_gram(const TileParams& P, cudaStream_t st) {
   if (const char* g = getenv("PF_WS_GRID")) grid = atoi(g) > 0 ? atoi(g) : grid;  // debug knob
   if (grid < 1) grid = 1;
   cudaMemsetAsync(P.work_count, 0, sizeof(int32_t), st);
+  if (P.wlist) cudaMemsetAsync(P.wcount, 0, sizeof(int32_t), st);
   k_collect_work<<<grid_for(32 * (ntiles + 4 * (int64_t)P.max_sub2), 256, 148 * 8), 256, 0, st>>>(P);
   if (int rc = check_launch("collect_work")) return rc;
   const bool debug = getenv("PF_WS_DEBUG") != nullptr;
@@ -1100,7 +1106,12 @@ int run_tile_gram(const TileParams& P, cudaStream_t st) {
   } else {
     k_tile_gram<false, false><<<grid, kThreads, smem, st>>>(Q);
   }
-  const int rc = check_launch("tile_gram");
+  int rc = check_launch("tile_gram");
+  if (rc == PF_OK && P.wlist) {  // the split 128 / 32-row items (a device-side list, maybe empty)
+    TileParams W = P;
+    W.kt_max = kGramKt;
+    rc = run_tile_ws(W, st);
+  }
   if (debug && rc == PF_OK) {
     static unsigned long long h[32 * 1024];
     cudaMemcpyAsync(h, dbg, sizeof(unsigned long long) * 32 * grid, cudaMemcpyDeviceToHost, st);

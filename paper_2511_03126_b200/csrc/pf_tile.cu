@@ -957,6 +957,7 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d, bool 
   L.sub2 = take(sizeof(int32_t) * ((size_t)L.max_sub2 + 1));
   L.ovf = take(sizeof(int32_t) * (size_t)(n + 1));
   L.work = tr == kTile ? 0 : take(sizeof(int4) * (size_t)(items + 1));  // [count | pad] then entries
+  L.wlist = tr == kTile ? 0 : take(sizeof(int4) * (size_t)(items + 1));  // split items for k_tile_ws
   L.bytes = off;
   return L;
 }

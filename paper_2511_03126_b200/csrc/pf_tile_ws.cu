@@ -113,11 +113,21 @@ __device__ __forceinline__ int ktp_of(int kt, bool& ok, int kt_max) {
   return ktp;
 }
 __device__ __forceinline__ int kt_at(const TileParams& P, int64_t tile, int64_t ntiles) {
+  if (P.wlist) return tile < ntiles ? (P.wlist[tile].z >> 16) : 0;  // ntiles = list length here
   return tile < ntiles ? P.tile_kt[tile] : 0;
 }
+// descriptor row of work item t (the Gram path's list names the item whose windows it uses)
+__device__ __forceinline__ int64_t desc_item(const TileParams& P, int64_t t) { return P.wlist ? P.wlist[t].x : t; }
 
 // work item t -> (tile, first row, row count): tiles first, then the sub-tiles of overflow tiles
+// (list mode: the entry's first row and row count, inside one 128-row tile)
 __device__ __forceinline__ int64_t item_tile(const TileParams& P, int64_t t, int64_t ntiles, int& rlo, int& rhi) {
+  if (P.wlist) {
+    const int4 e = P.wlist[t];
+    rlo = e.y % kTile;
+    rhi = rlo + (e.z & 0xffff);
+    return e.y / kTile;
+  }
   if (t < ntiles) {
     rlo = 0;
     rhi = kTile;
@@ -213,7 +223,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nd = P.d >> 6, ns = P.kpadg >> 6, nch = nd + ns;
   const int64_t ntiles = (P.n + kTile - 1) / kTile;
-  const int64_t nitems = ntiles + 4 * (int64_t)min(*P.sub_count, P.max_sub_tiles);
+  const int64_t nitems = P.wlist ? (int64_t)*P.wcount : ntiles + 4 * (int64_t)min(*P.sub_count, P.max_sub_tiles);
   // PROF (PF_WS_DEBUG=1): per-role mbarrier wait / issue cycles, printed by the host
   long long wait_cyc[15] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long issue_cyc = 0;
@@ -309,12 +319,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     uint32_t published = 0, pub_tile = 0, pub_group = 0;  // PROF trace bookkeeping (warp 0)
     uint32_t t_local = 0;
     int kt_nx = kt_at(P, blockIdx.x, nitems);
-    uint2 ds_nx = (tid < P.nv && blockIdx.x < nitems) ? P.tile_desc[blockIdx.x * P.nv + tid] : make_uint2(0u, 0u);
+    uint2 ds_nx = (tid < P.nv && blockIdx.x < nitems) ? P.tile_desc[desc_item(P, blockIdx.x) * P.nv + tid]
+                                                      : make_uint2(0u, 0u);
     for (int64_t tile = blockIdx.x; tile < nitems; tile += gridDim.x) {
       const int kt = kt_nx;
       const uint2 ds_cur = ds_nx;
       kt_nx = kt_at(P, tile + gridDim.x, nitems);
-      if (tid < P.nv && tile + gridDim.x < nitems) ds_nx = P.tile_desc[(tile + gridDim.x) * P.nv + tid];
+      if (tid < P.nv && tile + gridDim.x < nitems) ds_nx = P.tile_desc[desc_item(P, tile + gridDim.x) * P.nv + tid];
       bool ok;
       const int ktp = ktp_of(kt, ok, X3 ? kKtX3 : kKtWs);
       if (!ok) continue;
@@ -483,7 +494,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       mm = make_uint2(0u, 0u);  // rows outside the work item: empty mask
       cd = -1;
       if (t >= nitems) return;
-      if (bt < P.nv) ds = P.tile_desc[t * P.nv + bt];
+      if (bt < P.nv) ds = P.tile_desc[desc_item(P, t) * P.nv + bt];
       int64_t jr;
       if (item_row(P, t, ntiles, row, jr)) {
         pp = ld_pref_f4(P.spts + jr);
@@ -1056,7 +1067,8 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
   cudaFuncSetAttribute(k_tile_ws<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_tile_ws<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_tile_ws<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t ntiles = (P.n + kTile - 1) / kTile;  // (+ sub-tiles, known on the device only)
+  // (+ sub-tiles, known on the device only; list mode: the list length is on the device too)
+  const int64_t ntiles = P.wlist ? (int64_t)sms : (P.n + kTile - 1) / kTile;
   int grid = (int)(ntiles < sms ? ntiles : sms);
   if (const char* g = getenv("PF_WS_GRID")) grid = (int)(ntiles < atoi(g) ? ntiles : atoi(g));  // debug knob
   static unsigned long long* dbg = nullptr;
