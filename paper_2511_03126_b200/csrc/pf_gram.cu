@@ -1027,9 +1027,10 @@ __global__ void k_collect_work(TileParams P) {
   auto push = [&](int64_t item, int64_t row0, int rows, int kt) {
     if (lane != 0) return;
     const int4 e = make_int4((int)item, (int)row0, rows | (kt << 16), 0);
-    // split items (128 / 32 rows) run in the feature-product kernel: per 128 rows the Gram product
-    // (kt^2 D) costs more than the feature product (128 kt D) once kt exceeds ~128
-    if (P.wlist && rows < P.tr) P.wlist[atomicAdd(P.wcount, 1)] = e;
+    // split items (128 / 32 rows: item ids >= nt) run in the feature-product kernel: per 128 rows the
+    // Gram product (kt^2 D) costs more than the feature product (128 kt D) once kt exceeds ~128. (Not
+    // by row count: the last 512-row tile of an object may be short but is still a 512-row item.)
+    if (P.wlist && item >= nt) P.wlist[atomicAdd(P.wcount, 1)] = e;
     else P.work[atomicAdd(P.work_count, 1)] = e;
   };
   auto overflow = [&](int64_t row0, int rows) {

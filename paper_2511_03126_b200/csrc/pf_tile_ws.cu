@@ -112,17 +112,25 @@ __device__ __forceinline__ int ktp_of(int kt, bool& ok, int kt_max) {
   ok = kt > 0 && ktp <= kt_max;
   return ktp;
 }
+// LIST: the Gram path's list of split items (P.wlist) instead of this kernel's own tiles / sub-tiles
+// (a template parameter: the own-items instantiation carries none of the list logic)
+template <bool LIST>
 __device__ __forceinline__ int kt_at(const TileParams& P, int64_t tile, int64_t ntiles) {
-  if (P.wlist) return tile < ntiles ? (P.wlist[tile].z >> 16) : 0;  // ntiles = list length here
+  if constexpr (LIST) return tile < ntiles ? (P.wlist[tile].z >> 16) : 0;  // ntiles = list length here
   return tile < ntiles ? P.tile_kt[tile] : 0;
 }
 // descriptor row of work item t (the Gram path's list names the item whose windows it uses)
-__device__ __forceinline__ int64_t desc_item(const TileParams& P, int64_t t) { return P.wlist ? P.wlist[t].x : t; }
+template <bool LIST>
+__device__ __forceinline__ int64_t desc_item(const TileParams& P, int64_t t) {
+  if constexpr (LIST) return P.wlist[t].x;
+  return t;
+}
 
 // work item t -> (tile, first row, row count): tiles first, then the sub-tiles of overflow tiles
 // (list mode: the entry's first row and row count, inside one 128-row tile)
+template <bool LIST>
 __device__ __forceinline__ int64_t item_tile(const TileParams& P, int64_t t, int64_t ntiles, int& rlo, int& rhi) {
-  if (P.wlist) {
+  if constexpr (LIST) {
     const int4 e = P.wlist[t];
     rlo = e.y % kTile;
     rhi = rlo + (e.z & 0xffff);
@@ -139,9 +147,10 @@ __device__ __forceinline__ int64_t item_tile(const TileParams& P, int64_t t, int
   return P.sub_tiles[b];
 }
 // does work item t cover tile row `row` (and is the point real)?
+template <bool LIST>
 __device__ __forceinline__ bool item_row(const TileParams& P, int64_t t, int64_t ntiles, int row, int64_t& jpt) {
   int rlo, rhi;
-  const int64_t tl = item_tile(P, t, ntiles, rlo, rhi);
+  const int64_t tl = item_tile<LIST>(P, t, ntiles, rlo, rhi);
   jpt = tl * kTile + row;
   return row >= rlo && row < rhi && jpt < P.n;
 }
@@ -212,7 +221,7 @@ __device__ __forceinline__ float ex2(float x) {
 
 // PROF: wait accounting + trace (PF_WS_DEBUG); OUTS: validation outputs (features, similarities,
 // softmax weights) -- a separate instantiation keeps their fully unrolled stores out of the hot code
-template <bool PROF, bool OUTS, bool X3>
+template <bool PROF, bool OUTS, bool X3, bool LIST = false>
 __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant__ TileParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nd = P.d >> 6, ns = P.kpadg >> 6, nch = nd + ns;
   const int64_t ntiles = (P.n + kTile - 1) / kTile;
-  const int64_t nitems = P.wlist ? (int64_t)*P.wcount : ntiles + 4 * (int64_t)min(*P.sub_count, P.max_sub_tiles);
+  const int64_t nitems = LIST ? (int64_t)*P.wcount : ntiles + 4 * (int64_t)min(*P.sub_count, P.max_sub_tiles);
   // PROF (PF_WS_DEBUG=1): per-role mbarrier wait / issue cycles, printed by the host
   long long wait_cyc[15] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long issue_cyc = 0;
@@ -274,9 +283,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   // instead keeps the exponents in [-2c, 0]: no overflow, and the row's largest term cannot underflow
   // while 2c <= 120. Beyond that (tiny T or long text rows) the row max is subtracted per point.
   // The 1.05 margin covers the bf16 rounding of the text / G operands.
-  const float cbound = 1.05f * __ldg(P.tbound) * P.inv_temp * 1.4426950408889634f;
-  const int need_max = (2.f * cbound <= 120.f) ? 0 : 1;  // NaN / inf bound: per-row max
-  const float shift = need_max ? 0.f : -cbound;
+  float shift;
+  {
+    const float cbound = 1.05f * __ldg(P.tbound) * P.inv_temp * 1.4426950408889634f;
+    shift = (2.f * cbound <= 120.f) ? -cbound : 0.f;  // NaN / inf bound: per-row max (acc branch)
+  }
   for (int j = tid; j < kMaxKpadTC / 2; j += kWsThreads) {
     auto val = [&](int kk, int pp) { return (kk < P.k && pp < P.p) ? P.values[kk * P.p + pp] : 0.f; };
     const int a = 2 * j, b = 2 * j + 1;
@@ -318,14 +329,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     uint32_t phase = 0;
     uint32_t published = 0, pub_tile = 0, pub_group = 0;  // PROF trace bookkeeping (warp 0)
     uint32_t t_local = 0;
-    int kt_nx = kt_at(P, blockIdx.x, nitems);
-    uint2 ds_nx = (tid < P.nv && blockIdx.x < nitems) ? P.tile_desc[desc_item(P, blockIdx.x) * P.nv + tid]
+    int kt_nx = kt_at<LIST>(P, blockIdx.x, nitems);
+    uint2 ds_nx = (tid < P.nv && blockIdx.x < nitems) ? P.tile_desc[desc_item<LIST>(P, blockIdx.x) * P.nv + tid]
                                                       : make_uint2(0u, 0u);
     for (int64_t tile = blockIdx.x; tile < nitems; tile += gridDim.x) {
       const int kt = kt_nx;
       const uint2 ds_cur = ds_nx;
-      kt_nx = kt_at(P, tile + gridDim.x, nitems);
-      if (tid < P.nv && tile + gridDim.x < nitems) ds_nx = P.tile_desc[desc_item(P, tile + gridDim.x) * P.nv + tid];
+      kt_nx = kt_at<LIST>(P, tile + gridDim.x, nitems);
+      if (tid < P.nv && tile + gridDim.x < nitems) ds_nx = P.tile_desc[desc_item<LIST>(P, tile + gridDim.x) * P.nv + tid];
       bool ok;
       const int ktp = ktp_of(kt, ok, X3 ? kKtX3 : kKtWs);
       if (!ok) continue;
@@ -401,10 +412,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     uint32_t dcount = 0;  // chunk pairs issued so far (selects the TMEM accumulator slot)
     uint32_t t_local = 0;
     const uint32_t idesc = tc::idesc_bf16_f32(128, kDCols, false, true);
-    int kt_nx = kt_at(P, blockIdx.x, nitems);
+    int kt_nx = kt_at<LIST>(P, blockIdx.x, nitems);
     for (int64_t tile = blockIdx.x; tile < nitems; tile += gridDim.x) {
       const int kt = kt_nx;
-      kt_nx = kt_at(P, tile + gridDim.x, nitems);
+      kt_nx = kt_at<LIST>(P, tile + gridDim.x, nitems);
       bool ok;
       const int ktp = ktp_of(kt, ok, X3 ? kKtX3 : kKtWs);
       if (!ok) continue;
@@ -489,14 +500,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     uint32_t t_local = 0;
     static_assert(kMaxViewsTC <= kBuildThreads, "one window per builder thread");
     auto fetch = [&](int64_t t, int& kt, uint2& ds, float4& pp, uint2& mm, int32_t& cd) {
-      kt = kt_at(P, t, nitems);
+      kt = kt_at<LIST>(P, t, nitems);
       pp = make_float4(0.f, 0.f, 0.f, 0.f);
       mm = make_uint2(0u, 0u);  // rows outside the work item: empty mask
       cd = -1;
       if (t >= nitems) return;
-      if (bt < P.nv) ds = P.tile_desc[desc_item(P, t) * P.nv + bt];
+      if (bt < P.nv) ds = P.tile_desc[desc_item<LIST>(P, t) * P.nv + bt];
       int64_t jr;
-      if (item_row(P, t, ntiles, row, jr)) {
+      if (item_row<LIST>(P, t, ntiles, row, jr)) {
         pp = ld_pref_f4(P.spts + jr);
         const uint4 r4 = ld_pref_u4(P.srec + jr);
         mm = make_uint2(r4.x, r4.y);
@@ -526,7 +537,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         const uint32_t peers = __match_any_sync(0xffffffffu, cd);
         const bool first = (peers & ((1u << lane) - 1u)) == 0u;
         int64_t jr;
-        if (cd >= 0 && item_row(P, tile, ntiles, row, jr)) P.vox_list[jr] = first ? cd : -1;
+        if (cd >= 0 && item_row<LIST>(P, tile, ntiles, row, jr)) P.vox_list[jr] = first ? cd : -1;
       }
       if (bt == 0) WS_TRACE(t_local, 0);
       const int ab = (int)(t_local & 1u);
@@ -536,7 +547,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       // lane groups through shared memory)
       float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
       int64_t jrow;
-      if (item_row(P, tile, ntiles, row, jrow)) {
+      if (item_row<LIST>(P, tile, ntiles, row, jrow)) {
         lo[0] = hi[0] = p.x;
         lo[1] = hi[1] = p.y;
         lo[2] = hi[2] = p.z;
@@ -768,6 +779,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
   } else {
     // ================= accumulators: two warps per TMEM lane group, split by columns =================
     reg_alloc<kRegAcc>();
+    const int need_max = (2.f * (1.05f * __ldg(P.tbound) * P.inv_temp * 1.4426950408889634f) <= 120.f) ? 0 : 1;
     const int half = (warp - kAccWarp0) >> 2;          // 0 / 1
     const int row = 32 * (warp & 3) + lane;            // TMEM lane = tile row
     const uint32_t t_lane = (uint32_t)(32 * (warp & 3)) << 16;
@@ -782,11 +794,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
     float pm_sum = 0.f, pmx = 0.f, pmy = 0.f, pmz = 0.f, featured_n = 0.f, pairs = 0.f;
     const bool outs = OUTS && (P.sims || P.weights);
     const bool p_wide = P.p > 2;
-    int kt_nx = kt_at(P, blockIdx.x, nitems);
+    int kt_nx = kt_at<LIST>(P, blockIdx.x, nitems);
     uint2 rec_nx = make_uint2(0u, 0u);  // record words 2, 3: visible-view count, voxel code
     float4 p_nx = make_float4(0.f, 0.f, 0.f, 0.f);
     int64_t j_nx = 0;
-    bool v_nx = blockIdx.x < nitems && item_row(P, blockIdx.x, ntiles, row, j_nx);
+    bool v_nx = blockIdx.x < nitems && item_row<LIST>(P, blockIdx.x, ntiles, row, j_nx);
     if (v_nx) {
       rec_nx = ld_pref_u2(reinterpret_cast<const uint32_t*>(P.srec + j_nx) + 2);
       p_nx = ld_pref_f4(P.spts + j_nx);
@@ -797,8 +809,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       const float4 pcur = p_nx;
       const int64_t jpt = j_nx;
       const bool valid = v_nx;
-      kt_nx = kt_at(P, tile + gridDim.x, nitems);
-      v_nx = tile + gridDim.x < nitems && item_row(P, tile + gridDim.x, ntiles, row, j_nx);
+      kt_nx = kt_at<LIST>(P, tile + gridDim.x, nitems);
+      v_nx = tile + gridDim.x < nitems && item_row<LIST>(P, tile + gridDim.x, ntiles, row, j_nx);
       if (v_nx) {
         rec_nx = ld_pref_u2(reinterpret_cast<const uint32_t*>(P.srec + j_nx) + 2);
         p_nx = ld_pref_f4(P.spts + j_nx);
@@ -1087,6 +1099,13 @@ int run_tile_ws(const TileParams& P, cudaStream_t st) {
     Q.trace = trace;
   }
   const bool outs = P.sims || P.weights || P.features;
+  if (P.wlist) {  // the Gram path's split items (bf16)
+    cudaFuncSetAttribute(k_tile_ws<false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_tile_ws<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (outs) k_tile_ws<false, true, false, true><<<grid, kWsThreads, smem, st>>>(Q);
+    else k_tile_ws<false, false, false, true><<<grid, kWsThreads, smem, st>>>(Q);
+    return check_launch("tile_ws_list");
+  }
   if (P.x3) {  // f32 maps: the hi / lo split instantiation (the bf16 code is untouched by it)
     if (debug && outs) k_tile_ws<true, true, true><<<grid, kWsThreads, smem, st>>>(Q);
     else if (debug) k_tile_ws<true, false, true><<<grid, kWsThreads, smem, st>>>(Q);
