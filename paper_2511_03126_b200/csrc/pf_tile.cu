@@ -231,17 +231,17 @@ __device__ __forceinline__ int classify_fast(const ViewF& w, const float4& b, co
 enum : int { kViewOff = 0, kViewFull = 1, kViewMixed = 2, kViewExact = 3 };
 constexpr int kScanMax = 64;  // pixels of depth scanned per (tile, view) at most
 
-// Per-(tile, view) affine model of a MIXED view: u, v, z = c0 + g . (p - o) with rigorous bounds
-// eu, ev, ez on |model - numpy's fp64 value| over the tile box (see classify_tile_view).
-struct ViewAff {
-  float4 r0, r1, r2;     // camera rotation rows {R_i0, R_i1, R_i2, -}: a, c, b = R . d
-  float4 u, v;           // {value at o, d/da, d/db, d/d(ab)}; the b^2 coefficient is in z.w / q
-  float4 q;              // {u: b^2 coeff, v: b^2 coeff, v: d/dc, v: d/d(cb)}
-  float z0;
-  float eu, ev, ez, pad;
-  float hu, hv;          // 0.5 - eu, 0.5 - ev (rounded down)
-  int W, H;
-  const float* dmap;     // this view's depth map
+// Per-(tile, view) second-order model of a MIXED view (see classify_tile_view), 7 x 16 B read by
+// every point of the tile as broadcast shared-memory loads: u, v from a = R0.d, c = R1.d, b = R2.d
+// (d = p - o) with rigorous bounds eu, ev, ez on |model - numpy's fp64 value| over the tile box.
+struct MixModel {
+  float4 ra;  // {R00, R01, R02, u0}
+  float4 rc;  // {R10, R11, R12, v0}
+  float4 rb;  // {R20, R21, R22, z0}
+  float4 cu;  // u = b (qu b + ku a + kb) + (su a + u0): {su, kb, ku, qu}
+  float4 cv;  // v = b (qv b + kv c + kc) + (sv c + v0): {sv, kc, kv, qv}
+  float4 e;   // {0.5 - eu, 0.5 - ev (rounded down), ez, box window (packed bytes, MIXED -> seen)}
+  int4 g;     // {W, H, depth offset lo, hi}
 };
 
 // Decide one view for every point of a tile at once. The points lie in the box [lo, hi] (exact:
@@ -276,7 +276,7 @@ __device__ __forceinline__ double rcp_f64(double z) {
 
 __device__ __forceinline__ int classify_tile_view(const ViewF& v, const float4& vb, const pf_view_t& v64,
                                   const float* __restrict__ depth, const float* lo, const float* hi, float eps,
-                                  int4& win, ViewAff& aff) {
+                                  int4& win, MixModel& aff) {
   float zmin = 1e30f, zmax = -1e30f, umin = 1e30f, umax = -1e30f, vmin = 1e30f, vmax = -1e30f;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -339,13 +339,6 @@ __device__ __forceinline__ int classify_tile_view(const ViewF& v, const float4& 
   //   X/Z = X0/Z0 + a/Z0 - X0 b/Z0^2 - a b/Z0^2 + X0 b^2/Z0^3 + R3,
   //   R3 = a b^2/Z0^3 - (X0 + a) b^3 / (Z0^3 Z),  |R3| <= r^3 ((|X0| + r)/(Z0^3 zmin) + 1/Z0^3)
   const double su = v64.fx * rz0, sv = v64.fy * rz0, xr = X0 * rz0, yr = Y0 * rz0;
-  aff.r0 = make_float4(v.R[0], v.R[1], v.R[2], 0.f);
-  aff.r1 = make_float4(v.R[3], v.R[4], v.R[5], 0.f);
-  aff.r2 = make_float4(v.R[6], v.R[7], v.R[8], 0.f);
-  aff.u = make_float4(u0, (float)su, (float)(-su * xr), (float)(-su * rz0));
-  aff.v = make_float4(v0, (float)sv, (float)(-sv * yr), (float)(-sv * rz0));
-  aff.q = make_float4((float)(su * xr * rz0), (float)(sv * yr * rz0), 0.f, 0.f);
-  aff.z0 = (float)Z0;
   const double z0 = Z0, rr = (double)r, zl = (double)zmin;
   const double r3 = rr * rr * rr * (rz0 * rz0 * rz0);  // bounds below carry a 1.05 factor
   const double rzl = rcp_f64(zl);
@@ -356,16 +349,18 @@ __device__ __forceinline__ int classify_tile_view(const ViewF& v, const float4& 
                     1e-5 * (gu + qu) + 1e-5;
   const double ev = fabs(v64.fy) * r3 * ((fabs(Y0) + rr) * rzl + 1.0) * 1.05 + 7e-7 * (fabs(v0) + gv + qv) +
                     1e-5 * (gv + qv) + 1e-5;
-  aff.eu = (float)eu;
-  aff.ev = (float)ev;
-  aff.ez = 4.7e-7f * (fabsf((float)z0) + 2.f * r) + 1e-7f;  // z = z0 + b is exactly affine: rounding only
-  aff.W = v.W;
-  aff.H = v.H;
-  aff.dmap = depth + v.depth_off;
-  aff.hu = __fsub_rd(0.5f, aff.eu);
-  aff.hv = __fsub_rd(0.5f, aff.ev);
-  aff.ez = aff.ez * 1.0001f + 2e-9f;  // + the 1e-9 floor and the margin / difference roundings
-  if (!(aff.eu < 0.25f && aff.ev < 0.25f)) return kViewExact;
+  if (!(eu < 0.25 && ev < 0.25)) return kViewExact;
+  aff.ra = make_float4(v.R[0], v.R[1], v.R[2], u0);
+  aff.rc = make_float4(v.R[3], v.R[4], v.R[5], v0);
+  aff.rb = make_float4(v.R[6], v.R[7], v.R[8], (float)Z0);
+  aff.cu = make_float4((float)su, (float)(-su * xr), (float)(-su * rz0), (float)(su * xr * rz0));
+  aff.cv = make_float4((float)sv, (float)(-sv * yr), (float)(-sv * rz0), (float)(sv * yr * rz0));
+  const float ez = 4.7e-7f * (fabsf((float)z0) + 2.f * r) + 1e-7f;  // z = z0 + b is exactly affine: rounding only
+  // + the 1e-9 floor and the margin / difference roundings
+  aff.e = make_float4(__fsub_rd(0.5f, __double2float_ru(eu)), __fsub_rd(0.5f, __double2float_ru(ev)), ez * 1.0001f + 2e-9f,
+                      0.f);
+  const int64_t doff = v.depth_off;
+  aff.g = make_int4(v.W, v.H, (int)(uint32_t)doff, (int)(doff >> 32));
   return kViewMixed;
 }
 
@@ -427,29 +422,30 @@ __device__ __forceinline__ bool point_visible(const ViewF& v, const float4& b, c
   return vis;
 }
 
-// MIXED-view decision through the second-order model; kAmbiguous sends the sample to point_visible
-__device__ __forceinline__ int affine_visible(const ViewAff& m, const float* __restrict__ depth, float dx,
-                                              float dy, float dz, float eps_f) {
-  const float a = fmaf(m.r0.z, dz, fmaf(m.r0.y, dy, m.r0.x * dx));
-  const float c = fmaf(m.r1.z, dz, fmaf(m.r1.y, dy, m.r1.x * dx));
-  const float b = fmaf(m.r2.z, dz, fmaf(m.r2.y, dy, m.r2.x * dx));
-  const float u = fmaf(b, fmaf(m.q.x, b, fmaf(m.u.w, a, m.u.z)), fmaf(m.u.y, a, m.u.x));
-  const float v = fmaf(b, fmaf(m.q.y, b, fmaf(m.v.w, c, m.v.z)), fmaf(m.v.y, c, m.v.x));
-  // |u - rint(u)| (exact in fp32) >= 0.5 - eu  <=>  u within eu of a pixel boundary (m.pad: 0.5 - eu
-  // and 0.5 - ev rounded down)
+// MIXED-view decision through the second-order model, branch-free: vis = visible for sure; amb =
+// within the model's bound of a pixel boundary or of the depth threshold (the caller re-tests those
+// samples exactly). Otherwise invisible (off-image, empty pixel, or behind the stored depth).
+__device__ __forceinline__ void affine_visible(const MixModel& m, const float* __restrict__ depth, float dx, float dy,
+                                               float dz, float eps_f, bool& vis, bool& amb) {
+  const float a = fmaf(m.ra.z, dz, fmaf(m.ra.y, dy, m.ra.x * dx));
+  const float c = fmaf(m.rc.z, dz, fmaf(m.rc.y, dy, m.rc.x * dx));
+  const float b = fmaf(m.rb.z, dz, fmaf(m.rb.y, dy, m.rb.x * dx));
+  const float u = fmaf(b, fmaf(m.cu.w, b, fmaf(m.cu.z, a, m.cu.y)), fmaf(m.cu.x, a, m.ra.w));
+  const float v = fmaf(b, fmaf(m.cv.w, b, fmaf(m.cv.z, c, m.cv.y)), fmaf(m.cv.x, c, m.rc.w));
+  // |u - rint(u)| (exact in fp32) >= 0.5 - eu  <=>  u within eu of a pixel boundary
   const float ru = rintf(u), rv = rintf(v);
-  if (fabsf(u - ru) >= m.hu || fabsf(v - rv) >= m.hv) return kAmbiguous;
+  const bool amb_uv = fabsf(u - ru) >= m.e.x || fabsf(v - rv) >= m.e.y;
   // one unsigned compare per axis (finite u, v: the model of finite points)
   const int iu = (int)ru, iv = (int)rv;
-  if ((unsigned)iu >= (unsigned)m.W || (unsigned)iv >= (unsigned)m.H) return kInvisible;
-  const float stored = __ldg(m.dmap + iv * m.W + iu);  // a view's map has < 2^31 pixels
-  if (!(stored > 0.f)) return kInvisible;
-  const float thr = __fadd_rn(stored, eps_f);  // > 0
-  const float mz = fmaf(2.4e-7f, thr, m.ez);    // m.ez includes the 1e-9 floor
-  const float dz_ = (m.z0 + b) - thr;
-  if (dz_ < -mz) return kNeedDepth;  // visible (z + mz < thr, up to the margin's own rounding slack)
-  if (dz_ > mz) return kInvisible;
-  return kAmbiguous;
+  const bool inb = !amb_uv && (unsigned)iu < (unsigned)m.g.x && (unsigned)iv < (unsigned)m.g.y;
+  const int64_t off = ((int64_t)m.g.w << 32) | (uint32_t)m.g.z;
+  const float stored = inb ? __ldg(depth + off + iv * m.g.x + iu) : 0.f;  // a view's map has < 2^31 pixels
+  const float thr = __fadd_rn(stored, eps_f);  // > 0 when stored > 0
+  const float mz = fmaf(2.4e-7f, thr, m.e.z);  // m.e.z includes the 1e-9 floor
+  const float dz_ = (m.rb.w + b) - thr;
+  const bool hit = stored > 0.f;               // (inb folded in: stored = 0 otherwise)
+  vis = hit && dz_ < -mz;                      // z + mz < thr, up to the margin's own rounding slack
+  amb = amb_uv || (hit && !(dz_ < -mz) && !(dz_ > mz));
 }
 
 // ---- k_tile_prep ---------------------------------------------------------------------------------------
@@ -473,7 +469,7 @@ __device__ __forceinline__ void window_reduce(bool vis, const TapF& t, int* wx0,
 template <int TR>
 __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParams P) {
   __shared__ ViewF sv[kMaxViewsTC];
-  __shared__ ViewAff saff[kMaxViewsTC];
+  __shared__ MixModel saff[kMaxViewsTC];
   __shared__ float4 sbound[kMaxViewsTC];
   __shared__ int wx0[kMaxViewsTC], wx1[kMaxViewsTC], wy0[kMaxViewsTC], wy1[kMaxViewsTC];
   __shared__ unsigned char s_cls[kMaxViewsTC];
@@ -486,20 +482,21 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
   const int64_t jpt = tile * TR + tid;
   const bool valid = jpt < P.n;
   const float4 p = valid ? P.spts[jpt] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const bool live = valid && !isnan(p.x);  // NaN point: a padding slot (pf_shard_pack_padded)
   {
-    float b[6] = {valid ? p.x : INFINITY, valid ? p.y : INFINITY, valid ? p.z : INFINITY,
-                  valid ? p.x : -INFINITY, valid ? p.y : -INFINITY, valid ? p.z : -INFINITY};
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        b[a] = fminf(b[a], __shfl_xor_sync(0xffffffffu, b[a], o));
-        b[a + 3] = fmaxf(b[a + 3], __shfl_xor_sync(0xffffffffu, b[a + 3], o));
-      }
-    }
+    const bool inbox = live && !isnan(p.y) && !isnan(p.z);
+    // tile box: warp min / max as order-preserving integer reductions (one REDUX each); rows past n
+    // and padding slots contribute nothing
+    auto key = [](float f) { const int i = __float_as_int(f); return i >= 0 ? i : i ^ 0x7fffffff; };
+    const int b[6] = {__reduce_min_sync(0xffffffffu, key(inbox ? p.x : INFINITY)),
+                      __reduce_min_sync(0xffffffffu, key(inbox ? p.y : INFINITY)),
+                      __reduce_min_sync(0xffffffffu, key(inbox ? p.z : INFINITY)),
+                      __reduce_max_sync(0xffffffffu, key(inbox ? p.x : -INFINITY)),
+                      __reduce_max_sync(0xffffffffu, key(inbox ? p.y : -INFINITY)),
+                      __reduce_max_sync(0xffffffffu, key(inbox ? p.z : -INFINITY))};
     if (lane == 0)
 #pragma unroll
-      for (int a = 0; a < 6; ++a) sbb[tid >> 5][a] = b[a];
+      for (int a = 0; a < 6; ++a) sbb[tid >> 5][a] = __int_as_float(b[a] >= 0 ? b[a] : b[a] ^ 0x7fffffff);
   }
   if (tid < 2) s_seen[tid] = 0u;
   __syncthreads();
@@ -519,7 +516,7 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
     const ViewF v = P.viewf[tid];  // per-view fp32 camera + constant error bounds (k_view_setup)
     const float4 vb = P.vbound[tid];
     int4 win = make_int4(INT_MAX, INT_MAX, -1, -1);
-    ViewAff aff;
+    MixModel aff;
     const int cls = classify_tile_view(v, vb, P.views[tid], P.depth, lo, hi, eps_f, win, aff);
     s_cls[tid] = (unsigned char)cls;
     // FULL: box window now; MIXED: box window once a point is seen visible; EXACT: per-point union
@@ -534,7 +531,11 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
       sbound[tid] = vb;
     }
     // stash the MIXED box window in the EXACT-only slots until visibility is known
-    if (cls == kViewMixed) saff[tid].pad = __int_as_float(win.x | (win.y << 8) | (win.z << 16) | (win.w << 24));
+    if (cls == kViewMixed) saff[tid].e.w = __int_as_float(win.x | (win.y << 8) | (win.z << 16) | (win.w << 24));
+    if (P.dbg && cls == kViewMixed) {  // mean eu of the models
+      atomicAdd(P.dbg + 16 * 1000 + 9, (unsigned long long)((0.5f - aff.e.x) * 1e6f));
+      atomicAdd(P.dbg + 16 * 1000 + 10, 1ull);
+    }
   }
   __syncthreads();
   if (tid < 32) {  // ballot compaction: FULL bitmask, MIXED then EXACT list (<= 64 views: two per lane)
@@ -568,32 +569,32 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
   __syncthreads();
   const int nmixed = s_nmixed, nexact = s_nexact;
   uint32_t w0 = s_full[0], w1 = s_full[1];
-  const bool live = valid && !isnan(p.x);  // NaN point: a padding slot (pf_shard_pack_padded)
   const float dx = p.x - 0.5f * (lo[0] + hi[0]), dy = p.y - 0.5f * (lo[1] + hi[1]), dz = p.z - 0.5f * (lo[2] + hi[2]);
-  uint64_t wm = 0ull, seen = 0ull;  // this point's MIXED verdicts; MIXED views this warp saw visible
+  // MIXED views: every point against the tile's model (branch-free); the few samples the model
+  // cannot decide (0.1 % at C5) are re-tested exactly afterwards, per lane
+  uint64_t wm = 0ull, am = 0ull;  // this point's MIXED verdicts: visible / ambiguous
+#pragma unroll 2
   for (int l = 0; l < nmixed; ++l) {
     const int v = s_list[l];
-    const int s = live ? affine_visible(saff[v], P.depth, dx, dy, dz, eps_f) : kInvisible;
-    if (P.dbg && valid) {
-      atomicAdd(P.dbg + 16 * 1000 + 7, 1ull);
-      if (s == kAmbiguous) atomicAdd(P.dbg + 16 * 1000 + 8, 1ull);
-      if (tid == 0) {  // mean bounds
-        atomicAdd(P.dbg + 16 * 1000 + 9, (unsigned long long)(saff[v].eu * 1e6f));
-        atomicAdd(P.dbg + 16 * 1000 + 10, 1ull);
-      }
-    }
-    bool vis = s == kNeedDepth;
-    if (s == kAmbiguous) {  // rare (0.1 % at C5): the exact test
-      TapF t;
-      vis = point_visible(sv[v], sbound[v], P.views[v], P.depth, p, P.eps, eps_f, t);
-    }
+    bool vis, amb;
+    affine_visible(saff[v], P.depth, dx, dy, dz, eps_f, vis, amb);
     const uint64_t bit = 1ull << v;
     wm |= vis ? bit : 0ull;
-    seen |= __any_sync(0xffffffffu, vis) ? bit : 0ull;
+    am |= amb ? bit : 0ull;
+  }
+  if (!live) wm = am = 0ull;
+  if (P.dbg && tid == 0) atomicAdd(P.dbg + 16 * 1000 + 7, (unsigned long long)nmixed * 128ull);
+  if (P.dbg && am) atomicAdd(P.dbg + 16 * 1000 + 8, (unsigned long long)__popcll(am));
+  while (am) {  // rare: the exact test
+    const int v = __ffsll((long long)am) - 1;
+    am &= am - 1ull;
+    TapF t;
+    if (point_visible(sv[v], sbound[v], P.views[v], P.depth, p, P.eps, eps_f, t)) wm |= 1ull << v;
   }
   w0 |= (uint32_t)wm;
   w1 |= (uint32_t)(wm >> 32);
-  const uint32_t seen0 = (uint32_t)seen, seen1 = (uint32_t)(seen >> 32);
+  // MIXED views this warp saw visible
+  const uint32_t seen0 = __reduce_or_sync(0xffffffffu, (uint32_t)wm), seen1 = __reduce_or_sync(0xffffffffu, (uint32_t)(wm >> 32));
   if (lane == 0 && (seen0 | seen1)) {
     atomicOr(&s_seen[0], seen0);
     atomicOr(&s_seen[1], seen1);
@@ -626,7 +627,7 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
   }
   __syncthreads();
   if (tid < P.nv && s_cls[tid] == kViewMixed && ((s_seen[tid >> 5] >> (tid & 31)) & 1u)) {
-    const uint32_t w = __float_as_uint(saff[tid].pad);  // the box window (every visible point's taps)
+    const uint32_t w = __float_as_uint(saff[tid].e.w);  // the box window (every visible point's taps)
     wx0[tid] = (int)(w & 0xff);
     wy0[tid] = (int)((w >> 8) & 0xff);
     wx1[tid] = (int)((w >> 16) & 0xff);
