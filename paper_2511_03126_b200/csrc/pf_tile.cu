@@ -241,8 +241,10 @@ struct MixModel {
   float4 cu;  // u = b (qu b + ku a + kb) + (su a + u0): {su, kb, ku, qu}
   float4 cv;  // v = b (qv b + kv c + kc) + (sv c + v0): {sv, kc, kv, qv}
   float4 e;   // {0.5 - eu, 0.5 - ev (rounded down), ez, box window (packed bytes, MIXED -> seen)}
-  int4 g;     // {W, H, depth offset lo, hi}
+  int2 wh;    // depth map W, H
+  const float* dmap;  // this view's depth map
 };
+static_assert(sizeof(MixModel) == 112, "7 x 16 B");
 
 // Decide one view for every point of a tile at once. The points lie in the box [lo, hi] (exact:
 // min / max of their f32 coordinates). Camera coordinates are affine in p, so the camera depth over
@@ -274,27 +276,43 @@ __device__ __forceinline__ double rcp_f64(double z) {
   return fma(r, fma(-z, r, 1.0), r);
 }
 
+// Two threads per view (lanes 2j, 2j + 1 of a warp: `h` = 0 / 1, `pm` = the pair's lane mask) share
+// the work: corners with z = lo / hi, alternate rows of the depth scan, and the u / v halves of the
+// MIXED model; shuffles combine them, so both threads take the same decision. The MIXED model is
+// written straight into `aff` (shared memory).
+__device__ __forceinline__ float pair_min(unsigned pm, float x) { return fminf(x, __shfl_xor_sync(pm, x, 1)); }
+__device__ __forceinline__ float pair_max(unsigned pm, float x) { return fmaxf(x, __shfl_xor_sync(pm, x, 1)); }
+
 __device__ __forceinline__ int classify_tile_view(const ViewF& v, const float4& vb, const pf_view_t& v64,
-                                  const float* __restrict__ depth, const float* lo, const float* hi, float eps,
-                                  int4& win, MixModel& aff) {
+                                                  const float* __restrict__ depth, const float* lo, const float* hi,
+                                                  float eps, int h, unsigned pm, bool store, int4& win,
+                                                  MixModel& aff) {
   float zmin = 1e30f, zmax = -1e30f, umin = 1e30f, umax = -1e30f, vmin = 1e30f, vmax = -1e30f;
+  {
+    const float pz = h ? hi[2] : lo[2];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const float px = (c & 1) ? hi[0] : lo[0];
-    const float py = (c & 2) ? hi[1] : lo[1];
-    const float pz = (c & 4) ? hi[2] : lo[2];
-    const float X = fmaf(v.R[2], pz, fmaf(v.R[1], py, v.R[0] * px)) + v.t[0];
-    const float Y = fmaf(v.R[5], pz, fmaf(v.R[4], py, v.R[3] * px)) + v.t[1];
-    const float Z = fmaf(v.R[8], pz, fmaf(v.R[7], py, v.R[6] * px)) + v.t[2];
-    zmin = fminf(zmin, Z);
-    zmax = fmaxf(zmax, Z);
-    const float rz = 1.f / Z;
-    const float u = fmaf(v.fx, X * rz, v.cx), w = fmaf(v.fy, Y * rz, v.cy);
-    umin = fminf(umin, u);
-    umax = fmaxf(umax, u);
-    vmin = fminf(vmin, w);
-    vmax = fmaxf(vmax, w);
+    for (int c = 0; c < 4; ++c) {
+      const float px = (c & 1) ? hi[0] : lo[0];
+      const float py = (c & 2) ? hi[1] : lo[1];
+      const float X = fmaf(v.R[2], pz, fmaf(v.R[1], py, v.R[0] * px)) + v.t[0];
+      const float Y = fmaf(v.R[5], pz, fmaf(v.R[4], py, v.R[3] * px)) + v.t[1];
+      const float Z = fmaf(v.R[8], pz, fmaf(v.R[7], py, v.R[6] * px)) + v.t[2];
+      zmin = fminf(zmin, Z);
+      zmax = fmaxf(zmax, Z);
+      const float rz = __frcp_rn(Z);  // (the 0.01 px widening below covers the fp32 corner error)
+      const float u = fmaf(v.fx, X * rz, v.cx), w = fmaf(v.fy, Y * rz, v.cy);
+      umin = fminf(umin, u);
+      umax = fmaxf(umax, u);
+      vmin = fminf(vmin, w);
+      vmax = fmaxf(vmax, w);
+    }
   }
+  zmin = pair_min(pm, zmin);
+  zmax = pair_max(pm, zmax);
+  umin = pair_min(pm, umin);
+  umax = pair_max(pm, umax);
+  vmin = pair_min(pm, vmin);
+  vmax = pair_max(pm, vmax);
   if (!(zmin > 1e-3f)) return kViewExact;  // the box reaches the camera plane
   const float ulo = fmaxf(umin - 0.01f, -1e6f), uhi = fminf(umax + 0.01f, 1e6f);
   const float vlo = fmaxf(vmin - 0.01f, -1e6f), vhi = fminf(vmax + 0.01f, 1e6f);
@@ -303,14 +321,18 @@ __device__ __forceinline__ int classify_tile_view(const ViewF& v, const float4& 
   if (cx1 < cx0 || cy1 < cy0) return kViewOff;
   const int bw = cx1 - cx0 + 1, bh = cy1 - cy0 + 1;
   if (bw * bh > kScanMax) return kViewExact;
-  const float* d = depth + v.depth_off + (int64_t)cy0 * v.W + cx0;
   float dmax = 0.f, dmin = 1e30f;
-  for (int y = 0; y < bh; ++y, d += v.W)
-    for (int x = 0; x < bw; x += 2) {  // two independent loads per step
-      const float s0 = __ldg(d + x), s1 = __ldg(d + min(x + 1, bw - 1));
-      dmax = fmaxf(dmax, fmaxf(s0, s1));
-      dmin = fminf(dmin, fminf(s0, s1));
-    }
+  {
+    const float* d = depth + v.depth_off + (int64_t)(cy0 + h) * v.W + cx0;
+    for (int y = h; y < bh; y += 2, d += 2 * v.W)
+      for (int x = 0; x < bw; x += 2) {  // two independent loads per step
+        const float s0 = __ldg(d + x), s1 = __ldg(d + min(x + 1, bw - 1));
+        dmax = fmaxf(dmax, fmaxf(s0, s1));
+        dmin = fminf(dmin, fminf(s0, s1));
+      }
+  }
+  dmax = pair_max(pm, dmax);
+  dmin = pair_min(pm, dmin);
   if (zmin - 1e-5f > dmax + eps + 1e-5f) return kViewOff;
   // tap window of every point (taps_f32 on the widened range; fu is monotone in u)
   const float fu0 = __fsub_rn(__fmul_rn(__fadd_rn(ulo, 0.5f), v.ru), 0.5f);
@@ -325,42 +347,50 @@ __device__ __forceinline__ int classify_tile_view(const ViewF& v, const float4& 
   const bool inside = x0 >= 0 && y0 >= 0 && x1 < v.W && y1 < v.H;
   if (inside && dmin > 0.f && zmax + 2e-5f < dmin + eps) return kViewFull;
   if (!(vb.w > 0.f)) return kViewExact;  // no constant fp32 bound for this view
-  // MIXED: affine model around the box centre
+  // MIXED: second-order model around the box centre
   const float ox = 0.5f * (lo[0] + hi[0]), oy = 0.5f * (lo[1] + hi[1]), oz = 0.5f * (lo[2] + hi[2]);
   const float hx = 0.5f * (hi[0] - lo[0]), hy = 0.5f * (hi[1] - lo[1]), hz = 0.5f * (hi[2] - lo[2]);
   const float r = sqrtf(hx * hx + hy * hy + hz * hz) * 1.0001f + 1e-7f;
   // the model's value at o in fp64 with the reference's camera: |u0 - u64(o)| is only the final
-  // rounding to fp32 (+ ~1e-13), so no fp32 projection bound enters
-  const double X0 = cam_row(v64.R, 0, ox, oy, oz, v64.t[0]), Y0 = cam_row(v64.R, 1, ox, oy, oz, v64.t[1]);
+  // rounding to fp32 (+ ~1e-13), so no fp32 projection bound enters. Thread h builds the u (h = 0)
+  // or the v (h = 1) half: W0 = X0 or Y0, f = fx or fy, ...
   const double Z0 = cam_row(v64.R, 2, ox, oy, oz, v64.t[2]);
+  const double W0 = cam_row(v64.R, h, ox, oy, oz, v64.t[h]);
+  const double f = h ? v64.fy : v64.fx, cc = h ? v64.cy : v64.cx;
   const double rz0 = rcp_f64(Z0);
-  const float u0 = (float)fma(v64.fx * X0, rz0, v64.cx), v0 = (float)fma(v64.fy * Y0, rz0, v64.cy);
-  // second-order model in a = R0.d, c = R1.d, b = R2.d (d = p - o):
+  const float w0 = (float)fma(f * W0, rz0, cc);
+  // second-order model in a = R0.d (c = R1.d for v), b = R2.d (d = p - o):
   //   X/Z = X0/Z0 + a/Z0 - X0 b/Z0^2 - a b/Z0^2 + X0 b^2/Z0^3 + R3,
   //   R3 = a b^2/Z0^3 - (X0 + a) b^3 / (Z0^3 Z),  |R3| <= r^3 ((|X0| + r)/(Z0^3 zmin) + 1/Z0^3)
-  const double su = v64.fx * rz0, sv = v64.fy * rz0, xr = X0 * rz0, yr = Y0 * rz0;
-  const double z0 = Z0, rr = (double)r, zl = (double)zmin;
-  const double r3 = rr * rr * rr * (rz0 * rz0 * rz0);  // bounds below carry a 1.05 factor
-  const double rzl = rcp_f64(zl);
-  const double gu = fabs(su) * (1.0 + fabs(xr)) * rr, gv = fabs(sv) * (1.0 + fabs(yr)) * rr;  // |linear part|
-  const double qu = fabs(su) * rz0 * (1.0 + fabs(xr)) * rr * rr, qv = fabs(sv) * rz0 * (1.0 + fabs(yr)) * rr * rr;
-  // remainder + fp32 rounding of u0 and of the ~6 rounded ops of the evaluation + the fp32 coefficients
-  const double eu = fabs(v64.fx) * r3 * ((fabs(X0) + rr) * rzl + 1.0) * 1.05 + 7e-7 * (fabs(u0) + gu + qu) +
-                    1e-5 * (gu + qu) + 1e-5;
-  const double ev = fabs(v64.fy) * r3 * ((fabs(Y0) + rr) * rzl + 1.0) * 1.05 + 7e-7 * (fabs(v0) + gv + qv) +
-                    1e-5 * (gv + qv) + 1e-5;
-  if (!(eu < 0.25 && ev < 0.25)) return kViewExact;
-  aff.ra = make_float4(v.R[0], v.R[1], v.R[2], u0);
-  aff.rc = make_float4(v.R[3], v.R[4], v.R[5], v0);
-  aff.rb = make_float4(v.R[6], v.R[7], v.R[8], (float)Z0);
-  aff.cu = make_float4((float)su, (float)(-su * xr), (float)(-su * rz0), (float)(su * xr * rz0));
-  aff.cv = make_float4((float)sv, (float)(-sv * yr), (float)(-sv * rz0), (float)(sv * yr * rz0));
-  const float ez = 4.7e-7f * (fabsf((float)z0) + 2.f * r) + 1e-7f;  // z = z0 + b is exactly affine: rounding only
-  // + the 1e-9 floor and the margin / difference roundings
-  aff.e = make_float4(__fsub_rd(0.5f, __double2float_ru(eu)), __fsub_rd(0.5f, __double2float_ru(ev)), ez * 1.0001f + 2e-9f,
-                      0.f);
-  const int64_t doff = v.depth_off;
-  aff.g = make_int4(v.W, v.H, (int)(uint32_t)doff, (int)(doff >> 32));
+  const double sw = f * rz0, wr = W0 * rz0;
+  const double rr = (double)r;
+  const double r3 = rr * rr * rr * (rz0 * rz0 * rz0);  // the bound carries a 1.05 factor
+  const double rzl = rcp_f64((double)zmin);
+  const double gw = fabs(sw) * (1.0 + fabs(wr)) * rr;                 // |linear part|
+  const double qw = fabs(sw) * rz0 * (1.0 + fabs(wr)) * rr * rr;      // |quadratic part|
+  // remainder + fp32 rounding of w0 and of the ~6 rounded ops of the evaluation + the fp32 coefficients
+  const double ew = fabs(f) * r3 * ((fabs(W0) + rr) * rzl + 1.0) * 1.05 + 7e-7 * (fabs(w0) + gw + qw) +
+                    1e-5 * (gw + qw) + 1e-5;
+  const bool ok = ew < 0.25;
+  if (!(ok && __shfl_xor_sync(pm, ok, 1))) return kViewExact;
+  const float4 row = h ? make_float4(v.R[3], v.R[4], v.R[5], w0) : make_float4(v.R[0], v.R[1], v.R[2], w0);
+  const float4 co = make_float4((float)sw, (float)(-sw * wr), (float)(-sw * rz0), (float)(sw * wr * rz0));
+  const float hw = __fsub_rd(0.5f, __double2float_ru(ew));
+  if (!store) {
+  } else if (h == 0) {
+    aff.ra = row;
+    aff.cu = co;
+    aff.e.x = hw;
+    aff.rb = make_float4(v.R[6], v.R[7], v.R[8], (float)Z0);
+    // z = z0 + b is exactly affine: rounding only; + the 1e-9 floor and the margin / difference roundings
+    aff.e.z = (4.7e-7f * (fabsf((float)Z0) + 2.f * r) + 1e-7f) * 1.0001f + 2e-9f;
+    aff.wh = make_int2(v.W, v.H);
+    aff.dmap = depth + v.depth_off;
+  } else {
+    aff.rc = row;
+    aff.cv = co;
+    aff.e.y = hw;
+  }
   return kViewMixed;
 }
 
@@ -425,27 +455,29 @@ __device__ __forceinline__ bool point_visible(const ViewF& v, const float4& b, c
 // MIXED-view decision through the second-order model, branch-free: vis = visible for sure; amb =
 // within the model's bound of a pixel boundary or of the depth threshold (the caller re-tests those
 // samples exactly). Otherwise invisible (off-image, empty pixel, or behind the stored depth).
-__device__ __forceinline__ void affine_visible(const MixModel& m, const float* __restrict__ depth, float dx, float dy,
-                                               float dz, float eps_f, bool& vis, bool& amb) {
+__device__ __forceinline__ void affine_visible(const MixModel& m, float dx, float dy, float dz, float eps_f, bool& vis,
+                                               bool& amb) {
   const float a = fmaf(m.ra.z, dz, fmaf(m.ra.y, dy, m.ra.x * dx));
   const float c = fmaf(m.rc.z, dz, fmaf(m.rc.y, dy, m.rc.x * dx));
   const float b = fmaf(m.rb.z, dz, fmaf(m.rb.y, dy, m.rb.x * dx));
   const float u = fmaf(b, fmaf(m.cu.w, b, fmaf(m.cu.z, a, m.cu.y)), fmaf(m.cu.x, a, m.ra.w));
   const float v = fmaf(b, fmaf(m.cv.w, b, fmaf(m.cv.z, c, m.cv.y)), fmaf(m.cv.x, c, m.rc.w));
-  // |u - rint(u)| (exact in fp32) >= 0.5 - eu  <=>  u within eu of a pixel boundary
+  // |u - rint(u)| (exact in fp32) >= 0.5 - eu  <=>  u within eu of a pixel boundary (bitwise ops: no
+  // short-circuit branches)
   const float ru = rintf(u), rv = rintf(v);
-  const bool amb_uv = fabsf(u - ru) >= m.e.x || fabsf(v - rv) >= m.e.y;
+  const bool amb_uv = (fabsf(u - ru) >= m.e.x) | (fabsf(v - rv) >= m.e.y);
   // one unsigned compare per axis (finite u, v: the model of finite points)
   const int iu = (int)ru, iv = (int)rv;
-  const bool inb = !amb_uv && (unsigned)iu < (unsigned)m.g.x && (unsigned)iv < (unsigned)m.g.y;
-  const int64_t off = ((int64_t)m.g.w << 32) | (uint32_t)m.g.z;
-  const float stored = inb ? __ldg(depth + off + iv * m.g.x + iu) : 0.f;  // a view's map has < 2^31 pixels
+  const bool inb = ((unsigned)iu < (unsigned)m.wh.x) & ((unsigned)iv < (unsigned)m.wh.y) & !amb_uv;
+  float stored = 0.f;
+  if (inb) stored = __ldg(m.dmap + (iv * m.wh.x + iu));  // a view's map has < 2^31 pixels
   const float thr = __fadd_rn(stored, eps_f);  // > 0 when stored > 0
   const float mz = fmaf(2.4e-7f, thr, m.e.z);  // m.e.z includes the 1e-9 floor
   const float dz_ = (m.rb.w + b) - thr;
   const bool hit = stored > 0.f;               // (inb folded in: stored = 0 otherwise)
-  vis = hit && dz_ < -mz;                      // z + mz < thr, up to the margin's own rounding slack
-  amb = amb_uv || (hit && !(dz_ < -mz) && !(dz_ > mz));
+  const bool near = dz_ < -mz;                 // z + mz < thr, up to the margin's own rounding slack
+  vis = hit & near;
+  amb = amb_uv | (hit & !near & !(dz_ > mz));
 }
 
 // ---- k_tile_prep ---------------------------------------------------------------------------------------
@@ -512,29 +544,35 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
     }
   }
   const float eps_f = (float)P.eps;
-  if (tid < P.nv) {
-    const ViewF v = P.viewf[tid];  // per-view fp32 camera + constant error bounds (k_view_setup)
-    const float4 vb = P.vbound[tid];
+  {
+    // two threads per view; every thread runs (a view index past nv repeats the last view and writes
+    // nothing), so the pair shuffles always see both lanes
+    const int cv = tid >> 1, h = tid & 1;
+    const int vj = min(cv, P.nv - 1);
+    const unsigned pm = 3u << (lane & 30);
+    const ViewF v = P.viewf[vj];  // per-view fp32 camera + constant error bounds (k_view_setup)
+    const float4 vb = P.vbound[vj];
     int4 win = make_int4(INT_MAX, INT_MAX, -1, -1);
-    MixModel aff;
-    const int cls = classify_tile_view(v, vb, P.views[tid], P.depth, lo, hi, eps_f, win, aff);
-    s_cls[tid] = (unsigned char)cls;
-    // FULL: box window now; MIXED: box window once a point is seen visible; EXACT: per-point union
-    const bool boxwin = cls == kViewFull;
-    wx0[tid] = boxwin ? win.x : INT_MAX;
-    wy0[tid] = boxwin ? win.y : INT_MAX;
-    wx1[tid] = boxwin ? win.z : -1;
-    wy1[tid] = boxwin ? win.w : -1;
-    if (cls == kViewMixed) saff[tid] = aff;
-    if (cls == kViewMixed || cls == kViewExact) {
-      sv[tid] = v;
-      sbound[tid] = vb;
-    }
-    // stash the MIXED box window in the EXACT-only slots until visibility is known
-    if (cls == kViewMixed) saff[tid].e.w = __int_as_float(win.x | (win.y << 8) | (win.z << 16) | (win.w << 24));
-    if (P.dbg && cls == kViewMixed) {  // mean eu of the models
-      atomicAdd(P.dbg + 16 * 1000 + 9, (unsigned long long)((0.5f - aff.e.x) * 1e6f));
-      atomicAdd(P.dbg + 16 * 1000 + 10, 1ull);
+    const bool mine = cv < P.nv;
+    const int cls = classify_tile_view(v, vb, P.views[vj], P.depth, lo, hi, eps_f, h, pm, mine, win, saff[vj]);
+    if (mine && h == 0) {
+      s_cls[cv] = (unsigned char)cls;
+      // FULL: box window now; MIXED: box window once a point is seen visible; EXACT: per-point union
+      const bool boxwin = cls == kViewFull;
+      wx0[cv] = boxwin ? win.x : INT_MAX;
+      wy0[cv] = boxwin ? win.y : INT_MAX;
+      wx1[cv] = boxwin ? win.z : -1;
+      wy1[cv] = boxwin ? win.w : -1;
+      if (cls == kViewMixed || cls == kViewExact) {  // (re-read: keeps v out of the live range)
+        sv[cv] = P.viewf[cv];
+        sbound[cv] = P.vbound[cv];
+      }
+      // stash the MIXED box window in the model's spare slot until visibility is known
+      if (cls == kViewMixed) saff[cv].e.w = __int_as_float(win.x | (win.y << 8) | (win.z << 16) | (win.w << 24));
+      if (P.dbg && cls == kViewMixed) {  // mean eu of the models
+        atomicAdd(P.dbg + 16 * 1000 + 9, (unsigned long long)((0.5f - saff[cv].e.x) * 1e6f));
+        atomicAdd(P.dbg + 16 * 1000 + 10, 1ull);
+      }
     }
   }
   __syncthreads();
@@ -577,10 +615,10 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
   for (int l = 0; l < nmixed; ++l) {
     const int v = s_list[l];
     bool vis, amb;
-    affine_visible(saff[v], P.depth, dx, dy, dz, eps_f, vis, amb);
+    affine_visible(saff[v], dx, dy, dz, eps_f, vis, amb);
     const uint64_t bit = 1ull << v;
-    wm |= vis ? bit : 0ull;
-    am |= amb ? bit : 0ull;
+    if (vis) wm |= bit;
+    if (amb) am |= bit;
   }
   if (!live) wm = am = 0ull;
   if (P.dbg && tid == 0) atomicAdd(P.dbg + 16 * 1000 + 7, (unsigned long long)nmixed * 128ull);
