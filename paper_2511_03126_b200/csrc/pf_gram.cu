@@ -509,16 +509,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
           }
         }
         const int ab = (int)(wuse & 1u);
-        // expansion centre: box of this warp's valid rows
-        float lo[3] = {rv ? p.x : INFINITY, rv ? p.y : INFINITY, rv ? p.z : INFINITY};
-        float hi[3] = {rv ? p.x : -INFINITY, rv ? p.y : -INFINITY, rv ? p.z : -INFINITY};
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+        // expansion centre: box of this warp's valid rows (order-preserving integer keys: one REDUX
+        // per bound; padding slots (NaN) and rows past the item contribute nothing)
+        float lo[3], hi[3];
+        {
+          const bool bx = rv && !isnan(p.x) && !isnan(p.y) && !isnan(p.z);
+          const float c[3] = {p.x, p.y, p.z};
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
-            lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
-            hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+            lo[a] = key_float(__reduce_min_sync(0xffffffffu, float_key(bx ? c[a] : INFINITY)));
+            hi[a] = key_float(__reduce_max_sync(0xffffffffu, float_key(bx ? c[a] : -INFINITY)));
           }
+        }
         const bool any = lo[0] <= hi[0];
         const float ox = any ? 0.5f * (lo[0] + hi[0]) : 0.f, oy = any ? 0.5f * (lo[1] + hi[1]) : 0.f,
                     oz = any ? 0.5f * (lo[2] + hi[2]) : 0.f;
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
           const float X = fmaf(q0.z, oz, fmaf(q0.y, oy, q0.x * ox)) + q0.w;
           const float Y = fmaf(q1.z, oz, fmaf(q1.y, oy, q1.x * ox)) + q1.w;
           const float Z = fmaf(q2.z, oz, fmaf(q2.y, oy, q2.x * ox)) + q2.w;
-          const float rz = 1.f / Z, xr = X * rz, yr = Y * rz;
+          const float rz = __frcp_rn(Z), xr = X * rz, yr = Y * rz;  // (a first-order model: no IEEE division)
           const float su = mm.x * kk.x * rz, sv = mm.y * kk.z * rz;  // d fu / d X_cam, d fv / d Y_cam
           wc[2 * lane] = make_float4((fmaf(kk.x, xr, kk.y) + 0.5f) * mm.x - 0.5f - (float)(wk.z & 0xff),
                                      su * (q0.x - xr * q2.x), su * (q0.y - xr * q2.y), su * (q0.z - xr * q2.z));

@@ -519,16 +519,15 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
     const bool inbox = live && !isnan(p.y) && !isnan(p.z);
     // tile box: warp min / max as order-preserving integer reductions (one REDUX each); rows past n
     // and padding slots contribute nothing
-    auto key = [](float f) { const int i = __float_as_int(f); return i >= 0 ? i : i ^ 0x7fffffff; };
-    const int b[6] = {__reduce_min_sync(0xffffffffu, key(inbox ? p.x : INFINITY)),
-                      __reduce_min_sync(0xffffffffu, key(inbox ? p.y : INFINITY)),
-                      __reduce_min_sync(0xffffffffu, key(inbox ? p.z : INFINITY)),
-                      __reduce_max_sync(0xffffffffu, key(inbox ? p.x : -INFINITY)),
-                      __reduce_max_sync(0xffffffffu, key(inbox ? p.y : -INFINITY)),
-                      __reduce_max_sync(0xffffffffu, key(inbox ? p.z : -INFINITY))};
+    const int b[6] = {__reduce_min_sync(0xffffffffu, float_key(inbox ? p.x : INFINITY)),
+                      __reduce_min_sync(0xffffffffu, float_key(inbox ? p.y : INFINITY)),
+                      __reduce_min_sync(0xffffffffu, float_key(inbox ? p.z : INFINITY)),
+                      __reduce_max_sync(0xffffffffu, float_key(inbox ? p.x : -INFINITY)),
+                      __reduce_max_sync(0xffffffffu, float_key(inbox ? p.y : -INFINITY)),
+                      __reduce_max_sync(0xffffffffu, float_key(inbox ? p.z : -INFINITY))};
     if (lane == 0)
 #pragma unroll
-      for (int a = 0; a < 6; ++a) sbb[tid >> 5][a] = __int_as_float(b[a] >= 0 ? b[a] : b[a] ^ 0x7fffffff);
+      for (int a = 0; a < 6; ++a) sbb[tid >> 5][a] = key_float(b[a]);
   }
   if (tid < 2) s_seen[tid] = 0u;
   __syncthreads();

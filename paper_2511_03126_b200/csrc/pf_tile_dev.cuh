@@ -8,6 +8,13 @@
 namespace pf {
 namespace tile {
 
+// order-preserving float <-> int keys (signed compare), for warp min / max bounds with one REDUX
+__device__ __forceinline__ int float_key(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float key_float(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
+
 // ---- fp32 projection with a rigorous error bound ----------------------------------------------------
 __device__ __forceinline__ ViewF make_viewf(const pf_view_t& v, int d) {
   ViewF w;
