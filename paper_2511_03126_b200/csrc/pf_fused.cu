@@ -649,6 +649,7 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.max_sub2 = L.max_sub2;
     T.work_count = tr == tile::kGramTile ? reinterpret_cast<int32_t*>(ws + L.work) : nullptr;
     T.work = tr == tile::kGramTile ? reinterpret_cast<int4*>(ws + L.work) + 1 : nullptr;
+    T.work_raw = tr == tile::kGramTile ? reinterpret_cast<int4*>(ws + L.work_raw) : nullptr;
     // split items to the feature-product kernel (PF_GRAM_SPLIT=0: all items in the Gram kernel)
     static const bool split = [] {
       const char* e = getenv("PF_GRAM_SPLIT");
@@ -658,6 +659,7 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.wlist = tr == tile::kGramTile && split ? reinterpret_cast<int4*>(ws + L.wlist) + 1 : nullptr;
     T.partials = a->partials;
     T.tbound = reinterpret_cast<const float*>(ws + L.tbound);
+    T.tbox = tr == tile::kGramTile ? reinterpret_cast<float4*>(ws + L.tbox) : nullptr;
     if (int rc = tile::run_tile_path(T, L, ws, a->points, a->n, st)) return rc;
     // sorted records -> caller's order; then the overflow points (tiles with more taps than fit in
     // shared memory) run through the SIMT kernel, which writes their outputs directly

@@ -223,6 +223,15 @@ __device__ __forceinline__ int4 ld_pref_i4(const void* p) {
   asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
+
+// the k-th item of this CTA: the list is sorted by tap count, descending (k_sort_work), and CTA c
+// takes positions c, 2G - 1 - c, 2G + c, ... (boustrophedon), so every CTA gets a similar mix of
+// heavy and light items (a plain stride left the slowest CTA 3 % behind the mean at C5)
+__device__ __forceinline__ int4 item_at(const TileParams& P, int nwork, int k) {
+  const int g = gridDim.x, c = blockIdx.x;
+  const int i = k * g + ((k & 1) ? g - 1 - c : c);
+  return i < nwork ? ld_pref_i4(P.work + i) : make_int4(-1, 0, 0, 0);
+}
 // work-list entry {item, first row, rows | taps << 16, -}
 __device__ __forceinline__ int e_rows(const int4& e) { return e.z & 0xffff; }
 __device__ __forceinline__ int e_kt(const int4& e) { return e.z >> 16; }
@@ -259,6 +268,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nd = P.d >> 6;
   const int nwork = *P.work_count;
+  unsigned long long t_cta0 = 0;  // PF_GRAM_CTATIME: per-CTA start / end (%globaltimer, ns)
+  if (P.ctatime && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_cta0));
 
   // ---- setup (as k_tile_ws) ----------------------------------------------------------------------
   for (int j = tid; j < P.nv; j += kThreads) {
@@ -305,7 +316,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = S.tmem_base;
-  const int i0 = blockIdx.x, istep = gridDim.x;
 
   if (warp < kMmaWarp || (warp > kMmaWarp && warp < kBuildWarp0)) {
     // ================= loaders: tap rows (D / 64 chunks), then G rows (2 chunks) =================
@@ -314,8 +324,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
     const int q = lt & 7, r0 = lt >> 3;
     int stage = 0;
     uint32_t phase = 0, il = 0;
-    for (int i = i0; i < nwork; i += istep) {
-      const int4 e = P.work[i];
+    for (int k = 0;; ++k) {
+      const int4 e = item_at(P, nwork, k);
+      if (e.x < 0) break;
       const int kt = e_kt(e), ktp = (kt + 15) & ~15;
       int32_t* cell = S.cell[il & 1];
       asm volatile("bar.sync 3, %0;" ::"n"(kLoadThreads) : "memory");
@@ -376,10 +387,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
     uint32_t phase = 0, ruse = 0, wuse = 0;
     const uint32_t idS = tc::idesc_bf16_f32(128, kMaxKpadTC, false, true);
     const uint32_t mt0 = tc::smem_u32(sM);
-    int4 e_nx = i0 < nwork ? ld_pref_i4(P.work + i0) : make_int4(0, 0, 0, 0);
-    for (int i = i0; i < nwork; i += istep) {
-      const int4 e = e_nx;
-      if (i + istep < nwork) e_nx = ld_pref_i4(P.work + i + istep);
+    for (int k = 0;; ++k) {
+      const int4 e = item_at(P, nwork, k);
+      if (e.x < 0) break;
       const int ktp = (e_kt(e) + 15) & ~15, nb = e_nb(e);
       // ---- Gram: block 0 = taps 0..127 x all, block 1 = taps 128.. x taps 128.. ----
       const uint32_t idG0 = tc::idesc_bf16_f32(128, ktp, false, false);
@@ -454,14 +464,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
     int4* wl = S.wlist[bj];     // this warp's views: {view, window base | shape << 16, x0 | y0 << 8 | w << 16 | h << 24, -}
     float4* wc = S.wcoef[bj];   // and their expansion coefficients {A0, A1} for the current block
     uint32_t wuse = 0;
-    int4 e_nx = i0 < nwork ? ld_pref_i4(P.work + i0) : make_int4(0, 0, 0, 0);
-    for (int i = i0; i < nwork; i += istep) {
-      const int4 e = e_nx;
+    for (int k = 0;; ++k) {
+      const int4 e = item_at(P, nwork, k);
+      if (e.x < 0) break;
       PT(23);
       // this item's windows: views lane and lane + 32
       const uint2 d0 = lane < P.nv ? ld_pref_u2(P.tile_desc + (int64_t)e.x * P.nv + lane) : make_uint2(0u, 0u);
       const uint2 d1 = lane + 32 < P.nv ? ld_pref_u2(P.tile_desc + (int64_t)e.x * P.nv + lane + 32) : make_uint2(0u, 0u);
-      if (i + istep < nwork) e_nx = ld_pref_i4(P.work + i + istep);
       const int kt = e_kt(e), ktp = (kt + 15) & ~15, nb = e_nb(e), nrows = e_rows(e);
       float4 p_nx = make_float4(0.f, 0.f, 0.f, 0.f);
       uint2 mw_nx = make_uint2(0u, 0u);
@@ -494,6 +503,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
         if (mine1) put(pos1, lane + 32, d1, c1);
         __syncwarp();
       }
+      // expansion centre: the item's box, the union of the boxes prep recorded for its 128-row tiles
+      // (a superset of its rows' box); the coefficients then serve every 128-row block of the item
+      float ox = 0.f, oy = 0.f, oz = 0.f;
+      bool exact;
+      {
+        float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        const int64_t t0 = (int64_t)e.y / kTile, t1 = ((int64_t)e.y + nrows - 1) / kTile;
+        for (int64_t t = t0; t <= t1; ++t) {
+          const float4 a = ld_pref_f4(P.tbox + 2 * t), c = ld_pref_f4(P.tbox + 2 * t + 1);
+          lo[0] = fminf(lo[0], a.x);
+          lo[1] = fminf(lo[1], a.y);
+          lo[2] = fminf(lo[2], a.z);
+          hi[0] = fmaxf(hi[0], c.x);
+          hi[1] = fmaxf(hi[1], c.y);
+          hi[2] = fmaxf(hi[2], c.z);
+        }
+        const bool any = lo[0] <= hi[0];
+        if (any) {
+          ox = 0.5f * (lo[0] + hi[0]);
+          oy = 0.5f * (lo[1] + hi[1]);
+          oz = 0.5f * (lo[2] + hi[2]);
+        }
+        const float ex = any ? hi[0] - lo[0] : 0.f, ey = any ? hi[1] - lo[1] : 0.f, ez = any ? hi[2] - lo[2] : 0.f;
+        exact = ex * ex + ey * ey + ez * ez > 4.f * kAffineR * kAffineR;
+      }
+      if (!exact && lane < nmine) {  // lane k: coefficients of the warp's k-th view (relative to its window origin)
+        const int4 wk = wl[lane];
+        const float4* vp = S.vpk[wk.x];
+        const float4 q0 = vp[0], q1 = vp[1], q2 = vp[2], kk = vp[3], mm = vp[4];
+        const float X = fmaf(q0.z, oz, fmaf(q0.y, oy, q0.x * ox)) + q0.w;
+        const float Y = fmaf(q1.z, oz, fmaf(q1.y, oy, q1.x * ox)) + q1.w;
+        const float Z = fmaf(q2.z, oz, fmaf(q2.y, oy, q2.x * ox)) + q2.w;
+        const float rz = __frcp_rn(Z), xr = X * rz, yr = Y * rz;  // (a first-order model: no IEEE division)
+        const float su = mm.x * kk.x * rz, sv = mm.y * kk.z * rz;  // d fu / d X_cam, d fv / d Y_cam
+        wc[2 * lane] = make_float4((fmaf(kk.x, xr, kk.y) + 0.5f) * mm.x - 0.5f - (float)(wk.z & 0xff),
+                                   su * (q0.x - xr * q2.x), su * (q0.y - xr * q2.y), su * (q0.z - xr * q2.z));
+        wc[2 * lane + 1] = make_float4((fmaf(kk.z, yr, kk.w) + 0.5f) * mm.y - 0.5f - (float)((wk.z >> 8) & 0xff),
+                                       sv * (q1.x - yr * q2.x), sv * (q1.y - yr * q2.y), sv * (q1.z - yr * q2.z));
+      }
+      __syncwarp();
       PT(12);
       for (int b = 0; b < nb; ++b) {
         const float4 p = p_nx;
@@ -509,38 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
           }
         }
         const int ab = (int)(wuse & 1u);
-        // expansion centre: box of this warp's valid rows (order-preserving integer keys: one REDUX
-        // per bound; padding slots (NaN) and rows past the item contribute nothing)
-        float lo[3], hi[3];
-        {
-          const bool bx = rv && !isnan(p.x) && !isnan(p.y) && !isnan(p.z);
-          const float c[3] = {p.x, p.y, p.z};
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            lo[a] = key_float(__reduce_min_sync(0xffffffffu, float_key(bx ? c[a] : INFINITY)));
-            hi[a] = key_float(__reduce_max_sync(0xffffffffu, float_key(bx ? c[a] : -INFINITY)));
-          }
-        }
-        const bool any = lo[0] <= hi[0];
-        const float ox = any ? 0.5f * (lo[0] + hi[0]) : 0.f, oy = any ? 0.5f * (lo[1] + hi[1]) : 0.f,
-                    oz = any ? 0.5f * (lo[2] + hi[2]) : 0.f;
-        const float ex = any ? hi[0] - lo[0] : 0.f, ey = any ? hi[1] - lo[1] : 0.f, ez = any ? hi[2] - lo[2] : 0.f;
-        const bool exact = ex * ex + ey * ey + ez * ez > 4.f * kAffineR * kAffineR;
         const float dxp = p.x - ox, dyp = p.y - oy, dzp = p.z - oz;
-        if (!exact && lane < nmine) {  // lane k: coefficients of the warp's k-th view (relative to its window origin)
-          const int4 wk = wl[lane];
-          const float4* vp = S.vpk[wk.x];
-          const float4 q0 = vp[0], q1 = vp[1], q2 = vp[2], kk = vp[3], mm = vp[4];
-          const float X = fmaf(q0.z, oz, fmaf(q0.y, oy, q0.x * ox)) + q0.w;
-          const float Y = fmaf(q1.z, oz, fmaf(q1.y, oy, q1.x * ox)) + q1.w;
-          const float Z = fmaf(q2.z, oz, fmaf(q2.y, oy, q2.x * ox)) + q2.w;
-          const float rz = __frcp_rn(Z), xr = X * rz, yr = Y * rz;  // (a first-order model: no IEEE division)
-          const float su = mm.x * kk.x * rz, sv = mm.y * kk.z * rz;  // d fu / d X_cam, d fv / d Y_cam
-          wc[2 * lane] = make_float4((fmaf(kk.x, xr, kk.y) + 0.5f) * mm.x - 0.5f - (float)(wk.z & 0xff),
-                                     su * (q0.x - xr * q2.x), su * (q0.y - xr * q2.y), su * (q0.z - xr * q2.z));
-          wc[2 * lane + 1] = make_float4((fmaf(kk.z, yr, kk.w) + 0.5f) * mm.y - 0.5f - (float)((wk.z >> 8) & 0xff),
-                                         sv * (q1.x - yr * q2.x), sv * (q1.y - yr * q2.y), sv * (q1.z - yr * q2.z));
-        }
         __syncwarp();
         PT(13);
         GWAITP(&S.a_empty[ab], ((wuse >> 1) & 1u) ^ 1u, 6);
@@ -746,10 +764,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
     for (int q = 0; q < kHalfK / 32; ++q) wsum[q] = 0.f;
     float pm_sum = 0.f, pmx = 0.f, pmy = 0.f, pmz = 0.f, featured_n = 0.f, pairs = 0.f;
     const bool p_wide = P.p > 2;
-    int4 e_nx = i0 < nwork ? ld_pref_i4(P.work + i0) : make_int4(0, 0, 0, 0);
-    for (int i = i0; i < nwork; i += istep) {
-      const int4 e = e_nx;
-      if (i + istep < nwork) e_nx = ld_pref_i4(P.work + i + istep);
+    for (int k = 0;; ++k) {
+      const int4 e = item_at(P, nwork, k);
+      if (e.x < 0) break;
       const int ktp = (e_kt(e) + 15) & ~15, nb = e_nb(e), nrows = e_rows(e);
       uint2 rec_nx = make_uint2(0u, 0u);
       float4 pc_nx = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1015,6 +1032,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
   tc::fence_before_sync();
   __syncthreads();
   if (warp == kAccWarp0) tc::tmem_dealloc(tbase, 512);
+  if (P.ctatime && threadIdx.x == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    P.ctatime[2 * blockIdx.x] = t_cta0;
+    P.ctatime[2 * blockIdx.x + 1] = t1;
+  }
 #undef PT
 }
 
@@ -1033,7 +1056,7 @@ __global__ void k_collect_work(TileParams P) {
     // Gram product (kt^2 D) costs more than the feature product (128 kt D) once kt exceeds ~128. (Not
     // by row count: the last 512-row tile of an object may be short but is still a 512-row item.)
     if (P.wlist && item >= nt) P.wlist[atomicAdd(P.wcount, 1)] = e;
-    else P.work[atomicAdd(P.work_count, 1)] = e;
+    else P.work_raw[atomicAdd(P.work_count, 1)] = e;
   };
   auto overflow = [&](int64_t row0, int rows) {
     for (int r = lane; r < rows; r += 32) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(P.spts[row0 + r].w);
@@ -1075,6 +1098,33 @@ __global__ void k_collect_work(TileParams P) {
   }
 }
 
+// The collected list (arbitrary order: atomics) -> P.work sorted by estimated cost, descending: a
+// counting sort over 32 buckets of rows x taps in one CTA (C5: 32k items, a few microseconds).
+__global__ void __launch_bounds__(1024) k_sort_work(TileParams P) {
+  __shared__ int cnt[32];
+  const int n = *P.work_count, tid = threadIdx.x;
+  auto key = [](const int4& e) { return 31 - min((e_nb(e) * e_kt(e)) >> 5, 31); };
+  if (tid < 32) cnt[tid] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) atomicAdd(&cnt[key(P.work_raw[i])], 1);
+  __syncthreads();
+  if (tid < 32) {  // exclusive scan of the 32 bucket counts
+    const int c = cnt[tid];
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (tid >= o) incl += t;
+    }
+    cnt[tid] = incl - c;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) {
+    const int4 e = P.work_raw[i];
+    P.work[atomicAdd(&cnt[key(e)], 1)] = e;
+  }
+}
+
 }  // namespace
 
 int run_tile_gram(const TileParams& P, cudaStream_t st) {
@@ -1095,9 +1145,17 @@ int run_tile_gram(const TileParams& P, cudaStream_t st) {
   if (P.wlist) cudaMemsetAsync(P.wcount, 0, sizeof(int32_t), st);
   k_collect_work<<<grid_for(32 * (ntiles + 4 * (int64_t)P.max_sub2), 256, 148 * 8), 256, 0, st>>>(P);
   if (int rc = check_launch("collect_work")) return rc;
+  k_sort_work<<<1, 1024, 0, st>>>(P);
+  if (int rc = check_launch("sort_work")) return rc;
   const bool debug = getenv("PF_WS_DEBUG") != nullptr;
   static unsigned long long* dbg = nullptr;
   TileParams Q = P;
+  static unsigned long long* ctat = nullptr;
+  const bool ctatime = getenv("PF_GRAM_CTATIME") != nullptr;
+  if (ctatime) {
+    if (!ctat) cudaMalloc(&ctat, sizeof(unsigned long long) * 2 * 1024);
+    Q.ctatime = ctat;
+  }
   if (const char* ab = getenv("PF_GRAM_ABLATE")) Q.ablate = atoi(ab);
   if (debug) {
     if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 32 * 1024);
@@ -1110,6 +1168,21 @@ int run_tile_gram(const TileParams& P, cudaStream_t st) {
     k_tile_gram<false, false><<<grid, kThreads, smem, st>>>(Q);
   }
   int rc = check_launch("tile_gram");
+  if (ctatime && rc == PF_OK) {  // CTA time spread of this launch (production instantiation)
+    static unsigned long long h[2 * 1024];
+    cudaMemcpyAsync(h, ctat, sizeof(unsigned long long) * 2 * grid, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long s0 = ~0ull, e1 = 0, e0 = ~0ull;
+    double mean = 0;
+    for (int b = 0; b < grid; ++b) {
+      s0 = h[2 * b] < s0 ? h[2 * b] : s0;
+      e1 = h[2 * b + 1] > e1 ? h[2 * b + 1] : e1;
+      e0 = h[2 * b + 1] < e0 ? h[2 * b + 1] : e0;
+      mean += (double)(h[2 * b + 1] - h[2 * b]) / grid;
+    }
+    fprintf(stderr, "[gram ctatime] span %.3f ms, first CTA done at %.3f ms, mean CTA %.3f ms\n", (e1 - s0) * 1e-6,
+            (e0 - s0) * 1e-6, mean * 1e-6);
+  }
   if (rc == PF_OK && P.wlist) {  // the split 128 / 32-row items (a device-side list, maybe empty)
     TileParams W = P;
     W.kt_max = kGramKt;
@@ -1130,7 +1203,12 @@ int run_tile_gram(const TileParams& P, cudaStream_t st) {
       for (int b = 0; b < grid; ++b) sum += (double)h[b * 32 + q];
       fprintf(stderr, " %s=%.3g", names[q], sum / grid);
     }
-    fprintf(stderr, "\n");
+    double tmin = 1e300, tmax = 0;  // per-CTA spread of the total (static item striding)
+    for (int b = 0; b < grid; ++b) {
+      tmin = h[b * 32 + 11] < tmin ? (double)h[b * 32 + 11] : tmin;
+      tmax = h[b * 32 + 11] > tmax ? (double)h[b * 32 + 11] : tmax;
+    }
+    fprintf(stderr, " total_min=%.3g total_max=%.3g\n", tmin, tmax);
   }
   return rc;
 }

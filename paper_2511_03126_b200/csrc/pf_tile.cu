@@ -543,6 +543,10 @@ __global__ void __launch_bounds__(TR, TR == kTile ? 8 : 2) k_tile_prep(TileParam
     }
   }
   const float eps_f = (float)P.eps;
+  if (P.tbox && tid == 0) {
+    P.tbox[2 * tile] = make_float4(lo[0], lo[1], lo[2], 0.f);
+    P.tbox[2 * tile + 1] = make_float4(hi[0], hi[1], hi[2], 0.f);
+  }
   {
     // two threads per view; every thread runs (a view index past nv repeats the last view and writes
     // nothing), so the pair shuffles always see both lanes
@@ -996,6 +1000,8 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d, bool 
   L.ovf = take(sizeof(int32_t) * (size_t)(n + 1));
   L.work = tr == kTile ? 0 : take(sizeof(int4) * (size_t)(items + 1));  // [count | pad] then entries
   L.wlist = tr == kTile ? 0 : take(sizeof(int4) * (size_t)(items + 1));  // split items for k_tile_ws
+  L.work_raw = tr == kTile ? 0 : take(sizeof(int4) * (size_t)items);  // unsorted work list
+  L.tbox = tr == kTile ? 0 : take(2 * sizeof(float4) * (size_t)((n + kTile - 1) / kTile));  // 128-row tile boxes
   L.bytes = off;
   return L;
 }

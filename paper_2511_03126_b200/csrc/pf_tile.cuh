@@ -112,17 +112,22 @@ struct TileParams {
   // rows | taps << 16, 0}, k_collect_work) and its length
   int4* work;
   int32_t* work_count;
+  int4* work_raw;  // k_collect_work's output (arbitrary order); k_sort_work -> work
   // Gram path: the 128- and 32-row items (split tiles) run in k_tile_ws from this list instead
   // (same entry format); nullptr: k_tile_ws walks its own tile / sub-tile items
   int4* wlist;
   int32_t* wcount;
   const float* tbound;  // max_k |t_k| (run_text_bound, per object): bounds the softmax exponents
+  // Gram path: box of every 128-row tile ({lo.xyz, -}, {hi.xyz, -}; k_tile_prep): the builders'
+  // expansion centre of an item
+  float4* tbox;
+  unsigned long long* ctatime;  // optional per-CTA start / end times of the Gram kernel (PF_GRAM_CTATIME)
 };
 
 struct TileLayout {
   int64_t ntiles;
   int32_t max_sub_tiles, max_sub2;
-  size_t keys, hist, totals, keys_out, idx, idx_out, sort_tmp, inv, spts, srec, desc, kt, ovf, sub, sub2, work, wlist, gbf, textbf, viewf, vbound, vox, tbound, glo, fhi, flo, textlo,
+  size_t keys, hist, totals, keys_out, idx, idx_out, sort_tmp, inv, spts, srec, desc, kt, ovf, sub, sub2, work, work_raw, wlist, tbox, gbf, textbf, viewf, vbound, vox, tbound, glo, fhi, flo, textlo,
       bytes;
 };
 
