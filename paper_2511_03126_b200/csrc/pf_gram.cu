@@ -1102,11 +1102,17 @@ __global__ void k_collect_work(TileParams P) {
 // counting sort over 32 buckets of rows x taps in one CTA (C5: 32k items, a few microseconds).
 __global__ void __launch_bounds__(1024) k_sort_work(TileParams P) {
   __shared__ int cnt[32];
-  const int n = *P.work_count, tid = threadIdx.x;
+  const int n = *P.work_count, tid = threadIdx.x, lane = tid & 31;
   auto key = [](const int4& e) { return 31 - min((e_nb(e) * e_kt(e)) >> 5, 31); };
   if (tid < 32) cnt[tid] = 0;
   __syncthreads();
-  for (int i = tid; i < n; i += blockDim.x) atomicAdd(&cnt[key(P.work_raw[i])], 1);
+  // warp-aggregated counts (most items of a warp share a bucket); the loop bound is warp-uniform
+  for (int i0 = tid - lane; i0 < n; i0 += blockDim.x) {
+    const int i = i0 + lane;
+    const int kk = i < n ? key(P.work_raw[i]) : -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, kk);
+    if (kk >= 0 && (peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&cnt[kk], __popc(peers));
+  }
   __syncthreads();
   if (tid < 32) {  // exclusive scan of the 32 bucket counts
     const int c = cnt[tid];
@@ -1119,9 +1125,16 @@ __global__ void __launch_bounds__(1024) k_sort_work(TileParams P) {
     cnt[tid] = incl - c;
   }
   __syncthreads();
-  for (int i = tid; i < n; i += blockDim.x) {
-    const int4 e = P.work_raw[i];
-    P.work[atomicAdd(&cnt[key(e)], 1)] = e;
+  for (int i0 = tid - lane; i0 < n; i0 += blockDim.x) {
+    const int i = i0 + lane;
+    const int4 e = i < n ? P.work_raw[i] : make_int4(0, 0, 0, 0);
+    const int kk = i < n ? key(e) : -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, kk);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (kk >= 0 && lane == leader) base = atomicAdd(&cnt[kk], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    if (kk >= 0) P.work[base + __popc(peers & ((1u << lane) - 1u))] = e;
   }
 }
 
