@@ -518,6 +518,10 @@ def run_ours(args, cfg):
                     # the SURVEY §8d algorithmic count (8 D per visible sample + 2 N D K) the formulation
                     # avoids most of (similarity through the G table, |F| through the Gram matrix)
                     "effective_frac": eff / tc_peak, "algorithmic_flop_per_launch": algo_flop,
+                    "effective_note": "SURVEY 8d FLOPs / kernel time / peak: may exceed 1, the Gram formulation "
+                                      "executes fewer FLOPs than the reference algorithm",
+                    "kernel_scope": "the tile stage on its stream: work-list build + sort, the tcgen05 kernel, and "
+                                    "(Gram path) the feature-product kernel over the split items",
                     "hbm": {"algorithmic_bytes_per_launch": algo,
                             "achieved_gbs": algo / (t_dom * 1e-3) / 1e9, "peak_gbs": hbm_peak,
                             "frac": algo / (t_dom * 1e-3) / 1e9 / hbm_peak,

@@ -471,6 +471,15 @@ static bool tile_gram(const pf_fuse_args_t* a) {
   return !off && a->fmap_dtype == PF_BF16 && !(a->flags & (PF_FUSE_WRITE_FEATURES | PF_FUSE_FEATURE_KERNEL));
 }
 static int tile_rows(const pf_fuse_args_t* a) { return tile_gram(a) ? tile::kGramTile : tile::kTile; }
+// Gram path: split items (128 / 32 rows) to the feature-product kernel (PF_GRAM_SPLIT=0: all items in
+// the Gram kernel)
+static bool gram_split() {
+  static const bool split = [] {
+    const char* e = getenv("PF_GRAM_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return split;
+}
 
 static uint64_t g_bytes(const pf_fuse_args_t* a) {
   const uint64_t g = (uint64_t)total_cells(a) * (uint64_t)(32 * kpl_of(a->k)) * sizeof(float);
@@ -650,11 +659,7 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.work_count = tr == tile::kGramTile ? reinterpret_cast<int32_t*>(ws + L.work) : nullptr;
     T.work = tr == tile::kGramTile ? reinterpret_cast<int4*>(ws + L.work) + 1 : nullptr;
     T.work_raw = tr == tile::kGramTile ? reinterpret_cast<int4*>(ws + L.work_raw) : nullptr;
-    // split items to the feature-product kernel (PF_GRAM_SPLIT=0: all items in the Gram kernel)
-    static const bool split = [] {
-      const char* e = getenv("PF_GRAM_SPLIT");
-      return !(e && e[0] == '0');
-    }();
+    const bool split = gram_split();
     T.wcount = tr == tile::kGramTile && split ? reinterpret_cast<int32_t*>(ws + L.wlist) : nullptr;
     T.wlist = tr == tile::kGramTile && split ? reinterpret_cast<int4*>(ws + L.wlist) + 1 : nullptr;
     T.partials = a->partials;
@@ -722,6 +727,17 @@ int pf_tile_executed_flops(const pf_fuse_args_t* a, double* flops, void* stream)
       const int rows = w[i].z & 0xffff, kt = w[i].z >> 16, ktp = (kt + 15) & ~15, nb = (rows + 127) / 128;
       f += 2.0 * 128.0 * ktp * a->d + (ktp > 128 ? 2.0 * 128.0 * (ktp - 128) * a->d : 0.0);
       f += (double)nb * 2.0 * 128.0 * ktp * (double)(tile::kMaxKpadTC + ktp);
+    }
+    // the split items the feature-product kernel ran from its list (M = 128 per item)
+    int32_t nl = 0;
+    if (gram_split()) cudaMemcpy(&nl, ws + L.wlist, sizeof(int32_t), cudaMemcpyDeviceToHost);
+    if (nl > 0) {
+      std::vector<int4> wl((size_t)nl);
+      cudaMemcpy(wl.data(), ws + L.wlist + sizeof(int4), sizeof(int4) * nl, cudaMemcpyDeviceToHost);
+      for (const int4& e : wl) {
+        const int ktp = ((e.z >> 16) + 15) & ~15;
+        f += 2.0 * 128.0 * ktp * (double)(a->d + tile::kMaxKpadTC);
+      }
     }
     *flops = f;
     return check_launch("tile_executed_flops");
