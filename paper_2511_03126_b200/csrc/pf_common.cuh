@@ -16,6 +16,25 @@
 
 namespace pf {
 
+// PF_CHECK builds (nvcc -DPF_CHECK): device-side bounds checks on the indexed accesses of the tile
+// path (gathered tap rows, window slots, sorted-record rows, work-list slots); a violation prints
+// its site and traps, turning a silent out-of-bounds access into a launch error. The substitute for
+// compute-sanitizer memcheck, which is closed on this pool.
+#ifdef PF_CHECK
+#define PF_DCHECK(cond, what)                                                                          \
+  do {                                                                                                 \
+    if (!(cond)) {                                                                                     \
+      printf("PF_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                        \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define PF_DCHECK(cond, what) \
+  do {                        \
+  } while (0)
+#endif
+
 constexpr int kWarp = 32;
 
 // ---- host-side status plumbing (defined in pf_host.cu) ---------------------------------------

@@ -44,20 +44,26 @@ namespace tile {
 namespace {
 
 #ifndef PF_GRAM_BUILD_GROUPS
-#define PF_GRAM_BUILD_GROUPS 2  // 8 builder warps, 7 loader warps (measured: 3 groups + 3 loaders is slower)
+#define PF_GRAM_BUILD_GROUPS 2  // 8 builder warps (3 groups with 3 loader warps was measured slower)
 #endif
-// warps 0-2 (and 4 .. kBuildWarp0-1): tap-row loaders; warp 3: MMA issuer; kBuildWarp0 ..15: W builders
-// (kBuildGroups per TMEM lane quarter); warps 16-23: accumulators
+#ifndef PF_GRAM_LOAD_WARPS
+#define PF_GRAM_LOAD_WARPS 7
+#endif
+#ifndef PF_GRAM_REG_ACC
+#define PF_GRAM_REG_ACC 144
+#endif
+// warps 0-2 and 4 .. kBuildWarp0-1: tap-row loaders; warp 3: MMA issuer; kBuildWarp0 ..: W builders
+// (kBuildGroups per TMEM lane quarter); the last 8 warps: accumulators (two per lane quarter)
 constexpr int kBuildGroups = PF_GRAM_BUILD_GROUPS;
 constexpr int kBuildWarps = 4 * kBuildGroups;
-constexpr int kBuildWarp0 = 16 - kBuildWarps;
-constexpr int kLoadWarps = kBuildWarp0 - 1;
+constexpr int kLoadWarps = PF_GRAM_LOAD_WARPS;
+constexpr int kBuildWarp0 = kLoadWarps + 1;
 constexpr int kLoadThreads = 32 * kLoadWarps;
 constexpr int kMmaWarp = 3;
 constexpr int kBuildThreads = 32 * kBuildWarps;
-constexpr int kAccWarp0 = 16;       // warps 16-23: accumulators (two per lane quarter)
+constexpr int kAccWarp0 = kBuildWarp0 + kBuildWarps;
 constexpr int kAccThreads = 256;
-constexpr int kThreads = 768;
+constexpr int kThreads = 32 * (kAccWarp0 + 8);
 constexpr float kAffineR = 12e-3f;  // blocks wider than 2 kAffineR build with the exact projection
 constexpr int kKt = kGramKt;        // taps per work item
 constexpr int kStageBytes = kKt * 128;
@@ -67,11 +73,14 @@ constexpr int kMtBytes = 3 * kChunkBytes;
 constexpr int kRowStep = kLoadThreads / 8;
 constexpr int kRowsPer = (kKt + kRowStep - 1) / kRowStep;
 constexpr int kHalfK = kMaxKpadTC / 2;
-constexpr int kRegProducer = 48, kRegAcc = 144;
+constexpr int kRegProducer = 48, kRegAcc = PF_GRAM_REG_ACC;
+// registers per thread at launch (the pool setmaxnreg redistributes): 64K / threads, multiple of 8
+constexpr int kRegLaunch = (65536 / kThreads) & ~7;
 constexpr uint32_t kColS = 0, kColY = 128, kColG0 = 0, kColG1 = 192, kColW = 320, kWCols = kKt / 2;
 static_assert(kColY + kKt <= kColW && kColW + 2 * kWCols <= 512, "TMEM budget");
 static_assert(kRowsPer * kRowStep >= kKt, "loader rows");
-static_assert(4 * 128 * kRegProducer + 2 * 128 * kRegAcc <= kThreads * 80, "register pool");
+static_assert((kThreads - kAccThreads) * (kRegLaunch - kRegProducer) >= kAccThreads * (kRegAcc - kRegLaunch),
+              "register pool");
 static_assert(kBuildWarp0 % 4 == 0 && kAccWarp0 % 4 == 0, "TMEM lane quarter = warp % 4");
 static_assert(kStages % 2 == 0, "G chunk pairs never wrap the ring");
 
@@ -328,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
       const int4 e = item_at(P, nwork, k);
       if (e.x < 0) break;
       const int kt = e_kt(e), ktp = (kt + 15) & ~15;
+      PF_DCHECK(kt > 0 && ktp <= kKt && e.y >= 0 && (int64_t)e.y + e_rows(e) <= ((P.n + P.tr - 1) / P.tr) * P.tr, "work item");
       int32_t* cell = S.cell[il & 1];
       asm volatile("bar.sync 3, %0;" ::"n"(kLoadThreads) : "memory");
       for (int v = lt; v < P.nv; v += kLoadThreads) {
@@ -336,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
         const int ww = ds.y & 0xff, hh = (ds.y >> 8) & 0xff;
         const ViewF& vw = S.sv[v];
         const int sz = (ww * hh + 1) & ~1;  // padding tap: a valid row (zero weight)
+        PF_DCHECK(sz == 0 || (base + sz <= ktp && x0 + ww <= vw.Wf && y0 + hh <= vw.Hf), "window inside the item / map");
         for (int a = 0; a < sz; ++a) {
           const int aa = a < ww * hh ? a : 0;
           cell[base + a] = vw.cell_base + (y0 + aa / ww) * vw.Wf + x0 + aa % ww;
@@ -347,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
       for (int j = 0; j < kRowsPer; ++j) {
         const int r = r0 + kRowStep * j;
         rc[j] = r < ktp ? cell[r < kt ? r : 0] : -1;  // rows kt..ktp-1 repeat tap 0 (finite, zero weight)
+        PF_DCHECK(rc[j] < 0 || rc[j] < S.sv[P.nv - 1].cell_base + S.sv[P.nv - 1].Hf * S.sv[P.nv - 1].Wf, "tap row inside the maps");
       }
       for (int c = 0; c < nd + 2; ++c) {
         if constexpr (PROF) {
@@ -497,6 +509,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
         n22 = ncls[0];
         nmine = tot;
         auto put = [&](int k, int v, uint2 d, int c) {
+          PF_DCHECK((int)(d.x & 0xffff) + (((int)(d.y & 0xff) * (int)((d.y >> 8) & 0xff) + 1) & ~1) <= ktp &&
+                        k < kMaxViewsTC / kBuildGroups + 1,
+                    "builder window slot");
           wl[k] = make_int4(v, (int)(d.x & 0xffff) | (c << 16), (int)((d.x >> 16) & 0xffff) | (int)((d.y & 0xffff) << 16), 0);
         };
         if (mine0) put(pos0, lane, d0, c0);
@@ -1055,8 +1070,16 @@ __global__ void k_collect_work(TileParams P) {
     // split items (128 / 32 rows: item ids >= nt) run in the feature-product kernel: per 128 rows the
     // Gram product (kt^2 D) costs more than the feature product (128 kt D) once kt exceeds ~128. (Not
     // by row count: the last 512-row tile of an object may be short but is still a 512-row item.)
-    if (P.wlist && item >= nt) P.wlist[atomicAdd(P.wcount, 1)] = e;
-    else P.work_raw[atomicAdd(P.work_count, 1)] = e;
+    const int64_t cap = nt + 4 * (int64_t)P.max_sub_tiles + 4 * (int64_t)P.max_sub2;  // list capacity
+    if (P.wlist && item >= nt) {
+      const int slot = atomicAdd(P.wcount, 1);
+      PF_DCHECK(slot < cap, "split-item list slot");
+      P.wlist[slot] = e;
+    } else {
+      const int slot = atomicAdd(P.work_count, 1);
+      PF_DCHECK(slot < cap, "work list slot");
+      P.work_raw[slot] = e;
+    }
   };
   auto overflow = [&](int64_t row0, int rows) {
     for (int r = lane; r < rows; r += 32) P.ovf_list[atomicAdd(P.ovf_count, 1)] = __float_as_int(P.spts[row0 + r].w);

@@ -904,6 +904,7 @@ __global__ void k_unsort(const SRec* __restrict__ srec, const int32_t* __restric
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = __ldg(inv + i);
+    PF_DCHECK(j >= 0 && j < n + 512, "inverse permutation");
     const uint4 a = __ldg(reinterpret_cast<const uint4*>(srec + j));
     const float4 b = __ldg(reinterpret_cast<const float4*>(srec + j) + 1);
     if (nwords == 2) {

@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
         const int w = ds.y & 0xff, h = (ds.y >> 8) & 0xff;
         const ViewF& vw = S.sv[v];
         const int sz = (w * h + 1) & ~1;  // padding column (zero weights) reads a valid row
+        PF_DCHECK(sz == 0 || (base + sz <= ktp && x0 + w <= vw.Wf && y0 + h <= vw.Hf), "window inside the item / map");
         for (int a = 0; a < sz; ++a) {
           const int aa = a < w * h ? a : 0;
           cell[base + a] = vw.cell_base + (y0 + aa / w) * vw.Wf + x0 + aa % w;
@@ -362,6 +363,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tile_ws(const __grid_constant
       for (int j = 0; j < kRowsPer; ++j) {
         const int r = r0 + kRowStep * j;
         rc[j] = r < ktp ? cell[r < kt ? r : 0] : -1;
+        PF_DCHECK(rc[j] < 0 || rc[j] < S.sv[P.nv - 1].cell_base + S.sv[P.nv - 1].Hf * S.sv[P.nv - 1].Wf, "tap row inside the maps");
       }
       const int nstage = X3 ? 2 * nch : nch;  // x3: per chunk pair [hi c][hi c+1][lo c][lo c+1]
       for (int qs = 0; qs < nstage; ++qs) {
