@@ -145,9 +145,9 @@ struct GramShared {
   float4 wcoef[kBuildWarps][2 * (kMaxViewsTC / kBuildGroups + 1)];  // builders: per-warp expansion coefficients
   float4 yp[kMaxKpadTC];
   float2 yv2[kMaxKpadTC];
-  float xss[2][kTile];
-  float xm[2][kTile];
-  float xsum[2][6][kTile];
+  float xss[2][2][kTile];  // [block parity][half][row]: double-buffered, so a block needs no closing barrier
+  float xm[2][2][kTile];
+  float xsum[2][2][6][kTile];
   double red[kMaxKpadTC + 8];
 };
 
@@ -201,6 +201,23 @@ __device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32], int lane)
     }
   }
   return v[0];
+}
+// two independent reduce-scatters interleaved level by level (twice the shuffles in flight)
+__device__ __forceinline__ void warp_reduce_scatter32x2(float (&a)[32], float (&b)[32], int lane, float& ra, float& rb) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < o; ++j) {
+      const float ka = up ? a[j + o] : a[j], sa = up ? a[j] : a[j + o];
+      const float kb = up ? b[j + o] : b[j], sb = up ? b[j] : b[j + o];
+      const float xa = __shfl_xor_sync(0xffffffffu, sa, o), xb = __shfl_xor_sync(0xffffffffu, sb, o);
+      a[j] = ka + xa;
+      b[j] = kb + xb;
+    }
+  }
+  ra = a[0];
+  rb = b[0];
 }
 // 16 columns of this warp's lanes (bf16 pairs of W)
 __device__ __forceinline__ void tmem_ld16u(uint32_t taddr, uint32_t (&r)[16]) {
@@ -858,6 +875,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
           }
         }
         const int ab = (int)(wuse & 1u);
+        const int bp = ab;  // exchange-slot parity of this block
         ++wuse;
         GWAITP(&S.r_full, ruse & 1u, 8);
         ++ruse;
@@ -892,10 +910,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
         }
         PT(19);
         if (P.ablate & 2) continue;
-        S.xss[half][row] = ss;
+        S.xss[bp][half][row] = ss;
         asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
         PT(20);
-        const float fss = S.xss[0][row] + S.xss[1][row];
+        const float fss = S.xss[bp][0][row] + S.xss[bp][1][row];
         const int count = (int)rec.x;
         const bool featured = valid && count > 0;
         const float inv = fss > 0.f ? rsqrtf(fss) : 0.f;
@@ -914,9 +932,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
             const float4 yb = S.yp[2 * ((k0 + q) >> 1) + 1];
             mx = fmaxf(mx, fmaf(v[q], sc, (q & 1) ? yb.w : yb.z));
           }
-          S.xm[half][row] = mx;
+          S.xm[bp][half][row] = mx;
           asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
-          m2 = fmaxf(S.xm[0][row], S.xm[1][row]);
+          m2 = fmaxf(S.xm[bp][0][row], S.xm[bp][1][row]);
           if (!(m2 > -INFINITY)) m2 = 0.f;
         }
         float se, pl0, pl1, pl2 = 0.f, pl3 = 0.f, pml;
@@ -958,15 +976,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
           up2(pmp, a, c);
           pml = a + c;
         }
-        S.xsum[half][0][row] = se;
-        S.xsum[half][1][row] = pl0;
-        S.xsum[half][2][row] = pl1;
-        S.xsum[half][3][row] = pl2;
-        S.xsum[half][4][row] = pl3;
-        S.xsum[half][5][row] = pml;
+        S.xsum[bp][half][0][row] = se;
+        S.xsum[bp][half][1][row] = pl0;
+        S.xsum[bp][half][2][row] = pl1;
+        S.xsum[bp][half][3][row] = pl2;
+        S.xsum[bp][half][4][row] = pl3;
+        S.xsum[bp][half][5][row] = pml;
         asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
         PT(21);
-        const float se_t = S.xsum[0][0][row] + S.xsum[1][0][row];
+        const float se_t = S.xsum[bp][0][0][row] + S.xsum[bp][1][0][row];
         if (featured && !(se_t <= 3.4e38f)) atomicOr(P.status, isnan(se_t) ? 1 : 2);
         const float rs = featured ? 1.f / se_t : 0.f;
         {
@@ -979,13 +997,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
           for (int q = 0; q < kHalfK; ++q)
             if (k0 + q < P.k) P.weights[(int64_t)pi * P.k + k0 + q] = v[q];
         }
-#pragma unroll
-        for (int c = 0; c < kHalfK / 32; ++c) wsum[c] += warp_reduce_scatter32(*reinterpret_cast<float(*)[32]>(v + 32 * c), lane);
+        static_assert(kHalfK == 64, "two 32-material chunks per half");
+        {
+          float r0, r1;
+          warp_reduce_scatter32x2(*reinterpret_cast<float(*)[32]>(v), *reinterpret_cast<float(*)[32]>(v + 32), lane, r0, r1);
+          wsum[0] += r0;
+          wsum[1] += r1;
+        }
         if (valid && half == 0) {
           float prop[4];
 #pragma unroll
-          for (int pp = 0; pp < 4; ++pp) prop[pp] = (S.xsum[0][1 + pp][row] + S.xsum[1][1 + pp][row]) * rs;
-          const float pm = (S.xsum[0][5][row] + S.xsum[1][5][row]) * rs;
+          for (int pp = 0; pp < 4; ++pp) prop[pp] = (S.xsum[bp][0][1 + pp][row] + S.xsum[bp][1][1 + pp][row]) * rs;
+          const float pm = (S.xsum[bp][0][5][row] + S.xsum[bp][1][5][row]) * rs;
           *(reinterpret_cast<float4*>(P.srec + jpt) + 1) = make_float4(prop[0], prop[1], prop[2], prop[3]);
           if (P.grid_partials && (int32_t)rec.y >= 0) {  // code -1: a padding slot
             const int32_t code = (int32_t)rec.y;
@@ -1002,8 +1025,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
           featured_n += featured ? 1.f : 0.f;
           pairs += (float)count;
         }
-        // the xsum / xm slots are rewritten by the next block: every thread has read them
-        asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
+        // (no closing barrier: the next block writes the other parity's slots, and the block after
+        // that only gets past the next block's barriers once every thread has read these)
         PT(22);
       }
     }
