@@ -202,6 +202,11 @@ __device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32], int lane)
   }
   return v[0];
 }
+// the two accumulator warps of TMEM lane quarter qd (the same 32 rows, the two material halves)
+// exchange per-row values through shared memory: a 64-thread named barrier per quarter (ids 4-7)
+__device__ __forceinline__ void acc_pair_sync(int qd) {
+  asm volatile("bar.sync %0, 64;" ::"r"(4 + qd) : "memory");
+}
 // two independent reduce-scatters interleaved level by level (twice the shuffles in flight)
 __device__ __forceinline__ void warp_reduce_scatter32x2(float (&a)[32], float (&b)[32], int lane, float& ra, float& rb) {
 #pragma unroll
@@ -911,7 +916,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
         PT(19);
         if (P.ablate & 2) continue;
         S.xss[bp][half][row] = ss;
-        asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
+        acc_pair_sync(qd);
         PT(20);
         const float fss = S.xss[bp][0][row] + S.xss[bp][1][row];
         const int count = (int)rec.x;
@@ -933,7 +938,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
             mx = fmaxf(mx, fmaf(v[q], sc, (q & 1) ? yb.w : yb.z));
           }
           S.xm[bp][half][row] = mx;
-          asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
+          acc_pair_sync(qd);
           m2 = fmaxf(S.xm[bp][0][row], S.xm[bp][1][row]);
           if (!(m2 > -INFINITY)) m2 = 0.f;
         }
@@ -982,7 +987,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
         S.xsum[bp][half][3][row] = pl2;
         S.xsum[bp][half][4][row] = pl3;
         S.xsum[bp][half][5][row] = pml;
-        asm volatile("bar.sync 2, %0;" ::"n"(kAccThreads) : "memory");
+        acc_pair_sync(qd);
         PT(21);
         const float se_t = S.xsum[bp][0][0][row] + S.xsum[bp][1][0][row];
         if (featured && !(se_t <= 3.4e38f)) atomicOr(P.status, isnan(se_t) ? 1 : 2);
