@@ -225,6 +225,16 @@ __device__ __forceinline__ void warp_reduce_scatter32x2(float (&a)[32], float (&
   rb = b[0];
 }
 // 16 columns of this warp's lanes (bf16 pairs of W)
+// a 32-column Y chunk and the matching 16 columns of W (bf16 pairs) under one wait
+__device__ __forceinline__ void tmem_ld_yw(uint32_t ty, uint32_t tw, uint32_t (&y)[32], uint32_t (&w)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%48];\n\t"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47}, [%49];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3]), "=r"(y[4]), "=r"(y[5]), "=r"(y[6]), "=r"(y[7]), "=r"(y[8]), "=r"(y[9]), "=r"(y[10]), "=r"(y[11]), "=r"(y[12]), "=r"(y[13]), "=r"(y[14]), "=r"(y[15]), "=r"(y[16]), "=r"(y[17]), "=r"(y[18]), "=r"(y[19]), "=r"(y[20]), "=r"(y[21]), "=r"(y[22]), "=r"(y[23]), "=r"(y[24]), "=r"(y[25]), "=r"(y[26]), "=r"(y[27]), "=r"(y[28]), "=r"(y[29]), "=r"(y[30]), "=r"(y[31]), "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+      : "r"(ty), "r"(tw)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld16u(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -891,14 +901,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
         {
           uint64_t ss2 = 0ull;
           for (int c = half; 32 * c < ktp; c += 2) {  // whole chunks: columns ktp.. are zero
-            float y[32];
-            tc::tmem_ld32(tbase + kColY + 32u * c + t_lane, y);
-            uint32_t wr[16];
-            tmem_ld16u(tW + 16u * c, wr);
+            uint32_t y[32], wr[16];
+            tmem_ld_yw(tbase + kColY + 32u * c + t_lane, tW + 16u * c, y, wr);
 #pragma unroll
             for (int q = 0; q < 16; ++q)  // bf16 pair -> two floats (exact: bf16 is the top half)
               ss2 = ffma2(pk2(__uint_as_float(wr[q] << 16), __uint_as_float(wr[q] & 0xffff0000u)),
-                          pk2(y[2 * q], y[2 * q + 1]), ss2);
+                          pk2(__uint_as_float(y[2 * q]), __uint_as_float(y[2 * q + 1])), ss2);
           }
           float s_a, s_b;
           up2(ss2, s_a, s_b);
