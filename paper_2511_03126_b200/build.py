@@ -41,7 +41,8 @@ def source_hash() -> str:
     for p in _deps():
         h.update(p.name.encode())
         h.update(p.read_bytes())
-    h.update(" ".join(ARCH + FLAGS).encode())
+    # flags without the checkout-specific include path (the GPU box runs from another directory)
+    h.update(" ".join(ARCH + [f for f in FLAGS if not f.startswith("-I")]).encode())
     return h.hexdigest()[:16]
 
 
