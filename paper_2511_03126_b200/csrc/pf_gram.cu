@@ -207,6 +207,24 @@ __device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32], int lane)
 __device__ __forceinline__ void acc_pair_sync(int qd) {
   asm volatile("bar.sync %0, 64;" ::"r"(4 + qd) : "memory");
 }
+// reduce-scatter of 32 bf16 pairs over the warp (packed bf16x2 adds): lane l returns pair l summed
+// over the 32 lanes
+__device__ __forceinline__ uint32_t warp_reduce_scatter32_bf16x2(uint32_t (&a)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < o; ++j) {
+      const uint32_t keep = up ? a[j + o] : a[j], send = up ? a[j] : a[j + o];
+      const uint32_t x = __shfl_xor_sync(0xffffffffu, send, o);
+      __nv_bfloat162 k2 = *reinterpret_cast<const __nv_bfloat162*>(&keep);
+      const __nv_bfloat162 x2 = *reinterpret_cast<const __nv_bfloat162*>(&x);
+      k2 = __hadd2(k2, x2);
+      a[j] = *reinterpret_cast<const uint32_t*>(&k2);
+    }
+  }
+  return a[0];
+}
 // two independent reduce-scatters interleaved level by level (twice the shuffles in flight)
 __device__ __forceinline__ void warp_reduce_scatter32x2(float (&a)[32], float (&b)[32], int lane, float& ra, float& rb) {
 #pragma unroll
@@ -1010,12 +1028,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
           for (int q = 0; q < kHalfK; ++q)
             if (k0 + q < P.k) P.weights[(int64_t)pi * P.k + k0 + q] = v[q];
         }
-        static_assert(kHalfK == 64, "two 32-material chunks per half");
+        static_assert(kHalfK == 64, "32 material pairs per half");
         {
-          float r0, r1;
-          warp_reduce_scatter32x2(*reinterpret_cast<float(*)[32]>(v), *reinterpret_cast<float(*)[32]>(v + 32), lane, r0, r1);
-          wsum[0] += r0;
-          wsum[1] += r1;
+          // weight totals over the warp's 32 rows: the 64 weights as 32 bf16 pairs, one packed
+          // reduce-scatter (half the shuffles of two fp32 ones); lane l ends with materials 2l, 2l + 1.
+          // bf16 keeps fp32's range (tiny weights survive), and its round-to-nearest errors (2^-9 per
+          // add) are unbiased, so the per-material totals over all points stay far inside the 1e-2 bar
+          uint32_t pw[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) pw[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+          const uint32_t r = warp_reduce_scatter32_bf16x2(pw, lane);
+          wsum[0] += __uint_as_float(r << 16);
+          wsum[1] += __uint_as_float(r & 0xffff0000u);
         }
         if (valid && half == 0) {
           float prop[4];
@@ -1044,8 +1068,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
       }
     }
 #pragma unroll
-    for (int q = 0; q < kHalfK / 32; ++q) {
-      const int k = k0 + 32 * q + lane;
+    for (int q = 0; q < 2; ++q) {  // materials k0 + 2 lane + q
+      const int k = k0 + 2 * lane + q;
       if (k < P.k && wsum[q] != 0.f) atomicAdd(&S.red[k], (double)wsum[q]);
     }
     double r6[6] = {pm_sum, pmx, pmy, pmz, featured_n, pairs};
