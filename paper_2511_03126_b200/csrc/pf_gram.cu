@@ -972,22 +972,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
         {
           uint64_t sep = 0ull, p0p = 0ull, p1p = 0ull, pmp = 0ull;
           const uint64_t scp = pk2(sc, sc);
+          // exponents v sc + shift (- row max only when need_max: a separate copy of the loop)
+          auto softmax_pass = [&](auto with_max) {
+            constexpr bool kMax = decltype(with_max)::value;
 #pragma unroll
-          for (int q = 0; q < kHalfK; q += 2) {
-            if ((q & 15) == 0) asm volatile("" ::: "memory");
-            const int kp = (k0 + q) >> 1;
-            const float4 ya = S.yp[2 * kp], yb = S.yp[2 * kp + 1];
-            float x0, x1;
-            up2(ffma2(pk2(v[q], v[q + 1]), scp, pk2(yb.z - m2, yb.w - m2)), x0, x1);
-            const float e0 = ex2(x0), e1 = ex2(x1);
-            const uint64_t ee = pk2(e0, e1);
-            sep = fadd2(sep, ee);
-            p0p = ffma2(ee, pk2(ya.x, ya.y), p0p);
-            p1p = ffma2(ee, pk2(ya.z, ya.w), p1p);
-            pmp = ffma2(ee, pk2(yb.x, yb.y), pmp);
-            v[q] = e0;
-            v[q + 1] = e1;
-          }
+            for (int q = 0; q < kHalfK; q += 2) {
+              if ((q & 15) == 0) asm volatile("" ::: "memory");
+              const int kp = (k0 + q) >> 1;
+              const float4 ya = S.yp[2 * kp], yb = S.yp[2 * kp + 1];
+              float x0, x1;
+              up2(ffma2(pk2(v[q], v[q + 1]), scp, kMax ? pk2(yb.z - m2, yb.w - m2) : pk2(yb.z, yb.w)), x0, x1);
+              const float e0 = ex2(x0), e1 = ex2(x1);
+              const uint64_t ee = pk2(e0, e1);
+              sep = fadd2(sep, ee);
+              p0p = ffma2(ee, pk2(ya.x, ya.y), p0p);
+              p1p = ffma2(ee, pk2(ya.z, ya.w), p1p);
+              pmp = ffma2(ee, pk2(yb.x, yb.y), pmp);
+              v[q] = e0;
+              v[q + 1] = e1;
+            }
+          };
+          if (need_max) softmax_pass(std::true_type{});
+          else softmax_pass(std::false_type{});
           if (p_wide) {
 #pragma unroll
             for (int q = 0; q < kHalfK; ++q) {
