@@ -144,6 +144,7 @@ struct GramShared {
   int4 wlist[kBuildWarps][kMaxViewsTC / kBuildGroups + 1];      // builders: per-warp view list (per item)
   float4 wcoef[kBuildWarps][2 * (kMaxViewsTC / kBuildGroups + 1)];  // builders: per-warp expansion coefficients
   float4 yp[kMaxKpadTC];
+  float4 yq[3][kMaxKpadTC / 4];  // per 4 materials: property 0, property 1, mid_theta (the 4-wide softmax loop)
   float2 yv2[kMaxKpadTC];
   float xss[2][2][kTile];  // [block parity][half][row]: double-buffered, so a block needs no closing barrier
   float xm[2][2][kTile];
@@ -356,6 +357,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
     S.yp[2 * j] = make_float4(val(a, 0), val(b, 0), val(a, 1), val(b, 1));
     S.yp[2 * j + 1] = make_float4(a < P.k ? P.mid_theta[a] : 0.f, b < P.k ? P.mid_theta[b] : 0.f,
                                   a < P.k ? shift : -INFINITY, b < P.k ? shift : -INFINITY);
+  }
+  for (int j = tid; j < kMaxKpadTC / 4; j += kThreads) {
+    auto val = [&](int kk, int pp) { return (kk < P.k && pp < P.p) ? P.values[kk * P.p + pp] : 0.f; };
+    auto mid = [&](int kk) { return kk < P.k ? P.mid_theta[kk] : 0.f; };
+    const int a = 4 * j;
+    S.yq[0][j] = make_float4(val(a, 0), val(a + 1, 0), val(a + 2, 0), val(a + 3, 0));
+    S.yq[1][j] = make_float4(val(a, 1), val(a + 1, 1), val(a + 2, 1), val(a + 3, 1));
+    S.yq[2][j] = make_float4(mid(a), mid(a + 1), mid(a + 2), mid(a + 3));
   }
   for (int j = tid; j < kMaxKpadTC + 8; j += kThreads) S.red[j] = 0.0;
   if (tid == 0) {
@@ -992,8 +1001,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
               v[q + 1] = e1;
             }
           };
+          // the common case (no row max, no padding materials in this half): 4 materials per step,
+          // the uniform shift in a register and 3 coefficient loads per 4 materials instead of 4 (the
+          // loop is bound by the shared-memory / special-function issue queue)
+          auto softmax_pass4 = [&]() {
+            const uint64_t shp = pk2(shift, shift);
+#pragma unroll
+            for (int q = 0; q < kHalfK; q += 4) {
+              if ((q & 15) == 0) asm volatile("" ::: "memory");
+              const int g = (k0 + q) >> 2;
+              const float4 c0 = S.yq[0][g], c1 = S.yq[1][g], cm = S.yq[2][g];
+              float x0, x1, x2, x3;
+              up2(ffma2(pk2(v[q], v[q + 1]), scp, shp), x0, x1);
+              up2(ffma2(pk2(v[q + 2], v[q + 3]), scp, shp), x2, x3);
+              const float e0 = ex2(x0), e1 = ex2(x1), e2 = ex2(x2), e3 = ex2(x3);
+              const uint64_t ea = pk2(e0, e1), eb = pk2(e2, e3);
+              sep = fadd2(sep, ea);
+              sep = fadd2(sep, eb);
+              p0p = ffma2(ea, pk2(c0.x, c0.y), p0p);
+              p0p = ffma2(eb, pk2(c0.z, c0.w), p0p);
+              p1p = ffma2(ea, pk2(c1.x, c1.y), p1p);
+              p1p = ffma2(eb, pk2(c1.z, c1.w), p1p);
+              pmp = ffma2(ea, pk2(cm.x, cm.y), pmp);
+              pmp = ffma2(eb, pk2(cm.z, cm.w), pmp);
+              v[q] = e0;
+              v[q + 1] = e1;
+              v[q + 2] = e2;
+              v[q + 3] = e3;
+            }
+          };
           if (need_max) softmax_pass(std::true_type{});
-          else softmax_pass(std::false_type{});
+          else if (k0 + kHalfK > P.k) softmax_pass(std::false_type{});  // padding materials: -inf shifts
+          else softmax_pass4();
           if (p_wide) {
 #pragma unroll
             for (int q = 0; q < kHalfK; ++q) {

@@ -32,9 +32,19 @@ def test_two_rank_bench_matches_one_rank(cuda):
     one = subprocess.run([sys.executable, *args], cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert one.returncode == 0, one.stderr[-2000:]
     env = dict(os.environ, PF_BENCH_DEVICE="0", PF_BENCH_BACKEND="gloo")
-    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                          "--master-addr", "127.0.0.1", "--master-port", str(_port()), *args, "--gpus", "2"],
-                         cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    # the 2-rank job takes ~15 s; one run of the suite saw the torchrun job hang (a rendezvous /
+    # gloo connect on the shared host, not a kernel: every collective is a host-side step), so a
+    # stuck attempt is killed and retried once on a fresh port
+    two = None
+    for attempt in range(2):
+        try:
+            two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                                  "--master-addr", "127.0.0.1", "--master-port", str(_port()), *args, "--gpus", "2"],
+                                 cwd=ROOT, capture_output=True, text=True, timeout=240, env=env)
+            break
+        except subprocess.TimeoutExpired as e:
+            print(f"2-rank attempt {attempt} timed out; stderr tail: {(e.stderr or b'')[-1500:]!r}")
+    assert two is not None, "the 2-rank job timed out twice"
     assert two.returncode == 0, two.stderr[-2000:]
     a, b = _line(one.stdout), _line(two.stdout)
     assert b["n_gpus"] == 2 and "cell-range x2" in b["config"]["parallelism"]
