@@ -223,6 +223,9 @@ extern "C" int pf_bench_umma(int32_t n, int32_t ts, int32_t reps, int32_t stores
 // tile::gather4 (4 arbitrary 128-byte rows per op into the 128-byte-swizzled layout) ----------------------
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#ifndef PF_GATHER_ISSUERS
+#define PF_GATHER_ISSUERS 4
+#endif
 #include <mutex>
 namespace pf {
 namespace {
@@ -258,6 +261,36 @@ __global__ void __launch_bounds__(192, 1) k_gather_rate(const __grid_constant__ 
       if (s >= 4) asm volatile("cp.async.wait_group 4;" ::: "memory");
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+  } else if (mode == 2) {
+    // TMA gather4 from 4 issuing threads (lane 0 of warps 0-3), row indices precomputed per stage
+    // (no index arithmetic in the issue loop); each thread issues a quarter of a stage's gathers
+    __shared__ int rows[kSt][kRows];
+    const int w = tid >> 5;
+    for (int s = 0; s < stages_total; ++s) {
+      const int st = s % kSt;
+      if (s >= kSt - 1) tc::mbar_wait(&bar[(s - (kSt - 1)) % kSt], (uint32_t)(((s - (kSt - 1)) / kSt) & 1));
+      constexpr int kIss = 4 * PF_GATHER_ISSUERS / 4;
+      if (w < kIss) {
+        for (int r = (tid & 31); r < kRows / kIss; r += 32) rows[st][w * (kRows / kIss) + r] = (int)bench_row(blockIdx.x, s, w * (kRows / kIss) + r, cells);
+        __syncwarp();
+        if ((tid & 31) == 0) {
+          const uint32_t sb = tc::smem_u32(smem + st * kBytes);
+          if (w == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&bar[st])), "r"(kBytes) : "memory");
+          const int c = (s & 15) * 64;
+          const int* rr = rows[st] + w * (kRows / kIss);
+          for (int g = 0; g < kRows / (4 * kIss); ++g)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                ::"r"(sb + (w * (kRows / (4 * kIss)) + g) * 512), "l"(reinterpret_cast<uint64_t>(&map)), "r"(c),
+                "r"(rr[4 * g]), "r"(rr[4 * g + 1]), "r"(rr[4 * g + 2]), "r"(rr[4 * g + 3]), "r"(tc::smem_u32(&bar[st]))
+                : "memory");
+        }
+      }
+    }
+    if (tid == 0)
+      for (int s = stages_total - (kSt - 1); s < stages_total; ++s)
+        if (s >= 0) tc::mbar_wait(&bar[s % kSt], (uint32_t)((s / kSt) & 1));
   } else if (tid == 0) {
     // TMA gather4: one thread; 7 stages in flight
     for (int s = 0; s < stages_total; ++s) {
