@@ -97,9 +97,10 @@ def test_c3_full_object_vs_oracle(cuda):
     mass_ref, occ_ref = O.voxel_mass(ref["codes"], ref["props"][:, 0], ref["edge"])
     assert g["mass"] == pytest.approx(mass_ref, rel=TOL_BF16)
     np.testing.assert_allclose(g["partials"]["weight_totals"], ref["weight_totals"], rtol=TOL_BF16)
+    wt_rel = np.abs(g["partials"]["weight_totals"] - ref["weight_totals"]) / np.abs(ref["weight_totals"])
     assert g["partials"]["featured"] == int((ref["counts"] > 0).sum())
     print(f"C3 full object: density max rel {rel_d.max():.2e} (mean {rel_d.mean():.2e}), "
-          f"mass {g['mass']:.6f} vs {mass_ref:.6f}")
+          f"mass {g['mass']:.6f} vs {mass_ref:.6f}, weight totals max rel {wt_rel.max():.2e}")
 
 
 def test_c5_full_object_vs_oracle_slice(cuda):
