@@ -322,3 +322,13 @@ def test_sparse_voxel_mass_equals_dense_and_cleans_grid(workload, name):
         assert not bool(bufs.grid_partials.any())
         masses.append(res.mass_kg())
     assert max(masses) - min(masses) <= 1e-6 * masses[0]  # fp32 atomics: order-dependent rounding
+
+
+@pytest.mark.parametrize("n", [1, 127, 129, 511, 513, 1025])
+def test_gram_tile_boundaries(cuda, workload, n):
+    """Point counts around the 128-row and 512-row tile edges on the Gram path (a short last 512-row
+    tile must stay a Gram item; its 128-row tiles and 32-row splits must cover every row once)."""
+    wl = workload("mini_bf16")
+    assert wl.points.shape[0] >= n
+    pts = np.ascontiguousarray(wl.points[:n])
+    assert_parity(run_gpu(wl, pts, features=False), run_oracle(wl, pts), wl, pts, tol=TOL_BF16)
