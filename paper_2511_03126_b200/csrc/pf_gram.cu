@@ -25,10 +25,13 @@
 // The bf16 rounding of M~ changes |F| by ~1e-4 relative at C5 (scripts/gram_precision.py), well
 // inside the bf16-feature bar of 1e-2.
 //
-// Warp roles (24 warps, setmaxnreg as k_tile_ws): 0-5 loaders, 6 MMA, 7 idle, 8-15 accumulators
-// (two per TMEM lane quarter, column halves), 16-23 builders (two per lane quarter, view parity).
+// Warp roles (24 warps, setmaxnreg 48 / 144): 0-2 and 4-7 loaders, 3 MMA, 8-15 builders (two per
+// TMEM lane quarter, view parity), 16-23 accumulators (two per lane quarter, material halves).
 // TMEM (512 columns): region R [0, 320) holds the Gram (block 0 at 0, block 1 at 192) or one row
 // block's S (0..127) and Y (128..319); W buffers at 320 and 416 (96 columns of bf16 pairs each).
+// Work items come from a device-built list sorted by cost (k_collect_work, k_sort_work); CTA c takes
+// list positions c, 2G - 1 - c, 2G + c, ... The C5 timing history and the variants measured and
+// dropped are in profiles/r02_notes.md.
 #include <type_traits>
 #include <climits>
 #include <cstdio>
