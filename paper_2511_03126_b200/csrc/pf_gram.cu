@@ -395,8 +395,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
     const int q = lt & 7, r0 = lt >> 3;
     int stage = 0;
     uint32_t phase = 0, il = 0;
+    int4 e_nx = item_at(P, nwork, 0);
     for (int k = 0;; ++k) {
-      const int4 e = item_at(P, nwork, k);
+      const int4 e = e_nx;
+      if (e.x >= 0) e_nx = item_at(P, nwork, k + 1);  // the next item's entry, loaded during this one
       if (e.x < 0) break;
       const int kt = e_kt(e), ktp = (kt + 15) & ~15;
       PF_DCHECK(kt > 0 && ktp <= kKt && e.y >= 0 && (int64_t)e.y + e_rows(e) <= ((P.n + P.tr - 1) / P.tr) * P.tr, "work item");
@@ -461,8 +463,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
     uint32_t phase = 0, ruse = 0, wuse = 0;
     const uint32_t idS = tc::idesc_bf16_f32(128, kMaxKpadTC, false, true);
     const uint32_t mt0 = tc::smem_u32(sM);
+    int4 e_nx = item_at(P, nwork, 0);
     for (int k = 0;; ++k) {
-      const int4 e = item_at(P, nwork, k);
+      const int4 e = e_nx;
+      if (e.x >= 0) e_nx = item_at(P, nwork, k + 1);  // the next item's entry, loaded during this one
       if (e.x < 0) break;
       const int ktp = (e_kt(e) + 15) & ~15, nb = e_nb(e);
       // ---- Gram: block 0 = taps 0..127 x all, block 1 = taps 128.. x taps 128.. ----
@@ -538,8 +542,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
     int4* wl = S.wlist[bj];     // this warp's views: {view, window base | shape << 16, x0 | y0 << 8 | w << 16 | h << 24, -}
     float4* wc = S.wcoef[bj];   // and their expansion coefficients {A0, A1} for the current block
     uint32_t wuse = 0;
+    int4 e_nx = item_at(P, nwork, 0);
     for (int k = 0;; ++k) {
-      const int4 e = item_at(P, nwork, k);
+      const int4 e = e_nx;
+      if (e.x >= 0) e_nx = item_at(P, nwork, k + 1);  // the next item's entry, loaded during this one
       if (e.x < 0) break;
       PT(23);
       // this item's windows: views lane and lane + 32
@@ -841,8 +847,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_gram(const __grid_constant
     for (int q = 0; q < kHalfK / 32; ++q) wsum[q] = 0.f;
     float pm_sum = 0.f, pmx = 0.f, pmy = 0.f, pmz = 0.f, featured_n = 0.f, pairs = 0.f;
     const bool p_wide = P.p > 2;
+    int4 e_nx = item_at(P, nwork, 0);
     for (int k = 0;; ++k) {
-      const int4 e = item_at(P, nwork, k);
+      const int4 e = e_nx;
+      if (e.x >= 0) e_nx = item_at(P, nwork, k + 1);  // the next item's entry, loaded during this one
       if (e.x < 0) break;
       const int ktp = (e_kt(e) + 15) & ~15, nb = e_nb(e), nrows = e_rows(e);
       uint2 rec_nx = make_uint2(0u, 0u);
