@@ -36,7 +36,7 @@ def _config(seed):
     return cfg, p, rng
 
 
-@pytest.mark.parametrize("seed", range(32))
+@pytest.mark.parametrize("seed", range(128))
 def test_random_shapes_vs_oracle(cuda, seed):
     import torch
 
