@@ -372,7 +372,10 @@ __device__ __forceinline__ int classify_tile_view(const ViewF& v, const float4& 
   const double ew = fabs(f) * r3 * ((fabs(W0) + rr) * rzl + 1.0) * 1.05 + 7e-7 * (fabs(w0) + gw + qw) +
                     1e-5 * (gw + qw) + 1e-5;
   const bool ok = ew < 0.25;
-  if (!(ok && __shfl_xor_sync(pm, ok, 1))) return kViewExact;
+  // both lanes must reach the shuffle: a short-circuit `ok && shfl(...)` would leave the partner of a
+  // lane with ok == false waiting forever
+  const bool ok_pair = __shfl_xor_sync(pm, ok, 1);
+  if (!(ok && ok_pair)) return kViewExact;
   const float4 row = h ? make_float4(v.R[3], v.R[4], v.R[5], w0) : make_float4(v.R[0], v.R[1], v.R[2], w0);
   const float4 co = make_float4((float)sw, (float)(-sw * wr), (float)(-sw * rz0), (float)(sw * wr * rz0));
   const float hw = __fsub_rd(0.5f, __double2float_ru(ew));
