@@ -64,7 +64,7 @@ def test_random_shapes_vs_oracle(cuda, seed):
     assert res.mass_kg() == pytest.approx(ref["mass"], rel=tol, abs=1e-12)
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(32))
 def test_random_medium_bf16_gram_vs_oracle(cuda, seed):
     """Medium objects (100k-250k points, bf16 maps, D % 128 == 0) through the production Gram path:
     several 512-row tiles per object, 128 / 32-row splits and SIMT overflow in one call, against
@@ -100,3 +100,40 @@ def test_random_medium_bf16_gram_vs_oracle(cuda, seed):
     scale = np.abs(ref["props"]).max(axis=0, keepdims=True) + 1e-30
     assert (np.abs(props - ref["props"])[ok] / scale).max() <= 1e-2, cfg
     np.testing.assert_allclose(res.host_partials()["weight_totals"], ref["weight_totals"], rtol=1e-2)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_medium_f32_x3_vs_oracle(cuda, seed):
+    """Medium objects with f32 maps (70k-150k points, D % 128 == 0): the x3 tile path (hi / lo bf16
+    splits in the feature-product kernel) against the parallel oracle at the fp32 bar."""
+    import torch
+
+    from oracle_parallel import oracle_rows, unpack_mask_bits
+
+    rng = np.random.default_rng(7000 + seed)
+    views = int(rng.choice([4, 8, 17, 32]))
+    cfg = workloads.Config(
+        f"medium_f32_{seed}", n=int(rng.choice([70_000, 150_000])), rings=(), fib=views,
+        radius=float(rng.uniform(1.2, 2.5)), image=int(rng.choice([96, 128, 192])),
+        fmap=(int(rng.integers(8, 24)), int(rng.integers(8, 24)), int(rng.choice([128, 256]))), bf16=False,
+        k=int(rng.integers(1, 129)), grid=int(rng.integers(8, 96)), n_ellipsoids=int(rng.integers(1, 4)),
+        temperature=float(rng.uniform(0.05, 1.0)), seed=seed)
+    wl = workloads.generate(cfg)
+    views_dev = pf.ViewSet.from_views(wl.views())
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta)
+    res = pf.fuse_and_query(torch.from_numpy(wl.points).cuda(), views_dev, tables, temperature=cfg.temperature,
+                            epsilon=cfg.eps, grid=cfg.grid, check=True)
+    torch.cuda.synchronize()
+    ref = oracle_rows(wl)
+    vis_g = unpack_mask_bits(res.mask_bits.cpu().numpy(), cfg.nviews)
+    vis_r = np.unpackbits(ref["vis_bits"], axis=1, bitorder="little")[:, :cfg.nviews].astype(bool)
+    diff = vis_g != vis_r
+    if diff.any():
+        assert not (diff & ~knife_edge_pairs(wl, wl.points, cfg.eps)).any(), "mask mismatch"
+    np.testing.assert_array_equal(res.codes.cpu().numpy(), ref["codes"])
+    ok = ~diff.any(axis=1)
+    np.testing.assert_array_equal(res.counts.cpu().numpy()[ok], ref["counts"][ok])
+    props = res.props.cpu().numpy().astype(np.float64)
+    scale = np.abs(ref["props"]).max(axis=0, keepdims=True) + 1e-30
+    assert (np.abs(props - ref["props"])[ok] / scale).max() <= 1e-4, cfg
+    np.testing.assert_allclose(res.host_partials()["weight_totals"], ref["weight_totals"], rtol=1e-4)
