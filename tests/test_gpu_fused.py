@@ -332,3 +332,34 @@ def test_gram_tile_boundaries(cuda, workload, n):
     assert wl.points.shape[0] >= n
     pts = np.ascontiguousarray(wl.points[:n])
     assert_parity(run_gpu(wl, pts, features=False), run_oracle(wl, pts), wl, pts, tol=TOL_BF16)
+
+
+@pytest.mark.parametrize("name,features", [("mini_bf16", False), ("mini_bf16", True), ("mini", True)])
+def test_views_with_different_depth_sizes(cuda, workload, name, features):
+    """Depth maps of different sizes per view (the feature maps stay uniform, as the tile path needs):
+    odd views get their depth zero-padded to a larger W x H, which changes their feature-coordinate
+    scale Wf / W (fusion.py:83-86) and adds never-visible pixels. Gram, feature-product and SIMT
+    paths against the oracle on the same view list."""
+    import dataclasses
+
+    import torch
+
+    wl = workload(name)
+    vg, vo = wl.views(), wl.views(f32_maps=True)
+    for j in range(1, len(vg), 2):
+        dep = np.pad(vg[j].depth, ((0, 13), (0, 7)))
+        vg[j] = dataclasses.replace(vg[j], depth=dep)
+        vo[j] = dataclasses.replace(vo[j], depth=dep)
+    views = pf.ViewSet.from_views(vg)
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta, density_col=0)
+    res = pf.fuse_and_query(torch.from_numpy(wl.points).cuda(), views, tables, temperature=wl.cfg.temperature,
+                            epsilon=wl.cfg.eps, grid=wl.cfg.grid, write_features=features, write_sims=True,
+                            write_weights=True, check=True)
+    torch.cuda.synchronize()
+    ref = O.fuse_and_query(wl.points, vo, wl.text, wl.values, wl.cfg.temperature, wl.cfg.eps, wl.cfg.grid)
+    assert np.array_equal(res.counts.cpu().numpy(), ref["counts"])
+    assert np.array_equal(res.codes.cpu().numpy(), ref["codes"])
+    tol = tol_for(wl)
+    props = res.props.cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(props, ref["props"], rtol=tol, atol=1e-6)
+    assert res.mass_kg() == pytest.approx(ref["mass"], rel=tol)
