@@ -363,3 +363,36 @@ def test_views_with_different_depth_sizes(cuda, workload, name, features):
     props = res.props.cpu().numpy().astype(np.float64)
     np.testing.assert_allclose(props, ref["props"], rtol=tol, atol=1e-6)
     assert res.mass_kg() == pytest.approx(ref["mass"], rel=tol)
+
+
+@pytest.mark.parametrize("name", ["mini_bf16", "mini"])
+def test_camera_inside_the_point_cloud(cuda, workload, name):
+    """One view's camera sits at the centre of the object, so points lie in front of, beside and
+    behind its image plane (tiles that reach z <= 0 take the exact per-point test; the depth map is
+    the reference's own visibility rule applied to whatever it stores). Tile / SIMT paths against the
+    oracle on the same views."""
+    import dataclasses
+
+    import torch
+
+    from paper_2511_03126_b200.types import CameraPose
+
+    wl = workload(name)
+    vg, vo = wl.views(), wl.views(f32_maps=True)
+    c = wl.points.astype(np.float64).mean(axis=0)
+    rot = np.asarray(vg[0].camera.rotation)
+    cam = CameraPose(rotation=rot, translation=-rot @ c)
+    dep = np.full_like(vg[0].depth, 0.05)  # a near wall: only points within 0.05 + eps in front pass
+    vg[0] = dataclasses.replace(vg[0], camera=cam, depth=dep)
+    vo[0] = dataclasses.replace(vo[0], camera=cam, depth=dep)
+    views = pf.ViewSet.from_views(vg)
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta, density_col=0)
+    res = pf.fuse_and_query(torch.from_numpy(wl.points).cuda(), views, tables, temperature=wl.cfg.temperature,
+                            epsilon=wl.cfg.eps, grid=wl.cfg.grid, check=True)
+    torch.cuda.synchronize()
+    ref = O.fuse_and_query(wl.points, vo, wl.text, wl.values, wl.cfg.temperature, wl.cfg.eps, wl.cfg.grid)
+    assert np.array_equal(res.visibility().cpu().numpy(), ref["visibility"])
+    assert np.array_equal(res.counts.cpu().numpy(), ref["counts"])
+    assert np.array_equal(res.codes.cpu().numpy(), ref["codes"])
+    tol = tol_for(wl)
+    np.testing.assert_allclose(res.props.cpu().numpy().astype(np.float64), ref["props"], rtol=tol, atol=1e-6)
