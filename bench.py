@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-simt", action="store_true")
     ap.add_argument("--feature-kernel", action="store_true", help="bf16: the feature-product tile kernel (A/B)")
+    ap.add_argument("--serial-prepare", action="store_true",
+                    help="A/B: build the per-object G table on the step's stream before fuse_query")
     return ap.parse_args()
 
 
@@ -337,12 +339,15 @@ def run_ours(args, cfg):
             bufs.reset()
             if ev:
                 ev[0].record(stream)
-            pf.fuse_prepare(views, tables, bufs)
+            if args.serial_prepare:  # A/B knob: the per-object tables on the step's stream first
+                pf.fuse_prepare(views, tables, bufs)
             if ev:
                 ev[1].record(stream)
+            # default: pf_fuse_query builds the tables itself on a forked stream, concurrently with
+            # the point sort and the tile prep
             res = pf.fuse_and_query(pts, views, tables, temperature=cfg.temperature, epsilon=cfg.eps,
                                     grid=cfg.grid, buffers=bufs, reduce=False,
-                                    prepared=True, force_simt=args.force_simt, reset=False,
+                                    prepared=args.serial_prepare, force_simt=args.force_simt, reset=False,
                                     feature_kernel=args.feature_kernel)
             if ev:
                 ev[2].record(stream)
@@ -557,8 +562,11 @@ def run_ours(args, cfg):
                                                        if world > 1 else "single GPU"),
                    "l2": ("inputs larger than L2" if not flush else "L2 flushed between steps")},
         "stages_ms": {"fuse_query": t_kern, **{k: v for k, v in stage_avg.items()},
-                      "prepare_G": sum(prep_ms) / args.steps,
+                      **({"prepare_G": sum(prep_ms) / args.steps} if args.serial_prepare or world > 1 else {}),
                       "rest(bbox,zero,voxel-mass,allreduce)": t_step - t_kern - sum(prep_ms) / args.steps},
+        **({} if args.serial_prepare or world > 1 else
+           {"prepare_G_note": "the per-object G table is built on a forked stream inside fuse_query, "
+                              "concurrently with the sort and prep stages (no serial stage)"}),
         "roofline": roofline,
         "gpu_launches": int(launches),
         "clocks": clocks,

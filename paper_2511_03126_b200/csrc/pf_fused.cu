@@ -19,6 +19,7 @@
 //      integrate_mass partial sums (integrate.py:133-155), reduced per block then atomically.
 // Featureless points (count 0) get zero probability / property rows (pipeline.py:279-280).
 #include <climits>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -423,6 +424,55 @@ int launch_fuse(const FuseParams& prm, size_t smem, cudaStream_t st) {
 
 using namespace pf;
 
+namespace {
+// one forked stream (+ fork / join events) per host thread and device: a stream shared between
+// threads could start one caller's prepare at another caller's fork point
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+constexpr int kMaxDevices = 64;
+
+SideStream* side_stream() {
+  static thread_local SideStream per_dev[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+  SideStream& x = per_dev[dev];
+  if (!x.s) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (getenv("PF_SIDE_LOWPRI")) hi = lo;  // A/B knob: the forked stream at the default priority
+    if (cudaStreamCreateWithPriority(&x.s, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      x = SideStream{};
+      return nullptr;  // run the prepare inline on the caller's stream
+    }
+  }
+  return &x;
+}
+}  // namespace
+
+extern "C" int pf_fuse_prepare(const pf_fuse_args_t* a, void* stream);
+
+namespace {
+// ForkHook of pf_fuse_query: the per-object tables on the forked stream, after the point sort
+cudaEvent_t fork_prepare(void* ctx, cudaStream_t st, int* rc) {
+  SideStream* side = side_stream();
+  const pf_fuse_args_t* a = static_cast<const pf_fuse_args_t*>(ctx);
+  if (!side) {
+    *rc = pf_fuse_prepare(a, st);
+    return nullptr;
+  }
+  cudaEventRecord(side->fork, st);
+  cudaStreamWaitEvent(side->s, side->fork, 0);
+  *rc = pf_fuse_prepare(a, side->s);
+  cudaEventRecord(side->join, side->s);
+  return side->join;
+}
+}  // namespace
+
 extern "C" {
 
 static int64_t total_cells(const pf_fuse_args_t* a) {
@@ -591,8 +641,18 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
   if (a->n == 0) return PF_OK;
   if (!a->workspace) return set_error(PF_ERR_VALUE, "fuse_query: workspace missing");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (!(a->flags & PF_FUSE_PREPARED))
-    if (int rc = pf_fuse_prepare(a, stream)) return rc;
+  // tile path: the per-object tables (G = fmap . text^T on the tensor cores) are built on a forked
+  // high-priority stream while the point sort and the tile prep run on `st` (neither reads them);
+  // the tensor-core kernel joins it. Fork / join by events, so a captured `st` captures both.
+  tile::ForkHook fork;
+  if (!(a->flags & PF_FUSE_PREPARED)) {
+    if (tile_path_ok(a) && side_stream()) {
+      fork.fn = fork_prepare;
+      fork.ctx = const_cast<pf_fuse_args_t*>(a);
+    } else if (int rc = pf_fuse_prepare(a, stream)) {
+      return rc;
+    }
+  }
   const int kpl = kpl_of(a->k), kpad = 32 * kpl;
   float* G = reinterpret_cast<float*>(a->workspace);
 
@@ -665,7 +725,11 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
     T.partials = a->partials;
     T.tbound = reinterpret_cast<const float*>(ws + L.tbound);
     T.tbox = tr == tile::kGramTile ? reinterpret_cast<float4*>(ws + L.tbox) : nullptr;
-    if (int rc = tile::run_tile_path(T, L, ws, a->points, a->n, st)) return rc;
+    cudaEvent_t joined = nullptr;
+    if (int rc = tile::run_tile_path(T, L, ws, a->points, a->n, st, fork, &joined)) {
+      if (joined) cudaStreamWaitEvent(st, joined, 0);  // rejoin the fork (keeps a capture well formed)
+      return rc;
+    }
     // sorted records -> caller's order; then the overflow points (tiles with more taps than fit in
     // shared memory) run through the SIMT kernel, which writes their outputs directly
     if (int rc = tile::run_unsort(T, st)) return rc;

@@ -1080,9 +1080,18 @@ int run_unsort(const TileParams& P, cudaStream_t st) {
 }
 
 int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const float* points,
-                  int64_t n, cudaStream_t st) {
+                  int64_t n, cudaStream_t st, ForkHook fork, cudaEvent_t* joined) {
+  cudaEvent_t g_ready = nullptr;
   uint32_t* keys = reinterpret_cast<uint32_t*>(ws + L.keys);
   stage_mark(0, st);
+  // the tables overlap the sort (forking at the prep instead measured slower: prep is issue-bound
+  // and the G projection took its SMs, +0.15 ms against the 0.1 ms it hid)
+  if (fork.fn) {
+    int frc = PF_OK;
+    g_ready = fork.fn(fork.ctx, st, &frc);
+    if (joined) *joined = g_ready;
+    if (frc) return frc;
+  }
   const int bits = sort_bits_for(n);
   cudaMemsetAsync(P.ovf_count, 0, sizeof(int32_t), st);
   if (P.deterministic) {
@@ -1142,6 +1151,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
     k_item_prep<32><<<(unsigned)(L.max_sub2 < 148 * 16 ? L.max_sub2 : 148 * 16), 128, 0, st>>>(P, L.ntiles, 2);
     if (int rc = check_launch("item_prep2")) return rc;
     stage_mark(2, st);
+    if (g_ready) cudaStreamWaitEvent(st, g_ready, 0);  // G, bf16 text, text bound
     const int rc = run_tile_gram(P, st);
     stage_mark(3, st);
     return rc;
@@ -1213,6 +1223,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
     fprintf(stderr, "[prep debug] MIXED samples ambiguous under the affine model: %.2f%%, mean eu %.4f px\n",
             100.0 * h[8] / (double)(h[7] ? h[7] : 1), 1e-6 * h[9] / (double)(h[10] ? h[10] : 1));
   }
+  if (g_ready) cudaStreamWaitEvent(st, g_ready, 0);  // G (and the x3 map splits)
   const int rc = run_tile_ws(P, st);
   stage_mark(3, st);
   return rc;

@@ -135,8 +135,15 @@ TileLayout tile_layout(int64_t n, int nv, int64_t cells, int kpadg, int d = 0, b
 // x3 operands of f32 maps: hi = bf16(x), lo = bf16(x - hi), for the maps and the G table
 int run_split_f32(const float* src, int64_t rows, int cols, int src_ld, int dst_ld, uint16_t* hi, uint16_t* lo,
                   cudaStream_t st);
+// fork (optional): called before the point sort is enqueued; it enqueues the per-object tables
+// (pf_fuse_prepare) on a forked stream and returns the event the tensor-core kernels wait on (null:
+// nothing to wait for), so the tables are built while the points are sorted
+struct ForkHook {
+  cudaEvent_t (*fn)(void* ctx, cudaStream_t st, int* rc) = nullptr;
+  void* ctx = nullptr;
+};
 int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const float* points,
-                  int64_t n, cudaStream_t st);
+                  int64_t n, cudaStream_t st, ForkHook fork = ForkHook{}, cudaEvent_t* joined = nullptr);
 int run_unsort(const TileParams& P, cudaStream_t st);
 int run_tile_ws(const TileParams& P, cudaStream_t st);
 // Gram formulation (pf_gram.cu): bf16 maps, no mean-feature output

@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .device import ViewSet, require_cuda, torch
-from .fused import FuseBuffers, QueryTables, fuse_and_query, fuse_prepare
+from .fused import FuseBuffers, QueryTables, fuse_and_query
 
 
 @dataclass
@@ -156,9 +156,9 @@ class FusePipeline:
                 else:
                     bufs = s["bufs"]
                     bufs.reset()
-                    fuse_prepare(s["views"], s["tables"], bufs)
+                    # (the per-object G table is built inside, on a forked stream overlapping the sort)
                     fuse_and_query(s["pts"], s["views"], s["tables"], temperature=self.temperature,
-                                   epsilon=self.epsilon, grid=self.grid, buffers=bufs, prepared=True, reset=False)
+                                   epsilon=self.epsilon, grid=self.grid, buffers=bufs, reset=False)
                     props_dev, mass_dev = bufs.props, bufs.mass
                 self.ev_comp[slot].record(self.comp)
             with t.cuda.stream(self.d2h):
