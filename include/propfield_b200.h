@@ -226,6 +226,13 @@ typedef struct pf_fuse_args {
    * [n, n + *vox_count) appended by the SIMT kernel                                             */
   int32_t* vox_list;        /* (2n,) or NULL                                                     */
   int32_t* vox_count;       /* (1,) device int32, caller-zeroed                                  */
+  /* optional staged inputs: cudaEvent_t handles recorded after the upload of the depth maps /
+   * of the feature maps and text table (NULL: ready when the call is enqueued). The call then waits
+   * for the depth maps only before the visibility stage and for the feature maps only before the G
+   * table and the feature gather, so an object's point sort overlaps its own remaining uploads.
+   * Points, view records, values and mid_theta must be ready when the call is enqueued.       */
+  void* depth_ready;
+  void* fmap_ready;
 } pf_fuse_args_t;
 
 uint64_t pf_fuse_workspace_bytes(const pf_fuse_args_t* args);

@@ -91,6 +91,8 @@ class FuseArgs(C.Structure):
         ("workspace", C.c_void_p),
         ("vox_list", C.c_void_p),
         ("vox_count", C.c_void_p),
+        ("depth_ready", C.c_void_p),
+        ("fmap_ready", C.c_void_p),
     ]
 
 

@@ -462,11 +462,13 @@ cudaEvent_t fork_prepare(void* ctx, cudaStream_t st, int* rc) {
   SideStream* side = side_stream();
   const pf_fuse_args_t* a = static_cast<const pf_fuse_args_t*>(ctx);
   if (!side) {
+    if (a->fmap_ready) cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(a->fmap_ready), 0);
     *rc = pf_fuse_prepare(a, st);
     return nullptr;
   }
   cudaEventRecord(side->fork, st);
   cudaStreamWaitEvent(side->s, side->fork, 0);
+  if (a->fmap_ready) cudaStreamWaitEvent(side->s, static_cast<cudaEvent_t>(a->fmap_ready), 0);
   *rc = pf_fuse_prepare(a, side->s);
   cudaEventRecord(side->join, side->s);
   return side->join;
@@ -645,12 +647,23 @@ int pf_fuse_query(const pf_fuse_args_t* a, void* stream) {
   // high-priority stream while the point sort and the tile prep run on `st` (neither reads them);
   // the tensor-core kernel joins it. Fork / join by events, so a captured `st` captures both.
   tile::ForkHook fork;
+  const bool tile = tile_path_ok(a);
+  cudaEvent_t depth_ready = static_cast<cudaEvent_t>(a->depth_ready);
+  cudaEvent_t fmap_ready = static_cast<cudaEvent_t>(a->fmap_ready);
+  if (tile) {  // staged inputs: waited on where they are first read (run_tile_path / fork_prepare)
+    fork.depth_ready = depth_ready;
+    fork.fmap_ready = fmap_ready;
+  } else {     // SIMT path: every input is read from the first kernel on
+    if (depth_ready) cudaStreamWaitEvent(st, depth_ready, 0);
+    if (fmap_ready) cudaStreamWaitEvent(st, fmap_ready, 0);
+  }
   if (!(a->flags & PF_FUSE_PREPARED)) {
-    if (tile_path_ok(a) && side_stream()) {
+    if (tile && side_stream()) {
       fork.fn = fork_prepare;
       fork.ctx = const_cast<pf_fuse_args_t*>(a);
-    } else if (int rc = pf_fuse_prepare(a, stream)) {
-      return rc;
+    } else {
+      if (tile && fmap_ready) cudaStreamWaitEvent(st, fmap_ready, 0);
+      if (int rc = pf_fuse_prepare(a, stream)) return rc;
     }
   }
   const int kpl = kpl_of(a->k), kpad = 32 * kpl;

@@ -1122,6 +1122,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
     if (int rc = check_launch("sort_scatter")) return rc;
   }
   stage_mark(1, st);
+  if (fork.depth_ready) cudaStreamWaitEvent(st, fork.depth_ready, 0);  // first read by the prep
   static unsigned long long* pdbg = nullptr;
   const bool debug = getenv("PF_WS_DEBUG") != nullptr;
   TileParams Q = P;
@@ -1152,6 +1153,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
     if (int rc = check_launch("item_prep2")) return rc;
     stage_mark(2, st);
     if (g_ready) cudaStreamWaitEvent(st, g_ready, 0);  // G, bf16 text, text bound
+    if (fork.fmap_ready) cudaStreamWaitEvent(st, fork.fmap_ready, 0);
     const int rc = run_tile_gram(P, st);
     stage_mark(3, st);
     return rc;
@@ -1224,6 +1226,7 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
             100.0 * h[8] / (double)(h[7] ? h[7] : 1), 1e-6 * h[9] / (double)(h[10] ? h[10] : 1));
   }
   if (g_ready) cudaStreamWaitEvent(st, g_ready, 0);  // G (and the x3 map splits)
+  if (fork.fmap_ready) cudaStreamWaitEvent(st, fork.fmap_ready, 0);
   const int rc = run_tile_ws(P, st);
   stage_mark(3, st);
   return rc;

@@ -141,6 +141,8 @@ int run_split_f32(const float* src, int64_t rows, int cols, int src_ld, int dst_
 struct ForkHook {
   cudaEvent_t (*fn)(void* ctx, cudaStream_t st, int* rc) = nullptr;
   void* ctx = nullptr;
+  cudaEvent_t depth_ready = nullptr;  // staged inputs (pf_fuse_args_t): waited on before the prep
+  cudaEvent_t fmap_ready = nullptr;   // ... and before the tensor-core kernel
 };
 int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const float* points,
                   int64_t n, cudaStream_t st, ForkHook fork = ForkHook{}, cudaEvent_t* joined = nullptr);

@@ -225,7 +225,8 @@ def fuse_and_query(points, views: ViewSet, tables: QueryTables, *, temperature: 
                    write_features: bool = False, write_sims: bool = False,
                    write_weights: bool = False, reduce: bool = True, check: bool = False,
                    force_simt: bool = False, prepared: bool = False,
-                   reset: bool = True, feature_kernel: bool = False, deterministic: bool = False) -> FusedResult:
+                   reset: bool = True, feature_kernel: bool = False, deterministic: bool = False,
+                   depth_ready=None, fmap_ready=None) -> FusedResult:
     """Run the whole path on `points` (N,3) f32 device tensor (numpy is uploaded).
 
     lo_hi: voxel domain (6,) f64 device tensor; None = this call's bbox (pf_bbox). Multi-GPU
@@ -234,6 +235,9 @@ def fuse_and_query(points, views: ViewSet, tables: QueryTables, *, temperature: 
     bf16 maps run the Gram-formulation tile kernel; write_features (a validation output only the
     feature-product kernel produces) or feature_kernel=True select k_tile_ws instead.
     deterministic=True: run-to-run identical results (stable sort of the points; slower).
+    depth_ready / fmap_ready: torch.cuda.Event recorded after the upload of `views`' depth maps /
+    feature maps (and `tables.text`), still in flight: the call waits for each only where it is
+    first read, so the point sort overlaps the object's remaining uploads (stream.FusePipeline).
     """
     if temperature <= 0:
         raise ValueError(f"temperature must be positive, got {temperature}")
@@ -275,6 +279,8 @@ def fuse_and_query(points, views: ViewSet, tables: QueryTables, *, temperature: 
     if deterministic:
         flags |= _lib.PF_FUSE_DETERMINISTIC
     args = _make_args(pts, n, views, tables, temperature, epsilon, grid, buffers, flags)
+    args.depth_ready = depth_ready.cuda_event if depth_ready is not None else None
+    args.fmap_ready = fmap_ready.cuda_event if fmap_ready is not None else None
     _lib.call("pf_fuse_query", args, st)
     res = FusedResult(buffers, views.nviews, tables.k, n)
     # the grid now holds this call's voxels until finalize() re-zeroes the touched ones (sparse) or

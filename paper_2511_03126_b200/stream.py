@@ -79,7 +79,9 @@ class FusePipeline:
         self.comp = t.cuda.Stream(device=dev)
         self.d2h = t.cuda.Stream(device=dev)
         mk = lambda: t.cuda.Event()  # noqa: E731
-        self.ev_h2d = [mk(), mk()]
+        self.ev_h2d = [mk(), mk()]   # whole upload (the feature maps last)
+        self.ev_pts = [mk(), mk()]   # records, property tables and points
+        self.ev_depth = [mk(), mk()]  # + depth maps
         self.ev_comp = [mk(), mk()]
         self.ev_d2h = [mk(), mk()]
         # host output ring: a result stays valid while the next LAG objects are issued (the host never
@@ -111,17 +113,21 @@ class FusePipeline:
         rec_host = s["records"]
         self.ev_h2d[slot].synchronize()  # the pinned record block of object i-2 has been read
         rec_host.copy_(t.from_numpy(rec.view(np.uint8).reshape(-1)))
+        # staged: small tables + points (the compute starts on these), then the depth maps (first read
+        # by the tile prep), then the feature maps and text (the G table and the gather)
+        tb = s["tables"]
+        v.records_dev.copy_(rec_host, non_blocking=True)
+        tb.values.copy_(obj.values, non_blocking=True)
+        tb.mid_theta.copy_(obj.mid_theta, non_blocking=True)
         s["pts"].copy_(obj.points, non_blocking=True)
+        self.ev_pts[slot].record(self.h2d)
         s["depth"].view(-1).copy_(obj.depth.reshape(-1), non_blocking=True)
+        self.ev_depth[slot].record(self.h2d)
+        tb.text.copy_(obj.text, non_blocking=True)
         if self.bf16:
             s["fmap"].view(t.int16).view(-1).copy_(obj.fmap.reshape(-1), non_blocking=True)
         else:
             s["fmap"].view(-1).copy_(obj.fmap.reshape(-1), non_blocking=True)
-        tb = s["tables"]
-        tb.text.copy_(obj.text, non_blocking=True)
-        tb.values.copy_(obj.values, non_blocking=True)
-        tb.mid_theta.copy_(obj.mid_theta, non_blocking=True)
-        v.records_dev.copy_(rec_host, non_blocking=True)
         self.h2d_bytes = (obj.points.numel() * 4 + obj.depth.numel() * 4 + obj.fmap.numel() * obj.fmap.element_size()
                           + (obj.text.numel() + obj.values.numel() + obj.mid_theta.numel()) * 4 + rec_host.numel())
 
@@ -142,7 +148,9 @@ class FusePipeline:
                 self._upload(slot, obj)
                 self.ev_h2d[slot].record(self.h2d)
             with t.cuda.stream(self.comp):
-                self.comp.wait_event(self.ev_h2d[slot])
+                # unsharded: only the points gate the start; the depth / feature-map events go into the
+                # call, which waits for them where they are first read
+                self.comp.wait_event(self.ev_pts[slot] if not self.sharded else self.ev_h2d[slot])
                 self.comp.wait_event(self.ev_d2h[slot])  # object i-2's outputs have been downloaded
                 if self.sharded:
                     from .dist import cell_sharded_steps, run_dist
@@ -158,7 +166,8 @@ class FusePipeline:
                     bufs.reset()
                     # (the per-object G table is built inside, on a forked stream overlapping the sort)
                     fuse_and_query(s["pts"], s["views"], s["tables"], temperature=self.temperature,
-                                   epsilon=self.epsilon, grid=self.grid, buffers=bufs, reset=False)
+                                   epsilon=self.epsilon, grid=self.grid, buffers=bufs, reset=False,
+                                   depth_ready=self.ev_depth[slot], fmap_ready=self.ev_h2d[slot])
                     props_dev, mass_dev = bufs.props, bufs.mass
                 self.ev_comp[slot].record(self.comp)
             with t.cuda.stream(self.d2h):

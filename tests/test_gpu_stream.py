@@ -44,3 +44,40 @@ def test_pipeline_equals_single_calls(cuda, name):
         tol = 1e-2 if cfg.bf16 else 1e-5
         torch.testing.assert_close(props, one.props.cpu(), rtol=tol, atol=tol)
         assert mass == pytest.approx(one.mass_kg(), rel=tol)
+
+
+@pytest.mark.parametrize("name,n", [("mini", None), ("mini_bf16", None), ("c5", 40_000), ("c2", 30_000)])
+def test_staged_inputs_are_waited_for(cuda, workload, name, n):
+    """depth_ready / fmap_ready: the depth maps, feature maps and text land on another stream ~50 ms
+    after the call is enqueued (a spin kernel first); the call must wait for each where it is first
+    read, and give bit for bit the outputs of a call on resident inputs."""
+    import torch
+
+    wl = workload(name, n=n) if n else workload(name)
+    views = pf.ViewSet.from_views(wl.views())
+    tables = pf.QueryTables.build(wl.text, wl.values, wl.mid_theta)
+    pts = torch.from_numpy(wl.points).cuda()
+    kw = dict(temperature=wl.cfg.temperature, epsilon=wl.cfg.eps, grid=wl.cfg.grid, deterministic=True)
+    ref = pf.fuse_and_query(pts, views, tables, **kw)
+    want = {k: getattr(ref, k).cpu().numpy().copy() for k in ("counts", "codes", "mask_bits", "props")}
+    want_mass = ref.mass_kg()
+    depth_ok, fmap_ok, text_ok = views.depth.clone(), views.fmap.clone(), tables.text.clone()
+    views.depth.zero_()
+    views.fmap.zero_()
+    tables.text.zero_()
+    torch.cuda.synchronize()
+    up = torch.cuda.Stream()
+    ev_depth, ev_fmap = torch.cuda.Event(), torch.cuda.Event()
+    with torch.cuda.stream(up):
+        torch.cuda._sleep(100_000_000)
+        views.depth.copy_(depth_ok)
+        ev_depth.record(up)
+        torch.cuda._sleep(50_000_000)
+        tables.text.copy_(text_ok)
+        views.fmap.copy_(fmap_ok)
+        ev_fmap.record(up)
+    got = pf.fuse_and_query(pts, views, tables, depth_ready=ev_depth, fmap_ready=ev_fmap, **kw)
+    torch.cuda.synchronize()
+    for k in want:
+        assert np.array_equal(getattr(got, k).cpu().numpy(), want[k]), f"{name}: {k} differs"
+    assert got.mass_kg() == pytest.approx(want_mass, rel=1e-6)
