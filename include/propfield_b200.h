@@ -384,6 +384,14 @@ int pf_stage_times(float* ms, int32_t n);
  * 2 * 128 * ktp * D (+ the taps-128.. block) per item + 2 * 128 * ktp * (128 + ktp) per 128-row
  * block; 0 for the SIMT path. Synchronises the stream. */
 int pf_tile_executed_flops(const pf_fuse_args_t* args, double* flops, void* stream);
+/* The tile path's point-sort key: the 24-state automaton of the 3-D Hilbert curve (Skilling's
+ * transpose algorithm), entry [state * 8 + octant] = key digit | 8 * next state, root state 0.
+ * pf_hilbert_table copies its 192 bytes to host memory `out` (n >= 192) and returns the state count;
+ * pf_hilbert_keys writes the key of every point's cell of the 2^bits grid (bits 7 or 8) over the
+ * bbox lo_hi (the sort's cell mapping) to keys (n,) uint32 on the device. */
+int pf_hilbert_table(uint8_t* out, int32_t n);
+int pf_hilbert_keys(const float* points, int64_t n, const double* lo_hi, int32_t bits, uint32_t* keys,
+                    void* stream);
 
 /* C (128,n) f32 = A (128,k) bf16 row-major @ B (k,n) bf16 row-major through the tile kernel's
  * tcgen05 operand layouts / descriptors / TMEM read-back. k % 64 == 0 (<= 256), n % 16 == 0.

@@ -153,6 +153,8 @@ SIGNATURES = {
     "pf_bench_gather": ([_P, _I32, _I32, _I32, _P, _P], C.c_int),
     "pf_stage_times": ([_P, _I32], C.c_int),
     "pf_tile_executed_flops": ([C.POINTER(FuseArgs), _P, _P], C.c_int),
+    "pf_hilbert_table": ([_P, _I32], C.c_int),
+    "pf_hilbert_keys": ([_P, _I64, _P, _I32, _P, _P], C.c_int),
     "pf_selftest_umma": ([_P, _P, _P, _I32, _I32, _I32, _P], C.c_int),
 }
 

@@ -42,45 +42,65 @@ namespace tile {
 
 // ---- counting sort by a coarse space-filling-curve key ------------------------------------------------
 
-// 3-D Hilbert index of a cell of the 2^bits grid (Skilling's transpose algorithm): consecutive
-// keys are face-adjacent cells, so a run of consecutive sorted points (a tile) stays one compact
-// surface patch far more often than along a Morton (Z) curve, which jumps across the object.
-__device__ __forceinline__ uint32_t hilbert3(uint32_t x, uint32_t y, uint32_t z, int bits) {
-  uint32_t X[3] = {x, y, z};
-  const uint32_t M = 1u << (bits - 1);
+// 3-D Hilbert index of a cell of the 2^bits grid: consecutive keys are face-adjacent cells, so a run
+// of consecutive sorted points (a tile) stays one compact surface patch far more often than along a
+// Morton (Z) curve, which jumps across the object. The curve is Skilling's transpose algorithm
+// ("Programming the Hilbert curve", 2004) run as its equivalent 24-state automaton: reading the
+// octant o = (x_b, y_b, z_b) of each level from the top, entry = kHilbertFsm[state][o] holds the key
+// digit (bits 0-2) and 8 * the next state (bits 3-7); the root state is 0 for every grid order. The
+// table was derived from the transpose algorithm and is checked against it on every cell of the
+// 2^7 and 2^8 grids (tests/test_oracle.py::TestHilbertKeys via pf_hilbert_table, and on the device
+// through pf_hilbert_keys). ~6 instructions per level instead of the transpose's ~35.
+constexpr int kHilbertStates = 24;
+#define PF_HILBERT_FSM \
+      8,  17,  27,   2,  39,  46,  52,   5, \
+     56,  71,  73,  86,  91,  20,  10,  13, \
+     48,   1, 103, 110, 115,  18,  12,  21, \
+    126, 129,  29,  26,  79,  80, 140,   3, \
+    148,  43,  37,  34, 127, 128,  78,  81, \
+    156,  45,  35,  42,  31,   6, 160, 105, \
+     72,  87, 139,   4,  57,  70,  50,  53, \
+      0, 171, 111,  76,  49,  58, 102,  61, \
+    180, 143,  83, 184,  69,  54,  66,  97, \
+     16, 123,   9,  74,  47,  60,  38,  77, \
+    132,  95,  85,  14,  67, 144,  82,  33, \
+    142,  55, 185,  96,  93, 116,  90,  11, \
+    188, 107, 175, 176, 101,  98,  62,  65, \
+    164, 109, 119,  22,  99, 106, 152,  41, \
+    174, 177,  63,  64, 117, 114,  92,  19, \
+     30, 125, 161, 122,   7, 172, 104,  75, \
+    130,  25, 133, 166, 179, 136,  84, 191, \
+     94,  15, 141,  28, 145,  32, 138,  51, \
+    146, 155, 149,  36, 137,  24, 190, 167, \
+    154, 157, 147,  44, 169, 182, 120, 135, \
+    162, 165, 121, 134, 187, 108, 168, 183, \
+    118, 173,  23, 124, 153, 170,  40,  59, \
+    178, 113, 131,  88, 181, 158,  68, 151, \
+    186, 163,  89, 112, 189, 100, 150, 159,
+__constant__ const unsigned char kHilbertFsmC[kHilbertStates * 8] = {PF_HILBERT_FSM};
+static const unsigned char kHilbertFsmH[kHilbertStates * 8] = {PF_HILBERT_FSM};  // pf_hilbert_table
+
+// key of the cell (x, y, z) from the table in shared memory (divergent per-lane lookups)
+__device__ __forceinline__ uint32_t hilbert_key(const unsigned char* fsm, uint32_t x, uint32_t y, uint32_t z,
+                                                int bits) {
+  uint32_t key = 0u, s8 = 0u;
 #pragma unroll
-  for (uint32_t Q = M; Q > 1; Q >>= 1) {  // inverse undo
-    const uint32_t Pm = Q - 1;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      if (X[i] & Q) {
-        X[0] ^= Pm;
-      } else {
-        const uint32_t t = (X[0] ^ X[i]) & Pm;
-        X[0] ^= t;
-        X[i] ^= t;
-      }
-    }
+  for (int b = 7; b >= 0; --b) {
+    if (b >= bits) continue;
+    const uint32_t o = (((x >> b) & 1u) << 2) | (((y >> b) & 1u) << 1) | ((z >> b) & 1u);
+    const uint32_t e = fsm[s8 | o];
+    key = (key << 3) | (e & 7u);
+    s8 = e & ~7u;
   }
-  X[1] ^= X[0];  // Gray encode
-  X[2] ^= X[1];
-  uint32_t t = 0;
-#pragma unroll
-  for (uint32_t Q = M; Q > 1; Q >>= 1)
-    if (X[2] & Q) t ^= Q - 1;
-  X[0] ^= t;
-  X[1] ^= t;
-  X[2] ^= t;
-  uint32_t key = 0;
-#pragma unroll
-  for (int b = bits - 1; b >= 0; --b)
-    key = (key << 3) | (((X[0] >> b) & 1u) << 2) | (((X[1] >> b) & 1u) << 1) | ((X[2] >> b) & 1u);
   return key;
 }
 
-template <int BITS>  // compile-time grid order: the Hilbert loops fully unrolled
+template <int BITS>  // compile-time grid order: the level loop fully unrolled
 __global__ void k_sort_keys(const float* __restrict__ p, int64_t n, const double* __restrict__ lo_hi,
                             uint32_t* __restrict__ keys, uint32_t* __restrict__ hist, uint32_t* __restrict__ iota) {
+  __shared__ unsigned char fsm[kHilbertStates * 8];
+  for (int j = threadIdx.x; j < kHilbertStates * 8; j += blockDim.x) fsm[j] = kHilbertFsmC[j];
+  __syncthreads();
   constexpr int cells = 1 << BITS;
   const float lx = (float)lo_hi[0], ly = (float)lo_hi[1], lz = (float)lo_hi[2];
   const float ext = fmaxf(fmaxf((float)(lo_hi[3] - lo_hi[0]), (float)(lo_hi[4] - lo_hi[1])),
@@ -91,8 +111,8 @@ __global__ void k_sort_keys(const float* __restrict__ p, int64_t n, const double
     const int cx = min(max((int)((__ldg(p + 3 * i) - lx) * inv), 0), cells - 1);
     const int cy = min(max((int)((__ldg(p + 3 * i + 1) - ly) * inv), 0), cells - 1);
     const int cz = min(max((int)((__ldg(p + 3 * i + 2) - lz) * inv), 0), cells - 1);
-    const uint32_t key = hilbert3((uint32_t)cx, (uint32_t)cy, (uint32_t)cz, BITS);
-    keys[i] = key;
+    const uint32_t key = hilbert_key(fsm, (uint32_t)cx, (uint32_t)cy, (uint32_t)cz, BITS);
+    if (keys) keys[i] = key;
     if (hist) atomicAdd(hist + key, 1u);
     if (iota) iota[i] = (uint32_t)i;
   }
@@ -1234,3 +1254,25 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
 
 }  // namespace tile
 }  // namespace pf
+
+// ---- diagnostics: the sort key of the tile path ------------------------------------------------------
+extern "C" {
+
+int pf_hilbert_table(uint8_t* out, int32_t n) {
+  if (!out || n < pf::tile::kHilbertStates * 8)
+    return pf::set_error(PF_ERR_VALUE, "hilbert_table: need %d bytes", pf::tile::kHilbertStates * 8);
+  memcpy(out, pf::tile::kHilbertFsmH, pf::tile::kHilbertStates * 8);
+  return pf::tile::kHilbertStates;
+}
+
+int pf_hilbert_keys(const float* points, int64_t n, const double* lo_hi, int32_t bits, uint32_t* keys,
+                    void* stream) {
+  if (bits != 7 && bits != 8) return pf::set_error(PF_ERR_VALUE, "hilbert_keys: bits must be 7 or 8, got %d", bits);
+  if (n <= 0) return PF_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (bits == 8) pf::tile::k_sort_keys<8><<<pf::grid_for(n, 256), 256, 0, st>>>(points, n, lo_hi, keys, nullptr, nullptr);
+  else pf::tile::k_sort_keys<7><<<pf::grid_for(n, 256), 256, 0, st>>>(points, n, lo_hi, keys, nullptr, nullptr);
+  return pf::check_launch("hilbert_keys");
+}
+
+}  // extern "C"
