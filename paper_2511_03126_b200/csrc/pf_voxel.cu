@@ -112,7 +112,30 @@ __global__ void k_vox_mass_sparse(float* __restrict__ grid, int64_t cells, const
                                   const int32_t* __restrict__ count, int64_t n, double* __restrict__ out) {
   const int64_t m = n + min((int64_t)*count, n);
   double acc = 0.0, occ = 0.0;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  // four list slots per thread and step: their claims (returning atomics) and sum reads are issued
+  // back to back, so each thread waits on one memory round trip per 4 slots instead of per slot (the
+  // loop is latency-bound). A voxel listed twice is claimed once: the second exchange returns 0.
+  const bool vec = (reinterpret_cast<uintptr_t>(list) & 15u) == 0u;
+  const int64_t m4 = vec ? m / 4 : 0;
+  for (int64_t q = t0; q < m4; q += stride) {
+    const int4 c4 = __ldg(reinterpret_cast<const int4*>(list) + q);
+    const int32_t c[4] = {c4.x, c4.y, c4.z, c4.w};
+    if ((c[0] & c[1] & c[2] & c[3]) < 0) continue;  // all four empty (-1)
+    float cnt[4], rho[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cnt[k] = c[k] >= 0 ? atomicExch(grid + cells + c[k], 0.0f) : 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rho[k] = cnt[k] > 0.0f ? grid[c[k]] : 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (cnt[k] > 0.0f) {
+        acc += (double)rho[k] / (double)cnt[k];
+        occ += 1.0;
+        grid[c[k]] = 0.0f;
+      }
+  }
+  for (int64_t j = 4 * m4 + t0; j < m; j += stride) {
     const int32_t c = __ldg(list + j);
     if (c < 0) continue;
     const float cnt = atomicExch(grid + cells + c, 0.0f);
