@@ -1245,12 +1245,21 @@ __global__ void __launch_bounds__(1024) k_sort_work(TileParams P) {
   auto key = [](const int4& e) { return 31 - min((e_nb(e) * e_kt(e)) >> 5, 31); };
   if (tid < 32) cnt[tid] = 0;
   __syncthreads();
-  // warp-aggregated counts (most items of a warp share a bucket); the loop bound is warp-uniform
-  for (int i0 = tid - lane; i0 < n; i0 += blockDim.x) {
-    const int i = i0 + lane;
-    const int kk = i < n ? key(P.work_raw[i]) : -1;
-    const uint32_t peers = __match_any_sync(0xffffffffu, kk);
-    if (kk >= 0 && (peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&cnt[kk], __popc(peers));
+  // warp-aggregated counts (most items of a warp share a bucket); the loop bound is warp-uniform.
+  // Both passes load kU entries per thread before using any (one CTA: the loop is latency-bound)
+  constexpr int kU = 4;
+  for (int i0 = tid - lane; i0 < n; i0 += kU * blockDim.x) {
+    int kk[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * blockDim.x + lane;
+      kk[u] = i < n ? key(P.work_raw[i]) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t peers = __match_any_sync(0xffffffffu, kk[u]);
+      if (kk[u] >= 0 && (peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&cnt[kk[u]], __popc(peers));
+    }
   }
   __syncthreads();
   if (tid < 32) {  // exclusive scan of the 32 bucket counts
@@ -1264,16 +1273,24 @@ __global__ void __launch_bounds__(1024) k_sort_work(TileParams P) {
     cnt[tid] = incl - c;
   }
   __syncthreads();
-  for (int i0 = tid - lane; i0 < n; i0 += blockDim.x) {
-    const int i = i0 + lane;
-    const int4 e = i < n ? P.work_raw[i] : make_int4(0, 0, 0, 0);
-    const int kk = i < n ? key(e) : -1;
-    const uint32_t peers = __match_any_sync(0xffffffffu, kk);
-    const int leader = __ffs(peers) - 1;
-    int base = 0;
-    if (kk >= 0 && lane == leader) base = atomicAdd(&cnt[kk], __popc(peers));
-    base = __shfl_sync(peers, base, leader);
-    if (kk >= 0) P.work[base + __popc(peers & ((1u << lane) - 1u))] = e;
+  for (int i0 = tid - lane; i0 < n; i0 += kU * blockDim.x) {
+    int4 e[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * blockDim.x + lane;
+      e[u] = i < n ? P.work_raw[i] : make_int4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * blockDim.x + lane;
+      const int kk = i < n ? key(e[u]) : -1;
+      const uint32_t peers = __match_any_sync(0xffffffffu, kk);
+      const int leader = __ffs(peers) - 1;
+      int base = 0;
+      if (kk >= 0 && lane == leader) base = atomicAdd(&cnt[kk], __popc(peers));
+      base = __shfl_sync(peers, base, leader);
+      if (kk >= 0) P.work[base + __popc(peers & ((1u << lane) - 1u))] = e[u];
+    }
   }
 }
 
