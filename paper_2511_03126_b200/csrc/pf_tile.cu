@@ -119,13 +119,14 @@ __global__ void k_sort_keys(const float* __restrict__ p, int64_t n, const double
 }
 
 __global__ void k_sort_scatter(const float* __restrict__ p, int64_t n, const uint32_t* __restrict__ keys,
-                               uint32_t* __restrict__ cursor, int32_t* __restrict__ inv,
-                               float4* __restrict__ spts) {
+                               uint32_t* __restrict__ cursor, const uint32_t* __restrict__ block_base,
+                               int32_t* __restrict__ inv, float4* __restrict__ spts) {
   // one scattered 16-byte write per point (the sorted point carries its original index in .w);
   // the inverse permutation is written coalesced
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t pos = atomicAdd(cursor + keys[i], 1u);
+    const uint32_t key = keys[i];
+    const uint32_t pos = atomicAdd(cursor + key, 1u) + __ldg(block_base + (key >> 12));
     inv[i] = (int32_t)pos;
     spts[pos] = make_float4(__ldg(p + 3 * i), __ldg(p + 3 * i + 1), __ldg(p + 3 * i + 2),
                             __int_as_float((int32_t)i));
@@ -1080,13 +1081,14 @@ int run_g_bf16(const float* G, int64_t cells, int kpad, int kpadg, uint16_t* Gbf
 }
 
 // exclusive scan of `nbins` (multiple of 4096, <= 16M) bucket counters in place (k_scan_*)
-int run_bucket_scan(uint32_t* hist, uint32_t* totals, int64_t nbins, cudaStream_t st) {
+int run_bucket_scan(uint32_t* hist, uint32_t* totals, int64_t nbins, cudaStream_t st, bool add_block_bases) {
   if (nbins % 4096 != 0 || nbins / 4096 > 4096) return set_error(PF_ERR_VALUE, "bucket scan: bad bin count");
   const int nb = (int)(nbins / 4096);
   k_scan_blocks<<<nb, 1024, 0, st>>>(hist, totals);
   if (int rc = check_launch("scan_blocks")) return rc;
   k_scan_totals<<<1, 1024, 0, st>>>(totals, nb);
   if (int rc = check_launch("scan_totals")) return rc;
+  if (!add_block_bases) return PF_OK;
   k_scan_add<<<(unsigned)(nbins / 256), 256, 0, st>>>(hist, totals);
   return check_launch("scan_add");
 }
@@ -1136,8 +1138,10 @@ int run_tile_path(TileParams P, const TileLayout& L, unsigned char* ws, const fl
     if (bits == 8) k_sort_keys<8><<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(points, n, P.lo_hi, keys, hist, nullptr);
     else k_sort_keys<7><<<grid_for(n, 256), 256, 0, st>>>(points, n, P.lo_hi, keys, hist, nullptr);
     if (int rc = check_launch("sort_keys")) return rc;
-    if (int rc = run_bucket_scan(hist, totals, nbins, st)) return rc;
-    k_sort_scatter<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(points, n, keys, hist, const_cast<int32_t*>(P.inv),
+    // block-local bucket offsets: the scatter adds its 4096-bin block's base itself (no pass over the
+    // 16M bins to add them)
+    if (int rc = run_bucket_scan(hist, totals, nbins, st, false)) return rc;
+    k_sort_scatter<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(points, n, keys, hist, totals, const_cast<int32_t*>(P.inv),
                                                              const_cast<float4*>(P.spts));
     if (int rc = check_launch("sort_scatter")) return rc;
   }

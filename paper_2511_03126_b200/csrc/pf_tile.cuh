@@ -160,7 +160,9 @@ int run_text_bound(const float* text, int k, int d, float* out, cudaStream_t st)
 int run_gproj_tc_x3(const uint16_t* fhi, const uint16_t* flo, int64_t cells, int d, const float* text, int k,
                     int kpadg, int kpad, uint16_t* Gbf, uint16_t* Gbf_lo, float* G32, uint16_t* text_hi,
                     uint16_t* text_lo, cudaStream_t st);
-int run_bucket_scan(uint32_t* hist, uint32_t* totals, int64_t nbins, cudaStream_t st);
+// add_block_bases = false leaves hist[i] block-local (exclusive within its 4096-bin block) and
+// totals[b] the exclusive base of block b: the consumer adds totals[i >> 12] itself
+int run_bucket_scan(uint32_t* hist, uint32_t* totals, int64_t nbins, cudaStream_t st, bool add_block_bases = true);
 // Hilbert order of the points for the SIMT path: order[t] = index of the t-th point along the curve
 // (7-bit key over the domain lo_hi), and *len = n (the kernel's list length). ws: point_order_bytes.
 size_t point_order_bytes(int64_t n);
