@@ -1,5 +1,5 @@
 """Race evidence for the warp-specialised kernels (compute-sanitizer is closed on
-this GPU pool, see profiles/r02_sanitizer_substitute.md).
+this GPU pool, see profiles/r02_checked_builds.md).
 
 Every work item of the tile kernels is processed start to finish by one CTA with fixed roles, so
 its per-point outputs must not depend on how items are spread over CTAs or on timing. A missing
